@@ -1,0 +1,197 @@
+/*
+ * tcb200.h -- C ABI of the B200-native TorchCor monodomain step
+ * (arXiv 2510.12011).  Plain C types only; no C++ / torch types cross it.
+ *
+ * What one time step computes (tc_step):
+ *   Eq. (2) row 1:  u^{k+1} = u^k + dt g(V^k, u^k)
+ *       (TT2006: Rush-Larsen gates, reading I1)
+ *   Eq. (3):  (chi Cm M + theta dt K) V^{k+1} = b,
+ *       b = chi M (Cm V^k - dt I_ion(V^k,u^{k+1}) + dt I_stim) - (1-theta) dt K V^k
+ *       (sign reading S1, unit reading U1)
+ *   Algorithm 1: Jacobi PCG from x0 = 2V^k - V^{k-1}
+ *   LAT / LRT.
+ *
+ * Conventions (apply to every entry point):
+ *  - Units: mm, ms, mV, S/m (== mS/mm), uF/mm^2, volumetric stimulus uA/mm^3.
+ *  - Ownership: every pointer argument is a HOST pointer owned by the caller;
+ *    the library copies what it needs during the call and never retains it.
+ *    Output buffers are caller-allocated with the documented length.  Device
+ *    memory is allocated and freed by the library (tc_destroy frees all).
+ *  - Node order: all per-node inputs/outputs use the caller's ORIGINAL node
+ *    numbering; the RCM permutation is internal.
+ *  - Errors: return codes only, no exception crosses the ABI; tc_last_error()
+ *    returns a message (owned by the context, valid until the next call on it).
+ *  - Threading: a context is used by one host thread at a time; independent
+ *    contexts are independent (cohort mode).
+ *  - All arithmetic of the step is IEEE fp64 on the GPU; there is no
+ *    CPU fallback: without a CUDA device tc_create returns TC_ECUDA.
+ */
+#ifndef TCB200_H
+#define TCB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tc_ctx tc_ctx;
+
+typedef enum {
+  TC_OK = 0,
+  TC_EINVAL = 1,   /* bad argument (index out of range, bad size, zero fibre ...) */
+  TC_ENOMEM = 2,   /* host or device allocation failed */
+  TC_ECUDA = 3,    /* CUDA runtime error / no device */
+  TC_ENCCL = 4,    /* communicator error (multi-GPU) */
+  TC_ESOLVER = 5,  /* PCG failed fail_budget consecutive steps */
+  TC_ENAN = 6,     /* NaN in a PCG inner product or in V */
+  TC_ESTATE = 7,   /* call out of order (e.g. tc_step before tc_assemble) */
+  TC_EDEGEN = 8,   /* zero-volume tetrahedron */
+  TC_EREGION = 9   /* region tag without conductivity, or sigma <= 0 */
+} tc_status;
+
+typedef enum {
+  TC_ION_TT2006_EPI = 0, /* ten Tusscher-Panfilov 2006, epicardial */
+  TC_ION_MS = 1,         /* Mitchell-Schaeffer 2003 (reading I5) */
+  TC_ION_MMS = 2         /* no ionic model: manufactured source r of Eq. 8 */
+} tc_ionic;
+
+typedef enum {
+  TC_REL_CONSECUTIVE = 0, /* ||z_{k+1}|| / ||z_k||  (Alg. 1 literal, reading C1) */
+  TC_REL_INITIAL = 1      /* ||z_{k+1}|| / ||z_0|| */
+} tc_relmode;
+
+/* Simulation settings. */
+typedef struct {
+  double theta;          /* 0 FE, 0.5 CN (default), 2/3, 1 BE (Table 2) */
+  double dt;             /* ms */
+  double chi;            /* surface-to-volume ratio, mm^-1 (Table 3: 140) */
+  double cm;             /* membrane capacitance, uF/mm^2 (Table 3: 0.01) */
+  double abs_tol;        /* eps_a of Alg. 1 (1e-5) */
+  double rel_tol;        /* eps_r of Alg. 1 */
+  int32_t max_iters;     /* m of Alg. 1 (100) */
+  int32_t rel_mode;      /* tc_relmode */
+  int32_t model;         /* tc_ionic */
+  int32_t fail_budget;   /* consecutive non-converged steps before TC_ESOLVER (3) */
+  double lat_threshold;  /* LAT: first V > this (0 mV) */
+  double lrt_threshold;  /* LRT: first later V < this with dV/dt < 0 (-70 mV) */
+  int32_t use_rcm;       /* 1: Reverse Cuthill-McKee reordering */
+  int32_t reserved;
+} tc_config;
+
+/* Per-step PCG report. */
+typedef struct {
+  int32_t iters;     /* iterations of Alg. 1's loop executed */
+  int32_t converged; /* 1 if the stopping test fired (incl. ||z_0|| < eps_a) */
+  double znorm;      /* last ||z|| */
+} tc_step_stat;
+
+/* Fills the defaults: theta 0.5, dt 0.01, chi 140, cm 0.01, tolerances 1e-5,
+ * max_iters 100, consecutive rel-mode, TT2006 epi, fail_budget 3,
+ * thresholds 0 / -70 mV, use_rcm 1. */
+void tc_config_default(tc_config* cfg);
+
+/* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
+ * (NULL = the library creates its own non-blocking stream); all device work
+ * of the context is ordered on it.  TC_ECUDA if no device is usable. */
+tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx** out);
+
+/* Frees every host and device resource of the context. NULL is accepted. */
+tc_status tc_destroy(tc_ctx* ctx);
+
+/* Message describing the last error on ctx ("" if none). */
+const char* tc_last_error(const tc_ctx* ctx);
+
+/* Mesh.  xyz: n_nodes*3 doubles (mm).  tets: n_tets*4
+ * zero-based node indices (any orientation; negatively oriented tets get two
+ * indices swapped).  region: n_tets tags (NULL = all 0).  fibre:
+ * n_tets*3 doubles, any non-zero length, normalised here (NULL = (1,0,0)).
+ * Errors: TC_EINVAL index out of range / zero fibre; TC_EDEGEN zero volume.
+ * Must precede tc_assemble; may be called once per context. */
+tc_status tc_set_mesh(tc_ctx* ctx, int64_t n_nodes, const double* xyz, int64_t n_tets,
+                      const int32_t* tets, const int32_t* region, const double* fibre);
+
+/* Region conductivities: sigma = sigma_t I + (sigma_l - sigma_t) f f^T
+ * (reading A13).  S/m, both > 0.  Replaces any previous table. */
+tc_status tc_set_conductivity(tc_ctx* ctx, int32_t n_regions, const int32_t* ids,
+                              const double* sigma_l, const double* sigma_t);
+
+/* Ionic-model parameter by name ("parameters ... programmatically
+ * reset"); TT2006 names: R T F CAP Vc Vsr Vss Ko Nao Cao GNa GK1 Gto GKr GKs pKNa
+ * GCaL GbNa GbCa GpCa KpCa GpK PNaK KmK KmNa kNaCa KmNai KmCa ksat gamma alpha
+ * Bufc Kbufc Bufsr Kbufsr Bufss Kbufss Vmaxup Kup Vrel k1p k2p k3 k4 EC maxsr
+ * minsr Vleak Vxfer;  MS: tau_in tau_out tau_open tau_close v_gate V_min V_max.
+ * TC_EINVAL for an unknown name.  Takes effect at the next tc_step. */
+tc_status tc_set_ionic_param(tc_ctx* ctx, const char* name, double value);
+tc_status tc_get_ionic_param(const tc_ctx* ctx, const char* name, double* value);
+
+/* Add a stimulus: nodes (original numbering) receive the
+ * volumetric current `amplitude` (uA/mm^3) for steps k with
+ * round(t_start/dt) <= k < round((t_start+duration)/dt) (reading T1);
+ * overlapping stimuli add.  Must precede tc_assemble. */
+tc_status tc_add_stimulus(tc_ctx* ctx, int64_t n_idx, const int32_t* nodes, double t_start,
+                          double duration, double amplitude);
+
+/* Manufactured-solution configuration (model TC_ION_MMS):
+ * source r(x,y,t) of Eq. 8 evaluated at t_k + theta dt, Dirichlet V = w(x,y,t_{k+1})
+ * on `nodes` (reading M3), initial V = w(x,y,0).  Must precede tc_assemble. */
+tc_status tc_set_mms(tc_ctx* ctx, double k, double w1, double w2, double lambda,
+                     int64_t n_dirichlet, const int32_t* nodes);
+
+/* Build the system (boundary, not timed per step): pattern, RCM, GPU
+ * assembly of M, K into A = chi Cm M + theta dt K and diag(A)^-1,
+ * initial state (model initial conditions, V^{-1} := V^0, step 0, LAT/LRT unset). */
+tc_status tc_assemble(tc_ctx* ctx);
+
+/* Advance n_steps time steps on the GPU.  stats (nullable) receives n_steps
+ * reports.  Non-convergence of a step is not an error; TC_ESOLVER after
+ * fail_budget consecutive failures, TC_ENAN on NaN (the context then refuses
+ * further steps).  Synchronises the stream once at the end. */
+tc_status tc_step(tc_ctx* ctx, int64_t n_steps, tc_step_stat* stats);
+
+/* Number of nodes, current step index k (t = k dt), state length. */
+int64_t tc_num_nodes(const tc_ctx* ctx);
+int64_t tc_current_step(const tc_ctx* ctx);
+
+/* V^k (n_nodes doubles, original order). */
+tc_status tc_get_v(tc_ctx* ctx, double* v_out);
+
+/* LAT and LRT (n_nodes doubles each, original order; -1.0 = unset). */
+tc_status tc_get_activation(tc_ctx* ctx, double* lat, double* lrt);
+
+/* Full cell state for checkpoint / state injection:
+ * [V^k (n) | V^{k-1} (n) | u_0 (n) ... u_{S-1} (n) | k | has_prev], original order,
+ * S = 18 (TT2006, state order Ki Nai Cai CaSS CaSR Rbar m h j xr1 xr2 xs r s d f
+ * f2 fCass), 1 (MS: h), 0 (MMS).  has_prev = 0 means V^{k-1} := V^k. */
+int64_t tc_state_len(const tc_ctx* ctx);
+tc_status tc_get_state(tc_ctx* ctx, double* buf, int64_t len);
+tc_status tc_set_state(tc_ctx* ctx, const double* buf, int64_t len);
+
+/* Device time (ms) spent per phase since the last reset, measured with CUDA
+ * events on the context stream when profiling is enabled:
+ * out[0] ionic kernel, out[1] PCG kernel (RHS + Alg. 1), out[2] other
+ * (stimulus, LAT epilogue); out[3] total PCG iterations; out[4] steps. */
+tc_status tc_profile(tc_ctx* ctx, int enable);
+tc_status tc_profile_read(tc_ctx* ctx, double out[5], int reset);
+
+/* ---- Minimum-slice operators on an uploaded CSR (no mesh needed) ---------- */
+/* Upload an n x n CSR (rowptr n+1, col/val nnz, columns sorted per row, the
+ * diagonal present for tc_pcg).  Replaces any previous matrix of the context. */
+tc_status tc_csr_upload(tc_ctx* ctx, int32_t n, int64_t nnz, const int32_t* rowptr,
+                        const int32_t* col, const double* val);
+/* y = A x, x and y host arrays of length n. */
+tc_status tc_spmv(tc_ctx* ctx, const double* x, double* y);
+/* Algorithm 1 with Jacobi preconditioner on the uploaded matrix; tolerances,
+ * max_iters and rel_mode from the context config.  Host arrays of length n. */
+tc_status tc_pcg(tc_ctx* ctx, const double* b, const double* x0, double* x_out,
+                 tc_step_stat* report);
+
+/* ---- Multi-GPU (row partition + halo) ------------------------- */
+/* Version of this ABI. */
+int32_t tc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCB200_H */

@@ -1,0 +1,316 @@
+"""B200-native TorchCor monodomain step (arXiv 2510.12011).
+
+Thin ctypes binding of ``libtcb200.so`` (C ABI in ``include/tcb200.h``): the
+functions below carry the ABI's names and only marshal numpy arrays; every step
+of the path runs in the library's sm_100a kernels.  There is no CPU fallback:
+importing this package without the built library raises ImportError, and
+``tc_create`` without a CUDA device raises TcError(TC_ECUDA).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _build
+
+__all__ = [
+    "TcError", "tc_config", "tc_step_stat", "tc_config_default", "tc_create", "tc_destroy",
+    "tc_last_error", "tc_set_mesh", "tc_set_conductivity", "tc_set_ionic_param",
+    "tc_get_ionic_param", "tc_add_stimulus", "tc_set_mms", "tc_assemble", "tc_step",
+    "tc_num_nodes", "tc_current_step", "tc_get_v", "tc_get_activation", "tc_state_len",
+    "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
+    "tc_spmv", "tc_pcg", "tc_abi_version", "Monodomain", "LIB_PATH",
+    "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS",
+]
+
+LIB_PATH = _build.LIB
+TC_OK, TC_EINVAL, TC_ENOMEM, TC_ECUDA, TC_ENCCL, TC_ESOLVER, TC_ENAN, TC_ESTATE, TC_EDEGEN, TC_EREGION = range(10)
+STATUS_NAMES = ["TC_OK", "TC_EINVAL", "TC_ENOMEM", "TC_ECUDA", "TC_ENCCL", "TC_ESOLVER", "TC_ENAN",
+                "TC_ESTATE", "TC_EDEGEN", "TC_EREGION"]
+TC_ION_TT2006_EPI, TC_ION_MS, TC_ION_MMS = 0, 1, 2
+MODELS = {"tt2006": TC_ION_TT2006_EPI, "ms": TC_ION_MS, "mms": TC_ION_MMS}
+
+
+class tc_config(C.Structure):
+    _fields_ = [("theta", C.c_double), ("dt", C.c_double), ("chi", C.c_double), ("cm", C.c_double),
+                ("abs_tol", C.c_double), ("rel_tol", C.c_double), ("max_iters", C.c_int32),
+                ("rel_mode", C.c_int32), ("model", C.c_int32), ("fail_budget", C.c_int32),
+                ("lat_threshold", C.c_double), ("lrt_threshold", C.c_double),
+                ("use_rcm", C.c_int32), ("reserved", C.c_int32)]
+
+
+class tc_step_stat(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("znorm", C.c_double)]
+
+
+STAT_DTYPE = np.dtype([("iters", np.int32), ("converged", np.int32), ("znorm", np.float64)])
+
+
+class TcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__(f"{name}: {msg}")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                          "(the CUDA path has no fallback)")
+    L = C.CDLL(LIB_PATH)
+    P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    sig = {
+        "tc_config_default": ([P], None),
+        "tc_create": ([P, C.c_int, P, P], I32),
+        "tc_destroy": ([P], I32),
+        "tc_last_error": ([P], C.c_char_p),
+        "tc_set_mesh": ([P, I64, P, I64, P, P, P], I32),
+        "tc_set_conductivity": ([P, I32, P, P, P], I32),
+        "tc_set_ionic_param": ([P, C.c_char_p, D], I32),
+        "tc_get_ionic_param": ([P, C.c_char_p, P], I32),
+        "tc_add_stimulus": ([P, I64, P, D, D, D], I32),
+        "tc_set_mms": ([P, D, D, D, D, I64, P], I32),
+        "tc_assemble": ([P], I32),
+        "tc_step": ([P, I64, P], I32),
+        "tc_num_nodes": ([P], I64),
+        "tc_current_step": ([P], I64),
+        "tc_get_v": ([P, P], I32),
+        "tc_get_activation": ([P, P, P], I32),
+        "tc_state_len": ([P], I64),
+        "tc_get_state": ([P, P, I64], I32),
+        "tc_set_state": ([P, P, I64], I32),
+        "tc_profile": ([P, C.c_int], I32),
+        "tc_profile_read": ([P, P, C.c_int], I32),
+        "tc_csr_upload": ([P, I32, I64, P, P, P], I32),
+        "tc_spmv": ([P, P, P], I32),
+        "tc_pcg": ([P, P, P, P, P], I32),
+        "tc_abi_version": ([], I32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+_L = _load()
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _check(ctx, st):
+    if st != TC_OK:
+        raise TcError(st, tc_last_error(ctx))
+
+
+# ---------------------------------------------------------------- ABI, same names
+def tc_abi_version() -> int:
+    return _L.tc_abi_version()
+
+
+def tc_config_default(**overrides) -> tc_config:
+    cfg = tc_config()
+    _L.tc_config_default(C.byref(cfg))
+    for k, v in overrides.items():
+        if k == "model" and isinstance(v, str):
+            v = MODELS[v]
+        setattr(cfg, k, v)
+    return cfg
+
+
+def tc_create(cfg: tc_config, device: int = 0, stream: int = 0):
+    out = C.c_void_p()
+    st = _L.tc_create(C.byref(cfg), device, C.c_void_p(stream or None), C.byref(out))
+    if st != TC_OK:
+        raise TcError(st, "tc_create failed (no usable CUDA device?)")
+    return out
+
+
+def tc_destroy(ctx) -> None:
+    _L.tc_destroy(ctx)
+
+
+def tc_last_error(ctx) -> str:
+    m = _L.tc_last_error(ctx)
+    return m.decode() if m else ""
+
+
+def tc_set_mesh(ctx, xyz, tets, region=None, fibre=None) -> None:
+    xyz, tets, region, fibre = _f64(xyz), _i32(tets), _i32(region), _f64(fibre)
+    _check(ctx, _L.tc_set_mesh(ctx, xyz.shape[0], _ptr(xyz), tets.shape[0], _ptr(tets),
+                               _ptr(region), _ptr(fibre)))
+
+
+def tc_set_conductivity(ctx, ids, sigma_l, sigma_t) -> None:
+    ids, sl, st = _i32(ids), _f64(sigma_l), _f64(sigma_t)
+    _check(ctx, _L.tc_set_conductivity(ctx, ids.shape[0], _ptr(ids), _ptr(sl), _ptr(st)))
+
+
+def tc_set_ionic_param(ctx, name: str, value: float) -> None:
+    _check(ctx, _L.tc_set_ionic_param(ctx, name.encode(), float(value)))
+
+
+def tc_get_ionic_param(ctx, name: str) -> float:
+    v = C.c_double()
+    _check(ctx, _L.tc_get_ionic_param(ctx, name.encode(), C.byref(v)))
+    return v.value
+
+
+def tc_add_stimulus(ctx, nodes, t_start, duration, amplitude) -> None:
+    nodes = _i32(nodes)
+    _check(ctx, _L.tc_add_stimulus(ctx, nodes.shape[0], _ptr(nodes), t_start, duration, amplitude))
+
+
+def tc_set_mms(ctx, k, w1, w2, lam, dirichlet_nodes) -> None:
+    nodes = _i32(dirichlet_nodes)
+    _check(ctx, _L.tc_set_mms(ctx, k, w1, w2, lam, nodes.shape[0], _ptr(nodes)))
+
+
+def tc_assemble(ctx) -> None:
+    _check(ctx, _L.tc_assemble(ctx))
+
+
+def tc_step(ctx, n_steps: int, want_stats: bool = True):
+    stats = np.zeros(n_steps, STAT_DTYPE) if want_stats else None
+    _check(ctx, _L.tc_step(ctx, n_steps, _ptr(stats)))
+    return stats
+
+
+def tc_num_nodes(ctx) -> int:
+    return _L.tc_num_nodes(ctx)
+
+
+def tc_current_step(ctx) -> int:
+    return _L.tc_current_step(ctx)
+
+
+def tc_get_v(ctx, out=None):
+    out = np.empty(tc_num_nodes(ctx)) if out is None else out
+    _check(ctx, _L.tc_get_v(ctx, _ptr(out)))
+    return out
+
+
+def tc_get_activation(ctx):
+    n = tc_num_nodes(ctx)
+    lat, lrt = np.empty(n), np.empty(n)
+    _check(ctx, _L.tc_get_activation(ctx, _ptr(lat), _ptr(lrt)))
+    return lat, lrt
+
+
+def tc_state_len(ctx) -> int:
+    return _L.tc_state_len(ctx)
+
+
+def tc_get_state(ctx, out=None):
+    m = tc_state_len(ctx)
+    out = np.empty(m) if out is None else out
+    _check(ctx, _L.tc_get_state(ctx, _ptr(out), m))
+    return out
+
+
+def tc_set_state(ctx, buf) -> None:
+    if not (isinstance(buf, np.ndarray) and buf.dtype == np.float64 and buf.flags.c_contiguous):
+        buf = _f64(buf)
+    _check(ctx, _L.tc_set_state(ctx, _ptr(buf), buf.shape[0]))
+
+
+def tc_profile(ctx, enable: bool = True) -> None:
+    _check(ctx, _L.tc_profile(ctx, int(enable)))
+
+
+def tc_profile_read(ctx, reset: bool = False):
+    out = np.zeros(5)
+    _check(ctx, _L.tc_profile_read(ctx, _ptr(out), int(reset)))
+    return dict(ionic_ms=out[0], pcg_ms=out[1], other_ms=out[2], iters=out[3], steps=out[4])
+
+
+def tc_csr_upload(ctx, rowptr, col, val) -> None:
+    rowptr, col, val = _i32(rowptr), _i32(col), _f64(val)
+    _check(ctx, _L.tc_csr_upload(ctx, rowptr.shape[0] - 1, col.shape[0], _ptr(rowptr), _ptr(col),
+                                 _ptr(val)))
+
+
+def tc_spmv(ctx, x):
+    x = _f64(x)
+    y = np.empty_like(x)
+    _check(ctx, _L.tc_spmv(ctx, _ptr(x), _ptr(y)))
+    return y
+
+
+def tc_pcg(ctx, b, x0):
+    b, x0 = _f64(b), _f64(x0)
+    x = np.empty_like(b)
+    rep = tc_step_stat()
+    _check(ctx, _L.tc_pcg(ctx, _ptr(b), _ptr(x0), _ptr(x), C.byref(rep)))
+    return x, dict(iters=rep.iters, converged=bool(rep.converged), znorm=rep.znorm)
+
+
+# ---------------------------------------------------------------- convenience wrapper
+class Monodomain:
+    """Owning wrapper: ``Monodomain(xyz, tets, region, fibre, {tag: (sl, st)}, cfg, stimuli)``.
+
+    ``stimuli`` are (nodes, t_start, duration, amplitude) tuples or objects with
+    those attributes.  Host-side orchestration only."""
+
+    def __init__(self, xyz, tets, region, fibre, conductivities: dict, cfg: tc_config,
+                 stimuli=(), device: int = 0, stream: int = 0, mms=None, params: dict | None = None):
+        self.ctx = tc_create(cfg, device, stream)
+        try:
+            tc_set_mesh(self.ctx, xyz, tets, region, fibre)
+            ids = sorted(conductivities)
+            tc_set_conductivity(self.ctx, ids, [conductivities[i][0] for i in ids],
+                                [conductivities[i][1] for i in ids])
+            for name, v in (params or {}).items():
+                tc_set_ionic_param(self.ctx, name, v)
+            for s in stimuli:
+                if isinstance(s, tuple):
+                    nodes, t0, dur, amp = s
+                else:
+                    nodes, t0, dur, amp = s.nodes, s.start, s.duration, s.amplitude
+                tc_add_stimulus(self.ctx, nodes, t0, dur, amp)
+            if mms is not None:
+                tc_set_mms(self.ctx, *mms)
+            tc_assemble(self.ctx)
+        except Exception:
+            tc_destroy(self.ctx)
+            self.ctx = None
+            raise
+
+    def step(self, n: int = 1):
+        return tc_step(self.ctx, n)
+
+    @property
+    def V(self):
+        return tc_get_v(self.ctx)
+
+    def activation(self):
+        return tc_get_activation(self.ctx)
+
+    def get_state(self):
+        return tc_get_state(self.ctx)
+
+    def set_state(self, buf):
+        tc_set_state(self.ctx, buf)
+
+    def close(self):
+        if self.ctx is not None:
+            tc_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

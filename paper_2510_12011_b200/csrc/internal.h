@@ -1,0 +1,159 @@
+// internal.h -- private declarations of libtcb200 (B200-native TorchCor step).
+// Nothing here crosses the C ABI (include/tcb200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tcb200.h"
+
+namespace tcb {
+
+// ---------------------------------------------------------------------------
+// SELL-32 sparse layout (one warp = one slice of 32 consecutive rows; slot k of
+// row 32*s + lane at slice_ptr[s] + 32*k + lane).  Rows keep the ascending column
+// order of CSR, so the SpMV sums every row in the same order as a CSR loop.
+// Padding slots point at the row itself with value 0.
+// ---------------------------------------------------------------------------
+constexpr int kSellC = 32;
+constexpr int kCgThreads = 256;           // 8 warps per CTA
+constexpr int kCgWarps = kCgThreads / 32;
+
+struct HostSell {
+  int32_t n = 0;
+  int32_t nslices = 0;
+  int64_t n_pad = 0;
+  std::vector<int64_t> slice_ptr;  // nslices + 1
+  std::vector<int32_t> col;        // slice_ptr[nslices]
+  std::vector<int32_t> rowlen;     // n
+};
+
+// ---- TT2006 parameters (kernel-argument struct; names for tc_set_ionic_param)
+struct TTParams {
+  double R, T, F, CAP, Vc, Vsr, Vss, Ko, Nao, Cao;
+  double GNa, GK1, Gto, GKr, GKs, pKNa, GCaL, GbNa, GbCa, GpCa, KpCa, GpK;
+  double PNaK, KmK, KmNa, kNaCa, KmNai, KmCa, ksat, gamma, alpha;
+  double Bufc, Kbufc, Bufsr, Kbufsr, Bufss, Kbufss;
+  double Vmaxup, Kup, Vrel, k1p, k2p, k3, k4, EC, maxsr, minsr, Vleak, Vxfer;
+};
+constexpr int kTTStates = 18;
+struct MSParams {
+  double tau_in, tau_out, tau_open, tau_close, v_gate, V_min, V_max;
+};
+struct MMSParams {
+  double k, w1, w2, lam;
+};
+
+void tt_defaults(TTParams* p, double* V0, double u0[kTTStates]);
+void ms_defaults(MSParams* p);
+double* tt_param_slot(TTParams* p, const char* name);
+double* ms_param_slot(MSParams* p, const char* name);
+
+// ---------------------------------------------------------------------------
+// Kernel argument blocks
+// ---------------------------------------------------------------------------
+struct CgArgs {
+  const int64_t* slice_ptr;
+  const int32_t* col;
+  const double* A;
+  const double* K;     // RHS mode only
+  const double* dinv;  // 1 / A_ii (0 on Dirichlet and padding rows)
+  int32_t nslices;
+  double* x;           // in: x0, out: V^{k+1}
+  double* r;
+  double* z;
+  double* q;
+  double* p0;
+  double* p1;
+  const double* up;    // u' (RHS mode)
+  const double* vp;    // v' (RHS mode)
+  const double* b;     // plain mode: r0 = b - A x0
+  double2* part;       // 2 * gridDim.x partial sums (double-buffered)
+  double eps_a, eps_r;
+  int32_t max_iters, rel_mode;
+  tc_step_stat* stat;  // where this solve's report goes
+  int32_t* flags;      // [0] abort [1] nan [2] consecutive fails [3] fail budget [4] step of abort
+  int32_t step_tag;    // step index recorded on abort
+};
+
+struct IonArgs {
+  int32_t n;
+  int64_t stride;      // n_pad (SoA state stride)
+  const double* Vk;
+  const double* Vkm1;
+  double* U;
+  double* x0;
+  double* up;
+  double* vp;
+  uint8_t* act;        // 0 none, 1 LAT set, 2 LRT set
+  double* lat;
+  double* lrt;
+  int32_t do_lat;
+  int32_t has_prev;
+  double t_k;          // time of V^k (for LAT/LRT)
+  double lat_thr, lrt_thr;
+  double dt, theta;
+  const int32_t* flags;
+  // MMS only
+  const double* xyz;
+  const uint8_t* dirichlet;
+  double t_src, t_next;
+};
+
+struct AsmArgs {
+  int32_t n;
+  const double* xyz;
+  const int32_t* tets;
+  const int32_t* ereg;
+  const double* fibre;
+  const double* sig_l;
+  const double* sig_t;
+  const int64_t* inc_ptr;
+  const int32_t* inc;  // 4*e + a
+  const int64_t* slice_ptr;
+  const int32_t* col;
+  const int32_t* rowlen;
+  double* A;
+  double* K;
+  double* dinv;
+  const uint8_t* dirichlet;  // nullable
+  double c_mass, c_stiff;
+  int32_t* err;
+};
+
+// ---- launchers (return cudaError_t of the launch) --------------------------
+cudaError_t launch_assemble(const AsmArgs& a, cudaStream_t s);
+cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s);
+cudaError_t launch_ionic_ms(const IonArgs& a, const MSParams& p, cudaStream_t s);
+cudaError_t launch_ionic_mms(const IonArgs& a, const MMSParams& p, cudaStream_t s);
+cudaError_t launch_stimulus(int32_t m, const int32_t* idx, const double* s, double* up, double* vp,
+                            double dt, double theta, const int32_t* flags, cudaStream_t st);
+cudaError_t launch_lat_epilogue(const IonArgs& a, cudaStream_t s);
+cudaError_t launch_gather(int64_t n, const int32_t* idx, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_scatter(int64_t n, const int32_t* idx, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_spmv(const int64_t* slice_ptr, const int32_t* col, const double* A, int32_t nslices,
+                        const double* x, double* y, cudaStream_t s);
+// PCG: mode 0 = plain (r0 = b - A x0), 1 = monodomain RHS (r0 = A u' - K v')
+int cg_grid_size(int mode, int32_t nslices, int device);
+cudaError_t launch_pcg(int mode, const CgArgs& a, int grid, cudaStream_t s);
+
+// ---- host setup (setup_host.cpp) --------------------------------------------
+struct HostMesh;
+std::string orient_and_validate(int64_t n, int64_t E, int32_t* tets, const double* xyz);
+void build_incidence(int64_t n, int64_t E, const int32_t* tets, std::vector<int64_t>& ptr,
+                     std::vector<int32_t>& inc);
+void build_pattern(int64_t n, const int32_t* tets, const std::vector<int64_t>& ptr,
+                   const std::vector<int32_t>& inc, std::vector<int64_t>& rowptr,
+                   std::vector<int32_t>& col);
+void rcm_order(int64_t n, const std::vector<int64_t>& rowptr, const std::vector<int32_t>& col,
+               std::vector<int32_t>& perm);
+void permute_csr(int64_t n, const std::vector<int64_t>& rowptr, const std::vector<int32_t>& col,
+                 const std::vector<int32_t>& perm, const std::vector<int32_t>& inv,
+                 std::vector<int64_t>& rowptr2, std::vector<int32_t>& col2);
+void csr_to_sell(int32_t n, const int64_t* rowptr, const int32_t* col, HostSell& s,
+                 std::vector<int64_t>* csr_slot = nullptr);
+
+}  // namespace tcb

@@ -1,0 +1,211 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+element by element, on seeded synthetic inputs.
+
+Tolerances: SpMV 1e-13 relative to the row's |A||x| sum
+(FMA contraction + summation order); PCG x to 1e-10 relative at tight tolerance
+and identical iteration counts; one monodomain step V to rel-L2 <= 1e-8
+(north_star); LAT within one dt."""
+import numpy as np
+import pytest
+
+import meshgen as G
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2510_12011_b200 as T
+    return T
+
+
+def _fem_matrix(nx=41, ny=15, nz=7, dx=0.5, permute=False):
+    xyz, tets = G.kuhn_box(nx, ny, nz, dx)
+    if permute:
+        xyz, tets, _ = G.permute_nodes(xyz, tets)
+    E = tets.shape[0]
+    rp, col, M, K = O.assemble(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E),
+                               {0: (0.1334177, 0.0173515)})
+    A = O.system_matrix(M, K, 140.0, 0.01, 0.5, 0.05)
+    return rp, col, A
+
+
+@pytest.mark.parametrize("case", ["fem", "fem_perm", "spd_ragged", "one_row", "33_rows"])
+def test_spmv_parity(T, case):
+    if case.startswith("fem"):
+        rp, col, A = _fem_matrix(permute=case == "fem_perm")
+    elif case == "spd_ragged":
+        rp, col, A, _ = G.random_spd_csr(1000, density=0.02, seed=3)
+    elif case == "one_row":
+        rp, col, A = np.array([0, 1], np.int32), np.array([0], np.int32), np.array([2.5])
+    else:
+        rp, col, A, _ = G.random_spd_csr(33, density=0.3, seed=4)
+    n = rp.shape[0] - 1
+    x = G.random_vector(n, seed=7, lo=-90, hi=40)
+    ctx = T.tc_create(T.tc_config_default())
+    try:
+        T.tc_csr_upload(ctx, rp, col, A)
+        y = T.tc_spmv(ctx, x)
+    finally:
+        T.tc_destroy(ctx)
+    yref = O.spmv(rp, col, A, x)
+    scale = O.spmv(rp, col, np.abs(A), np.abs(x)) + 1e-300
+    assert np.all(np.abs(y - yref) <= 1e-13 * scale)
+
+
+@pytest.mark.parametrize("case,rel_mode", [("fem", 0), ("fem_perm", 1), ("spd", 0), ("big", 0)])
+def test_pcg_parity(T, case, rel_mode):
+    if case == "fem":
+        rp, col, A = _fem_matrix()
+    elif case == "fem_perm":
+        rp, col, A = _fem_matrix(permute=True)
+    elif case == "big":
+        rp, col, A = _fem_matrix(101, 36, 16, 0.2)   # 58k rows, many CTAs, ragged tail
+    else:
+        rp, col, A, _ = G.random_spd_csr(777, density=0.03, seed=8)
+    n = rp.shape[0] - 1
+    b = G.random_vector(n, seed=1)
+    x0 = G.random_vector(n, seed=2, lo=-0.1, hi=0.1)
+    cfg = T.tc_config_default(abs_tol=1e-12, rel_tol=1e-3 if rel_mode else 0.0, rel_mode=rel_mode,
+                              max_iters=500)
+    ctx = T.tc_create(cfg)
+    try:
+        T.tc_csr_upload(ctx, rp, col, A)
+        x, rep = T.tc_pcg(ctx, b, x0)
+        # zero initial residual -> 0 iterations, x = x0 (reading C4)
+        xe, rep0 = T.tc_pcg(ctx, O.spmv(rp, col, A, x0), x0)
+    finally:
+        T.tc_destroy(ctx)
+    xr, rr = O.pcg(rp, col, A, b, x0, 1e-12, 1e-3 if rel_mode else 0.0, 500, rel_mode)
+    assert rep["iters"] == rr.iters and rep["converged"] == rr.converged
+    assert np.abs(x - xr).max() <= 1e-10 * np.abs(xr).max()
+    assert rep0["iters"] <= 1 and np.abs(xe - x0).max() <= 1e-10
+
+
+def _slab_case(model, nx=21, ny=8, nz=5, dx=0.5, permute=False, seed=0):
+    xyz, tets = G.kuhn_box(nx, ny, nz, dx)
+    if permute:
+        xyz, tets, _ = G.permute_nodes(xyz, tets, seed=seed + 1)
+    E = tets.shape[0]
+    region = np.zeros(E, np.int32)
+    fib = G.random_fibres(E, seed) if seed else G.uniform_fibres(E)
+    cond = {0: (0.1334177, 0.0173515)}
+    stim = O.Stimulus(G.nodes_in_box(xyz, (0, 0, 0), (1.5, 1.5, 1.5)), 0.0, 2.0, 50.0)
+    return xyz, tets, region, fib, cond, [stim]
+
+
+@pytest.mark.parametrize("model,permute,rcm", [("ms", False, 1), ("tt2006", False, 1),
+                                                ("tt2006", True, 1), ("tt2006", True, 0),
+                                                ("ms", True, 0)])
+def test_step_trajectory_parity(T, model, permute, rcm):
+    """Multi-step trajectory through the real stimulus window (upstroke), V per
+    step within rel-L2 1e-8, LAT within one dt, per-step iteration counts equal."""
+    xyz, tets, region, fib, cond, stims = _slab_case(model, permute=permute, seed=3 if permute else 0)
+    dt = 0.05
+    ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0), stims)
+    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, use_rcm=rcm)
+    sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+    try:
+        for k in range(120):
+            st = sim.step(1)
+            rep = ref.step()
+            v = sim.V
+            rel = np.linalg.norm(v - ref.Vk) / np.linalg.norm(ref.Vk)
+            assert rel <= 1e-8, (k, rel)
+            assert abs(int(st["iters"][0]) - rep.iters) <= 1
+        lat, lrt = sim.activation()
+        assert np.all((lat < 0) == (ref.lat < 0))
+        assert np.abs(lat - ref.lat).max() <= dt + 1e-12
+        # state vector round trip (original order)
+        s = sim.get_state()
+        n = xyz.shape[0]
+        assert np.allclose(s[:n], ref.Vk, rtol=0, atol=1e-8 * np.abs(ref.Vk).max())
+        U = s[2 * n:-2].reshape(-1, n)
+        assert np.allclose(U, ref.U, rtol=1e-8, atol=1e-14)
+    finally:
+        sim.close()
+
+
+def test_state_injection_one_step(T):
+    """One step from an injected mid-upstroke state: GPU == oracle (any size path)."""
+    xyz, tets, region, fib, cond, stims = _slab_case("tt2006", 31, 12, 7, 0.5, permute=True, seed=5)
+    dt = 0.02
+    ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, abs_tol=1e-9, rel_tol=0.0), stims)
+    ref.run(300)                       # 6 ms: front is propagating
+    n = xyz.shape[0]
+    buf = np.concatenate([ref.Vk, ref.Vkm1, ref.U.reshape(-1), [ref.k, 1.0]])
+    cfg = T.tc_config_default(dt=dt, abs_tol=1e-9, rel_tol=0.0)
+    sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+    try:
+        sim.set_state(buf)
+        assert np.array_equal(sim.get_state(), buf)
+        sim.step(1)
+        ref.step()
+        v = sim.V
+        assert np.linalg.norm(v - ref.Vk) / np.linalg.norm(ref.Vk) <= 1e-8
+    finally:
+        sim.close()
+
+
+def test_ionic_params_match_oracle_transcription(T):
+    """Two independent transcriptions of TT2006 / MS constants agree."""
+    for model, names, vals in (("tt2006", O.tt_param_names(), O.tt_default_params()),
+                               ("ms", O.MS_PARAM_NAMES, O.ms_default_params())):
+        ctx = T.tc_create(T.tc_config_default(model=model))
+        try:
+            for nme, v in zip(names, vals):
+                assert T.tc_get_ionic_param(ctx, nme) == v, nme
+            with pytest.raises(T.TcError):
+                T.tc_get_ionic_param(ctx, "no_such_parameter")
+        finally:
+            T.tc_destroy(ctx)
+
+
+def test_mms_on_gpu_matches_oracle_and_converges(T):
+    errs = []
+    for N in (8, 16):
+        xyz, tets = G.unit_cube(N)
+        B = G.box_boundary(xyz)
+        dt = 0.01 * 8 / N
+        out = O.run_mms(xyz, tets, B, dt=dt, T=0.5, tol=1e-10)
+        E = tets.shape[0]
+        cfg = T.tc_config_default(dt=dt, model="mms", chi=1.0, cm=1.0, abs_tol=1e-10, rel_tol=1e-10,
+                                  max_iters=1000)
+        sim = T.Monodomain(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: (1.0, 1.0)}, cfg,
+                           mms=(1.0, np.pi, np.pi, np.pi, B))
+        try:
+            sim.step(int(round(0.5 / dt)))
+            v = sim.V
+        finally:
+            sim.close()
+        assert np.abs(v - out["V"]).max() <= 1e-8
+        e = v - O.mms_w(xyz[:, 0], xyz[:, 1], 0.5)
+        rp, col, M, _ = O.assemble(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: (1.0, 1.0)})
+        errs.append(np.sqrt(e @ O.spmv(rp, col, M, e)))
+    order = np.log2(errs[0] / errs[1])
+    assert 1.7 < order < 2.3
+
+
+def test_errors_are_reported(T):
+    xyz, tets = G.kuhn_box(3, 3, 3, 1.0)
+    ctx = T.tc_create(T.tc_config_default())
+    try:
+        bad = tets.copy()
+        bad[0, 0] = 10_000
+        with pytest.raises(T.TcError) as ei:
+            T.tc_set_mesh(ctx, xyz, bad)
+        assert ei.value.status == T.TC_EINVAL
+        flat = xyz.copy()
+        flat[:, 2] = 0.0
+        with pytest.raises(T.TcError) as ei:
+            T.tc_set_mesh(ctx, flat, tets)
+        assert ei.value.status == T.TC_EDEGEN
+        with pytest.raises(T.TcError) as ei:
+            T.tc_step(ctx, 1)
+        assert ei.value.status == T.TC_ESTATE
+    finally:
+        T.tc_destroy(ctx)
