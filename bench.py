@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200-native TorchCor monodomain step.
+
+One "step" = one full time step of the hot path: ionic update
+(+ LAT/LRT, x0, u', v'), RHS + Jacobi-PCG (Algorithm 1) to tolerance, on one
+batch of synthetic input (a Kuhn-split tetrahedral slab).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  metric = node-steps/s (BASELINE.json metric);
+sim-ms per wall-s, PCG iterations, the roofline of the dominant kernel (the
+cooperative PCG kernel) and the oracle's CPU rate ride along.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import meshgen as G  # noqa: E402  (input generator: no method arithmetic)
+
+SIGMA = (0.1334177, 0.0173515)  # Table 3
+CHI, CM = 140.0, 0.01           # Table 3
+
+# BASELINE.json configs -> synthetic workloads
+WORKLOADS = {
+    # configs[4]: large synthetic slab ~20M nodes, Mitchell-Schaeffer (default at N=1)
+    "slab20M_ms": dict(cfg=4, dims=(400, 250, 200), dx=0.1, model="ms", dt=0.01,
+                       stim="face", preroll=500, sample_dims=(64, 64, 64)),
+    # north-star target: ~10M-node TT2006 slab
+    "slab10M_tt": dict(cfg="north_star", dims=(250, 200, 200), dx=0.1, model="tt2006", dt=0.01,
+                       stim="face", preroll=500, sample_dims=(48, 48, 48)),
+    # configs[2]: N-version dx = 0.1 mm (~442k nodes), TT2006 epi, dt 0.01
+    "nversion_dx0.1_tt": dict(cfg=2, dims=(201, 71, 31), dx=0.1, model="tt2006", dt=0.01,
+                              stim="corner", preroll=500, sample_dims=(48, 48, 31)),
+    # configs[0]: N-version dx = 0.5 mm (4305 nodes), TT2006 epi, dt 0.05, 40 ms
+    "nversion_dx0.5_tt": dict(cfg=0, dims=(41, 15, 7), dx=0.5, model="tt2006", dt=0.05,
+                              stim="corner", preroll=0, sample_dims=(41, 15, 7)),
+}
+DEFAULT_WORKLOAD = "slab20M_ms"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def make_inputs(w, dims=None):
+    nx, ny, nz = dims or w["dims"]
+    xyz, tets = G.kuhn_box(nx, ny, nz, w["dx"])
+    if w["stim"] == "face":      # planar stimulus on x <= 0.3 mm (SURVEY 8d, C5 / C*)
+        nodes = G.nodes_in_box(xyz, (0, -1, -1), (0.3, 1e9, 1e9))
+    else:                        # N-version corner box <= 1.5 mm (reading N2)
+        nodes = G.nodes_in_box(xyz, (0, 0, 0), (1.5, 1.5, 1.5))
+    return xyz, tets, [(nodes, 0.0, 2.0, 50.0)]
+
+
+def kuhn_nnz(nx, ny, nz):
+    """Stored entries of A on a Kuhn grid: n + 2 x edges (7 edge directions)."""
+    n = nx * ny * nz
+    axis = (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
+    face = (nx - 1) * (ny - 1) * nz + (nx - 1) * ny * (nz - 1) + nx * (ny - 1) * (nz - 1)
+    body = (nx - 1) * (ny - 1) * (nz - 1)
+    return n + 2 * (axis + face + body)
+
+
+def bytes_per_step(n, nnz, iters, model, steps):
+    """Algorithmic bytes: B_rhs + iters B_it per PCG launch; ionic per node."""
+    b_it = 12 * nnz + 4 * (n + 1) + 72 * n
+    b_rhs = 20 * nnz + 4 * (n + 1) + 44 * n
+    b_ion = (352 if model == "tt2006" else 80) * n
+    return b_rhs * steps + b_it * iters, b_ion * steps
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = [r.split(",") for r in self.out.strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({nm for r in rows for nm, v in zip(names, r[5:9]) if "Active" in v and "Not" not in v})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def oracle_sample(w, max_seconds=20.0):
+    """The CPU oracle (as it stands, single thread) on a bounded sample of the workload:
+    same dx, dt, model, stimulus style and tolerances on a smaller slab."""
+    import oracle as O
+    xyz, tets, stims = make_inputs(w, w["sample_dims"])
+    E = tets.shape[0]
+    cfg = O.Config(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5, max_iters=100)
+    sim = O.Monodomain(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: SIGMA}, cfg,
+                       [O.Stimulus(*s) for s in stims])
+    n = xyz.shape[0]
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        sim.step()
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= max_seconds or steps >= 200:
+            break
+    iters = float(np.mean([r.iters for r in sim.reports]))
+    return dict(value=n * steps / el, unit="node-steps/s", cores=1, kind="oracle",
+                sample=f"{w['sample_dims'][0]}x{w['sample_dims'][1]}x{w['sample_dims'][2]} nodes "
+                       f"({n} nodes, same dx/dt/model/stimulus), first {steps} steps from rest, "
+                       f"{el:.1f} s single-thread, mean PCG iters {iters:.1f}")
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def ncu_traffic(workload):
+    """Per-launch DRAM bytes of the PCG kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(workload)
+        return None if e is None else e
+    except Exception:
+        return None
+
+
+def run_reference(args, w):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cb = oracle_sample(w, max_seconds=max(5.0, min(60.0, 4.0 * (args.steps + args.warmup))))
+    line = {
+        "impl": "reference", "metric": "node-steps/s", "value": cb["value"], "unit": "node-steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "model": w["model"], "dt_ms": w["dt"],
+                   "note": "reference arm = the CPU oracle (no reference code exists; BASELINE.md)"},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "node-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-rcm", action="store_true")
+    ap.add_argument("--pcg-variant", type=int, default=0, help="0 direct loads (default), 1 TMA-staged")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--preroll", type=int, default=None)
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, w)
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    rank, world, local = dist_env()
+    if world > 1:
+        import bench_dist
+        return bench_dist.main(args, w)
+
+    import torch
+    import paper_2510_12011_b200 as T
+
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+    xyz, tets, stims = make_inputs(w)
+    E = tets.shape[0]
+    n = xyz.shape[0]
+    cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5,
+                              max_iters=100, use_rcm=0 if args.no_rcm else 1,
+                              pcg_variant=args.pcg_variant)
+    t0 = time.perf_counter()
+    sim = T.Monodomain(xyz, tets, np.zeros(E, np.int32), None, {0: SIGMA}, cfg, stims,
+                       device=local, stream=stream.cuda_stream)
+    t_setup = time.perf_counter() - t0
+    del tets
+    info = T.tc_matrix_info(sim.ctx)
+    preroll = w["preroll"] if args.preroll is None else args.preroll
+    if preroll:
+        sim.step(preroll)                   # move into the timing window (propagating front)
+    sim.step(args.warmup)
+    T.tc_profile(sim.ctx, True)
+    T.tc_profile_read(sim.ctx, reset=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        stats = sim.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = T.tc_profile_read(sim.ctx, reset=True)
+    T.tc_profile(sim.ctx, False)
+    iters = int(stats["iters"].sum())
+    value = n * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel: the cooperative PCG kernel (RHS + Alg. 1)
+    peaks, which = measured_peaks()
+    nnz = info["nnz"]
+    b_cg, b_ion = bytes_per_step(n, nnz, iters, w["model"], args.steps)
+    cg_s = prof["pcg_ms"] / 1e3
+    achieved = b_cg / cg_s / 1e9 if cg_s > 0 else None
+    traffic = ncu_traffic(args.workload)
+    roof = {"kernel": "pcg_kernel<1> (RHS + Alg. 1, one cooperative launch per step)", "bound": "hbm",
+            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"] if achieved else None,
+            "traffic": traffic, "peak_source": which,
+            "bytes_model": "per launch: 20nnz+4(n+1)+44n + iters*(12nnz+4(n+1)+72n) (SURVEY 8d)",
+            "share_of_step": prof["pcg_ms"] / ms,
+            "ionic_ms_per_step": prof["ionic_ms"] / args.steps,
+            "pcg_ms_per_step": prof["pcg_ms"] / args.steps,
+            "pcg_ms_per_iter": prof["pcg_ms"] / max(iters, 1)}
+
+    # end to end through the C ABI with host buffers: state H2D, step, V D2H
+    st = sim.get_state()
+    hin = torch.empty(st.shape[0], dtype=torch.float64, pin_memory=True).numpy()
+    hin[:] = st
+    hout = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    ke = max(1, args.e2e_steps)
+    T.tc_set_state(sim.ctx, hin)
+    sim.step(1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        T.tc_set_state(sim.ctx, hin)
+        T.tc_step(sim.ctx, 1, want_stats=False)
+        T.tc_get_v(sim.ctx, hout)
+    e2e_s = time.perf_counter() - t0
+    e2e = {"value": n * ke / e2e_s, "unit": "node-steps/s", "h2d_bytes_per_step": int(hin.nbytes),
+           "d2h_bytes_per_step": int(hout.nbytes),
+           "what": "per step: tc_set_state(V^k, V^{k-1}, u^k from pinned host) + tc_step(1) + tc_get_v(pinned host)"}
+    sim.close()
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = oracle_sample(w)
+        except Exception as ex:  # report, never fail the bench on the baseline leg
+            cpu = {"error": str(ex)}
+    line = {
+        "metric": "node-steps/s", "value": value, "unit": "node-steps/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "baseline_config": w["cfg"], "nodes": n, "nnz": nnz,
+                   "tets": int(E), "model": w["model"], "dt_ms": w["dt"], "dx_mm": w["dx"],
+                   "grid": list(w["dims"]), "tol": "abs=rel=1e-5, max 100 (P:316)",
+                   "rcm": not args.no_rcm, "preroll_steps": preroll, "pcg_variant": args.pcg_variant,
+                   "l2": f"inputs larger than L2 (A+K+col {(20 * info['nnz_pad']) / 1e9:.2f} GB >> 126 MB)"
+                         if n > 1_000_000 else "small problem: L2-resident",
+                   "parallelism": "1 GPU"},
+        "sim_ms_per_wall_s": args.steps * w["dt"] / (ms / 1e3),
+        "pcg_iters_per_step": iters / args.steps,
+        "setup_s": t_setup,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": prof["launches"],
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

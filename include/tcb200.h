@@ -77,7 +77,8 @@ typedef struct {
   double lat_threshold;  /* LAT: first V > this (0 mV) */
   double lrt_threshold;  /* LRT: first later V < this with dV/dt < 0 (-70 mV) */
   int32_t use_rcm;       /* 1: Reverse Cuthill-McKee reordering */
-  int32_t reserved;
+  int32_t pcg_variant;   /* PCG kernel memory pipeline: 0 direct loads at full occupancy
+                            (default), 1 TMA-staged matrix stream */
 } tc_config;
 
 /* Per-step PCG report. */
@@ -89,7 +90,7 @@ typedef struct {
 
 /* Fills the defaults: theta 0.5, dt 0.01, chi 140, cm 0.01, tolerances 1e-5,
  * max_iters 100, consecutive rel-mode, TT2006 epi, fail_budget 3,
- * thresholds 0 / -70 mV, use_rcm 1. */
+ * thresholds 0 / -70 mV, use_rcm 1, pcg_variant 0. */
 void tc_config_default(tc_config* cfg);
 
 /* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
@@ -170,10 +171,16 @@ tc_status tc_set_state(tc_ctx* ctx, const double* buf, int64_t len);
 
 /* Device time (ms) spent per phase since the last reset, measured with CUDA
  * events on the context stream when profiling is enabled:
- * out[0] ionic kernel, out[1] PCG kernel (RHS + Alg. 1), out[2] other
- * (stimulus, LAT epilogue); out[3] total PCG iterations; out[4] steps. */
+ * out[0] ionic + stimulus kernels, out[1] PCG kernel (RHS + Alg. 1),
+ * out[2] LAT epilogue; out[3] total PCG iterations; out[4] steps;
+ * out[5] kernel launches issued by tc_step (counted whether or not profiling). */
 tc_status tc_profile(tc_ctx* ctx, int enable);
-tc_status tc_profile_read(tc_ctx* ctx, double out[5], int reset);
+tc_status tc_profile_read(tc_ctx* ctx, double out[6], int reset);
+
+/* Sizes of the assembled system: out[0] n, out[1] nnz (stored entries of A,
+ * CSR count), out[2] padded SELL-32 slots, out[3] slices, out[4] PCG grid
+ * (CTAs of the cooperative kernel).  TC_ESTATE before tc_assemble/tc_csr_upload. */
+tc_status tc_matrix_info(const tc_ctx* ctx, int64_t out[5]);
 
 /* ---- Minimum-slice operators on an uploaded CSR (no mesh needed) ---------- */
 /* Upload an n x n CSR (rowptr n+1, col/val nnz, columns sorted per row, the

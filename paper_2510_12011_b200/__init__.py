@@ -21,11 +21,11 @@ __all__ = [
     "tc_get_ionic_param", "tc_add_stimulus", "tc_set_mms", "tc_assemble", "tc_step",
     "tc_num_nodes", "tc_current_step", "tc_get_v", "tc_get_activation", "tc_state_len",
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
-    "tc_spmv", "tc_pcg", "tc_abi_version", "Monodomain", "LIB_PATH",
+    "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "Monodomain", "LIB_PATH",
     "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS",
 ]
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("TCB200_LIB") or _build.LIB   # override: experiment variants only
 TC_OK, TC_EINVAL, TC_ENOMEM, TC_ECUDA, TC_ENCCL, TC_ESOLVER, TC_ENAN, TC_ESTATE, TC_EDEGEN, TC_EREGION = range(10)
 STATUS_NAMES = ["TC_OK", "TC_EINVAL", "TC_ENOMEM", "TC_ECUDA", "TC_ENCCL", "TC_ESOLVER", "TC_ENAN",
                 "TC_ESTATE", "TC_EDEGEN", "TC_EREGION"]
@@ -38,7 +38,7 @@ class tc_config(C.Structure):
                 ("abs_tol", C.c_double), ("rel_tol", C.c_double), ("max_iters", C.c_int32),
                 ("rel_mode", C.c_int32), ("model", C.c_int32), ("fail_budget", C.c_int32),
                 ("lat_threshold", C.c_double), ("lrt_threshold", C.c_double),
-                ("use_rcm", C.c_int32), ("reserved", C.c_int32)]
+                ("use_rcm", C.c_int32), ("pcg_variant", C.c_int32)]
 
 
 class tc_step_stat(C.Structure):
@@ -56,9 +56,11 @@ class TcError(RuntimeError):
 
 
 def _load():
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
-                          "(the CUDA path has no fallback)")
+    if LIB_PATH == _build.LIB and _build.stale():
+        try:  # in-tree rebuild when the sources are newer than the library
+            _build.build()
+        except Exception as e:  # no fallback: fail loudly
+            raise ImportError(f"{LIB_PATH} is missing or stale and nvcc failed: {e}") from e
     L = C.CDLL(LIB_PATH)
     P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
     sig = {
@@ -83,6 +85,7 @@ def _load():
         "tc_set_state": ([P, P, I64], I32),
         "tc_profile": ([P, C.c_int], I32),
         "tc_profile_read": ([P, P, C.c_int], I32),
+        "tc_matrix_info": ([P, P], I32),
         "tc_csr_upload": ([P, I32, I64, P, P, P], I32),
         "tc_spmv": ([P, P, P], I32),
         "tc_pcg": ([P, P, P, P, P], I32),
@@ -231,9 +234,17 @@ def tc_profile(ctx, enable: bool = True) -> None:
 
 
 def tc_profile_read(ctx, reset: bool = False):
-    out = np.zeros(5)
+    out = np.zeros(6)
     _check(ctx, _L.tc_profile_read(ctx, _ptr(out), int(reset)))
-    return dict(ionic_ms=out[0], pcg_ms=out[1], other_ms=out[2], iters=out[3], steps=out[4])
+    return dict(ionic_ms=out[0], pcg_ms=out[1], other_ms=out[2], iters=out[3], steps=out[4],
+                launches=int(out[5]))
+
+
+def tc_matrix_info(ctx) -> dict:
+    out = np.zeros(5, np.int64)
+    _check(ctx, _L.tc_matrix_info(ctx, _ptr(out)))
+    return dict(n=int(out[0]), nnz=int(out[1]), nnz_pad=int(out[2]), nslices=int(out[3]),
+                pcg_grid=int(out[4]))
 
 
 def tc_csr_upload(ctx, rowptr, col, val) -> None:

@@ -78,7 +78,8 @@ struct tc_ctx {
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> evs;
-  double t_ion = 0, t_cg = 0, t_other = 0, prof_iters = 0, prof_steps = 0;
+  double t_ion = 0, t_cg = 0, t_other = 0, prof_iters = 0, prof_steps = 0, launches = 0;
+  int64_t nnz = 0;
   std::vector<void*> allocs;
 };
 
@@ -130,14 +131,14 @@ void tc_config_default(tc_config* c) {
   c->lat_threshold = 0.0;
   c->lrt_threshold = -70.0;
   c->use_rcm = 1;
-  c->reserved = 0;
+  c->pcg_variant = 0;
 }
 
 tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx** out) {
   if (!cfg || !out) return TC_EINVAL;
   *out = nullptr;
   if (!(cfg->dt > 0) || !(cfg->theta >= 0 && cfg->theta <= 1) || !(cfg->chi > 0) || !(cfg->cm > 0) ||
-      cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 || cfg->model > 2)
+      cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 || cfg->model > 2 || cfg->pcg_variant < 0 || cfg->pcg_variant > 1)
     return TC_EINVAL;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0) return TC_ECUDA;
@@ -373,6 +374,7 @@ tc_status tc_assemble(tc_ctx* c) {
     for (int q = 0; q < 3; ++q) xyz2[3 * i + q] = c->xyz[3 * (int64_t)c->perm[i] + q];
   build_incidence(n, E, tets2.data(), iptr, inc);
   HostSell hs;
+  c->nnz = rp2[n];
   csr_to_sell((int32_t)n, rp2.data(), col2.data(), hs);
   rp2.clear(); rp2.shrink_to_fit(); col2.clear(); col2.shrink_to_fit();
   c->nslices = hs.nslices;
@@ -483,7 +485,7 @@ tc_status tc_assemble(tc_ctx* c) {
       CUDA_TRY(c, cudaMemcpyAsync(c->d_stim_s, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice, c->stream));
     }
   }
-  c->cg_grid = cg_grid_size(1, c->nslices, c->device);
+  c->cg_grid = cg_grid_size(1, c->cfg.pcg_variant, c->nslices, c->device);
   CUDA_TRY(c, dalloc(c, &c->d_part, 2 * (int64_t)c->cg_grid));
   int32_t flags[8] = {0, 0, 0, c->cfg.fail_budget, -1, 0, 0, 0};
   CUDA_TRY(c, cudaMemcpyAsync(c->d_flags, flags, sizeof(flags), cudaMemcpyHostToDevice, c->stream));
@@ -580,16 +582,20 @@ tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
     else if (model == TC_ION_MS) e = launch_ionic_ms(ia, c->ms, c->stream);
     else e = launch_ionic_mms(ia, c->mms, c->stream);
     CUDA_TRY(c, e);
+    c->launches += 1;
     // (2) stimulus of the epoch containing step k
     for (const Epoch& ep : c->epochs)
-      if (ep.k0 <= c->k && c->k < ep.k1)
+      if (ep.k0 <= c->k && c->k < ep.k1) {
         CUDA_TRY(c, launch_stimulus(ep.m, c->d_stim_idx + ep.off, c->d_stim_s + ep.off, c->d_up,
                                     c->d_vp, c->cfg.dt, c->cfg.theta, c->d_flags, c->stream));
+        c->launches += 1;
+      }
     if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (3) RHS + Algorithm 1 in one cooperative kernel
     CgArgs ca = cg_args(c);
     ca.stat = c->d_stats + s;
-    CUDA_TRY(c, launch_pcg(1, ca, c->cg_grid, c->stream));
+    CUDA_TRY(c, launch_pcg(1, c->cfg.pcg_variant, ca, c->cg_grid, c->stream));
+    c->launches += 1;
     if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (4) V^{k-1} <- V^k <- x
     int old = c->iVkm1;
@@ -600,7 +606,10 @@ tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
     c->has_prev = true;
   }
   // LAT/LRT of the last V (time t_k)
-  if (model != TC_ION_MMS) CUDA_TRY(c, launch_lat_epilogue(ion_args(c, 1), c->stream));
+  if (model != TC_ION_MMS) {
+    CUDA_TRY(c, launch_lat_epilogue(ion_args(c, 1), c->stream));
+    c->launches += 1;
+  }
   if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
   std::vector<tc_step_stat> hst(nsteps);
   int32_t flags[8];
@@ -636,14 +645,26 @@ tc_status tc_profile(tc_ctx* c, int enable) {
   return TC_OK;
 }
 
-tc_status tc_profile_read(tc_ctx* c, double out[5], int reset) {
+tc_status tc_profile_read(tc_ctx* c, double out[6], int reset) {
   if (!c || !out) return TC_EINVAL;
   out[0] = c->t_ion;
   out[1] = c->t_cg;
   out[2] = c->t_other;
   out[3] = c->prof_iters;
   out[4] = c->prof_steps;
-  if (reset) c->t_ion = c->t_cg = c->t_other = c->prof_iters = c->prof_steps = 0;
+  out[5] = c->launches;
+  if (reset) c->t_ion = c->t_cg = c->t_other = c->prof_iters = c->prof_steps = c->launches = 0;
+  return TC_OK;
+}
+
+tc_status tc_matrix_info(const tc_ctx* c, int64_t out[5]) {
+  if (!c || !out) return TC_EINVAL;
+  if (!c->assembled && !c->csr_mode) return TC_ESTATE;
+  out[0] = c->n;
+  out[1] = c->nnz;
+  out[2] = c->nnz_pad;
+  out[3] = c->nslices;
+  out[4] = c->cg_grid;
   return TC_OK;
 }
 
@@ -737,6 +758,7 @@ tc_status tc_csr_upload(tc_ctx* c, int32_t n, int64_t nnz, const int32_t* rowptr
   std::vector<double> sv(hs.slice_ptr[hs.nslices], 0.0);
   for (int64_t t = 0; t < nnz; ++t) sv[slot[t]] = val[t];
   c->n = n;
+  c->nnz = nnz;
   c->nslices = hs.nslices;
   c->n_pad = hs.n_pad;
   c->nnz_pad = hs.slice_ptr[hs.nslices];
@@ -750,7 +772,7 @@ tc_status tc_csr_upload(tc_ctx* c, int32_t n, int64_t nnz, const int32_t* rowptr
   CUDA_TRY(c, cudaMemcpyAsync(c->d_col, hs.col.data(), hs.col.size() * 4, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_A, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_dinv, dinv.data(), dinv.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  c->cg_grid = cg_grid_size(0, c->nslices, c->device);
+  c->cg_grid = cg_grid_size(0, c->cfg.pcg_variant, c->nslices, c->device);
   CUDA_TRY(c, dalloc(c, &c->d_part, 2 * (int64_t)c->cg_grid));
   if (ensure_stats(c, 1) != TC_OK) return TC_ECUDA;
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -780,7 +802,7 @@ tc_status tc_pcg(tc_ctx* c, const double* b, const double* x0, double* x, tc_ste
   CUDA_TRY(c, cudaMemcpyAsync(c->d_V[0], x0, c->n * 8, cudaMemcpyHostToDevice, c->stream));
   CgArgs ca = cg_args(c);
   ca.stat = c->d_stats;
-  CUDA_TRY(c, launch_pcg(0, ca, c->cg_grid, c->stream));
+  CUDA_TRY(c, launch_pcg(0, c->cfg.pcg_variant, ca, c->cg_grid, c->stream));
   tc_step_stat h;
   CUDA_TRY(c, cudaMemcpyAsync(&h, c->d_stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(x, c->d_V[0], c->n * 8, cudaMemcpyDeviceToHost, c->stream));

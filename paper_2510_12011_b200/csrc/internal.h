@@ -137,8 +137,9 @@ cudaError_t launch_scatter(int64_t n, const int32_t* idx, const double* in, doub
 cudaError_t launch_spmv(const int64_t* slice_ptr, const int32_t* col, const double* A, int32_t nslices,
                         const double* x, double* y, cudaStream_t s);
 // PCG: mode 0 = plain (r0 = b - A x0), 1 = monodomain RHS (r0 = A u' - K v')
-int cg_grid_size(int mode, int32_t nslices, int device);
-cudaError_t launch_pcg(int mode, const CgArgs& a, int grid, cudaStream_t s);
+// variant 0 = direct loads at full occupancy, 1 = TMA-staged matrix stream
+int cg_grid_size(int mode, int variant, int32_t nslices, int device);
+cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
 
 // ---- host setup (setup_host.cpp) --------------------------------------------
 struct HostMesh;

@@ -8,6 +8,14 @@
 //      x += alpha_{it-1} p_{it-1}, and the partial sums of p.q.
 //   U: alpha = rho / p.q;  r -= alpha q;  z = r / diag(A);  partials r.z, z.z;
 //      then every CTA evaluates the stopping test of Alg. 1 identically.
+// Two memory pipelines (measured side by side):
+//  * DIRECT (default): 32 registers/thread, 64 warps/SM; every warp streams its
+//    slice's values and column indices with evict-first loads and gathers the
+//    vectors from L1/L2; latency is hidden by occupancy.
+//  * TMA: the streamed matrix (values and column indices of a slice are two
+//    contiguous runs) is staged into shared memory by TMA bulk copies
+//    (cp.async.bulk + mbarrier, L2 evict-first) two slices ahead per warp;
+//    96 KB smem per CTA limits it to 16 warps/SM.
 // Reductions are deterministic: per-CTA partials in a fixed slot, then every
 // CTA sums all partials in the same order (bitwise-identical scalars => all
 // CTAs take the same branch).
@@ -19,6 +27,51 @@ namespace cg = cooperative_groups;
 
 namespace tcb {
 
+constexpr int kWMax = 16;                               // widest TMA-staged slice
+constexpr int kValBytes = kWMax * kSellC * 8;           // 4 KB of values
+constexpr int kStageBytes = kWMax * kSellC * (8 + 4);   // + 2 KB of column indices
+constexpr int kStages = 2;
+constexpr int kWarpSmem = kStages * kStageBytes;        // 12 KB per warp
+constexpr int kCgSmem = kCgWarps * kWarpSmem;           // 96 KB per CTA (2 CTAs / SM)
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 1-D TMA bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ reductions
 __device__ __forceinline__ double2 warp_sum2(double2 v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -56,53 +109,176 @@ __device__ __forceinline__ double2 grid_sum2(double2 v, double2* buf, double2* s
   return block_sum2(acc, sh);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kCgThreads) pcg_kernel(CgArgs a) {
+// ------------------------------------------------------------------ slice pipeline
+// One warp walks its slices s = gw, gw + nw, ... ; slice s's values and column
+// indices are staged in stage (j mod kStages) by lane 0's TMA copies issued
+// kStages slices ahead.  Slices wider than kWMax (irregular meshes) fall back
+// to direct loads.
+struct SlicePipe {
+  char* buf;
+  uint64_t* bar;
+  uint32_t phase;  // bit st = parity of the next completion of stage st
+  uint64_t pol;
+};
+
+__device__ __forceinline__ void slice_bounds(const int64_t* sp, int s, int64_t& base, int& w) {
+  base = __ldg(sp + s);
+  w = (int)((__ldg(sp + s + 1) - base) >> 5);
+}
+
+__device__ __forceinline__ void pipe_issue(SlicePipe& P, int st, const double* A, const int* col,
+                                           const int64_t* sp, int s, int ns) {
+  if (s >= ns) return;
+  int64_t base;
+  int w;
+  slice_bounds(sp, s, base, w);
+  if (w <= 0 || w > kWMax) return;
+  char* dst = P.buf + st * kStageBytes;
+  const uint32_t bv = (uint32_t)w * kSellC * 8, bc = (uint32_t)w * kSellC * 4;
+  mbar_expect_tx(P.bar + st, bv + bc);
+  tma_load(dst, A + base, bv, P.bar + st, P.pol);
+  tma_load(dst + kValBytes, col + base, bc, P.bar + st, P.pol);
+}
+
+// f(i, base, w, staged, As, Cs) for every slice of this warp (i = this lane's row).
+template <bool TMA, class F>
+__device__ __forceinline__ void for_slices(SlicePipe& P, const int64_t* sp, const double* A,
+                                           const int* col, int ns, int gw, int nw, int lane, F&& f);
+
+template <class F>
+__device__ __forceinline__ void for_slices_tma(SlicePipe& P, const int64_t* sp, const double* A,
+                                           const int* col, int ns, int gw, int nw, int lane, F&& f) {
+  if (lane == 0) {
+#pragma unroll
+    for (int st = 0; st < kStages; ++st) pipe_issue(P, st, A, col, sp, gw + st * nw, ns);
+  }
+  int st = 0;
+  for (int s = gw; s < ns; s += nw) {
+    int64_t base;
+    int w;
+    slice_bounds(sp, s, base, w);
+    const bool staged = w > 0 && w <= kWMax;
+    if (staged) {
+      mbar_wait(P.bar + st, (P.phase >> st) & 1u);
+      P.phase ^= 1u << st;
+    }
+    const char* sb = P.buf + st * kStageBytes;
+    f((int64_t)s * kSellC + lane, base, w, staged, reinterpret_cast<const double*>(sb),
+      reinterpret_cast<const int*>(sb + kValBytes));
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async();  // generic-proxy reads of the stage before the async overwrite
+      pipe_issue(P, st, A, col, sp, s + kStages * nw, ns);
+    }
+    st = (st + 1 == kStages) ? 0 : st + 1;
+  }
+}
+
+template <bool TMA, class F>
+__device__ __forceinline__ void for_slices(SlicePipe& P, const int64_t* sp, const double* A,
+                                           const int* col, int ns, int gw, int nw, int lane, F&& f) {
+  if (TMA) {
+    for_slices_tma(P, sp, A, col, ns, gw, nw, lane, f);
+  } else {
+    for (int s = gw; s < ns; s += nw) {
+      int64_t base;
+      int w;
+      slice_bounds(sp, s, base, w);
+      f((int64_t)s * kSellC + lane, base, w, false, (const double*)nullptr, (const int*)nullptr);
+    }
+  }
+}
+
+// q_i = sum_k A_ik p_c, p_c = z_c (+ beta pold_c); slots accumulated in
+// ascending order (the CSR order).  Staged: operands from shared memory.
+template <bool FIRST>
+__device__ __forceinline__ double row_Ap_staged(int w, int lane, const double* As, const int* Cs,
+                                                const double* z, const double* pold, double beta) {
+  double sum = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < w; ++k) {
+    const int c = Cs[k * kSellC + lane];
+    const double g = FIRST ? z[c] : z[c] + beta * pold[c];
+    sum += As[k * kSellC + lane] * g;
+  }
+  return sum;
+}
+
+template <bool FIRST>
+__device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, const int* col,
+                                                const double* A, const double* z, const double* pold,
+                                                double beta) {
+  double sum = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const int64_t t = base + (int64_t)k * kSellC + lane;
+    const int c = __ldcs(col + t);
+    const double g = FIRST ? z[c] : z[c] + beta * pold[c];
+    sum += __ldcs(A + t) * g;
+  }
+  return sum;
+}
+
+// ------------------------------------------------------------------ the kernel
+template <int MODE, bool TMA>
+__global__ void __launch_bounds__(kCgThreads, TMA ? 2 : 8) pcg_kernel(CgArgs a) {
   cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) char smem[];
   __shared__ double2 sh[kCgWarps];
+  __shared__ __align__(8) uint64_t bars[TMA ? kCgWarps : 1][kStages];
   if (a.flags[0]) return;  // context aborted earlier: uniform across the grid
 
-  const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kCgWarps + (threadIdx.x >> 5);
+  constexpr int UU = TMA ? 4 : 1;  // slices per warp pass in the streaming phases
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kCgWarps + warp;
   const int nw = gridDim.x * kCgWarps;
   const int32_t ns = a.nslices;
   const int64_t* __restrict__ sp = a.slice_ptr;
-  const int32_t* __restrict__ col = a.col;
+  const int* __restrict__ col = a.col;
   const double* __restrict__ Av = a.A;
   const double* __restrict__ dinv = a.dinv;
   double2* partA = a.part;
   double2* partB = a.part + gridDim.x;
 
+  SlicePipe P;
+  if (TMA) {
+    P.buf = smem + warp * kWarpSmem;
+    P.bar = bars[TMA ? warp : 0];
+    P.phase = 0;
+    P.pol = policy_evict_first();
+    if (lane == 0) {
+      for (int st = 0; st < kStages; ++st) mbar_init(P.bar + st, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
+
   // ---- r_0, z_0 = M^{-1} r_0, rho_0 = r.z, ||z_0||^2 ------------------------
   double2 acc = make_double2(0.0, 0.0);
-  for (int s = gw; s < ns; s += nw) {
-    const int64_t base = __ldg(sp + s);
-    const int w = (int)((__ldg(sp + s + 1) - base) >> 5);
-    const int64_t i = (int64_t)s * kSellC + lane;
-    double sum = 0.0;
-    if (MODE == 1) {
-      const double* __restrict__ Kv = a.K;
-      // r_0 = A u' - K v'  (== b - A x_0 with Eq. 3's b)
+  for_slices<TMA>(P, sp, Av, col, ns, gw, nw, lane,
+             [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
+               double sum = 0.0;
+               if (MODE == 1) {
+                 // r_0 = A u' - K v'  (== b - A x_0 with Eq. 3's b)
+                 const double* __restrict__ Kv = a.K;
 #pragma unroll 4
-      for (int k = 0; k < w; ++k) {
-        const int64_t t = base + (int64_t)k * kSellC + lane;
-        const int c = __ldg(col + t);
-        sum += __ldg(Av + t) * a.up[c] - __ldg(Kv + t) * a.vp[c];
-      }
-    } else {
-#pragma unroll 4
-      for (int k = 0; k < w; ++k) {
-        const int64_t t = base + (int64_t)k * kSellC + lane;
-        sum += __ldg(Av + t) * a.x[__ldg(col + t)];
-      }
-      sum = a.b[i] - sum;
-    }
-    const double zi = __ldg(dinv + i) * sum;
-    a.r[i] = sum;
-    a.z[i] = zi;
-    acc.x += sum * zi;
-    acc.y += zi * zi;
-  }
+                 for (int k = 0; k < w; ++k) {
+                   const int64_t t = base + (int64_t)k * kSellC + lane;
+                   const int c = staged ? Cs[k * kSellC + lane] : __ldcs(col + t);
+                   const double av = staged ? As[k * kSellC + lane] : __ldcs(Av + t);
+                   sum += av * a.up[c] - __ldcs(Kv + t) * a.vp[c];
+                 }
+               } else {
+                 const double ax = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.x, nullptr, 0.0)
+                                          : row_Ap_direct<true>(base, w, lane, col, Av, a.x, nullptr, 0.0);
+                 sum = a.b[i] - ax;
+               }
+               const double zi = __ldg(dinv + i) * sum;
+               a.r[i] = sum;
+               a.z[i] = zi;
+               acc.x += sum * zi;
+               acc.y += zi * zi;
+             });
   double2 tot = grid_sum2(acc, partA, sh, grid);
   double rho = tot.x;
   double zeta = sqrt(tot.y);
@@ -113,60 +289,68 @@ __global__ void __launch_bounds__(kCgThreads) pcg_kernel(CgArgs a) {
   if (!nan && zeta < a.eps_a) conv = 1;  // reading C4: return x0
 
   double alpha = 0.0, beta = 0.0;
-  double* pold = a.p1;
-  double* pnew = a.p0;
   bool last_valid = false;
-  double* plast = a.p0;
   if (!nan && !conv) {
     for (it = 0; it < a.max_iters;) {
       // ---- S: p = z + beta p_old (on the fly), q = A p, x += alpha_prev p_old
       acc = make_double2(0.0, 0.0);
-      const bool first = (it == 0);
-      for (int s = gw; s < ns; s += nw) {
-        const int64_t base = __ldg(sp + s);
-        const int w = (int)((__ldg(sp + s + 1) - base) >> 5);
-        const int64_t i = (int64_t)s * kSellC + lane;
-        double pi = a.z[i];
-        if (!first) {
-          const double po = pold[i];
-          pi += beta * po;
-          a.x[i] += alpha * po;
-        }
-        double sum = 0.0;
-        if (first) {
-#pragma unroll 4
-          for (int k = 0; k < w; ++k) {
-            const int64_t t = base + (int64_t)k * kSellC + lane;
-            sum += __ldg(Av + t) * a.z[__ldg(col + t)];
-          }
-        } else {
-#pragma unroll 4
-          for (int k = 0; k < w; ++k) {
-            const int64_t t = base + (int64_t)k * kSellC + lane;
-            const int c = __ldg(col + t);
-            sum += __ldg(Av + t) * (a.z[c] + beta * pold[c]);
-          }
-        }
-        pnew[i] = pi;
-        a.q[i] = sum;
-        acc.x += pi * sum;
+      double* __restrict__ pnew = (it & 1) ? a.p1 : a.p0;   // p_it
+      const double* __restrict__ pold = (it & 1) ? a.p0 : a.p1;  // p_{it-1}
+      if (it == 0) {
+        for_slices<TMA>(P, sp, Av, col, ns, gw, nw, lane,
+                   [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
+                     const double pi = a.z[i];
+                     const double sum = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.z, nullptr, 0.0)
+                                               : row_Ap_direct<true>(base, w, lane, col, Av, a.z, nullptr, 0.0);
+                     pnew[i] = pi;
+                     a.q[i] = sum;
+                     acc.x += pi * sum;
+                   });
+      } else {
+        for_slices<TMA>(P, sp, Av, col, ns, gw, nw, lane,
+                   [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
+                     const double po = pold[i];
+                     const double xi = a.x[i];
+                     const double pi = a.z[i] + beta * po;
+                     a.x[i] = xi + alpha * po;
+                     const double sum = staged ? row_Ap_staged<false>(w, lane, As, Cs, a.z, pold, beta)
+                                               : row_Ap_direct<false>(base, w, lane, col, Av, a.z, pold, beta);
+                     pnew[i] = pi;
+                     a.q[i] = sum;
+                     acc.x += pi * sum;
+                   });
       }
-      plast = pnew;
       last_valid = true;
       tot = grid_sum2(acc, partB, sh, grid);
       const double pq = tot.x;
       if (isnan(pq)) { nan = 1; break; }
       alpha = rho / pq;                                   // alpha_k = rho_k / p.q
-      // ---- U: r -= alpha q, z = r / d, partials of r.z and z.z
+      // ---- U: r -= alpha q, z = r / d, partials of r.z and z.z (UU slices / warp pass)
       acc = make_double2(0.0, 0.0);
-      for (int s = gw; s < ns; s += nw) {
-        const int64_t i = (int64_t)s * kSellC + lane;
-        const double ri = a.r[i] - alpha * a.q[i];
-        const double zi = __ldg(dinv + i) * ri;
-        a.r[i] = ri;
-        a.z[i] = zi;
-        acc.x += ri * zi;
-        acc.y += zi * zi;
+      for (int s = gw; s < ns; s += UU * nw) {
+        double rr[UU], qq[UU], dd[UU];
+#pragma unroll
+        for (int u = 0; u < UU; ++u) {
+          const int su = s + u * nw;
+          if (su < ns) {
+            const int64_t i = (int64_t)su * kSellC + lane;
+            rr[u] = a.r[i];
+            qq[u] = a.q[i];
+            dd[u] = __ldg(dinv + i);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UU; ++u) {
+          const int su = s + u * nw;
+          if (su < ns) {
+            const int64_t i = (int64_t)su * kSellC + lane;
+            const double ri = rr[u] - alpha * qq[u], zi = dd[u] * ri;
+            a.r[i] = ri;
+            a.z[i] = zi;
+            acc.x += ri * zi;
+            acc.y += zi * zi;
+          }
+        }
       }
       tot = grid_sum2(acc, partA, sh, grid);
       ++it;
@@ -177,14 +361,23 @@ __global__ void __launch_bounds__(kCgThreads) pcg_kernel(CgArgs a) {
       beta = tot.x / rho;                                 // beta_k = rho_{k+1} / rho_k
       rho = tot.x;
       if (a.rel_mode == 0) zref = zeta_new;
-      double* t = pold; pold = pnew; pnew = t;
     }
   }
   // deferred x += alpha p of the last iteration (Alg. 1 updates x before the test)
   if (last_valid && !nan) {
-    for (int s = gw; s < ns; s += nw) {
-      const int64_t i = (int64_t)s * kSellC + lane;
-      a.x[i] += alpha * plast[i];
+    const double* __restrict__ plast = ((it - 1) & 1) ? a.p1 : a.p0;  // p of the last iteration
+    for (int s = gw; s < ns; s += UU * nw) {
+      double xx[UU], pp[UU];
+#pragma unroll
+      for (int u = 0; u < UU; ++u)
+        if (s + u * nw < ns) {
+          const int64_t i = (int64_t)(s + u * nw) * kSellC + lane;
+          xx[u] = a.x[i];
+          pp[u] = plast[i];
+        }
+#pragma unroll
+      for (int u = 0; u < UU; ++u)
+        if (s + u * nw < ns) a.x[(int64_t)(s + u * nw) * kSellC + lane] = xx[u] + alpha * pp[u];
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -201,7 +394,7 @@ __global__ void __launch_bounds__(kCgThreads) pcg_kernel(CgArgs a) {
   }
 }
 
-__global__ void spmv_kernel(const int64_t* __restrict__ sp, const int32_t* __restrict__ col,
+__global__ void spmv_kernel(const int64_t* __restrict__ sp, const int* __restrict__ col,
                             const double* __restrict__ Av, int32_t ns, const double* __restrict__ x,
                             double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
@@ -232,12 +425,18 @@ static int sm_count(int dev) {
   return g_sm_count[dev];
 }
 
+static const void* pcg_fn(int mode, int variant) {
+  if (variant == 1) return mode == 1 ? (const void*)pcg_kernel<1, true> : (const void*)pcg_kernel<0, true>;
+  return mode == 1 ? (const void*)pcg_kernel<1, false> : (const void*)pcg_kernel<0, false>;
+}
+static int pcg_smem(int variant) { return variant == 1 ? kCgSmem : 0; }
+
 // Grid: enough CTAs for one slice per warp, capped at the co-resident maximum
-// (cooperative launch); large problems get every SM x occupancy.
-int cg_grid_size(int mode, int32_t nslices, int device) {
+// (cooperative launch); large problems get every SM x occupancy (2 CTAs / SM).
+int cg_grid_size(int mode, int variant, int32_t nslices, int device) {
+  cudaFuncSetAttribute(pcg_fn(mode, variant), cudaFuncAttributeMaxDynamicSharedMemorySize, pcg_smem(variant));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, mode == 1 ? (const void*)pcg_kernel<1> : (const void*)pcg_kernel<0>, kCgThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_fn(mode, variant), kCgThreads, pcg_smem(variant));
   if (per_sm < 1) per_sm = 1;
   int maxg = per_sm * sm_count(device);
   int need = (nslices + kCgWarps - 1) / kCgWarps;
@@ -245,10 +444,10 @@ int cg_grid_size(int mode, int32_t nslices, int device) {
   return need < maxg ? need : maxg;
 }
 
-cudaError_t launch_pcg(int mode, const CgArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s) {
   void* args[] = {(void*)&a};
-  const void* fn = mode == 1 ? (const void*)pcg_kernel<1> : (const void*)pcg_kernel<0>;
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kCgThreads), args, 0, s);
+  return cudaLaunchCooperativeKernel(pcg_fn(mode, variant), dim3(grid), dim3(kCgThreads), args,
+                                     pcg_smem(variant), s);
 }
 
 cudaError_t launch_spmv(const int64_t* sp, const int32_t* col, const double* A, int32_t ns,

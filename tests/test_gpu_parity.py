@@ -57,8 +57,9 @@ def test_spmv_parity(T, case):
     assert np.all(np.abs(y - yref) <= 1e-13 * scale)
 
 
+@pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("case,rel_mode", [("fem", 0), ("fem_perm", 1), ("spd", 0), ("big", 0)])
-def test_pcg_parity(T, case, rel_mode):
+def test_pcg_parity(T, case, rel_mode, variant):
     if case == "fem":
         rp, col, A = _fem_matrix()
     elif case == "fem_perm":
@@ -71,7 +72,7 @@ def test_pcg_parity(T, case, rel_mode):
     b = G.random_vector(n, seed=1)
     x0 = G.random_vector(n, seed=2, lo=-0.1, hi=0.1)
     cfg = T.tc_config_default(abs_tol=1e-12, rel_tol=1e-3 if rel_mode else 0.0, rel_mode=rel_mode,
-                              max_iters=500)
+                              max_iters=500, pcg_variant=variant)
     ctx = T.tc_create(cfg)
     try:
         T.tc_csr_upload(ctx, rp, col, A)
@@ -98,16 +99,17 @@ def _slab_case(model, nx=21, ny=8, nz=5, dx=0.5, permute=False, seed=0):
     return xyz, tets, region, fib, cond, [stim]
 
 
-@pytest.mark.parametrize("model,permute,rcm", [("ms", False, 1), ("tt2006", False, 1),
-                                                ("tt2006", True, 1), ("tt2006", True, 0),
-                                                ("ms", True, 0)])
-def test_step_trajectory_parity(T, model, permute, rcm):
+@pytest.mark.parametrize("model,permute,rcm,variant", [("ms", False, 1, 0), ("tt2006", False, 1, 0),
+                                                        ("tt2006", True, 1, 0), ("tt2006", True, 0, 1),
+                                                        ("ms", True, 0, 1), ("tt2006", False, 1, 1)])
+def test_step_trajectory_parity(T, model, permute, rcm, variant):
     """Multi-step trajectory through the real stimulus window (upstroke), V per
     step within rel-L2 1e-8, LAT within one dt, per-step iteration counts equal."""
     xyz, tets, region, fib, cond, stims = _slab_case(model, permute=permute, seed=3 if permute else 0)
     dt = 0.05
     ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0), stims)
-    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, use_rcm=rcm)
+    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, use_rcm=rcm,
+                              pcg_variant=variant)
     sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
     try:
         for k in range(120):
