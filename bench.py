@@ -193,7 +193,7 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-rcm", action="store_true")
-    ap.add_argument("--pcg-variant", type=int, default=0, help="0 direct loads (default), 1 TMA-staged")
+    ap.add_argument("--pcg-variant", type=int, default=0, help="0 direct loads (default), 1 TMA-staged, 2 direct + 16-bit indices")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--preroll", type=int, default=None)
@@ -296,6 +296,7 @@ def main():
                    "tets": int(E), "model": w["model"], "dt_ms": w["dt"], "dx_mm": w["dx"],
                    "grid": list(w["dims"]), "tol": "abs=rel=1e-5, max 100 (P:316)",
                    "rcm": not args.no_rcm, "preroll_steps": preroll, "pcg_variant": args.pcg_variant,
+                   "wide_slices": info.get("wide_slices"),
                    "l2": f"inputs larger than L2 (A+K+col {(20 * info['nnz_pad']) / 1e9:.2f} GB >> 126 MB)"
                          if n > 1_000_000 else "small problem: L2-resident",
                    "parallelism": "1 GPU"},

@@ -77,8 +77,9 @@ typedef struct {
   double lat_threshold;  /* LAT: first V > this (0 mV) */
   double lrt_threshold;  /* LRT: first later V < this with dV/dt < 0 (-70 mV) */
   int32_t use_rcm;       /* 1: Reverse Cuthill-McKee reordering */
-  int32_t pcg_variant;   /* PCG kernel memory pipeline: 0 direct loads at full occupancy
-                            (default), 1 TMA-staged matrix stream */
+  int32_t pcg_variant;   /* PCG kernel memory pipeline: 0 direct
+                            loads at full occupancy (default), 1 TMA-staged matrix stream,
+                            2 direct loads with 16-bit column offsets */
 } tc_config;
 
 /* Per-step PCG report. */
@@ -179,8 +180,9 @@ tc_status tc_profile_read(tc_ctx* ctx, double out[6], int reset);
 
 /* Sizes of the assembled system: out[0] n, out[1] nnz (stored entries of A,
  * CSR count), out[2] padded SELL-32 slots, out[3] slices, out[4] PCG grid
- * (CTAs of the cooperative kernel).  TC_ESTATE before tc_assemble/tc_csr_upload. */
-tc_status tc_matrix_info(const tc_ctx* ctx, int64_t out[5]);
+ * (CTAs of the cooperative kernel), out[5] slices kept at int32 indices.
+ * TC_ESTATE before tc_assemble/tc_csr_upload. */
+tc_status tc_matrix_info(const tc_ctx* ctx, int64_t out[6]);
 
 /* ---- Minimum-slice operators on an uploaded CSR (no mesh needed) ---------- */
 /* Upload an n x n CSR (rowptr n+1, col/val nnz, columns sorted per row, the

@@ -241,10 +241,10 @@ def tc_profile_read(ctx, reset: bool = False):
 
 
 def tc_matrix_info(ctx) -> dict:
-    out = np.zeros(5, np.int64)
+    out = np.zeros(6, np.int64)
     _check(ctx, _L.tc_matrix_info(ctx, _ptr(out)))
     return dict(n=int(out[0]), nnz=int(out[1]), nnz_pad=int(out[2]), nslices=int(out[3]),
-                pcg_grid=int(out[4]))
+                pcg_grid=int(out[4]), wide_slices=int(out[5]))
 
 
 def tc_csr_upload(ctx, rowptr, col, val) -> None:

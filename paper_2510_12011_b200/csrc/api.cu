@@ -54,6 +54,10 @@ struct tc_ctx {
   // device
   int64_t* d_sp = nullptr;
   int32_t* d_col = nullptr;
+  uint16_t* d_col16 = nullptr;
+  int32_t* d_kbase = nullptr;
+  uint8_t* d_fmt = nullptr;
+  int64_t n_wide = 0;
   double *d_A = nullptr, *d_K = nullptr, *d_dinv = nullptr;
   double* d_V[3] = {nullptr, nullptr, nullptr};
   int iVk = 0, iVkm1 = 1, iX = 2;
@@ -138,7 +142,7 @@ tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx*
   if (!cfg || !out) return TC_EINVAL;
   *out = nullptr;
   if (!(cfg->dt > 0) || !(cfg->theta >= 0 && cfg->theta <= 1) || !(cfg->chi > 0) || !(cfg->cm > 0) ||
-      cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 || cfg->model > 2 || cfg->pcg_variant < 0 || cfg->pcg_variant > 1)
+      cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 || cfg->model > 2 || cfg->pcg_variant < 0 || cfg->pcg_variant > 2)
     return TC_EINVAL;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0) return TC_ECUDA;
@@ -314,6 +318,21 @@ static tc_status init_state(tc_ctx* c) {
   return TC_OK;
 }
 
+// 16-bit index compression for the direct PCG pipeline
+static tc_status upload_compressed(tc_ctx* c, HostSell& hs) {
+  if (c->cfg.pcg_variant != 2) return TC_OK;  // variants 0 (default) and 1 (TMA) stream int32 indices
+  compress_sell(hs);
+  c->n_wide = hs.n_wide;
+  CUDA_TRY(c, dalloc(c, &c->d_col16, (int64_t)hs.col16.size()));
+  CUDA_TRY(c, dalloc(c, &c->d_kbase, (int64_t)hs.kbase.size()));
+  CUDA_TRY(c, dalloc(c, &c->d_fmt, (int64_t)hs.fmt.size()));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_col16, hs.col16.data(), hs.col16.size() * 2, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_kbase, hs.kbase.data(), hs.kbase.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_fmt, hs.fmt.data(), hs.fmt.size(), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TC_OK;
+}
+
 static tc_status alloc_vectors(tc_ctx* c) {
   const int64_t np = c->n_pad;
   for (int b = 0; b < 3; ++b) CUDA_TRY(c, dalloc(c, &c->d_V[b], np));
@@ -485,6 +504,7 @@ tc_status tc_assemble(tc_ctx* c) {
       CUDA_TRY(c, cudaMemcpyAsync(c->d_stim_s, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice, c->stream));
     }
   }
+  if (upload_compressed(c, hs) != TC_OK) return TC_ECUDA;
   c->cg_grid = cg_grid_size(1, c->cfg.pcg_variant, c->nslices, c->device);
   CUDA_TRY(c, dalloc(c, &c->d_part, 2 * (int64_t)c->cg_grid));
   int32_t flags[8] = {0, 0, 0, c->cfg.fail_budget, -1, 0, 0, 0};
@@ -532,6 +552,9 @@ static CgArgs cg_args(tc_ctx* c) {
   CgArgs a{};
   a.slice_ptr = c->d_sp;
   a.col = c->d_col;
+  a.col16 = c->d_col16;
+  a.kbase = c->d_kbase;
+  a.fmt = c->d_fmt;
   a.A = c->d_A;
   a.K = c->d_K;
   a.dinv = c->d_dinv;
@@ -595,7 +618,7 @@ tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
     CgArgs ca = cg_args(c);
     ca.stat = c->d_stats + s;
     CUDA_TRY(c, launch_pcg(1, c->cfg.pcg_variant, ca, c->cg_grid, c->stream));
-    c->launches += 1;
+    c->launches += 2;  // RHS kernel + cooperative PCG kernel
     if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (4) V^{k-1} <- V^k <- x
     int old = c->iVkm1;
@@ -657,7 +680,7 @@ tc_status tc_profile_read(tc_ctx* c, double out[6], int reset) {
   return TC_OK;
 }
 
-tc_status tc_matrix_info(const tc_ctx* c, int64_t out[5]) {
+tc_status tc_matrix_info(const tc_ctx* c, int64_t out[6]) {
   if (!c || !out) return TC_EINVAL;
   if (!c->assembled && !c->csr_mode) return TC_ESTATE;
   out[0] = c->n;
@@ -665,6 +688,7 @@ tc_status tc_matrix_info(const tc_ctx* c, int64_t out[5]) {
   out[2] = c->nnz_pad;
   out[3] = c->nslices;
   out[4] = c->cg_grid;
+  out[5] = c->n_wide;
   return TC_OK;
 }
 
@@ -772,6 +796,7 @@ tc_status tc_csr_upload(tc_ctx* c, int32_t n, int64_t nnz, const int32_t* rowptr
   CUDA_TRY(c, cudaMemcpyAsync(c->d_col, hs.col.data(), hs.col.size() * 4, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_A, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_dinv, dinv.data(), dinv.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  if (upload_compressed(c, hs) != TC_OK) return TC_ECUDA;
   c->cg_grid = cg_grid_size(0, c->cfg.pcg_variant, c->nslices, c->device);
   CUDA_TRY(c, dalloc(c, &c->d_part, 2 * (int64_t)c->cg_grid));
   if (ensure_stats(c, 1) != TC_OK) return TC_ECUDA;

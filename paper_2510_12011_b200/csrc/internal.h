@@ -29,6 +29,12 @@ struct HostSell {
   std::vector<int64_t> slice_ptr;  // nslices + 1
   std::vector<int32_t> col;        // slice_ptr[nslices]
   std::vector<int32_t> rowlen;     // n
+  // 16-bit index compression: col = kbase[slice_ptr[s]/32 + k] + col16[slot]
+  // for slices with fmt[s] == 0 (every slot row of the slice spans < 2^16).
+  std::vector<uint16_t> col16;     // slice_ptr[nslices]
+  std::vector<int32_t> kbase;      // slice_ptr[nslices] / 32
+  std::vector<uint8_t> fmt;        // nslices: 0 compressed, 1 plain int32
+  int64_t n_wide = 0;
 };
 
 // ---- TT2006 parameters (kernel-argument struct; names for tc_set_ionic_param)
@@ -58,6 +64,9 @@ double* ms_param_slot(MSParams* p, const char* name);
 struct CgArgs {
   const int64_t* slice_ptr;
   const int32_t* col;
+  const uint16_t* col16;  // nullable: 16-bit compressed indices
+  const int32_t* kbase;
+  const uint8_t* fmt;
   const double* A;
   const double* K;     // RHS mode only
   const double* dinv;  // 1 / A_ii (0 on Dirichlet and padding rows)
@@ -156,5 +165,6 @@ void permute_csr(int64_t n, const std::vector<int64_t>& rowptr, const std::vecto
                  std::vector<int64_t>& rowptr2, std::vector<int32_t>& col2);
 void csr_to_sell(int32_t n, const int64_t* rowptr, const int32_t* col, HostSell& s,
                  std::vector<int64_t>* csr_slot = nullptr);
+void compress_sell(HostSell& s);
 
 }  // namespace tcb

@@ -9,9 +9,11 @@
 //   U: alpha = rho / p.q;  r -= alpha q;  z = r / diag(A);  partials r.z, z.z;
 //      then every CTA evaluates the stopping test of Alg. 1 identically.
 // Two memory pipelines (measured side by side):
-//  * DIRECT (default): 32 registers/thread, 64 warps/SM; every warp streams its
-//    slice's values and column indices with evict-first loads and gathers the
-//    vectors from L1/L2; latency is hidden by occupancy.
+//  * DIRECT (default, variant 0): 32 registers/thread, 64 warps/SM; every warp
+//    streams its slice's values and column indices with evict-first loads and
+//    gathers the vectors from L1/L2; latency is hidden by occupancy.
+//    Variant 2 = the same with 16-bit column offsets (fewer bytes, more
+//    instructions; measured slower, kept for the record).
 //  * TMA: the streamed matrix (values and column indices of a slice are two
 //    contiguous runs) is staged into shared memory by TMA bulk copies
 //    (cp.async.bulk + mbarrier, L2 evict-first) two slices ahead per warp;
@@ -27,6 +29,9 @@ namespace cg = cooperative_groups;
 
 namespace tcb {
 
+#ifndef TCB_DIRECT_MINB
+#define TCB_DIRECT_MINB 8   // CTAs/SM of the direct variant: 8 -> 32 registers, 64 warps/SM
+#endif
 constexpr int kWMax = 16;                               // widest TMA-staged slice
 constexpr int kValBytes = kWMax * kSellC * 8;           // 4 KB of values
 constexpr int kStageBytes = kWMax * kSellC * (8 + 4);   // + 2 KB of column indices
@@ -204,24 +209,113 @@ __device__ __forceinline__ double row_Ap_staged(int w, int lane, const double* A
   return sum;
 }
 
+// Column index of slot t (slot row k) of one slice: either the plain int32
+// array, or (compressed slices) a per-(slice, k) int32 base, broadcast to the
+// warp, plus a 16-bit offset per slot.
+struct ColIdx {
+  const int* c32;
+  const uint16_t* c16;  // null: uncompressed slice
+  const int* kb;
+  __device__ __forceinline__ int operator()(int64_t t, int k) const {
+    return c16 ? __ldg(kb + k) + (int)__ldcs(c16 + t) : __ldcs(c32 + t);
+  }
+};
+
+template <bool COMP>
+__device__ __forceinline__ ColIdx col_of(const CgArgs& a, int64_t i, int64_t base) {
+  ColIdx ci;
+  ci.c32 = a.col;
+  ci.c16 = nullptr;
+  ci.kb = nullptr;
+  if (COMP && __ldg(a.fmt + (i >> 5)) == 0) {
+    ci.c16 = a.col16;
+    ci.kb = a.kbase + (base >> 5);
+  }
+  return ci;
+}
+
 template <bool FIRST>
-__device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, const int* col,
+__device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, const ColIdx& ci,
                                                 const double* A, const double* z, const double* pold,
                                                 double beta) {
   double sum = 0.0;
 #pragma unroll 4
   for (int k = 0; k < w; ++k) {
     const int64_t t = base + (int64_t)k * kSellC + lane;
-    const int c = __ldcs(col + t);
+    const int c = ci(t, k);
     const double g = FIRST ? z[c] : z[c] + beta * pold[c];
     sum += __ldcs(A + t) * g;
   }
   return sum;
 }
 
-// ------------------------------------------------------------------ the kernel
-template <int MODE, bool TMA>
-__global__ void __launch_bounds__(kCgThreads, TMA ? 2 : 8) pcg_kernel(CgArgs a) {
+// ------------------------------------------------------------------ kernels
+// VAR 0: direct loads, int32 indices (default), 1: TMA-staged, 2: direct loads + 16-bit indices
+#define TCB_MINB(VAR) ((VAR) == 1 ? 2 : TCB_DIRECT_MINB)
+
+__device__ __forceinline__ void setup_pipe(SlicePipe& P, char* smem, uint64_t* bars, int warp, int lane) {
+  P.buf = smem + warp * kWarpSmem;
+  P.bar = bars;
+  P.phase = 0;
+  P.pol = policy_evict_first();
+  if (lane == 0) {
+    for (int st = 0; st < kStages; ++st) mbar_init(P.bar + st, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
+
+// r_0 = b - A x_0 (MODE 0) or A u' - K v' (MODE 1, == b - A x_0 with Eq. 3's b;
+// DESIGN.md "RHS"), z_0 = r_0 / diag(A), and per-CTA partials of r.z, z.z.
+// Same grid as the PCG kernel that consumes the partials.
+template <int MODE, int VAR>
+__global__ void __launch_bounds__(kCgThreads, VAR == 1 ? 2 : 4) rhs_kernel(CgArgs a) {
+  constexpr bool TMA = VAR == 1;
+  constexpr bool COMP = VAR == 2;
+  extern __shared__ __align__(128) char smem[];
+  __shared__ double2 sh[kCgWarps];
+  __shared__ __align__(8) uint64_t bars[TMA ? kCgWarps : 1][kStages];
+  if (a.flags[0]) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kCgWarps + warp;
+  const int nw = gridDim.x * kCgWarps;
+  const double* __restrict__ Av = a.A;
+  SlicePipe P;
+  if (TMA) setup_pipe(P, smem, bars[TMA ? warp : 0], warp, lane);
+  double2 acc = make_double2(0.0, 0.0);
+  for_slices<TMA>(P, a.slice_ptr, Av, a.col, a.nslices, gw, nw, lane,
+             [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
+               double sum = 0.0;
+               if (MODE == 1) {
+                 const double* __restrict__ Kv = a.K;
+                 const ColIdx ci = col_of<COMP>(a, i, base);
+#pragma unroll 4
+                 for (int k = 0; k < w; ++k) {
+                   const int64_t t = base + (int64_t)k * kSellC + lane;
+                   const int c = staged ? Cs[k * kSellC + lane] : ci(t, k);
+                   const double av = staged ? As[k * kSellC + lane] : __ldcs(Av + t);
+                   sum += av * a.up[c] - __ldcs(Kv + t) * a.vp[c];
+                 }
+               } else {
+                 const double ax = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.x, nullptr, 0.0)
+                                          : row_Ap_direct<true>(base, w, lane, col_of<COMP>(a, i, base), Av, a.x, nullptr, 0.0);
+                 sum = a.b[i] - ax;
+               }
+               const double zi = __ldg(a.dinv + i) * sum;
+               a.r[i] = sum;
+               a.z[i] = zi;
+               acc.x += sum * zi;
+               acc.y += zi * zi;
+             });
+  const double2 b = block_sum2(acc, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = b;
+}
+
+// Algorithm 1's loop from r_0, z_0 and the RHS kernel's partials.
+template <int MODE, int VAR>
+__global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a) {
+  constexpr bool TMA = VAR == 1;
+  constexpr bool COMP = VAR == 2;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) char smem[];
   __shared__ double2 sh[kCgWarps];
@@ -241,45 +335,20 @@ __global__ void __launch_bounds__(kCgThreads, TMA ? 2 : 8) pcg_kernel(CgArgs a) 
   double2* partB = a.part + gridDim.x;
 
   SlicePipe P;
-  if (TMA) {
-    P.buf = smem + warp * kWarpSmem;
-    P.bar = bars[TMA ? warp : 0];
-    P.phase = 0;
-    P.pol = policy_evict_first();
-    if (lane == 0) {
-      for (int st = 0; st < kStages; ++st) mbar_init(P.bar + st, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-  }
+  if (TMA) setup_pipe(P, smem, bars[TMA ? warp : 0], warp, lane);
 
-  // ---- r_0, z_0 = M^{-1} r_0, rho_0 = r.z, ||z_0||^2 ------------------------
-  double2 acc = make_double2(0.0, 0.0);
-  for_slices<TMA>(P, sp, Av, col, ns, gw, nw, lane,
-             [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
-               double sum = 0.0;
-               if (MODE == 1) {
-                 // r_0 = A u' - K v'  (== b - A x_0 with Eq. 3's b)
-                 const double* __restrict__ Kv = a.K;
-#pragma unroll 4
-                 for (int k = 0; k < w; ++k) {
-                   const int64_t t = base + (int64_t)k * kSellC + lane;
-                   const int c = staged ? Cs[k * kSellC + lane] : __ldcs(col + t);
-                   const double av = staged ? As[k * kSellC + lane] : __ldcs(Av + t);
-                   sum += av * a.up[c] - __ldcs(Kv + t) * a.vp[c];
-                 }
-               } else {
-                 const double ax = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.x, nullptr, 0.0)
-                                          : row_Ap_direct<true>(base, w, lane, col, Av, a.x, nullptr, 0.0);
-                 sum = a.b[i] - ax;
-               }
-               const double zi = __ldg(dinv + i) * sum;
-               a.r[i] = sum;
-               a.z[i] = zi;
-               acc.x += sum * zi;
-               acc.y += zi * zi;
-             });
-  double2 tot = grid_sum2(acc, partA, sh, grid);
+  // ---- rho_0 = r.z, ||z_0|| from the RHS kernel's per-CTA partials ------------
+  double2 tot;
+  {
+    double2 acc0 = make_double2(0.0, 0.0);
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) {
+      const double2 u = partA[t];
+      acc0.x += u.x;
+      acc0.y += u.y;
+    }
+    tot = block_sum2(acc0, sh);
+  }
+  double2 acc;
   double rho = tot.x;
   double zeta = sqrt(tot.y);
   double zref = zeta;
@@ -301,7 +370,7 @@ __global__ void __launch_bounds__(kCgThreads, TMA ? 2 : 8) pcg_kernel(CgArgs a) 
                    [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
                      const double pi = a.z[i];
                      const double sum = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.z, nullptr, 0.0)
-                                               : row_Ap_direct<true>(base, w, lane, col, Av, a.z, nullptr, 0.0);
+                                               : row_Ap_direct<true>(base, w, lane, col_of<COMP>(a, i, base), Av, a.z, nullptr, 0.0);
                      pnew[i] = pi;
                      a.q[i] = sum;
                      acc.x += pi * sum;
@@ -314,7 +383,7 @@ __global__ void __launch_bounds__(kCgThreads, TMA ? 2 : 8) pcg_kernel(CgArgs a) 
                      const double pi = a.z[i] + beta * po;
                      a.x[i] = xi + alpha * po;
                      const double sum = staged ? row_Ap_staged<false>(w, lane, As, Cs, a.z, pold, beta)
-                                               : row_Ap_direct<false>(base, w, lane, col, Av, a.z, pold, beta);
+                                               : row_Ap_direct<false>(base, w, lane, col_of<COMP>(a, i, base), Av, a.z, pold, beta);
                      pnew[i] = pi;
                      a.q[i] = sum;
                      acc.x += pi * sum;
@@ -425,9 +494,15 @@ static int sm_count(int dev) {
   return g_sm_count[dev];
 }
 
+static const void* rhs_fn(int mode, int variant) {
+  if (variant == 1) return mode == 1 ? (const void*)rhs_kernel<1, 1> : (const void*)rhs_kernel<0, 1>;
+  if (variant == 2) return mode == 1 ? (const void*)rhs_kernel<1, 2> : (const void*)rhs_kernel<0, 2>;
+  return mode == 1 ? (const void*)rhs_kernel<1, 0> : (const void*)rhs_kernel<0, 0>;
+}
 static const void* pcg_fn(int mode, int variant) {
-  if (variant == 1) return mode == 1 ? (const void*)pcg_kernel<1, true> : (const void*)pcg_kernel<0, true>;
-  return mode == 1 ? (const void*)pcg_kernel<1, false> : (const void*)pcg_kernel<0, false>;
+  if (variant == 1) return mode == 1 ? (const void*)pcg_kernel<1, 1> : (const void*)pcg_kernel<0, 1>;
+  if (variant == 2) return mode == 1 ? (const void*)pcg_kernel<1, 2> : (const void*)pcg_kernel<0, 2>;
+  return mode == 1 ? (const void*)pcg_kernel<1, 0> : (const void*)pcg_kernel<0, 0>;
 }
 static int pcg_smem(int variant) { return variant == 1 ? kCgSmem : 0; }
 
@@ -435,6 +510,7 @@ static int pcg_smem(int variant) { return variant == 1 ? kCgSmem : 0; }
 // (cooperative launch); large problems get every SM x occupancy (2 CTAs / SM).
 int cg_grid_size(int mode, int variant, int32_t nslices, int device) {
   cudaFuncSetAttribute(pcg_fn(mode, variant), cudaFuncAttributeMaxDynamicSharedMemorySize, pcg_smem(variant));
+  cudaFuncSetAttribute(rhs_fn(mode, variant), cudaFuncAttributeMaxDynamicSharedMemorySize, pcg_smem(variant));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_fn(mode, variant), kCgThreads, pcg_smem(variant));
   if (per_sm < 1) per_sm = 1;
@@ -446,6 +522,9 @@ int cg_grid_size(int mode, int variant, int32_t nslices, int device) {
 
 cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s) {
   void* args[] = {(void*)&a};
+  cudaError_t e = cudaLaunchKernel(rhs_fn(mode, variant), dim3(grid), dim3(kCgThreads), args,
+                                   pcg_smem(variant), s);
+  if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(pcg_fn(mode, variant), dim3(grid), dim3(kCgThreads), args,
                                      pcg_smem(variant), s);
 }

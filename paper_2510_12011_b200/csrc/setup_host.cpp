@@ -195,4 +195,40 @@ void csr_to_sell(int32_t n, const int64_t* rowptr, const int32_t* col, HostSell&
   }
 }
 
+// 16-bit column compression per (slice, slot row): base = min over the 32
+// lanes, offsets < 2^16; slices where any slot row spans more stay int32.
+void compress_sell(HostSell& s) {
+  const int64_t total = s.slice_ptr[s.nslices];
+  s.col16.assign(total, 0);
+  s.kbase.assign(total / kSellC, 0);
+  s.fmt.assign(s.nslices, 0);
+  int64_t wide = 0;
+#pragma omp parallel for schedule(static) reduction(+ : wide)
+  for (int32_t sl = 0; sl < s.nslices; ++sl) {
+    const int64_t base = s.slice_ptr[sl], w = (s.slice_ptr[sl + 1] - base) / kSellC;
+    bool ok = true;
+    for (int64_t k = 0; k < w && ok; ++k) {
+      int32_t mn = s.col[base + k * kSellC], mx = mn;
+      for (int l = 1; l < kSellC; ++l) {
+        const int32_t c = s.col[base + k * kSellC + l];
+        mn = std::min(mn, c);
+        mx = std::max(mx, c);
+      }
+      if ((int64_t)mx - mn > 65535) ok = false;
+      s.kbase[base / kSellC + k] = mn;
+    }
+    if (!ok) {
+      s.fmt[sl] = 1;
+      wide += 1;
+      continue;
+    }
+    for (int64_t k = 0; k < w; ++k)
+      for (int l = 0; l < kSellC; ++l) {
+        const int64_t t = base + k * kSellC + l;
+        s.col16[t] = (uint16_t)(s.col[t] - s.kbase[base / kSellC + k]);
+      }
+  }
+  s.n_wide = wide;
+}
+
 }  // namespace tcb
