@@ -193,10 +193,12 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-rcm", action="store_true")
+    ap.add_argument("--partitions", type=int, default=1, help="row-block partitions on this GPU")
     ap.add_argument("--pcg-variant", type=int, default=0, help="0 direct loads (default), 1 TMA-staged, 2 direct + 16-bit indices")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--preroll", type=int, default=None)
+    ap.add_argument("--dist", action="store_true", help="use the NCCL path even at world size 1")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -204,7 +206,7 @@ def main():
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     rank, world, local = dist_env()
-    if world > 1:
+    if world > 1 or args.dist:
         import bench_dist
         return bench_dist.main(args, w)
 
@@ -218,7 +220,7 @@ def main():
     n = xyz.shape[0]
     cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5,
                               max_iters=100, use_rcm=0 if args.no_rcm else 1,
-                              pcg_variant=args.pcg_variant)
+                              pcg_variant=args.pcg_variant, partitions=args.partitions)
     t0 = time.perf_counter()
     sim = T.Monodomain(xyz, tets, np.zeros(E, np.int32), None, {0: SIGMA}, cfg, stims,
                        device=local, stream=stream.cuda_stream)

@@ -80,6 +80,12 @@ typedef struct {
   int32_t pcg_variant;   /* PCG kernel memory pipeline: 0 direct
                             loads at full occupancy (default), 1 TMA-staged matrix stream,
                             2 direct loads with 16-bit column offsets */
+  int32_t partitions;    /* row-block partitions of the RCM order held by this context on
+                            its GPU (1 = persistent single-kernel PCG; >1 = split-phase PCG
+                            with device-copy halos).  Ignored after tc_comm_init (one
+                            partition per rank). */
+  int32_t check_every;   /* split-phase PCG: iterations enqueued between host checks of the
+                            device convergence flag (4) */
 } tc_config;
 
 /* Per-step PCG report. */
@@ -91,7 +97,7 @@ typedef struct {
 
 /* Fills the defaults: theta 0.5, dt 0.01, chi 140, cm 0.01, tolerances 1e-5,
  * max_iters 100, consecutive rel-mode, TT2006 epi, fail_budget 3,
- * thresholds 0 / -70 mV, use_rcm 1, pcg_variant 0. */
+ * thresholds 0 / -70 mV, use_rcm 1, pcg_variant 0, partitions 1, check_every 4. */
 void tc_config_default(tc_config* cfg);
 
 /* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
@@ -179,10 +185,11 @@ tc_status tc_profile(tc_ctx* ctx, int enable);
 tc_status tc_profile_read(tc_ctx* ctx, double out[6], int reset);
 
 /* Sizes of the assembled system: out[0] n, out[1] nnz (stored entries of A,
- * CSR count), out[2] padded SELL-32 slots, out[3] slices, out[4] PCG grid
- * (CTAs of the cooperative kernel), out[5] slices kept at int32 indices.
+ * CSR count), out[2] padded SELL-32 slots of the parts held here, out[3] their
+ * slices, out[4] PCG grid (CTAs) of the first part, out[5] slices kept at int32
+ * indices (variant 2), out[6] partitions, out[7] ghost columns of the parts held.
  * TC_ESTATE before tc_assemble/tc_csr_upload. */
-tc_status tc_matrix_info(const tc_ctx* ctx, int64_t out[6]);
+tc_status tc_matrix_info(const tc_ctx* ctx, int64_t out[8]);
 
 /* ---- Minimum-slice operators on an uploaded CSR (no mesh needed) ---------- */
 /* Upload an n x n CSR (rowptr n+1, col/val nnz, columns sorted per row, the
@@ -196,7 +203,36 @@ tc_status tc_spmv(tc_ctx* ctx, const double* x, double* y);
 tc_status tc_pcg(tc_ctx* ctx, const double* b, const double* x0, double* x_out,
                  tc_step_stat* report);
 
-/* ---- Multi-GPU (row partition + halo) ------------------------- */
+/* ---- Multi-GPU (row partition + halo) ---
+ * One process per GPU.  Rank 0 creates an NCCL unique id (128 bytes) and
+ * broadcasts it (e.g. with torch.distributed); every rank then calls
+ * tc_comm_init before tc_set_mesh and passes the SAME global mesh, stimuli and
+ * conductivities.  The system in RCM order is cut into `world` contiguous row
+ * blocks; rank r owns block r.  Each PCG iteration exchanges the halo of p
+ * with ncclSend/ncclRecv (neighbouring blocks only) and all-reduces the two CG
+ * scalars (ncclAllReduce, identical bits on every rank -> identical stopping
+ * decisions).  Outputs (tc_get_v, tc_get_activation, tc_get_state) are
+ * all-gathered: every rank receives the full field.  TC_ENCCL on NCCL errors
+ * (NCCL is loaded at run time; without it tc_comm_init fails with TC_ENCCL). */
+tc_status tc_nccl_unique_id(uint8_t id[128]);
+tc_status tc_comm_init(tc_ctx* ctx, int rank, int world, const uint8_t id[128]);
+
+/* ---- Host-only helpers (no GPU needed; used by the CPU tests) ------------- */
+/* CSR pattern of a tet mesh: (i,j) iff an element holds both.  Call
+ * with col = NULL to get rowptr (n+1) first, then again with col (rowptr[n]). */
+tc_status tc_mesh_pattern(int64_t n, int64_t n_tets, const int32_t* tets, int64_t* rowptr,
+                          int32_t* col);
+/* Reverse Cuthill-McKee of a symmetric pattern (SPEC S:146 tie rules);
+ * perm[new] = old. */
+tc_status tc_rcm(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t* perm);
+/* The row-block partition plan of part `part` (of nparts) for a pattern in
+ * internal order: sizes = {ghosts, neighbours, send entries, owned rows};
+ * bounds (nparts+1), ghosts (sorted), nbr, recv_off (nbr+1), send_off (nbr+1),
+ * send_g (internal indices) -- each nullable. */
+tc_status tc_partition_plan(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t nparts,
+                            int32_t part, int64_t sizes[4], int64_t* bounds, int32_t* ghosts,
+                            int32_t* nbr, int64_t* recv_off, int64_t* send_off, int32_t* send_g);
+
 /* Version of this ABI. */
 int32_t tc_abi_version(void);
 

@@ -21,7 +21,8 @@ __all__ = [
     "tc_get_ionic_param", "tc_add_stimulus", "tc_set_mms", "tc_assemble", "tc_step",
     "tc_num_nodes", "tc_current_step", "tc_get_v", "tc_get_activation", "tc_state_len",
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
-    "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "Monodomain", "LIB_PATH",
+    "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "tc_nccl_unique_id", "tc_comm_init",
+    "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "Monodomain", "LIB_PATH",
     "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS",
 ]
 
@@ -38,7 +39,8 @@ class tc_config(C.Structure):
                 ("abs_tol", C.c_double), ("rel_tol", C.c_double), ("max_iters", C.c_int32),
                 ("rel_mode", C.c_int32), ("model", C.c_int32), ("fail_budget", C.c_int32),
                 ("lat_threshold", C.c_double), ("lrt_threshold", C.c_double),
-                ("use_rcm", C.c_int32), ("pcg_variant", C.c_int32)]
+                ("use_rcm", C.c_int32), ("pcg_variant", C.c_int32),
+                ("partitions", C.c_int32), ("check_every", C.c_int32)]
 
 
 class tc_step_stat(C.Structure):
@@ -90,6 +92,11 @@ def _load():
         "tc_spmv": ([P, P, P], I32),
         "tc_pcg": ([P, P, P, P, P], I32),
         "tc_abi_version": ([], I32),
+        "tc_nccl_unique_id": ([P], I32),
+        "tc_comm_init": ([P, C.c_int, C.c_int, P], I32),
+        "tc_mesh_pattern": ([I64, I64, P, P, P], I32),
+        "tc_rcm": ([I64, P, P, P], I32),
+        "tc_partition_plan": ([I64, P, P, I32, I32, P, P, P, P, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -241,10 +248,69 @@ def tc_profile_read(ctx, reset: bool = False):
 
 
 def tc_matrix_info(ctx) -> dict:
-    out = np.zeros(6, np.int64)
+    out = np.zeros(8, np.int64)
     _check(ctx, _L.tc_matrix_info(ctx, _ptr(out)))
     return dict(n=int(out[0]), nnz=int(out[1]), nnz_pad=int(out[2]), nslices=int(out[3]),
-                pcg_grid=int(out[4]), wide_slices=int(out[5]))
+                pcg_grid=int(out[4]), wide_slices=int(out[5]), partitions=int(out[6]),
+                ghosts=int(out[7]))
+
+
+def tc_nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    st = _L.tc_nccl_unique_id(buf)
+    if st != TC_OK:
+        raise TcError(st, "ncclGetUniqueId failed (NCCL not loadable?)")
+    return bytes(buf)
+
+
+def tc_comm_init(ctx, rank: int, world: int, unique_id: bytes) -> None:
+    buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+    _check(ctx, _L.tc_comm_init(ctx, rank, world, buf))
+
+
+# ---------------------------------------------------------------- host-only helpers
+def tc_mesh_pattern(n: int, tets):
+    tets = _i32(tets)
+    rowptr = np.zeros(n + 1, np.int64)
+    st = _L.tc_mesh_pattern(n, tets.shape[0], _ptr(tets), _ptr(rowptr), None)
+    if st != TC_OK:
+        raise TcError(st, "tc_mesh_pattern")
+    col = np.zeros(int(rowptr[n]), np.int32)
+    _L.tc_mesh_pattern(n, tets.shape[0], _ptr(tets), _ptr(rowptr), _ptr(col))
+    return rowptr, col
+
+
+def tc_rcm(rowptr, col):
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    col = _i32(col)
+    n = rowptr.shape[0] - 1
+    perm = np.zeros(n, np.int32)
+    st = _L.tc_rcm(n, _ptr(rowptr), _ptr(col), _ptr(perm))
+    if st != TC_OK:
+        raise TcError(st, "tc_rcm")
+    return perm
+
+
+def tc_partition_plan(rowptr, col, nparts: int, part: int) -> dict:
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    col = _i32(col)
+    n = rowptr.shape[0] - 1
+    sizes = np.zeros(4, np.int64)
+    st = _L.tc_partition_plan(n, _ptr(rowptr), _ptr(col), nparts, part, _ptr(sizes),
+                              None, None, None, None, None, None)
+    if st != TC_OK:
+        raise TcError(st, "tc_partition_plan")
+    ng, nn, ns, _ = (int(v) for v in sizes)
+    bounds = np.zeros(nparts + 1, np.int64)
+    ghosts = np.zeros(ng, np.int32)
+    nbr = np.zeros(nn, np.int32)
+    recv_off = np.zeros(nn + 1, np.int64)
+    send_off = np.zeros(nn + 1, np.int64)
+    send_g = np.zeros(ns, np.int32)
+    _L.tc_partition_plan(n, _ptr(rowptr), _ptr(col), nparts, part, _ptr(sizes), _ptr(bounds),
+                         _ptr(ghosts), _ptr(nbr), _ptr(recv_off), _ptr(send_off), _ptr(send_g))
+    return dict(bounds=bounds, ghosts=ghosts, nbr=nbr, recv_off=recv_off, send_off=send_off,
+                send_g=send_g)
 
 
 def tc_csr_upload(ctx, rowptr, col, val) -> None:
@@ -276,9 +342,12 @@ class Monodomain:
     those attributes.  Host-side orchestration only."""
 
     def __init__(self, xyz, tets, region, fibre, conductivities: dict, cfg: tc_config,
-                 stimuli=(), device: int = 0, stream: int = 0, mms=None, params: dict | None = None):
+                 stimuli=(), device: int = 0, stream: int = 0, mms=None, params: dict | None = None,
+                 comm=None):
         self.ctx = tc_create(cfg, device, stream)
         try:
+            if comm is not None:          # (rank, world, nccl_unique_id)
+                tc_comm_init(self.ctx, *comm)
             tc_set_mesh(self.ctx, xyz, tets, region, fibre)
             ids = sorted(conductivities)
             tc_set_conductivity(self.ctx, ids, [conductivities[i][0] for i in ids],

@@ -1,6 +1,14 @@
 // api.cu -- the C ABI of libtcb200 (include/tcb200.h): context, setup, the
 // per-step launch sequence and state I/O.  Every step of the path runs in the
-// CUDA kernels of ionic.cu / pcg.cu; this file only orchestrates.
+// CUDA kernels of ionic.cu / pcg.cu / pcg_split.cu; this file orchestrates.
+//
+// A context holds one or more row-block partitions ("parts") of the system in
+// the internal (RCM) node order:
+//   * 1 part, no communicator  -> persistent cooperative PCG kernel (pcg.cu);
+//   * cfg.partitions > 1      -> all parts on this GPU, split-phase PCG with
+//                                device-copy halos and an in-order partial sum;
+//   * tc_comm_init(world > 1) -> this rank's part only, split-phase PCG with
+//                                NCCL send/recv halos and NCCL all-reduces.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -10,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "internal.h"
 
 using namespace tcb;
@@ -19,8 +28,39 @@ struct Stim {
   double t0, dur, amp;
 };
 struct Epoch {
-  int64_t k0, k1;  // [k0, k1)
-  int32_t off, m;  // slice of the concatenated (node, s) list
+  int64_t k0, k1;  // step window [k0, k1)
+  int32_t off, m;  // slice of the part's (local index, s) list
+};
+
+struct Part {
+  PartPlan plan;
+  int64_t n = 0, n_pad = 0, n_ghost = 0, n_vec = 0, nnz = 0, nnz_pad = 0;
+  int32_t nslices = 0;
+  int64_t n_wide = 0;
+  int grid = 1;  // persistent kernel grid (1 part) or split-kernel grid
+  int64_t* d_sp = nullptr;
+  int32_t* d_col = nullptr;
+  uint16_t* d_col16 = nullptr;
+  int32_t* d_kbase = nullptr;
+  uint8_t* d_fmt = nullptr;
+  double *d_A = nullptr, *d_K = nullptr, *d_dinv = nullptr;
+  double* d_V[3] = {nullptr, nullptr, nullptr};
+  double* d_U = nullptr;
+  double *d_r = nullptr, *d_z = nullptr, *d_q = nullptr, *d_p0 = nullptr, *d_p1 = nullptr;
+  double *d_up = nullptr, *d_vp = nullptr, *d_b = nullptr, *d_tmp = nullptr;
+  uint8_t* d_act = nullptr;
+  double *d_lat = nullptr, *d_lrt = nullptr;
+  double* d_xyz = nullptr;
+  uint8_t* d_dir = nullptr;
+  double2* d_part = nullptr;
+  unsigned int* d_ticket = nullptr;
+  double2* d_red = nullptr;
+  Scalars* d_sc = nullptr;
+  int32_t* d_send_idx = nullptr;
+  double* d_send_buf = nullptr;  // 2 x n_send (u' and v' halves for the RHS halo)
+  std::vector<Epoch> epochs;
+  int32_t* d_stim_idx = nullptr;
+  double* d_stim_s = nullptr;
 };
 
 struct tc_ctx {
@@ -43,47 +83,31 @@ struct tc_ctx {
   MMSParams mms{1.0, M_PI, M_PI, M_PI};
   std::vector<Stim> stims;
   std::vector<int32_t> dirichlet_nodes;
+  // distribution
+  Comm comm;
+  bool use_comm = false;
+  int nparts = 1;
+  std::vector<Part> parts;       // partitions held by this context
+  std::vector<int> part_ids;     // their global partition indices
+  double2** d_reds = nullptr;    // loopback: red pointers of all parts
   // assembled system
   bool assembled = false;
   bool csr_mode = false;
   bool has_diag_zero = false;
-  std::vector<int32_t> perm, inv;  // perm[new] = old, inv[old] = new
-  int32_t nslices = 0;
-  int64_t n_pad = 0, nnz_pad = 0;
+  std::vector<int32_t> perm, inv;  // perm[internal] = original, inv[original] = internal
+  std::vector<int64_t> bounds;     // partition g0 per global part (+ end)
+  int64_t nnz = 0;
   int nstates = 0;
-  // device
-  int64_t* d_sp = nullptr;
-  int32_t* d_col = nullptr;
-  uint16_t* d_col16 = nullptr;
-  int32_t* d_kbase = nullptr;
-  uint8_t* d_fmt = nullptr;
-  int64_t n_wide = 0;
-  double *d_A = nullptr, *d_K = nullptr, *d_dinv = nullptr;
-  double* d_V[3] = {nullptr, nullptr, nullptr};
-  int iVk = 0, iVkm1 = 1, iX = 2;
-  double* d_U = nullptr;
-  double *d_r = nullptr, *d_z = nullptr, *d_q = nullptr, *d_p0 = nullptr, *d_p1 = nullptr;
-  double *d_up = nullptr, *d_vp = nullptr, *d_b = nullptr, *d_tmp = nullptr;
-  uint8_t* d_act = nullptr;
-  double *d_lat = nullptr, *d_lrt = nullptr;
-  int32_t *d_perm = nullptr, *d_inv = nullptr;
-  double2* d_part = nullptr;
   int32_t* d_flags = nullptr;
   tc_step_stat* d_stats = nullptr;
   int64_t stats_cap = 0;
-  double* d_xyz = nullptr;
-  uint8_t* d_dir = nullptr;
-  std::vector<Epoch> epochs;
-  int32_t* d_stim_idx = nullptr;
-  double* d_stim_s = nullptr;
+  int iVk = 0, iVkm1 = 1, iX = 2;
   int64_t k = 0;
   bool has_prev = false;
-  int cg_grid = 1;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> evs;
   double t_ion = 0, t_cg = 0, t_other = 0, prof_iters = 0, prof_steps = 0, launches = 0;
-  int64_t nnz = 0;
   std::vector<void*> allocs;
 };
 
@@ -92,11 +116,21 @@ static tc_status fail(tc_ctx* c, tc_status st, const std::string& msg) {
   if (c) c->err = msg;
   return st;
 }
-#define CUDA_TRY(c, expr)                                                           \
-  do {                                                                              \
-    cudaError_t e_ = (expr);                                                        \
-    if (e_ != cudaSuccess)                                                          \
+#define CUDA_TRY(c, expr)                                                             \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                            \
       return fail((c), TC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define NCCL_TRY(c, expr)                                         \
+  do {                                                            \
+    std::string m_ = (expr);                                      \
+    if (!m_.empty()) return fail((c), TC_ENCCL, m_);              \
+  } while (0)
+#define TC_TRY(expr)                \
+  do {                              \
+    tc_status s_ = (expr);          \
+    if (s_ != TC_OK) return s_;     \
   } while (0)
 
 template <class T>
@@ -110,6 +144,13 @@ static cudaError_t dalloc(tc_ctx* c, T** p, int64_t count) {
   return cudaMemsetAsync(v, 0, bytes, c->stream);
 }
 
+template <class T>
+static cudaError_t upload(tc_ctx* c, T** p, const std::vector<T>& h) {
+  cudaError_t e = dalloc(c, p, (int64_t)h.size());
+  if (e != cudaSuccess || h.empty()) return e;
+  return cudaMemcpyAsync(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream);
+}
+
 static void free_all(tc_ctx* c) {
   for (void* p : c->allocs) cudaFree(p);
   c->allocs.clear();
@@ -117,9 +158,11 @@ static void free_all(tc_ctx* c) {
   c->evs.clear();
 }
 
+static bool split_mode(const tc_ctx* c) { return c->nparts > 1 || c->use_comm; }
+
 extern "C" {
 
-int32_t tc_abi_version(void) { return 1; }
+int32_t tc_abi_version(void) { return 2; }
 
 void tc_config_default(tc_config* c) {
   c->theta = 0.5;
@@ -136,13 +179,17 @@ void tc_config_default(tc_config* c) {
   c->lrt_threshold = -70.0;
   c->use_rcm = 1;
   c->pcg_variant = 0;
+  c->partitions = 1;
+  c->check_every = 4;
 }
 
 tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx** out) {
   if (!cfg || !out) return TC_EINVAL;
   *out = nullptr;
   if (!(cfg->dt > 0) || !(cfg->theta >= 0 && cfg->theta <= 1) || !(cfg->chi > 0) || !(cfg->cm > 0) ||
-      cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 || cfg->model > 2 || cfg->pcg_variant < 0 || cfg->pcg_variant > 2)
+      cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 ||
+      cfg->model > 2 || cfg->pcg_variant < 0 || cfg->pcg_variant > 2 || cfg->partitions < 1 ||
+      cfg->partitions > 4096 || cfg->check_every < 1)
     return TC_EINVAL;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0) return TC_ECUDA;
@@ -150,6 +197,7 @@ tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx*
   tc_ctx* c = new tc_ctx();
   c->cfg = *cfg;
   c->device = device;
+  c->nparts = cfg->partitions;
   tt_defaults(&c->tt, &c->tt_V0, c->tt_u0);
   ms_defaults(&c->ms);
   if (cuda_stream) {
@@ -174,6 +222,7 @@ tc_status tc_destroy(tc_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   free_all(c);
+  c->comm.destroy();
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return TC_OK;
@@ -184,12 +233,31 @@ const char* tc_last_error(const tc_ctx* c) { return c ? c->err.c_str() : "null c
 int64_t tc_num_nodes(const tc_ctx* c) { return c ? c->n : 0; }
 int64_t tc_current_step(const tc_ctx* c) { return c ? c->k : 0; }
 
+tc_status tc_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return TC_EINVAL;
+  return nccl_unique_id(id).empty() ? TC_OK : TC_ENCCL;
+}
+
+tc_status tc_comm_init(tc_ctx* c, int rank, int world, const uint8_t id[128]) {
+  if (!c || !id || world < 1 || rank < 0 || rank >= world) return TC_EINVAL;
+  if (c->have_mesh || c->csr_mode) return fail(c, TC_ESTATE, "tc_comm_init must precede tc_set_mesh");
+  if (c->use_comm) return fail(c, TC_ESTATE, "tc_comm_init called twice");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  NCCL_TRY(c, c->comm.init(rank, world, id));  // world 1 too: exercises the NCCL split path
+  c->use_comm = true;
+  c->nparts = world;
+  c->comm.rank = rank;
+  c->comm.world = world;
+  return TC_OK;
+}
+
 tc_status tc_set_mesh(tc_ctx* c, int64_t n, const double* xyz, int64_t E, const int32_t* tets,
                       const int32_t* region, const double* fibre) {
   if (!c) return TC_EINVAL;
   if (c->have_mesh || c->csr_mode) return fail(c, TC_ESTATE, "tc_set_mesh: mesh already set");
   if (n <= 0 || E <= 0 || !xyz || !tets) return fail(c, TC_EINVAL, "tc_set_mesh: empty mesh");
-  if (n >= (1ll << 31) - 64 || 4 * E >= (1ll << 31)) return fail(c, TC_EINVAL, "tc_set_mesh: mesh too large for int32 indices");
+  if (n >= (1ll << 31) - 64 || 4 * E >= (1ll << 31))
+    return fail(c, TC_EINVAL, "tc_set_mesh: mesh too large for int32 indices");
   c->n = n;
   c->E = E;
   c->xyz.assign(xyz, xyz + 3 * n);
@@ -270,7 +338,8 @@ tc_status tc_set_mms(tc_ctx* c, double k, double w1, double w2, double lam, int6
                      const int32_t* nodes) {
   if (!c) return TC_EINVAL;
   if (c->cfg.model != TC_ION_MMS) return fail(c, TC_ESTATE, "tc_set_mms needs model TC_ION_MMS");
-  if (c->assembled || !c->have_mesh) return fail(c, TC_ESTATE, "tc_set_mms: call after tc_set_mesh, before tc_assemble");
+  if (c->assembled || !c->have_mesh)
+    return fail(c, TC_ESTATE, "tc_set_mms: call after tc_set_mesh, before tc_assemble");
   for (int64_t t = 0; t < m; ++t)
     if (nodes[t] < 0 || nodes[t] >= c->n) return fail(c, TC_EINVAL, "tc_set_mms: node out of range");
   c->mms = MMSParams{k, w1, w2, lam};
@@ -278,69 +347,10 @@ tc_status tc_set_mms(tc_ctx* c, double k, double w1, double w2, double lam, int6
   return TC_OK;
 }
 
+}  // extern "C"
+
 static double mms_w_host(const MMSParams& p, double x, double y, double t) {
   return std::exp(-p.k * t) * std::cos(p.w1 * x + p.w2 * y - p.lam * t);
-}
-
-// (re)initialise the cell state: model initial conditions everywhere
-static tc_status init_state(tc_ctx* c) {
-  const int64_t n = c->n, np = c->n_pad;
-  std::vector<double> v(np, 0.0);
-  if (c->cfg.model == TC_ION_TT2006_EPI) {
-    for (int64_t i = 0; i < n; ++i) v[i] = c->tt_V0;
-    std::vector<double> u((size_t)kTTStates * np, 0.0);
-    for (int s = 0; s < kTTStates; ++s)
-      for (int64_t i = 0; i < n; ++i) u[s * np + i] = c->tt_u0[s];
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_U, u.data(), u.size() * 8, cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  } else if (c->cfg.model == TC_ION_MS) {
-    for (int64_t i = 0; i < n; ++i) v[i] = c->ms.V_min;
-    std::vector<double> u(np, 0.0);
-    for (int64_t i = 0; i < n; ++i) u[i] = 1.0;
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_U, u.data(), u.size() * 8, cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  } else {
-    for (int64_t i = 0; i < n; ++i) {
-      int64_t o = c->perm[i];
-      v[i] = mms_w_host(c->mms, c->xyz[3 * o], c->xyz[3 * o + 1], 0.0);
-    }
-  }
-  for (int b = 0; b < 3; ++b)
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_V[b], v.data(), np * 8, cudaMemcpyHostToDevice, c->stream));
-  std::vector<double> unset(np, -1.0);
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_lat, unset.data(), np * 8, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_lrt, unset.data(), np * 8, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(c->d_act, 0, np, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  c->iVk = 0; c->iVkm1 = 1; c->iX = 2;
-  c->k = 0;
-  c->has_prev = false;
-  return TC_OK;
-}
-
-// 16-bit index compression for the direct PCG pipeline
-static tc_status upload_compressed(tc_ctx* c, HostSell& hs) {
-  if (c->cfg.pcg_variant != 2) return TC_OK;  // variants 0 (default) and 1 (TMA) stream int32 indices
-  compress_sell(hs);
-  c->n_wide = hs.n_wide;
-  CUDA_TRY(c, dalloc(c, &c->d_col16, (int64_t)hs.col16.size()));
-  CUDA_TRY(c, dalloc(c, &c->d_kbase, (int64_t)hs.kbase.size()));
-  CUDA_TRY(c, dalloc(c, &c->d_fmt, (int64_t)hs.fmt.size()));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_col16, hs.col16.data(), hs.col16.size() * 2, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_kbase, hs.kbase.data(), hs.kbase.size() * 4, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_fmt, hs.fmt.data(), hs.fmt.size(), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  return TC_OK;
-}
-
-static tc_status alloc_vectors(tc_ctx* c) {
-  const int64_t np = c->n_pad;
-  for (int b = 0; b < 3; ++b) CUDA_TRY(c, dalloc(c, &c->d_V[b], np));
-  for (double** p : {&c->d_r, &c->d_z, &c->d_q, &c->d_p0, &c->d_p1, &c->d_up, &c->d_vp, &c->d_b,
-                     &c->d_tmp})
-    CUDA_TRY(c, dalloc(c, p, np));
-  CUDA_TRY(c, dalloc(c, &c->d_dinv, np));
-  return TC_OK;
 }
 
 static tc_status ensure_stats(tc_ctx* c, int64_t m) {
@@ -351,13 +361,115 @@ static tc_status ensure_stats(tc_ctx* c, int64_t m) {
   return TC_OK;
 }
 
-tc_status tc_assemble(tc_ctx* c) {
+// vectors of one part: owned [0,n), padding [n,n_pad), ghosts [n_pad, n_vec)
+static tc_status alloc_part_vectors(tc_ctx* c, Part& P) {
+  const int64_t nv = P.n_vec;
+  for (int b = 0; b < 3; ++b) CUDA_TRY(c, dalloc(c, &P.d_V[b], nv));
+  for (double** p : {&P.d_r, &P.d_z, &P.d_q, &P.d_p0, &P.d_p1, &P.d_up, &P.d_vp, &P.d_b, &P.d_tmp})
+    CUDA_TRY(c, dalloc(c, p, nv));
+  CUDA_TRY(c, dalloc(c, &P.d_dinv, P.n_pad));
+  CUDA_TRY(c, dalloc(c, &P.d_ticket, 1));
+  CUDA_TRY(c, dalloc(c, &P.d_red, 2));
+  CUDA_TRY(c, dalloc(c, &P.d_sc, 1));
+  return TC_OK;
+}
+
+// 16-bit index compression for the direct PCG pipeline (variant 2, single part)
+static tc_status upload_compressed(tc_ctx* c, Part& P, HostSell& hs) {
+  if (c->cfg.pcg_variant != 2 || split_mode(c)) return TC_OK;
+  compress_sell(hs);
+  P.n_wide = hs.n_wide;
+  CUDA_TRY(c, upload(c, &P.d_col16, hs.col16));
+  CUDA_TRY(c, upload(c, &P.d_kbase, hs.kbase));
+  CUDA_TRY(c, upload(c, &P.d_fmt, hs.fmt));
+  return TC_OK;
+}
+
+// (re)initialise the cell state of every part: model initial conditions
+static tc_status init_state(tc_ctx* c) {
+  for (size_t pi = 0; pi < c->parts.size(); ++pi) {
+    Part& P = c->parts[pi];
+    const int64_t n = P.n, np = P.n_pad, g0 = P.plan.g0;
+    std::vector<double> v(P.n_vec, 0.0);
+    if (c->cfg.model == TC_ION_TT2006_EPI) {
+      for (int64_t i = 0; i < n; ++i) v[i] = c->tt_V0;
+      std::vector<double> u((size_t)kTTStates * np, 0.0);
+      for (int s = 0; s < kTTStates; ++s)
+        for (int64_t i = 0; i < n; ++i) u[s * np + i] = c->tt_u0[s];
+      CUDA_TRY(c, cudaMemcpyAsync(P.d_U, u.data(), u.size() * 8, cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    } else if (c->cfg.model == TC_ION_MS) {
+      for (int64_t i = 0; i < n; ++i) v[i] = c->ms.V_min;
+      std::vector<double> u(np, 0.0);
+      for (int64_t i = 0; i < n; ++i) u[i] = 1.0;
+      CUDA_TRY(c, cudaMemcpyAsync(P.d_U, u.data(), u.size() * 8, cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    } else {
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t o = c->perm[g0 + i];
+        v[i] = mms_w_host(c->mms, c->xyz[3 * o], c->xyz[3 * o + 1], 0.0);
+      }
+    }
+    for (int b = 0; b < 3; ++b)
+      CUDA_TRY(c, cudaMemcpyAsync(P.d_V[b], v.data(), P.n_vec * 8, cudaMemcpyHostToDevice, c->stream));
+    std::vector<double> unset(np, -1.0);
+    CUDA_TRY(c, cudaMemcpyAsync(P.d_lat, unset.data(), np * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(P.d_lrt, unset.data(), np * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(P.d_act, 0, np, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  c->iVk = 0;
+  c->iVkm1 = 1;
+  c->iX = 2;
+  c->k = 0;
+  c->has_prev = false;
+  return TC_OK;
+}
+
+// Local SELL of one part from the internal-order CSR rows [g0, g1): columns
+// stay sorted by internal index (same summation order as one part); local
+// index = g - g0 for owned, n_pad + (ghost rank) for ghosts.
+static void local_sell(const PartPlan& pl, const int64_t* rp, const int32_t* col, HostSell& hs,
+                       std::vector<int32_t>& colg) {
+  const int64_t n = pl.g1 - pl.g0;
+  std::vector<int64_t> lrp(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) lrp[i + 1] = lrp[i] + (rp[pl.g0 + i + 1] - rp[pl.g0 + i]);
+  std::vector<int32_t> lcol(lrp[n]);
+  std::copy(col + rp[pl.g0], col + rp[pl.g1], lcol.begin());
+  csr_to_sell((int32_t)n, lrp.data(), lcol.data(), hs);  // hs.col = internal (global) indices
+  colg = hs.col;
+  const int64_t np = hs.n_pad;
+  for (int64_t sl = 0; sl < hs.nslices; ++sl) {
+    const int64_t base = hs.slice_ptr[sl], w = (hs.slice_ptr[sl + 1] - base) / kSellC;
+    for (int l = 0; l < kSellC; ++l) {
+      const int64_t i = sl * kSellC + l;
+      for (int64_t k = 0; k < w; ++k) {
+        const int64_t t = base + k * kSellC + l;
+        if (i >= n || k >= hs.rowlen[i]) {
+          hs.col[t] = (int32_t)i;          // padding slot: own local row, value 0
+          colg[t] = (int32_t)(pl.g0 + std::min<int64_t>(i, n - 1));
+          continue;
+        }
+        const int32_t g = colg[t];
+        if (g >= pl.g0 && g < pl.g1) {
+          hs.col[t] = (int32_t)(g - pl.g0);
+        } else {
+          const int64_t gi = std::lower_bound(pl.ghosts.begin(), pl.ghosts.end(), g) - pl.ghosts.begin();
+          hs.col[t] = (int32_t)(np + gi);
+        }
+      }
+    }
+  }
+}
+
+extern "C" tc_status tc_assemble(tc_ctx* c) {
   if (!c) return TC_EINVAL;
   if (!c->have_mesh) return fail(c, TC_ESTATE, "tc_assemble before tc_set_mesh");
   if (c->assembled) return fail(c, TC_ESTATE, "tc_assemble called twice");
   if (c->reg_ids.empty()) return fail(c, TC_EREGION, "tc_assemble: no conductivity table");
   CUDA_TRY(c, cudaSetDevice(c->device));
   const int64_t n = c->n, E = c->E;
+  if (c->nparts > n) return fail(c, TC_EINVAL, "more partitions than nodes");
   // region tag -> table index
   std::map<int32_t, int32_t> rmap;
   for (size_t r = 0; r < c->reg_ids.size(); ++r) rmap[c->reg_ids[r]] = (int32_t)r;
@@ -369,7 +481,7 @@ tc_status tc_assemble(tc_ctx* c) {
                                      std::to_string(c->region[e]) + " without conductivity");
     ereg[e] = it->second;
   }
-  // pattern and RCM
+  // pattern and RCM, identical on every rank
   std::vector<int64_t> iptr, rp;
   std::vector<int32_t> inc, col;
   build_incidence(n, E, c->tets.data(), iptr, inc);
@@ -386,88 +498,134 @@ tc_status tc_assemble(tc_ctx* c) {
   std::vector<int32_t> col2;
   permute_csr(n, rp, col, c->perm, c->inv, rp2, col2);
   rp.clear(); rp.shrink_to_fit(); col.clear(); col.shrink_to_fit();
+  c->nnz = rp2[n];
   std::vector<int32_t> tets2(4 * E);
   for (int64_t t = 0; t < 4 * E; ++t) tets2[t] = c->inv[c->tets[t]];
   std::vector<double> xyz2(3 * n);
   for (int64_t i = 0; i < n; ++i)
     for (int q = 0; q < 3; ++q) xyz2[3 * i + q] = c->xyz[3 * (int64_t)c->perm[i] + q];
   build_incidence(n, E, tets2.data(), iptr, inc);
-  HostSell hs;
-  c->nnz = rp2[n];
-  csr_to_sell((int32_t)n, rp2.data(), col2.data(), hs);
-  rp2.clear(); rp2.shrink_to_fit(); col2.clear(); col2.shrink_to_fit();
-  c->nslices = hs.nslices;
-  c->n_pad = hs.n_pad;
-  c->nnz_pad = hs.slice_ptr[hs.nslices];
-  // device upload
-  const int64_t np = c->n_pad;
-  CUDA_TRY(c, dalloc(c, &c->d_sp, (int64_t)hs.slice_ptr.size()));
-  CUDA_TRY(c, dalloc(c, &c->d_col, c->nnz_pad));
-  CUDA_TRY(c, dalloc(c, &c->d_A, c->nnz_pad));
-  CUDA_TRY(c, dalloc(c, &c->d_K, c->nnz_pad));
-  if (alloc_vectors(c) != TC_OK) return TC_ECUDA;
+  // partitions
+  std::vector<PartPlan> plans;
+  plan_partitions(n, rp2.data(), col2.data(), c->nparts, plans);
+  c->bounds.resize(c->nparts + 1);
+  for (int p = 0; p < c->nparts; ++p) c->bounds[p] = plans[p].g0;
+  c->bounds[c->nparts] = n;
+  c->part_ids.clear();
+  if (c->use_comm) c->part_ids.push_back(c->comm.rank);
+  else for (int p = 0; p < c->nparts; ++p) c->part_ids.push_back(p);
+  c->parts.resize(c->part_ids.size());
   c->nstates = c->cfg.model == TC_ION_TT2006_EPI ? kTTStates : (c->cfg.model == TC_ION_MS ? 1 : 0);
-  CUDA_TRY(c, dalloc(c, &c->d_U, (int64_t)std::max(c->nstates, 1) * np));
-  CUDA_TRY(c, dalloc(c, &c->d_act, np));
-  CUDA_TRY(c, dalloc(c, &c->d_lat, np));
-  CUDA_TRY(c, dalloc(c, &c->d_lrt, np));
-  CUDA_TRY(c, dalloc(c, &c->d_perm, n));
-  CUDA_TRY(c, dalloc(c, &c->d_inv, n));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_sp, hs.slice_ptr.data(), hs.slice_ptr.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_col, hs.col.data(), hs.col.size() * 4, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_perm, c->perm.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_inv, c->inv.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
-  // setup-only buffers
+  // element data shared by all parts of this device (setup only)
   double *d_xyz = nullptr, *d_fib = nullptr, *d_sl = nullptr, *d_st = nullptr;
-  int32_t *d_tets = nullptr, *d_ereg = nullptr, *d_inc = nullptr, *d_rowlen = nullptr, *d_err = nullptr;
-  int64_t* d_iptr = nullptr;
+  int32_t *d_tets = nullptr, *d_ereg = nullptr, *d_err = nullptr;
   const size_t nr = c->reg_ids.size();
   bool ok = cudaMalloc(&d_xyz, 3 * n * 8) == cudaSuccess && cudaMalloc(&d_fib, 3 * E * 8) == cudaSuccess &&
             cudaMalloc(&d_sl, nr * 8) == cudaSuccess && cudaMalloc(&d_st, nr * 8) == cudaSuccess &&
             cudaMalloc(&d_tets, 4 * E * 4) == cudaSuccess && cudaMalloc(&d_ereg, E * 4) == cudaSuccess &&
-            cudaMalloc(&d_inc, 4 * E * 4) == cudaSuccess && cudaMalloc(&d_rowlen, n * 4) == cudaSuccess &&
-            cudaMalloc(&d_err, 4) == cudaSuccess && cudaMalloc(&d_iptr, (n + 1) * 8) == cudaSuccess;
+            cudaMalloc(&d_err, 4) == cudaSuccess;
   auto free_setup = [&]() {
     cudaFree(d_xyz); cudaFree(d_fib); cudaFree(d_sl); cudaFree(d_st); cudaFree(d_tets);
-    cudaFree(d_ereg); cudaFree(d_inc); cudaFree(d_rowlen); cudaFree(d_err); cudaFree(d_iptr);
+    cudaFree(d_ereg); cudaFree(d_err);
   };
   if (!ok) {
     free_setup();
     return fail(c, TC_ENOMEM, "tc_assemble: device allocation failed");
   }
-  // fibre in the element order is unchanged by the node permutation
   cudaMemcpyAsync(d_xyz, xyz2.data(), 3 * n * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_fib, c->fibre.data(), 3 * E * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_sl, c->sig_l.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_st, c->sig_t.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_tets, tets2.data(), 4 * E * 4, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_ereg, ereg.data(), E * 4, cudaMemcpyHostToDevice, c->stream);
-  cudaMemcpyAsync(d_inc, inc.data(), 4 * E * 4, cudaMemcpyHostToDevice, c->stream);
-  cudaMemcpyAsync(d_rowlen, hs.rowlen.data(), n * 4, cudaMemcpyHostToDevice, c->stream);
-  cudaMemcpyAsync(d_iptr, iptr.data(), (n + 1) * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemsetAsync(d_err, 0, 4, c->stream);
-  // Dirichlet mask (MMS)
+  std::vector<uint8_t> dir_all;
   if (c->cfg.model == TC_ION_MMS) {
-    std::vector<uint8_t> dir(np, 0);
-    for (int32_t o : c->dirichlet_nodes) dir[c->inv[o]] = 1;
-    CUDA_TRY(c, dalloc(c, &c->d_dir, np));
-    CUDA_TRY(c, dalloc(c, &c->d_xyz, 3 * np));
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_dir, dir.data(), np, cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_xyz, xyz2.data(), 3 * n * 8, cudaMemcpyHostToDevice, c->stream));
+    dir_all.assign(n, 0);
+    for (int32_t o : c->dirichlet_nodes) dir_all[c->inv[o]] = 1;
   }
-  AsmArgs a{};
-  a.n = (int32_t)n; a.xyz = d_xyz; a.tets = d_tets; a.ereg = d_ereg; a.fibre = d_fib;
-  a.sig_l = d_sl; a.sig_t = d_st; a.inc_ptr = d_iptr; a.inc = d_inc;
-  a.slice_ptr = c->d_sp; a.col = c->d_col; a.rowlen = d_rowlen;
-  a.A = c->d_A; a.K = c->d_K; a.dinv = c->d_dinv; a.dirichlet = c->d_dir;
-  a.c_mass = c->cfg.chi * c->cfg.cm; a.c_stiff = c->cfg.theta * c->cfg.dt; a.err = d_err;
-  cudaError_t le = launch_assemble(a, c->stream);
+  for (size_t pi = 0; pi < c->parts.size(); ++pi) {
+    Part& P = c->parts[pi];
+    P.plan = plans[c->part_ids[pi]];
+    const int64_t g0 = P.plan.g0, g1 = P.plan.g1;
+    P.n = g1 - g0;
+    HostSell hs;
+    std::vector<int32_t> colg;
+    local_sell(P.plan, rp2.data(), col2.data(), hs, colg);
+    P.nslices = hs.nslices;
+    P.n_pad = hs.n_pad;
+    P.n_ghost = (int64_t)P.plan.ghosts.size();
+    P.n_vec = P.n_pad + P.n_ghost;
+    P.nnz = rp2[g1] - rp2[g0];
+    P.nnz_pad = hs.slice_ptr[hs.nslices];
+    CUDA_TRY(c, upload(c, &P.d_sp, hs.slice_ptr));
+    CUDA_TRY(c, upload(c, &P.d_col, hs.col));
+    CUDA_TRY(c, dalloc(c, &P.d_A, P.nnz_pad));
+    CUDA_TRY(c, dalloc(c, &P.d_K, P.nnz_pad));
+    TC_TRY(alloc_part_vectors(c, P));
+    CUDA_TRY(c, dalloc(c, &P.d_U, (int64_t)std::max(c->nstates, 1) * P.n_pad));
+    CUDA_TRY(c, dalloc(c, &P.d_act, P.n_pad));
+    CUDA_TRY(c, dalloc(c, &P.d_lat, P.n_pad));
+    CUDA_TRY(c, dalloc(c, &P.d_lrt, P.n_pad));
+    // halo send list (local indices)
+    std::vector<int32_t> sidx(P.plan.send_g.size());
+    for (size_t t = 0; t < sidx.size(); ++t) sidx[t] = (int32_t)(P.plan.send_g[t] - g0);
+    CUDA_TRY(c, upload(c, &P.d_send_idx, sidx));
+    CUDA_TRY(c, dalloc(c, &P.d_send_buf, 2 * (int64_t)sidx.size()));
+    if (c->cfg.model == TC_ION_MMS) {
+      std::vector<uint8_t> dir(P.n_pad, 0);
+      std::vector<double> px(3 * P.n_pad, 0.0);
+      for (int64_t i = 0; i < P.n; ++i) {
+        dir[i] = dir_all[g0 + i];
+        for (int q = 0; q < 3; ++q) px[3 * i + q] = xyz2[3 * (g0 + i) + q];
+      }
+      CUDA_TRY(c, upload(c, &P.d_dir, dir));
+      CUDA_TRY(c, upload(c, &P.d_xyz, px));
+    }
+    // assembly of the owned rows (incidence sliced to [g0, g1))
+    std::vector<int64_t> liptr(P.n + 1);
+    for (int64_t i = 0; i <= P.n; ++i) liptr[i] = iptr[g0 + i] - iptr[g0];
+    std::vector<int32_t> linc(inc.begin() + iptr[g0], inc.begin() + iptr[g1]);
+    int64_t* d_iptr = nullptr;
+    int32_t *d_inc = nullptr, *d_rowlen = nullptr, *d_colg = nullptr;
+    if (cudaMalloc(&d_iptr, (P.n + 1) * 8) != cudaSuccess ||
+        cudaMalloc(&d_inc, std::max<size_t>(linc.size(), 1) * 4) != cudaSuccess ||
+        cudaMalloc(&d_rowlen, P.n * 4) != cudaSuccess ||
+        cudaMalloc(&d_colg, std::max<size_t>(colg.size(), 1) * 4) != cudaSuccess) {
+      cudaFree(d_iptr); cudaFree(d_inc); cudaFree(d_rowlen); cudaFree(d_colg);
+      free_setup();
+      return fail(c, TC_ENOMEM, "tc_assemble: device allocation failed");
+    }
+    cudaMemcpyAsync(d_iptr, liptr.data(), (P.n + 1) * 8, cudaMemcpyHostToDevice, c->stream);
+    if (!linc.empty()) cudaMemcpyAsync(d_inc, linc.data(), linc.size() * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_rowlen, hs.rowlen.data(), P.n * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_colg, colg.data(), colg.size() * 4, cudaMemcpyHostToDevice, c->stream);
+    AsmArgs a{};
+    a.n = (int32_t)P.n; a.row0 = (int32_t)g0; a.xyz = d_xyz; a.tets = d_tets; a.ereg = d_ereg;
+    a.fibre = d_fib; a.sig_l = d_sl; a.sig_t = d_st; a.inc_ptr = d_iptr; a.inc = d_inc;
+    a.slice_ptr = P.d_sp; a.col = d_colg; a.rowlen = d_rowlen;
+    a.A = P.d_A; a.K = P.d_K; a.dinv = P.d_dinv; a.dirichlet = P.d_dir;
+    a.c_mass = c->cfg.chi * c->cfg.cm; a.c_stiff = c->cfg.theta * c->cfg.dt; a.err = d_err;
+    cudaError_t le = launch_assemble(a, c->stream);
+    cudaError_t ss = cudaStreamSynchronize(c->stream);
+    cudaFree(d_iptr); cudaFree(d_inc); cudaFree(d_rowlen); cudaFree(d_colg);
+    if (le != cudaSuccess || ss != cudaSuccess) {
+      free_setup();
+      return fail(c, TC_ECUDA, std::string("assembly kernel: ") + cudaGetErrorString(le != cudaSuccess ? le : ss));
+    }
+    tc_status cs = upload_compressed(c, P, hs);
+    if (cs != TC_OK) { free_setup(); return cs; }
+    if (split_mode(c)) {
+      P.grid = split_grid(P.nslices);
+    } else {
+      P.grid = cg_grid_size(1, c->cfg.pcg_variant, P.nslices, c->device);
+    }
+    CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
+  }
   int32_t herr = 0;
-  cudaError_t se = cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, c->stream);
-  cudaError_t ss = cudaStreamSynchronize(c->stream);
+  CUDA_TRY(c, cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   free_setup();
-  if (le != cudaSuccess || se != cudaSuccess || ss != cudaSuccess)
-    return fail(c, TC_ECUDA, std::string("assembly kernel: ") + cudaGetErrorString(le != cudaSuccess ? le : (se != cudaSuccess ? se : ss)));
   if (herr == 1) return fail(c, TC_EDEGEN, "assembly: zero-volume element");
   if (herr == 2) return fail(c, TC_EINVAL, "assembly: pattern slot missing (internal)");
   // stimulus epochs: step windows [round(t0/dt), round((t0+dur)/dt)) (reading T1)
@@ -481,58 +639,59 @@ tc_status tc_assemble(tc_ctx* c) {
       cuts.insert(k1);
     }
     std::vector<int64_t> cv(cuts.begin(), cuts.end());
-    std::vector<int32_t> idx;
-    std::vector<double> sv;
     const double inv_chicm = 1.0 / (c->cfg.chi * c->cfg.cm);
-    for (size_t q = 0; q + 1 < cv.size(); ++q) {
-      std::map<int32_t, double> acc;  // new index -> summed amplitude
-      for (size_t s = 0; s < c->stims.size(); ++s)
-        if (win[s].first <= cv[q] && cv[q] < win[s].second)
-          for (int32_t o : c->stims[s].nodes) acc[c->inv[o]] += c->stims[s].amp;
-      if (acc.empty()) continue;
-      Epoch ep{cv[q], cv[q + 1], (int32_t)idx.size(), (int32_t)acc.size()};
-      for (auto& kv : acc) {
-        idx.push_back(kv.first);
-        sv.push_back(kv.second * inv_chicm);
+    for (Part& P : c->parts) {
+      std::vector<int32_t> idx;
+      std::vector<double> sv;
+      for (size_t q = 0; q + 1 < cv.size(); ++q) {
+        std::map<int32_t, double> acc;  // local index -> summed amplitude
+        for (size_t s = 0; s < c->stims.size(); ++s)
+          if (win[s].first <= cv[q] && cv[q] < win[s].second)
+            for (int32_t o : c->stims[s].nodes) {
+              const int64_t g = c->inv[o];
+              if (g >= P.plan.g0 && g < P.plan.g1) acc[(int32_t)(g - P.plan.g0)] += c->stims[s].amp;
+            }
+        Epoch ep{cv[q], cv[q + 1], (int32_t)idx.size(), (int32_t)acc.size()};
+        for (auto& kv : acc) {
+          idx.push_back(kv.first);
+          sv.push_back(kv.second * inv_chicm);
+        }
+        if (ep.m > 0) P.epochs.push_back(ep);
       }
-      c->epochs.push_back(ep);
-    }
-    if (!idx.empty()) {
-      CUDA_TRY(c, dalloc(c, &c->d_stim_idx, (int64_t)idx.size()));
-      CUDA_TRY(c, dalloc(c, &c->d_stim_s, (int64_t)sv.size()));
-      CUDA_TRY(c, cudaMemcpyAsync(c->d_stim_idx, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, c->stream));
-      CUDA_TRY(c, cudaMemcpyAsync(c->d_stim_s, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, upload(c, &P.d_stim_idx, idx));
+      CUDA_TRY(c, upload(c, &P.d_stim_s, sv));
     }
   }
-  if (upload_compressed(c, hs) != TC_OK) return TC_ECUDA;
-  c->cg_grid = cg_grid_size(1, c->cfg.pcg_variant, c->nslices, c->device);
-  CUDA_TRY(c, dalloc(c, &c->d_part, 2 * (int64_t)c->cg_grid));
+  if (split_mode(c) && !c->use_comm) {
+    std::vector<double2*> reds;
+    for (Part& P : c->parts) reds.push_back(P.d_red);
+    CUDA_TRY(c, upload(c, &c->d_reds, reds));
+  }
   int32_t flags[8] = {0, 0, 0, c->cfg.fail_budget, -1, 0, 0, 0};
   CUDA_TRY(c, cudaMemcpyAsync(c->d_flags, flags, sizeof(flags), cudaMemcpyHostToDevice, c->stream));
-  if (ensure_stats(c, 1024) != TC_OK) return TC_ECUDA;
-  // free the big host copies no longer needed
+  TC_TRY(ensure_stats(c, 1024));
   c->tets.clear(); c->tets.shrink_to_fit();
   c->fibre.clear(); c->fibre.shrink_to_fit();
   c->region.clear(); c->region.shrink_to_fit();
-  tc_status st = init_state(c);
-  if (st != TC_OK) return st;
+  TC_TRY(init_state(c));
   c->assembled = true;
   return TC_OK;
 }
 
-static IonArgs ion_args(tc_ctx* c, int do_lat) {
+// ------------------------------------------------------------------ the step
+static IonArgs ion_args(tc_ctx* c, Part& P, int do_lat) {
   IonArgs a{};
-  a.n = (int32_t)c->n;
-  a.stride = c->n_pad;
-  a.Vk = c->d_V[c->iVk];
-  a.Vkm1 = c->d_V[c->iVkm1];
-  a.U = c->d_U;
-  a.x0 = c->d_V[c->iX];
-  a.up = c->d_up;
-  a.vp = c->d_vp;
-  a.act = c->d_act;
-  a.lat = c->d_lat;
-  a.lrt = c->d_lrt;
+  a.n = (int32_t)P.n;
+  a.stride = P.n_pad;
+  a.Vk = P.d_V[c->iVk];
+  a.Vkm1 = P.d_V[c->iVkm1];
+  a.U = P.d_U;
+  a.x0 = P.d_V[c->iX];
+  a.up = P.d_up;
+  a.vp = P.d_vp;
+  a.act = P.d_act;
+  a.lat = P.d_lat;
+  a.lrt = P.d_lrt;
   a.do_lat = do_lat;
   a.has_prev = c->has_prev ? 1 : 0;
   a.t_k = c->k * c->cfg.dt;
@@ -541,38 +700,70 @@ static IonArgs ion_args(tc_ctx* c, int do_lat) {
   a.dt = c->cfg.dt;
   a.theta = c->cfg.theta;
   a.flags = c->d_flags;
-  a.xyz = c->d_xyz;
-  a.dirichlet = c->d_dir;
+  a.xyz = P.d_xyz;
+  a.dirichlet = P.d_dir;
   a.t_src = c->k * c->cfg.dt + c->cfg.theta * c->cfg.dt;
   a.t_next = (c->k + 1) * c->cfg.dt;
   return a;
 }
 
-static CgArgs cg_args(tc_ctx* c) {
+static CgArgs cg_args(tc_ctx* c, Part& P, double* x) {
   CgArgs a{};
-  a.slice_ptr = c->d_sp;
-  a.col = c->d_col;
-  a.col16 = c->d_col16;
-  a.kbase = c->d_kbase;
-  a.fmt = c->d_fmt;
-  a.A = c->d_A;
-  a.K = c->d_K;
-  a.dinv = c->d_dinv;
-  a.nslices = c->nslices;
-  a.x = c->csr_mode ? c->d_V[0] : c->d_V[c->iX];
-  a.r = c->d_r;
-  a.z = c->d_z;
-  a.q = c->d_q;
-  a.p0 = c->d_p0;
-  a.p1 = c->d_p1;
-  a.up = c->d_up;
-  a.vp = c->d_vp;
-  a.b = c->d_b;
-  a.part = c->d_part;
+  a.slice_ptr = P.d_sp;
+  a.col = P.d_col;
+  a.col16 = P.d_col16;
+  a.kbase = P.d_kbase;
+  a.fmt = P.d_fmt;
+  a.A = P.d_A;
+  a.K = P.d_K;
+  a.dinv = P.d_dinv;
+  a.nslices = P.nslices;
+  a.x = x;
+  a.r = P.d_r;
+  a.z = P.d_z;
+  a.q = P.d_q;
+  a.p0 = P.d_p0;
+  a.p1 = P.d_p1;
+  a.up = P.d_up;
+  a.vp = P.d_vp;
+  a.b = P.d_b;
+  a.part = P.d_part;
   a.eps_a = c->cfg.abs_tol;
   a.eps_r = c->cfg.rel_tol;
   a.max_iters = c->cfg.max_iters;
   a.rel_mode = c->cfg.rel_mode;
+  a.flags = c->d_flags;
+  a.step_tag = (int32_t)c->k;
+  return a;
+}
+
+static SplitArgs split_args(tc_ctx* c, Part& P) {
+  SplitArgs a{};
+  a.slice_ptr = P.d_sp;
+  a.col = P.d_col;
+  a.A = P.d_A;
+  a.K = P.d_K;
+  a.dinv = P.d_dinv;
+  a.nslices = P.nslices;
+  a.x = P.d_V[c->iX];
+  a.r = P.d_r;
+  a.z = P.d_z;
+  a.q = P.d_q;
+  a.p0 = P.d_p0;
+  a.p1 = P.d_p1;
+  a.up = P.d_up;
+  a.vp = P.d_vp;
+  a.part = P.d_part;
+  a.ticket = P.d_ticket;
+  a.red = P.d_red;
+  a.sc = P.d_sc;
+  a.eps_a = c->cfg.abs_tol;
+  a.eps_r = c->cfg.rel_tol;
+  a.max_iters = c->cfg.max_iters;
+  a.rel_mode = c->cfg.rel_mode;
+  a.send_idx = P.d_send_idx;
+  a.send_buf = P.d_send_buf;
+  a.n_send = (int64_t)P.plan.send_g.size();
   a.flags = c->d_flags;
   a.step_tag = (int32_t)c->k;
   return a;
@@ -587,38 +778,138 @@ static cudaEvent_t ev(tc_ctx* c, size_t i) {
   return c->evs[i];
 }
 
-tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
+// global partition id -> index into c->parts (loopback)
+static int local_index(const tc_ctx* c, int gid) {
+  for (size_t i = 0; i < c->part_ids.size(); ++i)
+    if (c->part_ids[i] == gid) return (int)i;
+  return -1;
+}
+
+// halo: values packed in each part's send buffer (at offset `half` x n_send)
+// land in the receivers' ghost regions of dst(part)
+template <class DstF>
+static tc_status halo_exchange(tc_ctx* c, int half, DstF dst) {
+  if (c->use_comm) {
+    Part& P = c->parts[0];
+    std::vector<HaloMsg> sends, recvs;
+    const int64_t ns = (int64_t)P.plan.send_g.size();
+    for (size_t j = 0; j < P.plan.nbr.size(); ++j) {
+      sends.push_back({P.plan.nbr[j], P.d_send_buf + half * ns + P.plan.send_off[j],
+                       (size_t)(P.plan.send_off[j + 1] - P.plan.send_off[j])});
+      recvs.push_back({P.plan.nbr[j], dst(P) + P.n_pad + P.plan.recv_off[j],
+                       (size_t)(P.plan.recv_off[j + 1] - P.plan.recv_off[j])});
+    }
+    NCCL_TRY(c, c->comm.exchange(sends, recvs, c->stream));
+    return TC_OK;
+  }
+  for (Part& R : c->parts) {  // receiver
+    for (size_t j = 0; j < R.plan.nbr.size(); ++j) {
+      Part& S = c->parts[local_index(c, R.plan.nbr[j])];
+      const int rid = c->part_ids[&R - &c->parts[0]];
+      const size_t js = std::find(S.plan.nbr.begin(), S.plan.nbr.end(), rid) - S.plan.nbr.begin();
+      const int64_t cnt = R.plan.recv_off[j + 1] - R.plan.recv_off[j];
+      const int64_t ns = (int64_t)S.plan.send_g.size();
+      if (cnt)
+        CUDA_TRY(c, cudaMemcpyAsync(dst(R) + R.n_pad + R.plan.recv_off[j],
+                                    S.d_send_buf + half * ns + S.plan.send_off[js], cnt * 8,
+                                    cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+  return TC_OK;
+}
+
+// all-reduce of red[slot] over every partition (bitwise identical everywhere)
+static tc_status allreduce(tc_ctx* c, int slot) {
+  if (c->use_comm) {
+    NCCL_TRY(c, c->comm.allreduce_sum(reinterpret_cast<double*>(c->parts[0].d_red + slot), 2, c->stream));
+    return TC_OK;
+  }
+  CUDA_TRY(c, launch_sum_partials(c->d_reds, (int)c->parts.size(), slot, c->stream));
+  return TC_OK;
+}
+
+// RHS + Algorithm 1 on the partitioned system
+static tc_status pcg_split(tc_ctx* c) {
+  cudaStream_t s = c->stream;
+  // halo of u' and v' (once per step)
+  for (Part& P : c->parts) {
+    const int64_t ns = (int64_t)P.plan.send_g.size();
+    CUDA_TRY(c, launch_pack_gather(ns, P.d_send_idx, P.d_up, P.d_send_buf, s));
+    CUDA_TRY(c, launch_pack_gather(ns, P.d_send_idx, P.d_vp, P.d_send_buf + ns, s));
+  }
+  TC_TRY(halo_exchange(c, 0, [](Part& P) { return P.d_up; }));
+  TC_TRY(halo_exchange(c, 1, [](Part& P) { return P.d_vp; }));
+  for (Part& P : c->parts) CUDA_TRY(c, launch_split_rhs(split_args(c, P), P.grid, s));
+  TC_TRY(allreduce(c, 0));
+  for (Part& P : c->parts) CUDA_TRY(c, launch_split_init(split_args(c, P), s));
+  for (Part& P : c->parts) c->launches += 2 + (P.plan.send_g.empty() ? 0 : 2);
+  c->launches += c->use_comm ? 0 : 1;
+  int enq = 0;
+  while (true) {
+    for (int q = 0; q < c->cfg.check_every; ++q) {
+      for (Part& P : c->parts) CUDA_TRY(c, launch_split_pack_p(split_args(c, P), s));
+      TC_TRY(halo_exchange(c, 0, [](Part& P) { return P.d_z; }));
+      for (Part& P : c->parts) CUDA_TRY(c, launch_split_S(split_args(c, P), P.grid, s));
+      TC_TRY(allreduce(c, 1));
+      for (Part& P : c->parts) CUDA_TRY(c, launch_split_U(split_args(c, P), P.grid, s));
+      TC_TRY(allreduce(c, 0));
+      for (Part& P : c->parts) CUDA_TRY(c, launch_split_scalar(split_args(c, P), s));
+      for (Part& P : c->parts) c->launches += 3 + (P.plan.send_g.empty() ? 0 : 1);
+      c->launches += c->use_comm ? 0 : 2;
+    }
+    enq += c->cfg.check_every;
+    Scalars h;
+    CUDA_TRY(c, cudaMemcpyAsync(&h, c->parts[0].d_sc, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (h.done || enq >= c->cfg.max_iters) break;
+  }
+  return TC_OK;
+}
+
+extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
   if (!c) return TC_EINVAL;
   if (!c->assembled || c->csr_mode) return fail(c, TC_ESTATE, "tc_step before tc_assemble");
   if (nsteps < 0) return fail(c, TC_EINVAL, "tc_step: negative step count");
   if (nsteps == 0) return TC_OK;
   CUDA_TRY(c, cudaSetDevice(c->device));
-  if (ensure_stats(c, nsteps) != TC_OK) return TC_ECUDA;
+  TC_TRY(ensure_stats(c, nsteps));
   const int model = c->cfg.model;
   size_t evi = 0;
-  for (int64_t s = 0; s < nsteps; ++s) {
+  for (int64_t st = 0; st < nsteps; ++st) {
     if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
-    // (1) ionic step + LAT/LRT of V^k + x0, u', v'
-    IonArgs ia = ion_args(c, (s > 0 && c->has_prev) ? 1 : 0);
-    cudaError_t e;
-    if (model == TC_ION_TT2006_EPI) e = launch_ionic_tt(ia, c->tt, c->stream);
-    else if (model == TC_ION_MS) e = launch_ionic_ms(ia, c->ms, c->stream);
-    else e = launch_ionic_mms(ia, c->mms, c->stream);
-    CUDA_TRY(c, e);
-    c->launches += 1;
-    // (2) stimulus of the epoch containing step k
-    for (const Epoch& ep : c->epochs)
-      if (ep.k0 <= c->k && c->k < ep.k1) {
-        CUDA_TRY(c, launch_stimulus(ep.m, c->d_stim_idx + ep.off, c->d_stim_s + ep.off, c->d_up,
-                                    c->d_vp, c->cfg.dt, c->cfg.theta, c->d_flags, c->stream));
+    // (1) ionic step + LAT/LRT of V^k + x0, u', v'; (2) stimulus of the epoch of step k
+    for (Part& P : c->parts) {
+      IonArgs ia = ion_args(c, P, (st > 0 && c->has_prev) ? 1 : 0);
+      cudaError_t e;
+      if (model == TC_ION_TT2006_EPI) e = launch_ionic_tt(ia, c->tt, c->stream);
+      else if (model == TC_ION_MS) e = launch_ionic_ms(ia, c->ms, c->stream);
+      else e = launch_ionic_mms(ia, c->mms, c->stream);
+      CUDA_TRY(c, e);
+      c->launches += 1;
+      for (const Epoch& ep : P.epochs)
+        if (ep.k0 <= c->k && c->k < ep.k1) {
+          CUDA_TRY(c, launch_stimulus(ep.m, P.d_stim_idx + ep.off, P.d_stim_s + ep.off, P.d_up,
+                                      P.d_vp, c->cfg.dt, c->cfg.theta, c->d_flags, c->stream));
+          c->launches += 1;
+        }
+    }
+    if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+    // (3) RHS + Algorithm 1
+    if (split_mode(c)) {
+      TC_TRY(pcg_split(c));
+      for (Part& P : c->parts) {
+        SplitArgs sa = split_args(c, P);
+        sa.stat = c->d_stats + st;
+        CUDA_TRY(c, launch_split_final(sa, P.grid, c->stream));
         c->launches += 1;
       }
-    if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
-    // (3) RHS + Algorithm 1 in one cooperative kernel
-    CgArgs ca = cg_args(c);
-    ca.stat = c->d_stats + s;
-    CUDA_TRY(c, launch_pcg(1, c->cfg.pcg_variant, ca, c->cg_grid, c->stream));
-    c->launches += 2;  // RHS kernel + cooperative PCG kernel
+    } else {
+      Part& P = c->parts[0];
+      CgArgs ca = cg_args(c, P, P.d_V[c->iX]);
+      ca.stat = c->d_stats + st;
+      CUDA_TRY(c, launch_pcg(1, c->cfg.pcg_variant, ca, P.grid, c->stream));
+      c->launches += 2;  // RHS kernel + cooperative PCG kernel
+    }
     if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (4) V^{k-1} <- V^k <- x
     int old = c->iVkm1;
@@ -629,10 +920,11 @@ tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
     c->has_prev = true;
   }
   // LAT/LRT of the last V (time t_k)
-  if (model != TC_ION_MMS) {
-    CUDA_TRY(c, launch_lat_epilogue(ion_args(c, 1), c->stream));
-    c->launches += 1;
-  }
+  if (model != TC_ION_MMS)
+    for (Part& P : c->parts) {
+      CUDA_TRY(c, launch_lat_epilogue(ion_args(c, P, 1), c->stream));
+      c->launches += 1;
+    }
   if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
   std::vector<tc_step_stat> hst(nsteps);
   int32_t flags[8];
@@ -662,6 +954,8 @@ tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
   return TC_OK;
 }
 
+extern "C" {
+
 tc_status tc_profile(tc_ctx* c, int enable) {
   if (!c) return TC_EINVAL;
   c->prof = enable != 0;
@@ -680,42 +974,95 @@ tc_status tc_profile_read(tc_ctx* c, double out[6], int reset) {
   return TC_OK;
 }
 
-tc_status tc_matrix_info(const tc_ctx* c, int64_t out[6]) {
+tc_status tc_matrix_info(const tc_ctx* c, int64_t out[8]) {
   if (!c || !out) return TC_EINVAL;
   if (!c->assembled && !c->csr_mode) return TC_ESTATE;
+  const Part& P = c->parts[0];
   out[0] = c->n;
   out[1] = c->nnz;
-  out[2] = c->nnz_pad;
-  out[3] = c->nslices;
-  out[4] = c->cg_grid;
-  out[5] = c->n_wide;
+  int64_t pad = 0, ns = 0, wide = 0, ghosts = 0;
+  for (const Part& Q : c->parts) {
+    pad += Q.nnz_pad;
+    ns += Q.nslices;
+    wide += Q.n_wide;
+    ghosts += Q.n_ghost;
+  }
+  out[2] = pad;
+  out[3] = ns;
+  out[4] = P.grid;
+  out[5] = wide;
+  out[6] = c->nparts;
+  out[7] = ghosts;
   return TC_OK;
 }
 
+}  // extern "C"
+
 // ------------------------------------------------------------------ outputs / state
-static tc_status to_host_orig(tc_ctx* c, const double* dvec, double* out) {
-  CUDA_TRY(c, launch_gather(c->n, c->d_inv, dvec, c->d_tmp, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(out, c->d_tmp, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+// internal-order owned values of every part -> original order host array
+static tc_status gather_field(tc_ctx* c, double* const* dvec_of_part, double* out) {
+  std::vector<double> internal(c->n);
+  if (c->use_comm) {
+    Part& P = c->parts[0];
+    int64_t maxn = 0;
+    for (int p = 0; p < c->nparts; ++p) maxn = std::max(maxn, c->bounds[p + 1] - c->bounds[p]);
+    double* d_all = nullptr;
+    CUDA_TRY(c, cudaMalloc(&d_all, (size_t)maxn * c->nparts * 8));
+    cudaMemcpyAsync(P.d_tmp, dvec_of_part[0], P.n * 8, cudaMemcpyDeviceToDevice, c->stream);
+    std::string m = c->comm.allgather(P.d_tmp, d_all, (size_t)maxn, c->stream);
+    std::vector<double> all((size_t)maxn * c->nparts);
+    cudaMemcpyAsync(all.data(), d_all, all.size() * 8, cudaMemcpyDeviceToHost, c->stream);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaFree(d_all);
+    if (!m.empty()) return fail(c, TC_ENCCL, m);
+    CUDA_TRY(c, e);
+    for (int p = 0; p < c->nparts; ++p)
+      std::copy(all.begin() + (size_t)p * maxn, all.begin() + (size_t)p * maxn + (c->bounds[p + 1] - c->bounds[p]),
+                internal.begin() + c->bounds[p]);
+  } else {
+    for (size_t pi = 0; pi < c->parts.size(); ++pi) {
+      Part& P = c->parts[pi];
+      CUDA_TRY(c, cudaMemcpyAsync(internal.data() + P.plan.g0, dvec_of_part[pi], P.n * 8,
+                                  cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  for (int64_t o = 0; o < c->n; ++o) out[o] = internal[c->inv[o]];
   return TC_OK;
 }
-static tc_status from_host_orig(tc_ctx* c, const double* in, double* dvec) {
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_tmp, in, c->n * 8, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, launch_gather(c->n, c->d_perm, c->d_tmp, dvec, c->stream));
+
+static tc_status scatter_field(tc_ctx* c, const double* in, double* const* dvec_of_part) {
+  for (size_t pi = 0; pi < c->parts.size(); ++pi) {
+    Part& P = c->parts[pi];
+    std::vector<double> loc(P.n);
+    for (int64_t i = 0; i < P.n; ++i) loc[i] = in[c->perm[P.plan.g0 + i]];
+    CUDA_TRY(c, cudaMemcpyAsync(dvec_of_part[pi], loc.data(), P.n * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
   return TC_OK;
 }
+
+template <class F>
+static std::vector<double*> per_part(tc_ctx* c, F f) {
+  std::vector<double*> v;
+  for (Part& P : c->parts) v.push_back(f(P));
+  return v;
+}
+
+extern "C" {
 
 tc_status tc_get_v(tc_ctx* c, double* v) {
   if (!c || !v) return TC_EINVAL;
   if (!c->assembled) return fail(c, TC_ESTATE, "tc_get_v before tc_assemble");
-  return to_host_orig(c, c->d_V[c->iVk], v);
+  const int iv = c->iVk;
+  return gather_field(c, per_part(c, [iv](Part& P) { return P.d_V[iv]; }).data(), v);
 }
 
 tc_status tc_get_activation(tc_ctx* c, double* lat, double* lrt) {
   if (!c) return TC_EINVAL;
   if (!c->assembled) return fail(c, TC_ESTATE, "tc_get_activation before tc_assemble");
-  if (lat) { tc_status s = to_host_orig(c, c->d_lat, lat); if (s) return s; }
-  if (lrt) { tc_status s = to_host_orig(c, c->d_lrt, lrt); if (s) return s; }
+  if (lat) TC_TRY(gather_field(c, per_part(c, [](Part& P) { return P.d_lat; }).data(), lat));
+  if (lrt) TC_TRY(gather_field(c, per_part(c, [](Part& P) { return P.d_lrt; }).data(), lrt));
   return TC_OK;
 }
 
@@ -729,11 +1076,12 @@ tc_status tc_get_state(tc_ctx* c, double* buf, int64_t len) {
   if (!c->assembled) return fail(c, TC_ESTATE, "tc_get_state before tc_assemble");
   if (len != tc_state_len(c)) return fail(c, TC_EINVAL, "tc_get_state: wrong length");
   const int64_t n = c->n;
-  tc_status s;
-  if ((s = to_host_orig(c, c->d_V[c->iVk], buf))) return s;
-  if ((s = to_host_orig(c, c->has_prev ? c->d_V[c->iVkm1] : c->d_V[c->iVk], buf + n))) return s;
+  const int iv = c->iVk, ip = c->has_prev ? c->iVkm1 : c->iVk;
+  TC_TRY(gather_field(c, per_part(c, [iv](Part& P) { return P.d_V[iv]; }).data(), buf));
+  TC_TRY(gather_field(c, per_part(c, [ip](Part& P) { return P.d_V[ip]; }).data(), buf + n));
   for (int q = 0; q < c->nstates; ++q)
-    if ((s = to_host_orig(c, c->d_U + q * c->n_pad, buf + (2 + q) * n))) return s;
+    TC_TRY(gather_field(c, per_part(c, [q](Part& P) { return P.d_U + q * P.n_pad; }).data(),
+                        buf + (2 + q) * n));
   buf[(2 + c->nstates) * n] = (double)c->k;
   buf[(2 + c->nstates) * n + 1] = c->has_prev ? 1.0 : 0.0;
   return TC_OK;
@@ -746,12 +1094,12 @@ tc_status tc_set_state(tc_ctx* c, const double* buf, int64_t len) {
   const int64_t n = c->n;
   const double kk = buf[(2 + c->nstates) * n], hp = buf[(2 + c->nstates) * n + 1];
   if (!(kk >= 0) || kk != std::floor(kk)) return fail(c, TC_EINVAL, "tc_set_state: bad step index");
-  tc_status s;
-  if ((s = from_host_orig(c, buf, c->d_V[c->iVk]))) return s;
-  if ((s = from_host_orig(c, buf + n, c->d_V[c->iVkm1]))) return s;
+  const int iv = c->iVk, ip = c->iVkm1;
+  TC_TRY(scatter_field(c, buf, per_part(c, [iv](Part& P) { return P.d_V[iv]; }).data()));
+  TC_TRY(scatter_field(c, buf + n, per_part(c, [ip](Part& P) { return P.d_V[ip]; }).data()));
   for (int q = 0; q < c->nstates; ++q)
-    if ((s = from_host_orig(c, buf + (2 + q) * n, c->d_U + q * c->n_pad))) return s;
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    TC_TRY(scatter_field(c, buf + (2 + q) * n,
+                         per_part(c, [q](Part& P) { return P.d_U + q * P.n_pad; }).data()));
   c->k = (int64_t)kk;
   c->has_prev = hp != 0.0;
   return TC_OK;
@@ -762,6 +1110,7 @@ tc_status tc_csr_upload(tc_ctx* c, int32_t n, int64_t nnz, const int32_t* rowptr
                         const double* val) {
   if (!c) return TC_EINVAL;
   if (c->have_mesh || c->csr_mode) return fail(c, TC_ESTATE, "tc_csr_upload: context already holds a system");
+  if (split_mode(c)) return fail(c, TC_ESTATE, "tc_csr_upload: single partition only");
   if (n <= 0 || nnz < 0 || !rowptr || (nnz > 0 && (!col || !val))) return fail(c, TC_EINVAL, "tc_csr_upload: bad arguments");
   if (rowptr[0] != 0 || rowptr[n] != nnz) return fail(c, TC_EINVAL, "tc_csr_upload: rowptr inconsistent with nnz");
   std::vector<int64_t> rp(n + 1);
@@ -783,36 +1132,43 @@ tc_status tc_csr_upload(tc_ctx* c, int32_t n, int64_t nnz, const int32_t* rowptr
   for (int64_t t = 0; t < nnz; ++t) sv[slot[t]] = val[t];
   c->n = n;
   c->nnz = nnz;
-  c->nslices = hs.nslices;
-  c->n_pad = hs.n_pad;
-  c->nnz_pad = hs.slice_ptr[hs.nslices];
-  CUDA_TRY(c, dalloc(c, &c->d_sp, (int64_t)hs.slice_ptr.size()));
-  CUDA_TRY(c, dalloc(c, &c->d_col, c->nnz_pad));
-  CUDA_TRY(c, dalloc(c, &c->d_A, c->nnz_pad));
-  if (alloc_vectors(c) != TC_OK) return TC_ECUDA;
-  std::vector<double> dinv(c->n_pad, 0.0);
+  c->parts.resize(1);
+  c->part_ids.assign(1, 0);
+  Part& P = c->parts[0];
+  P.plan.g0 = 0;
+  P.plan.g1 = n;
+  P.n = n;
+  P.nnz = nnz;
+  P.nslices = hs.nslices;
+  P.n_pad = hs.n_pad;
+  P.n_vec = hs.n_pad;
+  P.nnz_pad = hs.slice_ptr[hs.nslices];
+  CUDA_TRY(c, upload(c, &P.d_sp, hs.slice_ptr));
+  CUDA_TRY(c, upload(c, &P.d_col, hs.col));
+  CUDA_TRY(c, upload(c, &P.d_A, sv));
+  TC_TRY(alloc_part_vectors(c, P));
+  std::vector<double> dinv(P.n_pad, 0.0);
   for (int32_t i = 0; i < n; ++i) dinv[i] = diag[i] != 0.0 ? 1.0 / diag[i] : 0.0;
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_sp, hs.slice_ptr.data(), hs.slice_ptr.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_col, hs.col.data(), hs.col.size() * 4, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_A, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_dinv, dinv.data(), dinv.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  if (upload_compressed(c, hs) != TC_OK) return TC_ECUDA;
-  c->cg_grid = cg_grid_size(0, c->cfg.pcg_variant, c->nslices, c->device);
-  CUDA_TRY(c, dalloc(c, &c->d_part, 2 * (int64_t)c->cg_grid));
-  if (ensure_stats(c, 1) != TC_OK) return TC_ECUDA;
+  CUDA_TRY(c, cudaMemcpyAsync(P.d_dinv, dinv.data(), dinv.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  TC_TRY(upload_compressed(c, P, hs));
+  P.grid = cg_grid_size(0, c->cfg.pcg_variant, P.nslices, c->device);
+  CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
+  TC_TRY(ensure_stats(c, 1));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->csr_mode = true;
   c->has_diag_zero = false;
-  for (int32_t i = 0; i < n; ++i) if (diag[i] == 0.0) c->has_diag_zero = true;
+  for (int32_t i = 0; i < n; ++i)
+    if (diag[i] == 0.0) c->has_diag_zero = true;
   return TC_OK;
 }
 
 tc_status tc_spmv(tc_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return TC_EINVAL;
   if (!c->csr_mode) return fail(c, TC_ESTATE, "tc_spmv before tc_csr_upload");
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_r, x, c->n * 8, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, launch_spmv(c->d_sp, c->d_col, c->d_A, c->nslices, c->d_r, c->d_q, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(y, c->d_q, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
+  Part& P = c->parts[0];
+  CUDA_TRY(c, cudaMemcpyAsync(P.d_r, x, c->n * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, launch_spmv(P.d_sp, P.d_col, P.d_A, P.nslices, P.d_r, P.d_q, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(y, P.d_q, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return TC_OK;
 }
@@ -821,20 +1177,68 @@ tc_status tc_pcg(tc_ctx* c, const double* b, const double* x0, double* x, tc_ste
   if (!c || !b || !x0 || !x) return TC_EINVAL;
   if (!c->csr_mode) return fail(c, TC_ESTATE, "tc_pcg before tc_csr_upload");
   if (c->has_diag_zero) return fail(c, TC_EINVAL, "tc_pcg: zero diagonal entry (Jacobi undefined, S:216)");
+  Part& P = c->parts[0];
   int32_t flags[8] = {0, 0, 0, 0, -1, 0, 0, 0};
   CUDA_TRY(c, cudaMemcpyAsync(c->d_flags, flags, sizeof(flags), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_b, b, c->n * 8, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_V[0], x0, c->n * 8, cudaMemcpyHostToDevice, c->stream));
-  CgArgs ca = cg_args(c);
+  CUDA_TRY(c, cudaMemcpyAsync(P.d_b, b, c->n * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(P.d_V[0], x0, c->n * 8, cudaMemcpyHostToDevice, c->stream));
+  CgArgs ca = cg_args(c, P, P.d_V[0]);
   ca.stat = c->d_stats;
-  CUDA_TRY(c, launch_pcg(0, c->cfg.pcg_variant, ca, c->cg_grid, c->stream));
+  CUDA_TRY(c, launch_pcg(0, c->cfg.pcg_variant, ca, P.grid, c->stream));
   tc_step_stat h;
   CUDA_TRY(c, cudaMemcpyAsync(&h, c->d_stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(x, c->d_V[0], c->n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(x, P.d_V[0], c->n * 8, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(flags, c->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   if (rep) *rep = h;
   if (flags[1]) return fail(c, TC_ENAN, "tc_pcg: NaN in an inner product");
+  return TC_OK;
+}
+
+// ------------------------------------------------------------------ host-only helpers (no GPU)
+tc_status tc_mesh_pattern(int64_t n, int64_t E, const int32_t* tets, int64_t* rowptr, int32_t* col) {
+  if (n <= 0 || E < 0 || !tets || !rowptr) return TC_EINVAL;
+  for (int64_t t = 0; t < 4 * E; ++t)
+    if (tets[t] < 0 || tets[t] >= n) return TC_EINVAL;
+  std::vector<int64_t> iptr, rp;
+  std::vector<int32_t> inc, cl;
+  build_incidence(n, E, tets, iptr, inc);
+  build_pattern(n, tets, iptr, inc, rp, cl);
+  std::copy(rp.begin(), rp.end(), rowptr);
+  if (col) std::copy(cl.begin(), cl.end(), col);
+  return TC_OK;
+}
+
+tc_status tc_rcm(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t* perm) {
+  if (n <= 0 || !rowptr || !col || !perm) return TC_EINVAL;
+  std::vector<int64_t> rp(rowptr, rowptr + n + 1);
+  std::vector<int32_t> cl(col, col + rowptr[n]);
+  std::vector<int32_t> p;
+  rcm_order(n, rp, cl, p);
+  std::copy(p.begin(), p.end(), perm);
+  return TC_OK;
+}
+
+tc_status tc_partition_plan(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t nparts,
+                            int32_t part, int64_t sizes[4], int64_t* bounds, int32_t* ghosts,
+                            int32_t* nbr, int64_t* recv_off, int64_t* send_off, int32_t* send_g) {
+  if (n <= 0 || !rowptr || !col || nparts < 1 || part < 0 || part >= nparts || !sizes) return TC_EINVAL;
+  std::vector<PartPlan> plans;
+  plan_partitions(n, rowptr, col, nparts, plans);
+  const PartPlan& P = plans[part];
+  sizes[0] = (int64_t)P.ghosts.size();
+  sizes[1] = (int64_t)P.nbr.size();
+  sizes[2] = (int64_t)P.send_g.size();
+  sizes[3] = P.g1 - P.g0;
+  if (bounds) {
+    for (int p = 0; p < nparts; ++p) bounds[p] = plans[p].g0;
+    bounds[nparts] = n;
+  }
+  if (ghosts) std::copy(P.ghosts.begin(), P.ghosts.end(), ghosts);
+  if (nbr) std::copy(P.nbr.begin(), P.nbr.end(), nbr);
+  if (recv_off) std::copy(P.recv_off.begin(), P.recv_off.end(), recv_off);
+  if (send_off) std::copy(P.send_off.begin(), P.send_off.end(), send_off);
+  if (send_g) std::copy(P.send_g.begin(), P.send_g.end(), send_g);
   return TC_OK;
 }
 

@@ -1,5 +1,6 @@
 // assembly.cu -- GPU assembly of the P1 FEM matrices into
-// the SELL-32 layout: one thread per row gathers the contributions of the
+// the SELL-32 layout of a row block [row0, row0 + n) (col = internal indices
+// during assembly): one thread per row gathers the contributions of the
 // elements incident to its node in ascending element order, so every stored
 // entry is summed in the same order as an element-order scatter-add, without
 // atomics (deterministic).  Boundary (one-time) work, not on the step path.
@@ -87,7 +88,7 @@ __global__ void assemble_kernel(AsmArgs a) {
     const int64_t t = base + (int64_t)k * kSellC;
     const double Aval = a.c_mass * a.A[t] + a.c_stiff * a.K[t];
     a.A[t] = Aval;
-    if (k < len && a.col[t] == (int32_t)i) diag = Aval;
+    if (k < len && a.col[t] == (int32_t)(a.row0 + i)) diag = Aval;
   }
   const bool dir = a.dirichlet && a.dirichlet[i];
   a.dinv[i] = dir ? 0.0 : 1.0 / diag;  // Dirichlet rows never move (reading M3)

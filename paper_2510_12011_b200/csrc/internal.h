@@ -88,6 +88,41 @@ struct CgArgs {
   int32_t step_tag;    // step index recorded on abort
 };
 
+// ---- split-phase (partitioned) PCG: device scalar state of Algorithm 1 -----
+struct Scalars {
+  double rho, zeta, zref, alpha, beta;
+  int32_t it, conv, nan, done, plast;  // plast: p buffer (0/1) written by the last iteration
+};
+
+struct SplitArgs {
+  const int64_t* slice_ptr;
+  const int32_t* col;    // local column indices (owned [0,n), ghosts n_pad + g)
+  const double* A;
+  const double* K;
+  const double* dinv;
+  int32_t nslices;
+  double* x;
+  double* r;
+  double* z;             // ghost region receives the neighbours' p
+  double* q;
+  double* p0;            // ghost regions stay 0
+  double* p1;
+  const double* up;      // ghost regions filled by the per-step halo exchange
+  const double* vp;
+  double2* part;         // per-CTA partials
+  unsigned int* ticket;  // last-CTA-done counter (self-resetting)
+  double2* red;          // [0] (r.z, z.z) and [1] (p.q, 0): rank partials, all-reduced in place
+  Scalars* sc;
+  double eps_a, eps_r;
+  int32_t max_iters, rel_mode;
+  const int32_t* send_idx;
+  double* send_buf;
+  int64_t n_send;
+  tc_step_stat* stat;
+  int32_t* flags;
+  int32_t step_tag;
+};
+
 struct IonArgs {
   int32_t n;
   int64_t stride;      // n_pad (SoA state stride)
@@ -114,6 +149,7 @@ struct IonArgs {
 
 struct AsmArgs {
   int32_t n;
+  int32_t row0;        // global (internal) index of local row 0
   const double* xyz;
   const int32_t* tets;
   const int32_t* ereg;
@@ -150,6 +186,19 @@ cudaError_t launch_spmv(const int64_t* slice_ptr, const int32_t* col, const doub
 int cg_grid_size(int mode, int variant, int32_t nslices, int device);
 cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
 
+// split-phase PCG launchers (pcg_split.cu); grid = split_grid(nslices)
+int split_grid(int32_t nslices);
+cudaError_t launch_split_rhs(const SplitArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_split_init(const SplitArgs& a, cudaStream_t s);
+cudaError_t launch_split_pack_p(const SplitArgs& a, cudaStream_t s);
+cudaError_t launch_pack_gather(int64_t m, const int32_t* idx, const double* src, double* dst,
+                               cudaStream_t s);
+cudaError_t launch_split_S(const SplitArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_split_U(const SplitArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_split_scalar(const SplitArgs& a, cudaStream_t s);
+cudaError_t launch_split_final(const SplitArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_sum_partials(double2* const* reds, int nparts, int slot, cudaStream_t s);
+
 // ---- host setup (setup_host.cpp) --------------------------------------------
 struct HostMesh;
 std::string orient_and_validate(int64_t n, int64_t E, int32_t* tets, const double* xyz);
@@ -166,5 +215,18 @@ void permute_csr(int64_t n, const std::vector<int64_t>& rowptr, const std::vecto
 void csr_to_sell(int32_t n, const int64_t* rowptr, const int32_t* col, HostSell& s,
                  std::vector<int64_t>* csr_slot = nullptr);
 void compress_sell(HostSell& s);
+
+// Row-block partition of a system in internal (RCM) order: part p owns the
+// contiguous rows [g0, g1); ghosts = columns of owned rows outside the block.
+struct PartPlan {
+  int64_t g0 = 0, g1 = 0;
+  std::vector<int32_t> ghosts;     // sorted internal indices
+  std::vector<int32_t> nbr;        // neighbour parts, ascending
+  std::vector<int64_t> recv_off;   // nbr.size()+1 offsets into ghosts (ghosts of one owner are contiguous)
+  std::vector<int64_t> send_off;   // nbr.size()+1 offsets into send_g
+  std::vector<int32_t> send_g;     // owned internal indices each neighbour needs, grouped by neighbour
+};
+void plan_partitions(int64_t n, const int64_t* rowptr, const int32_t* col, int nparts,
+                     std::vector<PartPlan>& plans);
 
 }  // namespace tcb

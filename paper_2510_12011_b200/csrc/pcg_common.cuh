@@ -1,0 +1,236 @@
+// pcg_common.cuh -- device building blocks shared by the persistent PCG kernel
+// (pcg.cu) and the split-phase, partitioned PCG kernels (pcg_split.cu):
+// PTX helpers (mbarrier, TMA bulk copies), deterministic reductions, the
+// per-warp slice pipeline and the SELL row products.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace tcb {
+
+
+#ifndef TCB_DIRECT_MINB
+#define TCB_DIRECT_MINB 8   // CTAs/SM of the direct variant: 8 -> 32 registers, 64 warps/SM
+#endif
+constexpr int kWMax = 16;                               // widest TMA-staged slice
+constexpr int kValBytes = kWMax * kSellC * 8;           // 4 KB of values
+constexpr int kStageBytes = kWMax * kSellC * (8 + 4);   // + 2 KB of column indices
+constexpr int kStages = 2;
+constexpr int kWarpSmem = kStages * kStageBytes;        // 12 KB per warp
+constexpr int kCgSmem = kCgWarps * kWarpSmem;           // 96 KB per CTA (2 CTAs / SM)
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 1-D TMA bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ reductions
+__device__ __forceinline__ double2 warp_sum2(double2 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+// Sum of v over the CTA, result valid in every thread.
+__device__ __forceinline__ double2 block_sum2(double2 v, double2* sh) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  v = warp_sum2(v);
+  __syncthreads();  // sh may still be read from a previous call
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double2 t = make_double2(0.0, 0.0);
+  if (lane < kCgWarps) t = sh[lane];
+  t = warp_sum2(t);  // every warp reduces the 8 values identically
+  return t;
+}
+
+// Grid-wide deterministic sum.  buf holds gridDim.x slots.
+__device__ __forceinline__ double2 grid_sum2(double2 v, double2* buf, double2* sh,
+                                             cg::grid_group& grid) {
+  double2 b = block_sum2(v, sh);
+  if (threadIdx.x == 0) buf[blockIdx.x] = b;
+  grid.sync();
+  double2 acc = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) {
+    double2 u = buf[t];
+    acc.x += u.x;
+    acc.y += u.y;
+  }
+  return block_sum2(acc, sh);
+}
+
+// ------------------------------------------------------------------ slice pipeline
+// One warp walks its slices s = gw, gw + nw, ... ; slice s's values and column
+// indices are staged in stage (j mod kStages) by lane 0's TMA copies issued
+// kStages slices ahead.  Slices wider than kWMax (irregular meshes) fall back
+// to direct loads.
+struct SlicePipe {
+  char* buf;
+  uint64_t* bar;
+  uint32_t phase;  // bit st = parity of the next completion of stage st
+  uint64_t pol;
+};
+
+__device__ __forceinline__ void slice_bounds(const int64_t* sp, int s, int64_t& base, int& w) {
+  base = __ldg(sp + s);
+  w = (int)((__ldg(sp + s + 1) - base) >> 5);
+}
+
+__device__ __forceinline__ void pipe_issue(SlicePipe& P, int st, const double* A, const int* col,
+                                           const int64_t* sp, int s, int ns) {
+  if (s >= ns) return;
+  int64_t base;
+  int w;
+  slice_bounds(sp, s, base, w);
+  if (w <= 0 || w > kWMax) return;
+  char* dst = P.buf + st * kStageBytes;
+  const uint32_t bv = (uint32_t)w * kSellC * 8, bc = (uint32_t)w * kSellC * 4;
+  mbar_expect_tx(P.bar + st, bv + bc);
+  tma_load(dst, A + base, bv, P.bar + st, P.pol);
+  tma_load(dst + kValBytes, col + base, bc, P.bar + st, P.pol);
+}
+
+// f(i, base, w, staged, As, Cs) for every slice of this warp (i = this lane's row).
+template <bool TMA, class F>
+__device__ __forceinline__ void for_slices(SlicePipe& P, const int64_t* sp, const double* A,
+                                           const int* col, int ns, int gw, int nw, int lane, F&& f);
+
+template <class F>
+__device__ __forceinline__ void for_slices_tma(SlicePipe& P, const int64_t* sp, const double* A,
+                                           const int* col, int ns, int gw, int nw, int lane, F&& f) {
+  if (lane == 0) {
+#pragma unroll
+    for (int st = 0; st < kStages; ++st) pipe_issue(P, st, A, col, sp, gw + st * nw, ns);
+  }
+  int st = 0;
+  for (int s = gw; s < ns; s += nw) {
+    int64_t base;
+    int w;
+    slice_bounds(sp, s, base, w);
+    const bool staged = w > 0 && w <= kWMax;
+    if (staged) {
+      mbar_wait(P.bar + st, (P.phase >> st) & 1u);
+      P.phase ^= 1u << st;
+    }
+    const char* sb = P.buf + st * kStageBytes;
+    f((int64_t)s * kSellC + lane, base, w, staged, reinterpret_cast<const double*>(sb),
+      reinterpret_cast<const int*>(sb + kValBytes));
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async();  // generic-proxy reads of the stage before the async overwrite
+      pipe_issue(P, st, A, col, sp, s + kStages * nw, ns);
+    }
+    st = (st + 1 == kStages) ? 0 : st + 1;
+  }
+}
+
+template <bool TMA, class F>
+__device__ __forceinline__ void for_slices(SlicePipe& P, const int64_t* sp, const double* A,
+                                           const int* col, int ns, int gw, int nw, int lane, F&& f) {
+  if (TMA) {
+    for_slices_tma(P, sp, A, col, ns, gw, nw, lane, f);
+  } else {
+    for (int s = gw; s < ns; s += nw) {
+      int64_t base;
+      int w;
+      slice_bounds(sp, s, base, w);
+      f((int64_t)s * kSellC + lane, base, w, false, (const double*)nullptr, (const int*)nullptr);
+    }
+  }
+}
+
+// q_i = sum_k A_ik p_c, p_c = z_c (+ beta pold_c); slots accumulated in
+// ascending order (the CSR order).  Staged: operands from shared memory.
+template <bool FIRST>
+__device__ __forceinline__ double row_Ap_staged(int w, int lane, const double* As, const int* Cs,
+                                                const double* z, const double* pold, double beta) {
+  double sum = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < w; ++k) {
+    const int c = Cs[k * kSellC + lane];
+    const double g = FIRST ? z[c] : z[c] + beta * pold[c];
+    sum += As[k * kSellC + lane] * g;
+  }
+  return sum;
+}
+
+// Column index of slot t (slot row k) of one slice: either the plain int32
+// array, or (compressed slices) a per-(slice, k) int32 base, broadcast to the
+// warp, plus a 16-bit offset per slot.
+struct ColIdx {
+  const int* c32;
+  const uint16_t* c16;  // null: uncompressed slice
+  const int* kb;
+  __device__ __forceinline__ int operator()(int64_t t, int k) const {
+    return c16 ? __ldg(kb + k) + (int)__ldcs(c16 + t) : __ldcs(c32 + t);
+  }
+};
+
+template <bool COMP>
+__device__ __forceinline__ ColIdx col_of(const CgArgs& a, int64_t i, int64_t base) {
+  ColIdx ci;
+  ci.c32 = a.col;
+  ci.c16 = nullptr;
+  ci.kb = nullptr;
+  if (COMP && __ldg(a.fmt + (i >> 5)) == 0) {
+    ci.c16 = a.col16;
+    ci.kb = a.kbase + (base >> 5);
+  }
+  return ci;
+}
+
+template <bool FIRST>
+__device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, const ColIdx& ci,
+                                                const double* A, const double* z, const double* pold,
+                                                double beta) {
+  double sum = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const int64_t t = base + (int64_t)k * kSellC + lane;
+    const int c = ci(t, k);
+    const double g = FIRST ? z[c] : z[c] + beta * pold[c];
+    sum += __ldcs(A + t) * g;
+  }
+  return sum;
+}
+
+}  // namespace tcb

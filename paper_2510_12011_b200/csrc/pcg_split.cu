@@ -1,0 +1,290 @@
+// pcg_split.cu -- Algorithm 1 for a row-partitioned system
+// (multi-GPU over NCCL, or several partitions of one GPU): the same data flow
+// as the persistent kernel, cut at the two global reductions so that a
+// collective can sit between the phases.
+//
+// Per partition and iteration:
+//   pack_p : p_it = z + beta p_{it-1} of the owned nodes other partitions need
+//   (halo) : received into the ghost region of z (the ghost region of p stays 0,
+//            so z_c + beta p_c == p_c for every ghost column c)
+//   S      : q = A p_it, x += alpha_{it-1} p_{it-1}, rank partial of p.q
+//   (allreduce p.q)
+//   U      : alpha = rho / p.q, r -= alpha q, z = r / diag, rank partials r.z, z.z
+//   (allreduce)
+//   scalar : one thread: stopping test, beta, rho (identical on every partition,
+//            because the all-reduced sums are bitwise identical)
+// Every kernel returns at once when the scalar state says "done".
+#include "pcg_common.cuh"
+
+namespace tcb {
+
+constexpr int kSplitThreads = 256;
+
+// CTA partial -> part[blockIdx]; the last CTA to finish sums all partials in
+// index order (deterministic) into *out and re-arms the ticket.
+__device__ __forceinline__ void reduce_to_rank(double2 acc, double2* part, unsigned int* ticket,
+                                               double2* out, double2* sh) {
+  __shared__ bool last;
+  const double2 b = block_sum2(acc, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = b;
+    __threadfence();
+    const unsigned int t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double2 s = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) {
+    const double2 u = __ldcg(part + t);
+    s.x += u.x;
+    s.y += u.y;
+  }
+  s = block_sum2(s, sh);
+  if (threadIdx.x == 0) {
+    *out = s;
+    *ticket = 0u;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kSplitThreads, 4) split_rhs_kernel(SplitArgs a) {
+  __shared__ double2 sh[kCgWarps];
+  if (a.flags[0]) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kCgWarps + (threadIdx.x >> 5), nw = gridDim.x * kCgWarps;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int s = gw; s < a.nslices; s += nw) {
+    const int64_t base = __ldg(a.slice_ptr + s);
+    const int w = (int)((__ldg(a.slice_ptr + s + 1) - base) >> 5);
+    const int64_t i = (int64_t)s * kSellC + lane;
+    double sum = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < w; ++k) {
+      const int64_t t = base + (int64_t)k * kSellC + lane;
+      const int c = __ldcs(a.col + t);
+      sum += __ldcs(a.A + t) * a.up[c] - __ldcs(a.K + t) * a.vp[c];   // r_0 = A u' - K v'
+    }
+    const double zi = __ldg(a.dinv + i) * sum;
+    a.r[i] = sum;
+    a.z[i] = zi;
+    acc.x += sum * zi;
+    acc.y += zi * zi;
+  }
+  reduce_to_rank(acc, a.part, a.ticket, a.red, sh);
+}
+
+// rho_0 = r.z, ||z_0|| from the all-reduced sums (reading C4: ||z_0|| < eps_a -> done)
+__global__ void split_init_kernel(SplitArgs a) {
+  Scalars s{};
+  const double2 g = a.red[0];
+  s.rho = g.x;
+  s.zeta = sqrt(g.y);
+  s.zref = s.zeta;
+  s.plast = -1;
+  if (isnan(s.rho) || isnan(s.zeta)) { s.nan = 1; s.done = 1; }
+  else if (s.zeta < a.eps_a) { s.conv = 1; s.done = 1; }
+  if (a.flags[0]) s.done = 1;
+  *a.sc = s;
+}
+
+__global__ void split_pack_p_kernel(SplitArgs a) {
+  const Scalars s = *a.sc;
+  if (s.done) return;
+  const double* pold = (s.it & 1) ? a.p0 : a.p1;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < a.n_send;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = a.send_idx[j];
+    a.send_buf[j] = s.it == 0 ? a.z[i] : a.z[i] + s.beta * pold[i];
+  }
+}
+
+__global__ void pack_gather_kernel(int64_t m, const int32_t* __restrict__ idx,
+                                   const double* __restrict__ src, double* __restrict__ dst) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
+       j += (int64_t)gridDim.x * blockDim.x)
+    dst[j] = src[idx[j]];
+}
+
+__global__ void __launch_bounds__(kSplitThreads, 8) split_S_kernel(SplitArgs a) {
+  __shared__ double2 sh[kCgWarps];
+  const Scalars s = *a.sc;
+  if (s.done) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kCgWarps + (threadIdx.x >> 5), nw = gridDim.x * kCgWarps;
+  double* __restrict__ pnew = (s.it & 1) ? a.p1 : a.p0;
+  const double* __restrict__ pold = (s.it & 1) ? a.p0 : a.p1;
+  const bool first = s.it == 0;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int sl = gw; sl < a.nslices; sl += nw) {
+    const int64_t base = __ldg(a.slice_ptr + sl);
+    const int w = (int)((__ldg(a.slice_ptr + sl + 1) - base) >> 5);
+    const int64_t i = (int64_t)sl * kSellC + lane;
+    double pi = a.z[i];
+    if (!first) {
+      const double po = pold[i];
+      pi += s.beta * po;
+      a.x[i] += s.alpha * po;            // deferred x += alpha_{it-1} p_{it-1}
+    }
+    double sum = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < w; ++k) {
+      const int64_t t = base + (int64_t)k * kSellC + lane;
+      const int c = __ldcs(a.col + t);
+      const double g = first ? a.z[c] : a.z[c] + s.beta * pold[c];
+      sum += __ldcs(a.A + t) * g;
+    }
+    pnew[i] = pi;
+    a.q[i] = sum;
+    acc.x += pi * sum;
+  }
+  reduce_to_rank(acc, a.part, a.ticket, a.red + 1, sh);
+}
+
+__global__ void __launch_bounds__(kSplitThreads, 8) split_U_kernel(SplitArgs a) {
+  __shared__ double2 sh[kCgWarps];
+  const Scalars s = *a.sc;
+  if (s.done) return;
+  const double alpha = s.rho / a.red[1].x;   // alpha_k = rho_k / p.q (all-reduced)
+  double2 acc = make_double2(0.0, 0.0);
+  const int64_t n = (int64_t)a.nslices * kSellC;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = a.r[i] - alpha * a.q[i];
+    const double zi = __ldg(a.dinv + i) * ri;
+    a.r[i] = ri;
+    a.z[i] = zi;
+    acc.x += ri * zi;
+    acc.y += zi * zi;
+  }
+  reduce_to_rank(acc, a.part, a.ticket, a.red, sh);
+}
+
+// The stopping test of Algorithm 1 and the scalar recurrences (one thread).
+__global__ void split_scalar_kernel(SplitArgs a) {
+  Scalars s = *a.sc;
+  if (s.done) return;
+  const double pq = a.red[1].x;
+  const double2 g = a.red[0];
+  s.plast = s.it & 1;                  // p buffer written by this iteration
+  s.it += 1;
+  if (isnan(pq)) { s.nan = 1; s.done = 1; *a.sc = s; return; }
+  s.alpha = s.rho / pq;
+  const double zeta = sqrt(g.y);
+  s.zeta = zeta;
+  if (isnan(zeta) || isnan(g.x)) { s.nan = 1; s.done = 1; }
+  else if (zeta < a.eps_a || zeta / s.zref < a.eps_r) { s.conv = 1; s.done = 1; }
+  else if (s.it >= a.max_iters) { s.done = 1; }
+  else {
+    s.beta = g.x / s.rho;
+    s.rho = g.x;
+    if (a.rel_mode == 0) s.zref = zeta;
+  }
+  *a.sc = s;
+}
+
+// x += alpha p_last (Alg. 1 updates x before its test), step report, fail budget.
+__global__ void split_final_kernel(SplitArgs a) {
+  const Scalars s = *a.sc;
+  if (!s.nan && s.plast >= 0) {
+    const double* __restrict__ pl = s.plast ? a.p1 : a.p0;
+    const int64_t n = (int64_t)a.nslices * kSellC;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      a.x[i] += s.alpha * pl[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !a.flags[0]) {
+    a.stat->iters = s.it;
+    a.stat->converged = s.conv;
+    a.stat->znorm = s.zeta;
+    int32_t* f = a.flags;
+    if (s.nan) {
+      f[0] = 1; f[1] = 1; f[4] = a.step_tag;
+    } else {
+      f[2] = s.conv ? 0 : f[2] + 1;
+      if (f[3] > 0 && f[2] >= f[3]) { f[0] = 1; f[4] = a.step_tag; }
+    }
+  }
+}
+
+// loopback "allreduce": the partitions' rank partials summed in partition order
+__global__ void sum_partials_kernel(double2* const* reds, int nparts, int slot) {
+  double2 t = make_double2(0.0, 0.0);
+  for (int p = 0; p < nparts; ++p) {
+    const double2 u = reds[p][slot];
+    t.x += u.x;
+    t.y += u.y;
+  }
+  for (int p = 0; p < nparts; ++p) reds[p][slot] = t;
+}
+
+static int sm_count_split() {
+  static int v = 0;
+  if (!v) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
+
+// one full wave of the S kernel (grid-stride over slices)
+int split_grid(int32_t nslices) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, split_S_kernel, kSplitThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int need = (nslices + kCgWarps - 1) / kCgWarps;
+  int cap = sm_count_split() * per_sm;
+  return need < 1 ? 1 : (need < cap ? need : cap);
+}
+
+static int small_grid(int64_t m) {
+  int64_t b = (m + 255) / 256;
+  return (int)(b < 1 ? 1 : (b > 592 ? 592 : b));
+}
+
+cudaError_t launch_split_rhs(const SplitArgs& a, int grid, cudaStream_t s) {
+  split_rhs_kernel<1><<<grid, kSplitThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_split_init(const SplitArgs& a, cudaStream_t s) {
+  split_init_kernel<<<1, 1, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_split_pack_p(const SplitArgs& a, cudaStream_t s) {
+  if (a.n_send == 0) return cudaSuccess;
+  split_pack_p_kernel<<<small_grid(a.n_send), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_pack_gather(int64_t m, const int32_t* idx, const double* src, double* dst,
+                               cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  pack_gather_kernel<<<small_grid(m), 256, 0, s>>>(m, idx, src, dst);
+  return cudaGetLastError();
+}
+cudaError_t launch_split_S(const SplitArgs& a, int grid, cudaStream_t s) {
+  split_S_kernel<<<grid, kSplitThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_split_U(const SplitArgs& a, int grid, cudaStream_t s) {
+  split_U_kernel<<<grid, kSplitThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_split_scalar(const SplitArgs& a, cudaStream_t s) {
+  split_scalar_kernel<<<1, 1, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_split_final(const SplitArgs& a, int grid, cudaStream_t s) {
+  split_final_kernel<<<grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_sum_partials(double2* const* reds, int nparts, int slot, cudaStream_t s) {
+  sum_partials_kernel<<<1, 1, 0, s>>>(reds, nparts, slot);
+  return cudaGetLastError();
+}
+
+}  // namespace tcb

@@ -231,4 +231,50 @@ void compress_sell(HostSell& s) {
   s.n_wide = wide;
 }
 
+// Balanced contiguous row blocks of the internal (RCM) order.  With RCM's
+// level structure the ghosts of a block come from its neighbouring blocks.
+void plan_partitions(int64_t n, const int64_t* rowptr, const int32_t* col, int nparts,
+                     std::vector<PartPlan>& plans) {
+  plans.assign(nparts, PartPlan());
+  std::vector<int64_t> bounds(nparts + 1);
+  for (int p = 0; p <= nparts; ++p) bounds[p] = (n * p) / nparts;
+  auto owner = [&](int64_t g) {
+    return (int)(std::upper_bound(bounds.begin(), bounds.end(), g) - bounds.begin()) - 1;
+  };
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int p = 0; p < nparts; ++p) {
+    PartPlan& P = plans[p];
+    P.g0 = bounds[p];
+    P.g1 = bounds[p + 1];
+    std::vector<int32_t> gh;
+    for (int64_t i = P.g0; i < P.g1; ++i)
+      for (int64_t t = rowptr[i]; t < rowptr[i + 1]; ++t)
+        if (col[t] < P.g0 || col[t] >= P.g1) gh.push_back(col[t]);
+    std::sort(gh.begin(), gh.end());
+    gh.erase(std::unique(gh.begin(), gh.end()), gh.end());
+    P.ghosts = std::move(gh);
+    P.recv_off.push_back(0);
+    for (size_t t = 0; t < P.ghosts.size(); ++t) {
+      const int q = owner(P.ghosts[t]);
+      if (P.nbr.empty() || P.nbr.back() != q) {
+        if (!P.nbr.empty()) P.recv_off.push_back((int64_t)t);
+        P.nbr.push_back(q);
+      }
+    }
+    if (!P.nbr.empty()) P.recv_off.push_back((int64_t)P.ghosts.size());
+  }
+  // send lists: what neighbour q receives from p = q's ghosts inside p's block
+  for (int p = 0; p < nparts; ++p) {
+    PartPlan& P = plans[p];
+    P.send_off.assign(1, 0);
+    for (int q : P.nbr) {
+      const PartPlan& Q = plans[q];
+      auto lo = std::lower_bound(Q.ghosts.begin(), Q.ghosts.end(), (int32_t)P.g0);
+      auto hi = std::lower_bound(Q.ghosts.begin(), Q.ghosts.end(), (int32_t)P.g1);
+      P.send_g.insert(P.send_g.end(), lo, hi);
+      P.send_off.push_back((int64_t)P.send_g.size());
+    }
+  }
+}
+
 }  // namespace tcb

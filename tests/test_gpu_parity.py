@@ -133,6 +133,56 @@ def test_step_trajectory_parity(T, model, permute, rcm, variant):
         sim.close()
 
 
+@pytest.mark.parametrize("model,nparts,permute", [("ms", 2, False), ("tt2006", 3, True), ("tt2006", 2, False),
+                                                  ("ms", 5, True)])
+def test_partitioned_trajectory_parity(T, model, nparts, permute):
+    """Row-block partitions on one GPU (split-phase PCG, device-copy halos,
+    in-order scalar sums): same trajectory as the oracle and as 1 partition."""
+    xyz, tets, region, fib, cond, stims = _slab_case(model, 25, 9, 5, permute=permute, seed=2 if permute else 0)
+    dt = 0.05
+    ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0), stims)
+    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, partitions=nparts, check_every=3)
+    sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+    try:
+        info = T.tc_matrix_info(sim.ctx)
+        assert info["partitions"] == nparts and info["ghosts"] > 0
+        for k in range(80):
+            st = sim.step(1)
+            rep = ref.step()
+            rel = np.linalg.norm(sim.V - ref.Vk) / np.linalg.norm(ref.Vk)
+            assert rel <= 1e-8, (k, rel)
+            assert abs(int(st["iters"][0]) - rep.iters) <= 1
+        lat, _ = sim.activation()
+        assert np.abs(lat - ref.lat).max() <= dt + 1e-12
+        s = sim.get_state()
+        n = xyz.shape[0]
+        assert np.allclose(s[2 * n:-2].reshape(-1, n), ref.U, rtol=1e-8, atol=1e-14)
+    finally:
+        sim.close()
+
+
+def test_nccl_path_world1_parity(T):
+    """The NCCL split-phase path (communicator of one rank) against the oracle."""
+    xyz, tets, region, fib, cond, stims = _slab_case("tt2006", 21, 8, 5)
+    dt = 0.05
+    ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, abs_tol=1e-8, rel_tol=0.0), stims)
+    cfg = T.tc_config_default(dt=dt, abs_tol=1e-8, rel_tol=0.0)
+    try:
+        uid = T.tc_nccl_unique_id()
+    except T.TcError:
+        pytest.skip("NCCL not loadable")
+    sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims, comm=(0, 1, uid))
+    try:
+        for k in range(60):
+            sim.step(1)
+            ref.step()
+            assert np.linalg.norm(sim.V - ref.Vk) / np.linalg.norm(ref.Vk) <= 1e-8
+        lat, _ = sim.activation()
+        assert np.abs(lat - ref.lat).max() <= dt + 1e-12
+    finally:
+        sim.close()
+
+
 def test_state_injection_one_step(T):
     """One step from an injected mid-upstroke state: GPU == oracle (any size path)."""
     xyz, tets, region, fib, cond, stims = _slab_case("tt2006", 31, 12, 7, 0.5, permute=True, seed=5)
