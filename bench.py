@@ -155,14 +155,16 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def ncu_traffic(workload):
-    """Per-launch DRAM bytes of the PCG kernel from the committed ncu --set full summary."""
+def ncu_traffic(workload, iters_per_step):
+    """DRAM bytes per step of the PCG path (rhs_kernel + pcg_kernel) from the committed
+    ncu --set full capture, the pcg part rescaled to the timed mean iteration count."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        e = d.get(workload)
-        return None if e is None else e
+            e = json.load(f).get(workload)
+        if e is None:
+            return None
+        return e["rhs_bytes"] + e["pcg_bytes"] * iters_per_step / e["iters"]
     except Exception:
         return None
 
@@ -252,12 +254,15 @@ def main():
     b_cg, b_ion = bytes_per_step(n, nnz, iters, w["model"], args.steps)
     cg_s = prof["pcg_ms"] / 1e3
     achieved = b_cg / cg_s / 1e9 if cg_s > 0 else None
-    traffic = ncu_traffic(args.workload)
-    roof = {"kernel": "pcg_kernel<1> (RHS + Alg. 1, one cooperative launch per step)", "bound": "hbm",
+    traffic = ncu_traffic(args.workload, iters / args.steps)
+    roof = {"kernel": "PCG path per step: rhs_kernel + cooperative pcg_kernel (Eq. 3 RHS + Alg. 1)",
+            "bound": "hbm",
             "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"] if achieved else None,
             "traffic": traffic, "peak_source": which,
-            "bytes_model": "per launch: 20nnz+4(n+1)+44n + iters*(12nnz+4(n+1)+72n) (SURVEY 8d)",
+            "bytes_model": "per step: 20nnz+4(n+1)+44n + iters*(12nnz+4(n+1)+72n) (SURVEY 8d)",
+            "algorithmic_bytes_per_step": b_cg / args.steps,
+            "traffic_unit": "DRAM bytes per step of the same kernels (ncu, profiles/ncu_traffic.json)",
             "share_of_step": prof["pcg_ms"] / ms,
             "ionic_ms_per_step": prof["ionic_ms"] / args.steps,
             "pcg_ms_per_step": prof["pcg_ms"] / args.steps,

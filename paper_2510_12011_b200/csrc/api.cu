@@ -96,6 +96,11 @@ struct tc_ctx {
   bool has_diag_zero = false;
   std::vector<int32_t> perm, inv;  // perm[internal] = original, inv[original] = internal
   std::vector<int64_t> bounds;     // partition g0 per global part (+ end)
+  int32_t* d_perm_g = nullptr;     // perm on the device (internal -> original)
+  int32_t* d_pos = nullptr;        // NCCL mode: original -> position in the padded all-gather
+  double* d_io = nullptr;          // original-order staging for host I/O
+  double* d_all = nullptr;         // NCCL mode: all-gather buffer (nparts x max block)
+  int64_t max_block = 0;
   int64_t nnz = 0;
   int nstates = 0;
   int32_t* d_flags = nullptr;
@@ -662,6 +667,20 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
       CUDA_TRY(c, upload(c, &P.d_stim_s, sv));
     }
   }
+  CUDA_TRY(c, upload(c, &c->d_perm_g, c->perm));
+  CUDA_TRY(c, dalloc(c, &c->d_io, n));
+  if (c->use_comm) {
+    c->max_block = 0;
+    for (int p = 0; p < c->nparts; ++p) c->max_block = std::max(c->max_block, c->bounds[p + 1] - c->bounds[p]);
+    std::vector<int32_t> pos(n);
+    for (int64_t o = 0; o < n; ++o) {
+      const int64_t g = c->inv[o];
+      const int p = (int)(std::upper_bound(c->bounds.begin(), c->bounds.end(), g) - c->bounds.begin()) - 1;
+      pos[o] = (int32_t)(p * c->max_block + (g - c->bounds[p]));
+    }
+    CUDA_TRY(c, upload(c, &c->d_pos, pos));
+    CUDA_TRY(c, dalloc(c, &c->d_all, c->max_block * c->nparts));
+  }
   if (split_mode(c) && !c->use_comm) {
     std::vector<double2*> reds;
     for (Part& P : c->parts) reds.push_back(P.d_red);
@@ -999,46 +1018,31 @@ tc_status tc_matrix_info(const tc_ctx* c, int64_t out[8]) {
 }  // extern "C"
 
 // ------------------------------------------------------------------ outputs / state
-// internal-order owned values of every part -> original order host array
+// owned values of every part -> original-order host array (device-side permutation)
 static tc_status gather_field(tc_ctx* c, double* const* dvec_of_part, double* out) {
-  std::vector<double> internal(c->n);
   if (c->use_comm) {
     Part& P = c->parts[0];
-    int64_t maxn = 0;
-    for (int p = 0; p < c->nparts; ++p) maxn = std::max(maxn, c->bounds[p + 1] - c->bounds[p]);
-    double* d_all = nullptr;
-    CUDA_TRY(c, cudaMalloc(&d_all, (size_t)maxn * c->nparts * 8));
-    cudaMemcpyAsync(P.d_tmp, dvec_of_part[0], P.n * 8, cudaMemcpyDeviceToDevice, c->stream);
-    std::string m = c->comm.allgather(P.d_tmp, d_all, (size_t)maxn, c->stream);
-    std::vector<double> all((size_t)maxn * c->nparts);
-    cudaMemcpyAsync(all.data(), d_all, all.size() * 8, cudaMemcpyDeviceToHost, c->stream);
-    cudaError_t e = cudaStreamSynchronize(c->stream);
-    cudaFree(d_all);
-    if (!m.empty()) return fail(c, TC_ENCCL, m);
-    CUDA_TRY(c, e);
-    for (int p = 0; p < c->nparts; ++p)
-      std::copy(all.begin() + (size_t)p * maxn, all.begin() + (size_t)p * maxn + (c->bounds[p + 1] - c->bounds[p]),
-                internal.begin() + c->bounds[p]);
+    CUDA_TRY(c, cudaMemcpyAsync(P.d_tmp, dvec_of_part[0], P.n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    NCCL_TRY(c, c->comm.allgather(P.d_tmp, c->d_all, (size_t)c->max_block, c->stream));
+    CUDA_TRY(c, launch_gather(c->n, c->d_pos, c->d_all, c->d_io, c->stream));
   } else {
     for (size_t pi = 0; pi < c->parts.size(); ++pi) {
       Part& P = c->parts[pi];
-      CUDA_TRY(c, cudaMemcpyAsync(internal.data() + P.plan.g0, dvec_of_part[pi], P.n * 8,
-                                  cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, launch_scatter(P.n, c->d_perm_g + P.plan.g0, dvec_of_part[pi], c->d_io, c->stream));
     }
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   }
-  for (int64_t o = 0; o < c->n; ++o) out[o] = internal[c->inv[o]];
+  CUDA_TRY(c, cudaMemcpyAsync(out, c->d_io, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return TC_OK;
 }
 
 static tc_status scatter_field(tc_ctx* c, const double* in, double* const* dvec_of_part) {
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_io, in, c->n * 8, cudaMemcpyHostToDevice, c->stream));
   for (size_t pi = 0; pi < c->parts.size(); ++pi) {
     Part& P = c->parts[pi];
-    std::vector<double> loc(P.n);
-    for (int64_t i = 0; i < P.n; ++i) loc[i] = in[c->perm[P.plan.g0 + i]];
-    CUDA_TRY(c, cudaMemcpyAsync(dvec_of_part[pi], loc.data(), P.n * 8, cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, launch_gather(P.n, c->d_perm_g + P.plan.g0, c->d_io, dvec_of_part[pi], c->stream));
   }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return TC_OK;
 }
 
