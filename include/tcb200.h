@@ -86,6 +86,11 @@ typedef struct {
                             partition per rank). */
   int32_t check_every;   /* split-phase PCG: iterations enqueued between host checks of the
                             device convergence flag (4) */
+  int32_t peer;          /* partitioned systems: 1 (default) = one persistent kernel per GPU
+                            doing halos and reductions itself over peer memory (NVLink via
+                            CUDA IPC between ranks, plain device memory between the parts of
+                            one GPU); 0 = split-phase kernels + NCCL / device copies */
+  int32_t reserved;
 } tc_config;
 
 /* Per-step PCG report. */
@@ -97,7 +102,7 @@ typedef struct {
 
 /* Fills the defaults: theta 0.5, dt 0.01, chi 140, cm 0.01, tolerances 1e-5,
  * max_iters 100, consecutive rel-mode, TT2006 epi, fail_budget 3,
- * thresholds 0 / -70 mV, use_rcm 1, pcg_variant 0, partitions 1, check_every 4. */
+ * thresholds 0 / -70 mV, use_rcm 1, pcg_variant 0, partitions 1, check_every 4, peer 1. */
 void tc_config_default(tc_config* cfg);
 
 /* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
@@ -187,9 +192,11 @@ tc_status tc_profile_read(tc_ctx* ctx, double out[6], int reset);
 /* Sizes of the assembled system: out[0] n, out[1] nnz (stored entries of A,
  * CSR count), out[2] padded SELL-32 slots of the parts held here, out[3] their
  * slices, out[4] PCG grid (CTAs) of the first part, out[5] slices kept at int32
- * indices (variant 2), out[6] partitions, out[7] ghost columns of the parts held.
+ * indices (variant 2), out[6] partitions, out[7] ghost columns of the parts held,
+ * out[8] PCG path (0 persistent single part, 1 split-phase, 2 persistent peer),
+ * out[9] CTAs per partition of the peer kernel.
  * TC_ESTATE before tc_assemble/tc_csr_upload. */
-tc_status tc_matrix_info(const tc_ctx* ctx, int64_t out[8]);
+tc_status tc_matrix_info(const tc_ctx* ctx, int64_t out[10]);
 
 /* ---- Minimum-slice operators on an uploaded CSR (no mesh needed) ---------- */
 /* Upload an n x n CSR (rowptr n+1, col/val nnz, columns sorted per row, the

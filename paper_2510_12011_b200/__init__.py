@@ -40,7 +40,8 @@ class tc_config(C.Structure):
                 ("rel_mode", C.c_int32), ("model", C.c_int32), ("fail_budget", C.c_int32),
                 ("lat_threshold", C.c_double), ("lrt_threshold", C.c_double),
                 ("use_rcm", C.c_int32), ("pcg_variant", C.c_int32),
-                ("partitions", C.c_int32), ("check_every", C.c_int32)]
+                ("partitions", C.c_int32), ("check_every", C.c_int32),
+                ("peer", C.c_int32), ("reserved", C.c_int32)]
 
 
 class tc_step_stat(C.Structure):
@@ -248,11 +249,12 @@ def tc_profile_read(ctx, reset: bool = False):
 
 
 def tc_matrix_info(ctx) -> dict:
-    out = np.zeros(8, np.int64)
+    out = np.zeros(10, np.int64)
     _check(ctx, _L.tc_matrix_info(ctx, _ptr(out)))
     return dict(n=int(out[0]), nnz=int(out[1]), nnz_pad=int(out[2]), nslices=int(out[3]),
                 pcg_grid=int(out[4]), wide_slices=int(out[5]), partitions=int(out[6]),
-                ghosts=int(out[7]))
+                ghosts=int(out[7]), path=["persistent", "split", "peer"][int(out[8])],
+                peer_ctas=int(out[9]))
 
 
 def tc_nccl_unique_id() -> bytes:

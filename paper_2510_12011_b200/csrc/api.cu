@@ -10,6 +10,7 @@
 //   * tc_comm_init(world > 1) -> this rank's part only, split-phase PCG with
 //                                NCCL send/recv halos and NCCL all-reduces.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -61,6 +62,14 @@ struct Part {
   std::vector<Epoch> epochs;
   int32_t* d_stim_idx = nullptr;
   double* d_stim_s = nullptr;
+  // persistent peer-memory PCG (pcg_peer.cu)
+  char* d_inbox = nullptr;        // RedSlot[2 world] + uint64 halo flags[world]
+  int32_t* d_send_nbr = nullptr;
+  int32_t* d_send_off = nullptr;
+  unsigned int* d_bar = nullptr;  // group barrier {count, gen}
+  unsigned long long* d_epoch = nullptr;
+  double2* d_red0 = nullptr;
+  double2* d_ppart = nullptr;     // 2 x CTAs-per-group partials
 };
 
 struct tc_ctx {
@@ -90,6 +99,11 @@ struct tc_ctx {
   std::vector<Part> parts;       // partitions held by this context
   std::vector<int> part_ids;     // their global partition indices
   double2** d_reds = nullptr;    // loopback: red pointers of all parts
+  bool peer = false;             // persistent peer-memory PCG in use
+  int peer_bpg = 0;              // CTAs per group (loop kernel)
+  int peer_bpg_rhs = 0;          // CTAs per group (RHS kernel)
+  std::vector<XPart> xparts;     // host copies, passed by value at launch
+  std::vector<void*> ipc_opened; // peer mappings to close
   // assembled system
   bool assembled = false;
   bool csr_mode = false;
@@ -157,6 +171,8 @@ static cudaError_t upload(tc_ctx* c, T** p, const std::vector<T>& h) {
 }
 
 static void free_all(tc_ctx* c) {
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  c->ipc_opened.clear();
   for (void* p : c->allocs) cudaFree(p);
   c->allocs.clear();
   for (auto e : c->evs) cudaEventDestroy(e);
@@ -164,6 +180,12 @@ static void free_all(tc_ctx* c) {
 }
 
 static bool split_mode(const tc_ctx* c) { return c->nparts > 1 || c->use_comm; }
+
+static size_t inbox_bytes(int world) { return (size_t)2 * world * sizeof(RedSlot) + (size_t)world * 8; }
+static RedSlot* inbox_red(char* inbox) { return reinterpret_cast<RedSlot*>(inbox); }
+static unsigned long long* inbox_flags(char* inbox, int world) {
+  return reinterpret_cast<unsigned long long*>(inbox + (size_t)2 * world * sizeof(RedSlot));
+}
 
 extern "C" {
 
@@ -186,6 +208,8 @@ void tc_config_default(tc_config* c) {
   c->pcg_variant = 0;
   c->partitions = 1;
   c->check_every = 4;
+  c->peer = 1;
+  c->reserved = 0;
 }
 
 tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx** out) {
@@ -467,6 +491,148 @@ static void local_sell(const PartPlan& pl, const int64_t* rp, const int32_t* col
   }
 }
 
+
+// Persistent peer-memory PCG: an XPart per local part whose remote pointers
+// address the neighbours' ghost regions and every rank's inbox -- other parts
+// of this GPU (emulation) or other GPUs through CUDA IPC mappings (NCCL mode).
+// Falls back to the split-phase path (returns TC_OK, c->peer stays false) when
+// a limit is exceeded or peer mappings are unavailable.
+static tc_status setup_peer(tc_ctx* c, const std::vector<PartPlan>& plans) {
+  const int world = c->nparts;
+  // every rank must take the same decision: local checks, then (NCCL mode) a
+  // consensus all-reduce after the IPC attempt
+  bool ok = c->cfg.peer && world <= kMaxRanks && (int)c->parts.size() <= peer_max_groups();
+  for (Part& P : c->parts)
+    if ((int)P.plan.nbr.size() > kMaxNbr) ok = false;
+  if (!c->use_comm && !ok) return TC_OK;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int groups = (int)c->parts.size();
+  const int bpg = peer_blocks_per_sm(0) * sms / groups;
+  const int bpg_rhs = peer_blocks_per_sm(1) * sms / groups;
+  if (bpg_rhs < 1) ok = false;
+  if (bpg < 1) ok = false;
+  if (!c->use_comm && !ok) return TC_OK;
+  for (Part& P : c->parts) {
+    CUDA_TRY(c, dalloc(c, &P.d_inbox, (int64_t)inbox_bytes(world)));
+    CUDA_TRY(c, dalloc(c, &P.d_bar, 2));
+    CUDA_TRY(c, dalloc(c, &P.d_epoch, 2));
+    CUDA_TRY(c, dalloc(c, &P.d_red0, 1));
+    CUDA_TRY(c, dalloc(c, &P.d_ppart, 2 * (int64_t)std::max(std::max(bpg, bpg_rhs), 1)));
+    std::vector<int32_t> snbr(P.plan.send_g.size()), soff(P.plan.send_g.size());
+    for (size_t j = 0; j < P.plan.nbr.size(); ++j)
+      for (int64_t e = P.plan.send_off[j]; e < P.plan.send_off[j + 1]; ++e) {
+        snbr[e] = (int32_t)j;
+        soff[e] = (int32_t)(e - P.plan.send_off[j]);
+      }
+    CUDA_TRY(c, upload(c, &P.d_send_nbr, snbr));
+    CUDA_TRY(c, upload(c, &P.d_send_off, soff));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  // base pointers {z, u', v', inbox} of every rank
+  std::vector<std::array<void*, 4>> base(world, {nullptr, nullptr, nullptr, nullptr});
+  if (!c->use_comm) {
+    for (size_t pi = 0; pi < c->parts.size(); ++pi) {
+      Part& P = c->parts[pi];
+      base[c->part_ids[pi]] = {P.d_z, P.d_up, P.d_vp, P.d_inbox};
+    }
+  } else {
+    Part& P = c->parts[0];
+    const int me = c->comm.rank;
+    cudaIpcMemHandle_t mine[4];
+    std::memset(mine, 0, sizeof(mine));
+    void* ptrs[4] = {P.d_z, P.d_up, P.d_vp, P.d_inbox};
+    for (int t = 0; t < 4 && ok; ++t)
+      if (cudaIpcGetMemHandle(&mine[t], ptrs[t]) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+      }
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+    double *d_h = nullptr, *d_all = nullptr;
+    CUDA_TRY(c, cudaMalloc(&d_h, 256));
+    CUDA_TRY(c, cudaMalloc(&d_all, 256 * (size_t)world));
+    CUDA_TRY(c, cudaMemcpy(d_h, mine, 256, cudaMemcpyHostToDevice));
+    std::string m = c->comm.allgather(d_h, d_all, 32, c->stream);   // every rank, always
+    std::vector<cudaIpcMemHandle_t> all(4 * (size_t)world);
+    cudaMemcpyAsync(all.data(), d_all, 256 * (size_t)world, cudaMemcpyDeviceToHost, c->stream);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaFree(d_h);
+    if (!m.empty()) { cudaFree(d_all); return fail(c, TC_ENCCL, m); }
+    if (e != cudaSuccess) { cudaFree(d_all); CUDA_TRY(c, e); }
+    std::set<int> nb(P.plan.nbr.begin(), P.plan.nbr.end());
+    for (int r = 0; r < world && ok; ++r) {
+      if (r == me) {
+        base[r] = {P.d_z, P.d_up, P.d_vp, P.d_inbox};
+        continue;
+      }
+      for (int t = 0; t < 4 && ok; ++t) {
+        if (t < 3 && !nb.count(r)) continue;
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, all[4 * r + t], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          ok = false;
+          break;
+        }
+        c->ipc_opened.push_back(p);
+        base[r][t] = p;
+      }
+    }
+    // consensus: all ranks use the peer kernel or none does
+    double flag = ok ? 1.0 : 0.0;
+    CUDA_TRY(c, cudaMemcpy(d_all, &flag, 8, cudaMemcpyHostToDevice));
+    m = c->comm.allreduce_sum(d_all, 1, c->stream);
+    CUDA_TRY(c, cudaMemcpyAsync(&flag, d_all, 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    cudaFree(d_all);
+    if (!m.empty()) return fail(c, TC_ENCCL, m);
+    if (flag != (double)world) {
+      for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+      c->ipc_opened.clear();
+      return TC_OK;  // split-phase path on every rank
+    }
+  }
+  std::vector<XPart> xs(c->parts.size());
+  for (size_t pi = 0; pi < c->parts.size(); ++pi) {
+    Part& P = c->parts[pi];
+    const int gid = c->part_ids[pi];
+    XPart& X = xs[pi];
+    X = XPart{};
+    X.slice_ptr = P.d_sp; X.col = P.d_col; X.A = P.d_A; X.K = P.d_K; X.dinv = P.d_dinv;
+    X.nslices = P.nslices;
+    X.nbr_count = (int32_t)P.plan.nbr.size();
+    for (int b = 0; b < 3; ++b) X.V[b] = P.d_V[b];
+    X.r = P.d_r; X.z = P.d_z; X.q = P.d_q; X.p0 = P.d_p0; X.p1 = P.d_p1; X.up = P.d_up; X.vp = P.d_vp;
+    X.part = P.d_ppart;
+    X.send_idx = P.d_send_idx; X.send_nbr = P.d_send_nbr; X.send_off = P.d_send_off;
+    X.n_send = (int64_t)P.plan.send_g.size();
+    for (size_t j = 0; j < P.plan.nbr.size(); ++j) {
+      const int q = P.plan.nbr[j];
+      const PartPlan& Q = plans[q];
+      const size_t jq = std::find(Q.nbr.begin(), Q.nbr.end(), gid) - Q.nbr.begin();
+      const int64_t npad_q = ((Q.g1 - Q.g0 + kSellC - 1) / kSellC) * kSellC;
+      const int64_t ro = npad_q + Q.recv_off[jq];
+      X.rz[j] = static_cast<double*>(base[q][0]) + ro;
+      X.rup[j] = static_cast<double*>(base[q][1]) + ro;
+      X.rvp[j] = static_cast<double*>(base[q][2]) + ro;
+      X.rflag[j] = inbox_flags(static_cast<char*>(base[q][3]), world) + gid;
+      X.myflag[j] = inbox_flags(P.d_inbox, world) + q;
+    }
+    for (int r = 0; r < world; ++r) X.rred[r] = inbox_red(static_cast<char*>(base[r][3]));
+    X.myred = inbox_red(P.d_inbox);
+    X.bar_count = P.d_bar;
+    X.bar_gen = P.d_bar + 1;
+    X.epoch = P.d_epoch;
+    X.red0 = P.d_red0;
+    X.rank = gid;
+    X.world = world;
+  }
+  c->xparts = xs;
+  c->peer = true;
+  c->peer_bpg = bpg;
+  c->peer_bpg_rhs = bpg_rhs;
+  return TC_OK;
+}
+
 extern "C" tc_status tc_assemble(tc_ctx* c) {
   if (!c) return TC_EINVAL;
   if (!c->have_mesh) return fail(c, TC_ESTATE, "tc_assemble before tc_set_mesh");
@@ -686,6 +852,7 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
     for (Part& P : c->parts) reds.push_back(P.d_red);
     CUDA_TRY(c, upload(c, &c->d_reds, reds));
   }
+  if (split_mode(c)) TC_TRY(setup_peer(c, plans));
   int32_t flags[8] = {0, 0, 0, c->cfg.fail_budget, -1, 0, 0, 0};
   CUDA_TRY(c, cudaMemcpyAsync(c->d_flags, flags, sizeof(flags), cudaMemcpyHostToDevice, c->stream));
   TC_TRY(ensure_stats(c, 1024));
@@ -914,7 +1081,12 @@ extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
     }
     if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (3) RHS + Algorithm 1
-    if (split_mode(c)) {
+    if (c->peer) {
+      CUDA_TRY(c, launch_pcg_peer(c->xparts.data(), (int)c->parts.size(), c->peer_bpg, c->peer_bpg_rhs, c->iX, c->iVk,
+                                  c->cfg.abs_tol, c->cfg.rel_tol, c->cfg.max_iters, c->cfg.rel_mode,
+                                  c->d_stats + st, c->d_flags, (int32_t)c->k, c->stream));
+      c->launches += 2;  // RHS + loop kernels
+    } else if (split_mode(c)) {
       TC_TRY(pcg_split(c));
       for (Part& P : c->parts) {
         SplitArgs sa = split_args(c, P);
@@ -966,6 +1138,7 @@ extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
     c->prof_steps += nsteps;
   }
   if (flags[0]) {
+    if (flags[5]) return fail(c, TC_ENCCL, "peer wait timed out (a rank stopped responding) at step " + std::to_string(flags[4]));
     if (flags[1]) return fail(c, TC_ENAN, "NaN in a PCG inner product at step " + std::to_string(flags[4]));
     return fail(c, TC_ESOLVER, "PCG did not converge for " + std::to_string(flags[3]) +
                                    " consecutive steps (last at step " + std::to_string(flags[4]) + ")");
@@ -993,7 +1166,7 @@ tc_status tc_profile_read(tc_ctx* c, double out[6], int reset) {
   return TC_OK;
 }
 
-tc_status tc_matrix_info(const tc_ctx* c, int64_t out[8]) {
+tc_status tc_matrix_info(const tc_ctx* c, int64_t out[10]) {
   if (!c || !out) return TC_EINVAL;
   if (!c->assembled && !c->csr_mode) return TC_ESTATE;
   const Part& P = c->parts[0];
@@ -1012,6 +1185,8 @@ tc_status tc_matrix_info(const tc_ctx* c, int64_t out[8]) {
   out[5] = wide;
   out[6] = c->nparts;
   out[7] = ghosts;
+  out[8] = c->peer ? 2 : (split_mode(c) ? 1 : 0);  // PCG path: 0 persistent, 1 split-phase, 2 peer persistent
+  out[9] = c->peer_bpg;
   return TC_OK;
 }
 

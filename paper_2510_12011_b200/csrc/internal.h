@@ -123,6 +123,42 @@ struct SplitArgs {
   int32_t step_tag;
 };
 
+// ---- persistent multi-rank PCG over peer memory (pcg_peer.cu) -------------
+constexpr int kMaxNbr = 16;
+constexpr int kMaxRanks = 64;
+struct RedSlot {
+  double2 v;
+  unsigned long long e;
+  unsigned long long pad;
+};
+struct XPart {
+  const int64_t* slice_ptr;
+  const int32_t* col;
+  const double* A;
+  const double* K;
+  const double* dinv;
+  int32_t nslices, nbr_count;
+  double* V[3];
+  double *r, *z, *q, *p0, *p1, *up, *vp;
+  double2* part;                 // 2 x CTAs-per-group partials
+  const int32_t* send_idx;       // send entry -> local node
+  const int32_t* send_nbr;       // send entry -> neighbour slot
+  const int32_t* send_off;       // send entry -> offset in that neighbour's ghost region
+  int64_t n_send;
+  double* rz[kMaxNbr];           // neighbours' ghost-region bases (z, u', v'), remote
+  double* rup[kMaxNbr];
+  double* rvp[kMaxNbr];
+  unsigned long long* rflag[kMaxNbr];   // neighbour's inbox flag slot for this rank, remote
+  unsigned long long* myflag[kMaxNbr];  // this rank's inbox flag slot of each neighbour
+  RedSlot* rred[kMaxRanks];      // every rank's reduction slots (2 x world), remote
+  RedSlot* myred;
+  unsigned int* bar_count;
+  unsigned int* bar_gen;
+  unsigned long long* epoch;      // [0] epoch counter, [1] cross-rank reductions done
+  double2* red0;                  // rho_0, ||z_0||^2 handed from the RHS kernel to the loop
+  int32_t rank, world;
+};
+
 struct IonArgs {
   int32_t n;
   int64_t stride;      // n_pad (SoA state stride)
@@ -198,6 +234,12 @@ cudaError_t launch_split_U(const SplitArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_split_scalar(const SplitArgs& a, cudaStream_t s);
 cudaError_t launch_split_final(const SplitArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_sum_partials(double2* const* reds, int nparts, int slot, cudaStream_t s);
+int peer_blocks_per_sm(int which);  // 0 loop kernel, 1 RHS kernel
+int peer_max_groups();
+// parts: HOST array of `groups` XParts (passed by value in kernel-parameter space)
+cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, int iX, int iVk, double eps_a,
+                            double eps_r, int32_t max_iters, int32_t rel_mode, tc_step_stat* stat,
+                            int32_t* flags, int32_t step_tag, cudaStream_t s);
 
 // ---- host setup (setup_host.cpp) --------------------------------------------
 struct HostMesh;

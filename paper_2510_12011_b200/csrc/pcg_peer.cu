@@ -1,0 +1,379 @@
+// pcg_peer.cu -- the multi-GPU PCG as ONE persistent kernel per GPU, with the
+// halo exchange and the cross-GPU reductions done by the kernel itself over
+// NVLink peer memory (CUDA IPC mappings), DESIGN.md "Multi-GPU".
+//
+// Each rank ("group" of CTAs) owns a row block.  Per iteration of Alg. 1:
+//   halo  : p_it = z + beta p_{it-1} of the send-list nodes is stored straight
+//           into the neighbours' ghost regions of z (remote stores), then a
+//           per-neighbour flag carries the epoch; readers wait on their flags
+//   S     : q = A p, x += alpha p_{it-1}, p.q partial -> rank sum (group barrier)
+//   reduce: the rank sum is stored into slot [epoch&1][rank] of EVERY rank's
+//           inbox, then every CTA waits for all ranks' slots of this epoch and
+//           sums them in rank order -> bitwise-identical scalars on all ranks
+//   U     : r, z, (r.z, z.z) partials -> rank sum -> cross-rank reduce, test, beta
+// Memory ordering: data stores, __threadfence_system(), then the flag/epoch
+// store; readers poll with volatile loads, then __threadfence() (which also
+// drops stale L1 lines) before touching the data.  Slots are double-buffered
+// by epoch parity (a rank can be at most one reduction ahead of another).
+// Every wait is bounded (~2 s): on timeout the kernel records an error flag,
+// skips all further waits and finishes its iterations; tc_step reports
+// TC_ENCCL.  With several groups in one cooperative launch on one GPU the same
+// code runs the partitions of a single device ("peer emulation"), which is how
+// the protocol is tested without 8 GPUs.
+#include "pcg_common.cuh"
+
+namespace tcb {
+
+constexpr int kPeerThreads = 256;
+constexpr long long kWaitCycles = 4000000000LL;  // ~2 s at 1.9 GHz
+
+constexpr int kMaxGroups = 8;  // partitions of one GPU in a peer launch (kernel-parameter space)
+
+struct PeerRun {
+  XPart parts[kMaxGroups];  // one per group, in kernel-parameter (constant) space
+  int groups;          // groups in this launch (1 on real multi-GPU)
+  int bpg;             // CTAs per group
+  int iX, iVk;         // rotating V buffers
+  double eps_a, eps_r;
+  int32_t max_iters, rel_mode;
+  tc_step_stat* stat;
+  int32_t* flags;      // [0] abort [1] nan [2] fails [3] budget [4] step [5] peer timeout
+  int32_t step_tag;
+};
+
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ void vstore(unsigned long long* p, unsigned long long v) {
+  *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+__device__ __forceinline__ double2 vload2(const double2* p) {
+  const volatile double* q = reinterpret_cast<const volatile double*>(p);
+  return make_double2(q[0], q[1]);
+}
+__device__ __forceinline__ void vstore2(double2* p, double2 v) {
+  volatile double* q = reinterpret_cast<volatile double*>(p);
+  q[0] = v.x;
+  q[1] = v.y;
+}
+
+__device__ int32_t* g_peer_flags;  // flags of the running launch (timeouts)
+
+// Barrier of the CTAs of one group (sense-reversing generation counter),
+// bounded like every other wait.
+__device__ __forceinline__ void group_barrier(unsigned int* count, unsigned int* gen, int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vg = gen;
+    const unsigned int g = *vg;
+    __threadfence();
+    if (atomicAdd(count, 1u) == (unsigned int)nblocks - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      const long long t0 = clock64();
+      while (*vg == g) {
+        if (clock64() - t0 > kWaitCycles) {
+          atomicExch(g_peer_flags + 5, 1);
+          break;
+        }
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Deterministic sum over the group's CTAs (valid in every thread of every CTA).
+// part: 2 x nb slots, alternated by the caller's reduction counter (a CTA can be
+// one reduction ahead of another, never two: the next barrier separates them).
+__device__ __forceinline__ double2 group_sum2(double2 v, double2* part, int lb, int nb, double2* sh,
+                                              unsigned int* bc, unsigned int* bg) {
+  const double2 b = block_sum2(v, sh);
+  if (threadIdx.x == 0) part[lb] = b;
+  group_barrier(bc, bg, nb);
+  double2 acc = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+    const double2 u = __ldcg(part + t);
+    acc.x += u.x;
+    acc.y += u.y;
+  }
+  return block_sum2(acc, sh);
+}
+
+// Bounded spin until *p == want (GE: *p >= want), thread 0 of a CTA; false on timeout.
+template <bool GE>
+__device__ __forceinline__ bool wait_for(const unsigned long long* p, unsigned long long want,
+                                         int32_t* flags) {
+  const long long t0 = clock64();
+  while (GE ? vload(p) < want : vload(p) != want) {
+    if (*reinterpret_cast<volatile int32_t*>(flags + 5)) return false;
+    if (clock64() - t0 > kWaitCycles) {
+      atomicExch(flags + 5, 1);
+      return false;
+    }
+  }
+  return true;
+}
+
+// Cross-rank sum of the rank value v (identical in all CTAs of the group).
+// Slot parity follows the reduction count `nr` (not the epoch, which halos also
+// advance): a rank cannot start reduction nr+2 before every rank has read nr.
+__device__ __forceinline__ double2 cross_sum2(const XPart& X, double2 v, unsigned long long epoch,
+                                              unsigned long long nr, int lb, int32_t* flags,
+                                              double2* sh1) {
+  const int slot = (int)(nr & 1ull);
+  if (lb == 0 && threadIdx.x == 0) {
+    for (int r = 0; r < X.world; ++r) {
+      RedSlot* d = X.rred[r] + slot * X.world + X.rank;
+      vstore2(&d->v, v);
+      __threadfence_system();
+      vstore(&d->e, epoch);
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < X.world; ++r) wait_for<false>(&X.myred[slot * X.world + r].e, epoch, flags);
+    __threadfence();
+    double2 s = make_double2(0.0, 0.0);
+    for (int r = 0; r < X.world; ++r) {
+      const double2 u = vload2(&X.myred[slot * X.world + r].v);
+      s.x += u.x;
+      s.y += u.y;
+    }
+    *sh1 = s;
+  }
+  __syncthreads();
+  const double2 s = *sh1;
+  __syncthreads();
+  return s;
+}
+
+// Remote halo: for send entry j, value(j) lands in neighbour send_nbr[j]'s ghost
+// region of the vector selected by `which` (0 z, 1 u', 2 v'); then the flags.
+template <class ValF>
+__device__ __forceinline__ void halo_push(const XPart& X, int which, unsigned long long epoch, int lb,
+                                          int nb, ValF val) {
+  bool wrote = false;
+  for (int64_t j = (int64_t)lb * blockDim.x + threadIdx.x; j < X.n_send; j += (int64_t)nb * blockDim.x) {
+    const int q = X.send_nbr[j];
+    double* base = which == 0 ? X.rz[q] : (which == 1 ? X.rup[q] : X.rvp[q]);
+    base[X.send_off[j]] = val(X.send_idx[j]);
+    wrote = true;
+  }
+  if (wrote) __threadfence_system();   // this thread's remote stores before the flag
+  group_barrier(X.bar_count, X.bar_gen, nb);
+  if (lb == 0 && threadIdx.x < X.nbr_count) vstore(X.rflag[threadIdx.x], epoch);
+}
+
+__device__ __forceinline__ void halo_wait(const XPart& X, unsigned long long epoch, int32_t* flags) {
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < X.nbr_count; ++q) wait_for<true>(X.myflag[q], epoch, flags);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// RHS of the step on the partitioned system: halo of u', v' (remote stores),
+// r_0 = A u' - K v' (== b - A x_0), z_0, and the cross-rank
+// sums rho_0, ||z_0||^2 -> X.red0.  Own launch (64 registers); cooperative so
+// that every group's CTAs are resident while they wait for their neighbours.
+__global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_constant__ PeerRun R) {
+  __shared__ double2 sh[kCgWarps];
+  __shared__ double2 sh1;
+  const int group = blockIdx.x / R.bpg;
+  const int lb = blockIdx.x - group * R.bpg;
+  const int nb = R.bpg;
+  const XPart& X = R.parts[group];
+  if (R.flags[0]) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = lb * kCgWarps + (threadIdx.x >> 5), nw = nb * kCgWarps;
+  unsigned long long ep = X.epoch[0];
+  unsigned long long nrx = X.epoch[1];
+  ++ep;
+  halo_push(X, 1, ep, lb, nb, [&](int32_t i) { return X.up[i]; });
+  ++ep;
+  halo_push(X, 2, ep, lb, nb, [&](int32_t i) { return X.vp[i]; });
+  halo_wait(X, ep, R.flags);  // flags are monotone: >= ep covers both halos
+  double2 acc = make_double2(0.0, 0.0);
+  for (int s = gw; s < X.nslices; s += nw) {
+    const int64_t base = __ldg(X.slice_ptr + s);
+    const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
+    const int64_t i = (int64_t)s * kSellC + lane;
+    double sum = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < w; ++k) {
+      const int64_t t = base + (int64_t)k * kSellC + lane;
+      const int c = __ldcs(X.col + t);
+      sum += __ldcs(X.A + t) * X.up[c] - __ldcs(X.K + t) * X.vp[c];
+    }
+    const double zi = __ldg(X.dinv + i) * sum;
+    X.r[i] = sum;
+    X.z[i] = zi;
+    acc.x += sum * zi;
+    acc.y += zi * zi;
+  }
+  double2 tot = group_sum2(acc, X.part, lb, nb, sh, X.bar_count, X.bar_gen);
+  ++ep;
+  tot = cross_sum2(X, tot, ep, nrx++, lb, R.flags, &sh1);
+  group_barrier(X.bar_count, X.bar_gen, nb);  // every CTA is done with the counters
+  if (lb == 0 && threadIdx.x == 0) {
+    *X.red0 = tot;
+    X.epoch[0] = ep;
+    X.epoch[1] = nrx;
+  }
+}
+
+// Algorithm 1's loop on the partitioned system (after rhs_peer_kernel).
+__global__ void __launch_bounds__(kPeerThreads, 8) pcg_peer_kernel(const __grid_constant__ PeerRun R) {
+  __shared__ double2 sh[kCgWarps];
+  __shared__ double2 sh1;
+  const int group = blockIdx.x / R.bpg;
+  const int lb = blockIdx.x - group * R.bpg;  // CTA index inside the group
+  const int nb = R.bpg;
+  const XPart& X = R.parts[group];
+  if (R.flags[0]) return;  // aborted earlier: uniform over the launch
+  const int lane = threadIdx.x & 31;
+  const int gw = lb * kCgWarps + (threadIdx.x >> 5), nw = nb * kCgWarps;
+  const int ns = X.nslices;
+  double* __restrict__ x = X.V[R.iX];
+  unsigned long long ep = X.epoch[0];   // epoch counter (halos and reductions), same in every CTA
+  unsigned long long nrx = X.epoch[1];  // cross-rank reductions done (slot parity)
+  unsigned int nred = 0;                // partial-buffer parity
+  double2 acc;
+  double2 tot = *X.red0;
+  double rho = tot.x, zeta = sqrt(tot.y), zref = zeta, alpha = 0.0, beta = 0.0;
+  int it = 0, conv = 0, nan = 0, plast = -1;
+  if (isnan(rho) || isnan(zeta)) nan = 1;
+  if (!nan && zeta < R.eps_a) conv = 1;
+  if (!nan && !conv) {
+    for (it = 0; it < R.max_iters;) {
+      double* __restrict__ pnew = (it & 1) ? X.p1 : X.p0;
+      const double* __restrict__ pold = (it & 1) ? X.p0 : X.p1;
+      const bool first = it == 0;
+      // halo of p_it into the neighbours' z ghosts
+      ++ep;
+      halo_push(X, 0, ep, lb, nb, [&](int32_t i) { return first ? X.z[i] : X.z[i] + beta * pold[i]; });
+      halo_wait(X, ep, R.flags);
+      // S (separate first / later loops, as in the single-GPU kernel)
+      acc = make_double2(0.0, 0.0);
+      const ColIdx ci{X.col, nullptr, nullptr};
+      if (first) {
+        for (int s = gw; s < ns; s += nw) {
+          const int64_t base = __ldg(X.slice_ptr + s);
+          const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
+          const int64_t i = (int64_t)s * kSellC + lane;
+          const double pi = X.z[i];
+          const double sum = row_Ap_direct<true>(base, w, lane, ci, X.A, X.z, nullptr, 0.0);
+          pnew[i] = pi;
+          X.q[i] = sum;
+          acc.x += pi * sum;
+        }
+      } else {
+        for (int s = gw; s < ns; s += nw) {
+          const int64_t base = __ldg(X.slice_ptr + s);
+          const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
+          const int64_t i = (int64_t)s * kSellC + lane;
+          const double po = pold[i];
+          const double xi = x[i];
+          const double pi = X.z[i] + beta * po;
+          x[i] = xi + alpha * po;
+          const double sum = row_Ap_direct<false>(base, w, lane, ci, X.A, X.z, pold, beta);
+          pnew[i] = pi;
+          X.q[i] = sum;
+          acc.x += pi * sum;
+        }
+      }
+      plast = it & 1;
+      tot = group_sum2(acc, X.part + (nred++ & 1) * nb, lb, nb, sh, X.bar_count, X.bar_gen);
+      ++ep;
+      tot = cross_sum2(X, tot, ep, nrx++, lb, R.flags, &sh1);
+      const double pq = tot.x;
+      if (isnan(pq)) { nan = 1; break; }
+      alpha = rho / pq;
+      // U
+      acc = make_double2(0.0, 0.0);
+      for (int s = gw; s < ns; s += nw) {
+        const int64_t i = (int64_t)s * kSellC + lane;
+        const double ri = X.r[i] - alpha * X.q[i];
+        const double zi = __ldg(X.dinv + i) * ri;
+        X.r[i] = ri;
+        X.z[i] = zi;
+        acc.x += ri * zi;
+        acc.y += zi * zi;
+      }
+      tot = group_sum2(acc, X.part + (nred++ & 1) * nb, lb, nb, sh, X.bar_count, X.bar_gen);
+      ++ep;
+      tot = cross_sum2(X, tot, ep, nrx++, lb, R.flags, &sh1);
+      ++it;
+      zeta = sqrt(tot.y);
+      if (isnan(zeta) || isnan(tot.x)) { nan = 1; break; }
+      if (zeta < R.eps_a || zeta / zref < R.eps_r) { conv = 1; break; }
+      beta = tot.x / rho;
+      rho = tot.x;
+      if (R.rel_mode == 0) zref = zeta;
+    }
+  }
+  if (plast >= 0 && !nan) {
+    const double* __restrict__ pl = plast ? X.p1 : X.p0;
+    for (int s = gw; s < ns; s += nw) {
+      const int64_t i = (int64_t)s * kSellC + lane;
+      x[i] += alpha * pl[i];
+    }
+  }
+  // all CTAs of the group are past their last use of the epoch counter
+  group_barrier(X.bar_count, X.bar_gen, nb);
+  if (lb == 0 && threadIdx.x == 0) {
+    X.epoch[0] = ep;
+    X.epoch[1] = nrx;
+    if (group == 0) {
+      R.stat->iters = it;
+      R.stat->converged = conv;
+      R.stat->znorm = zeta;
+      int32_t* f = R.flags;
+      if (f[5]) {
+        f[0] = 1; f[4] = R.step_tag;
+      } else if (nan) {
+        f[0] = 1; f[1] = 1; f[4] = R.step_tag;
+      } else {
+        f[2] = conv ? 0 : f[2] + 1;
+        if (f[3] > 0 && f[2] >= f[3]) { f[0] = 1; f[4] = R.step_tag; }
+      }
+    }
+  }
+}
+
+int peer_blocks_per_sm(int which) {
+  static int v[2] = {0, 0};
+  if (!v[which]) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v[which], which ? (const void*)rhs_peer_kernel
+                                                                   : (const void*)pcg_peer_kernel,
+                                                  kPeerThreads, 0);
+    if (v[which] < 1) v[which] = 1;
+  }
+  return v[which];
+}
+
+int peer_max_groups() { return kMaxGroups; }
+
+cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, int iX, int iVk, double eps_a,
+                            double eps_r, int32_t max_iters, int32_t rel_mode, tc_step_stat* stat,
+                            int32_t* flags, int32_t step_tag, cudaStream_t s) {
+  if (groups < 1 || groups > kMaxGroups) return cudaErrorInvalidValue;
+  static PeerRun R;  // large: keep it off the stack (host, one launch at a time per process)
+  for (int g = 0; g < groups; ++g) R.parts[g] = parts[g];
+  R.groups = groups; R.iX = iX; R.iVk = iVk; R.eps_a = eps_a; R.eps_r = eps_r;
+  R.max_iters = max_iters; R.rel_mode = rel_mode; R.stat = stat; R.flags = flags; R.step_tag = step_tag;
+  cudaError_t e = cudaMemcpyToSymbolAsync(g_peer_flags, &flags, sizeof(flags), 0, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  void* args[] = {(void*)&R};
+  R.bpg = bpg_rhs;
+  e = cudaLaunchCooperativeKernel((const void*)rhs_peer_kernel, dim3(groups * bpg_rhs), dim3(kPeerThreads),
+                                  args, 0, s);
+  if (e != cudaSuccess) return e;
+  R.bpg = bpg;
+  return cudaLaunchCooperativeKernel((const void*)pcg_peer_kernel, dim3(groups * bpg), dim3(kPeerThreads),
+                                     args, 0, s);
+}
+
+}  // namespace tcb

@@ -133,19 +133,22 @@ def test_step_trajectory_parity(T, model, permute, rcm, variant):
         sim.close()
 
 
+@pytest.mark.parametrize("peer", [1, 0])
 @pytest.mark.parametrize("model,nparts,permute", [("ms", 2, False), ("tt2006", 3, True), ("tt2006", 2, False),
                                                   ("ms", 5, True)])
-def test_partitioned_trajectory_parity(T, model, nparts, permute):
+def test_partitioned_trajectory_parity(T, model, nparts, permute, peer):
     """Row-block partitions on one GPU (split-phase PCG, device-copy halos,
     in-order scalar sums): same trajectory as the oracle and as 1 partition."""
     xyz, tets, region, fib, cond, stims = _slab_case(model, 25, 9, 5, permute=permute, seed=2 if permute else 0)
     dt = 0.05
     ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0), stims)
-    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, partitions=nparts, check_every=3)
+    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, partitions=nparts, check_every=3,
+                              peer=peer)
     sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
     try:
         info = T.tc_matrix_info(sim.ctx)
         assert info["partitions"] == nparts and info["ghosts"] > 0
+        assert info["path"] == ("peer" if peer else "split")
         for k in range(80):
             st = sim.step(1)
             rep = ref.step()
@@ -161,12 +164,13 @@ def test_partitioned_trajectory_parity(T, model, nparts, permute):
         sim.close()
 
 
-def test_nccl_path_world1_parity(T):
-    """The NCCL split-phase path (communicator of one rank) against the oracle."""
+@pytest.mark.parametrize("peer", [1, 0])
+def test_nccl_path_world1_parity(T, peer):
+    """The NCCL paths (communicator of one rank; peer kernel or split phases) against the oracle."""
     xyz, tets, region, fib, cond, stims = _slab_case("tt2006", 21, 8, 5)
     dt = 0.05
     ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, abs_tol=1e-8, rel_tol=0.0), stims)
-    cfg = T.tc_config_default(dt=dt, abs_tol=1e-8, rel_tol=0.0)
+    cfg = T.tc_config_default(dt=dt, abs_tol=1e-8, rel_tol=0.0, peer=peer)
     try:
         uid = T.tc_nccl_unique_id()
     except T.TcError:

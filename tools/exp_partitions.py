@@ -8,9 +8,13 @@ dims = tuple(int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "200,125,100
 xyz, tets = G.kuhn_box(*dims, 0.1)
 stim = (G.nodes_in_box(xyz, (0, -1, -1), (0.3, 1e9, 1e9)), 0.0, 2.0, 50.0)
 E = len(tets)
-for parts, chk in [(1, 4), (2, 4), (2, 1), (2, 16), (4, 4)]:
-    cfg = T.tc_config_default(dt=0.01, model="ms", partitions=parts, check_every=chk)
-    sim = T.Monodomain(xyz, tets, None, None, {0: (0.1334177, 0.0173515)}, cfg, [stim])
+for parts, chk, peer, comm in [(1, 4, 1, None), (1, 4, 1, "nccl"), (1, 4, 0, "nccl"), (2, 4, 1, None),
+                               (2, 4, 0, None), (4, 4, 1, None)]:
+    if comm:
+        comm = (0, 1, T.tc_nccl_unique_id())
+    cfg = T.tc_config_default(dt=0.01, model="ms", partitions=parts, check_every=chk, peer=peer)
+    sim = T.Monodomain(xyz, tets, None, None, {0: (0.1334177, 0.0173515)}, cfg, [stim], comm=comm)
+    print(T.tc_matrix_info(sim.ctx)["path"], "comm" if comm else "", end=" ")
     sim.step(300)
     torch.cuda.synchronize()
     T.tc_profile(sim.ctx, True); T.tc_profile_read(sim.ctx, True)
