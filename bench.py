@@ -43,6 +43,9 @@ WORKLOADS = {
     # configs[2]: N-version dx = 0.1 mm (~442k nodes), TT2006 epi, dt 0.01
     "nversion_dx0.1_tt": dict(cfg=2, dims=(201, 71, 31), dx=0.1, model="tt2006", dt=0.01,
                               stim="corner", preroll=500, sample_dims=(48, 48, 31)),
+    # configs[3]: synthetic biventricular-sized tet mesh (~3M nodes), rotating fibres, TT2006
+    "biv3M_tt": dict(cfg=3, dims=None, h=0.33, dx=0.33, model="tt2006", dt=0.01, stim="biv",
+                     preroll=500, sample_h=1.2),
     # configs[0]: N-version dx = 0.5 mm (4305 nodes), TT2006 epi, dt 0.05, 40 ms
     "nversion_dx0.5_tt": dict(cfg=0, dims=(41, 15, 7), dx=0.5, model="tt2006", dt=0.05,
                               stim="corner", preroll=0, sample_dims=(41, 15, 7)),
@@ -56,13 +59,18 @@ def dist_env():
 
 
 def make_inputs(w, dims=None):
+    """-> xyz, tets, stimuli, region, fibre (region/fibre None = single region, (1,0,0))."""
+    if w["stim"] == "biv":
+        m = G.biv(dims if dims is not None else w["h"])
+        stims = [(nodes, 0.0, 2.0, 50.0) for nodes in G.biv_stimuli(m)]
+        return m["xyz"], m["tets"], stims, m["region"], m["fibre"]
     nx, ny, nz = dims or w["dims"]
     xyz, tets = G.kuhn_box(nx, ny, nz, w["dx"])
     if w["stim"] == "face":      # planar stimulus on x <= 0.3 mm (SURVEY 8d, C5 / C*)
         nodes = G.nodes_in_box(xyz, (0, -1, -1), (0.3, 1e9, 1e9))
     else:                        # N-version corner box <= 1.5 mm (reading N2)
         nodes = G.nodes_in_box(xyz, (0, 0, 0), (1.5, 1.5, 1.5))
-    return xyz, tets, [(nodes, 0.0, 2.0, 50.0)]
+    return xyz, tets, [(nodes, 0.0, 2.0, 50.0)], None, None
 
 
 def kuhn_nnz(nx, ny, nz):
@@ -127,10 +135,12 @@ def oracle_sample(w, max_seconds=20.0):
     """The CPU oracle (as it stands, single thread) on a bounded sample of the workload:
     same dx, dt, model, stimulus style and tolerances on a smaller slab."""
     import oracle as O
-    xyz, tets, stims = make_inputs(w, w["sample_dims"])
+    sample = w.get("sample_h") if w["stim"] == "biv" else w["sample_dims"]
+    xyz, tets, stims, region, fibre = make_inputs(w, sample)
     E = tets.shape[0]
     cfg = O.Config(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5, max_iters=100)
-    sim = O.Monodomain(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: SIGMA}, cfg,
+    sim = O.Monodomain(xyz, tets, np.zeros(E, np.int32) if region is None else region,
+                       G.uniform_fibres(E) if fibre is None else fibre, {0: SIGMA, 1: SIGMA}, cfg,
                        [O.Stimulus(*s) for s in stims])
     n = xyz.shape[0]
     steps, t0 = 0, time.perf_counter()
@@ -142,8 +152,9 @@ def oracle_sample(w, max_seconds=20.0):
             break
     iters = float(np.mean([r.iters for r in sim.reports]))
     return dict(value=n * steps / el, unit="node-steps/s", cores=1, kind="oracle",
-                sample=f"{w['sample_dims'][0]}x{w['sample_dims'][1]}x{w['sample_dims'][2]} nodes "
-                       f"({n} nodes, same dx/dt/model/stimulus), first {steps} steps from rest, "
+                sample=(f"BiV recipe at h={sample} mm" if w["stim"] == "biv" else
+                        f"{sample[0]}x{sample[1]}x{sample[2]} grid") +
+                       f" ({n} nodes, same dx/dt/model/stimulus style), first {steps} steps from rest, "
                        f"{el:.1f} s single-thread, mean PCG iters {iters:.1f}")
 
 
@@ -217,14 +228,14 @@ def main():
 
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
-    xyz, tets, stims = make_inputs(w)
+    xyz, tets, stims, region, fibre = make_inputs(w)
     E = tets.shape[0]
     n = xyz.shape[0]
     cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5,
                               max_iters=100, use_rcm=0 if args.no_rcm else 1,
                               pcg_variant=args.pcg_variant, partitions=args.partitions)
     t0 = time.perf_counter()
-    sim = T.Monodomain(xyz, tets, np.zeros(E, np.int32), None, {0: SIGMA}, cfg, stims,
+    sim = T.Monodomain(xyz, tets, region, fibre, {0: SIGMA, 1: SIGMA}, cfg, stims,
                        device=local, stream=stream.cuda_stream)
     t_setup = time.perf_counter() - t0
     del tets
@@ -301,7 +312,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": args.workload, "baseline_config": w["cfg"], "nodes": n, "nnz": nnz,
                    "tets": int(E), "model": w["model"], "dt_ms": w["dt"], "dx_mm": w["dx"],
-                   "grid": list(w["dims"]), "tol": "abs=rel=1e-5, max 100 (P:316)",
+                   "grid": list(w["dims"]) if w["dims"] else f"BiV h={w['h']} mm", "tol": "abs=rel=1e-5, max 100 (P:316)",
                    "rcm": not args.no_rcm, "preroll_steps": preroll, "pcg_variant": args.pcg_variant,
                    "wide_slices": info.get("wide_slices"),
                    "l2": f"inputs larger than L2 (A+K+col {(20 * info['nnz_pad']) / 1e9:.2f} GB >> 126 MB)"

@@ -1,8 +1,9 @@
 """bench_dist.py -- the N>1 leg of bench.py (one process per GPU under torchrun).
 
 Every rank passes the same global mesh to the library, which cuts the RCM-ordered
-system into WORLD_SIZE row blocks (rank r owns block r) and runs the
-split-phase PCG with NCCL halos and all-reduces.
+system into WORLD_SIZE row blocks (rank r owns block r) and runs the persistent
+peer-memory PCG (halos and reductions over NVLink by the kernel itself), or the
+split-phase PCG with NCCL when peer mappings are unavailable.
 Timing: barrier + cudaSynchronize on both sides, CUDA events on the library's
 stream, max over ranks; rank 0 prints the JSON line.  scaling = "strong"
 (the global workload is fixed as N grows)."""
@@ -28,13 +29,13 @@ def main(args, w):
     uid = [T.tc_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     stream = torch.cuda.current_stream()
-    xyz, tets, stims = bench.make_inputs(w)
+    xyz, tets, stims, region, fibre = bench.make_inputs(w)
     E = tets.shape[0]
     n = xyz.shape[0]
     cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=bench.CHI, cm=bench.CM, abs_tol=1e-5,
                               rel_tol=1e-5, max_iters=100, use_rcm=0 if args.no_rcm else 1)
     t0 = time.perf_counter()
-    sim = T.Monodomain(xyz, tets, np.zeros(E, np.int32), None, {0: bench.SIGMA}, cfg, stims,
+    sim = T.Monodomain(xyz, tets, region, fibre, {0: bench.SIGMA, 1: bench.SIGMA}, cfg, stims,
                        device=local, stream=stream.cuda_stream, comm=(rank, world, uid[0]))
     t_setup = time.perf_counter() - t0
     del tets
@@ -93,14 +94,16 @@ def main(args, w):
             "data": "synthetic",
             "config": {"workload": args.workload, "baseline_config": w["cfg"], "nodes": n,
                        "nnz": int(info["nnz"]), "model": w["model"], "dt_ms": w["dt"],
-                       "dx_mm": w["dx"], "grid": list(w["dims"]), "rcm": not args.no_rcm,
-                       "preroll_steps": preroll, "parallelism": f"row blocks x{world} (NCCL)",
+                       "dx_mm": w["dx"], "grid": list(w["dims"]) if w["dims"] else f"BiV h={w['h']} mm",
+                       "rcm": not args.no_rcm,
+                       "preroll_steps": preroll, "parallelism": f"row blocks x{world} ({info['path']} PCG: "
+                                      + ("NVLink peer memory" if info["path"] == "peer" else "NCCL") + ")",
                        "ghosts_rank0": int(info["ghosts"]),
                        "l2": "inputs larger than L2" if n > 1_000_000 else "small problem"},
             "sim_ms_per_wall_s": args.steps * w["dt"] / (ms / 1e3),
             "pcg_iters_per_step": iters / args.steps,
             "setup_s": t_setup,
-            "roofline": {"kernel": "split-phase PCG (rank 0 rows)", "bound": "hbm",
+            "roofline": {"kernel": f"{info['path']} PCG path (rank 0 rows)", "bound": "hbm",
                          "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"] if achieved else None,
                          "traffic": None, "peak_source": which,

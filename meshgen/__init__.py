@@ -155,3 +155,95 @@ def random_spd_csr(n: int, density=0.2, seed=SEED):
     rowptr = np.zeros(n + 1, np.int64)
     np.add.at(rowptr, rows + 1, 1)
     return np.cumsum(rowptr).astype(np.int32), cols.astype(np.int32), Adense[rows, cols].copy(), Adense
+
+
+# --------------------------------------------------------------------------
+# Synthetic biventricular-sized mesh (BASELINE configs[3]; recipe in DESIGN.md)
+# --------------------------------------------------------------------------
+LV_ENDO, LV_EPI = (25.0, 25.0, 45.0), (35.0, 35.0, 52.0)
+RV_ENDO, RV_EPI = (40.0, 28.0, 40.0), (46.0, 33.0, 46.0)
+RV_SHIFT = 18.0
+
+
+def _inside(p, ax, cx=0.0):
+    return ((p[..., 0] - cx) / ax[0]) ** 2 + (p[..., 1] / ax[1]) ** 2 + (p[..., 2] / ax[2]) ** 2 <= 1.0
+
+
+def _radial(p, ax, cx=0.0):
+    return np.sqrt(((p[..., 0] - cx) / ax[0]) ** 2 + (p[..., 1] / ax[1]) ** 2 + (p[..., 2] / ax[2]) ** 2)
+
+
+def biv(h: float, seed=SEED, jitter_frac=0.15, permute=True):
+    """Voxelised union of two truncated ellipsoidal shells (z <= 0), Kuhn-split.
+
+    Returns dict(xyz, tets, region (0 LV, 1 RV), fibre, endo_nodes).  Fibres:
+    helix angle 60 deg (endo) -> -60 deg (epi) about the local circumferential
+    direction, rotated towards the apex-base axis (rule-based, per element)."""
+    lo = np.array([-36.0, -36.0, -53.0])
+    hi = np.array([RV_SHIFT + 47.0, 36.0, 0.0])
+    nc = np.ceil((hi - lo) / h).astype(int)
+    ci = np.stack(np.meshgrid(*(np.arange(m) for m in nc), indexing="ij"), -1).reshape(-1, 3)
+    cen = lo + (ci + 0.5) * h
+    lv = _inside(cen, LV_EPI) & ~_inside(cen, LV_ENDO)
+    rv = _inside(cen, RV_EPI, RV_SHIFT) & ~_inside(cen, RV_ENDO, RV_SHIFT) & ~_inside(cen, LV_ENDO)
+    keep = (lv | rv) & (cen[:, 2] <= 0.0)
+    cells = ci[keep]
+    cell_rv = (rv & ~lv)[keep]
+    # nodes: corners of kept cells, compact numbering
+    nx, ny, nz = nc + 1
+    gid = lambda ijk: ijk[..., 0] + nx * (ijk[..., 1] + ny * ijk[..., 2])
+    corners = cells[:, None, :] + _KUHN_POS.reshape(-1, 3)[None, :, :]          # (C, 24, 3)
+    g = gid(corners).reshape(-1)
+    uniq, inv = np.unique(g, return_inverse=True)
+    tets = inv.reshape(-1, 6, 4).reshape(-1, 4).astype(np.int32)
+    region = np.repeat(cell_rv.astype(np.int32), 6)
+    k = uniq // (nx * ny)
+    j = (uniq // nx) % ny
+    i = uniq % nx
+    xyz = lo + np.stack([i, j, k], 1) * h
+    # jitter nodes, rejecting moves that flatten a tet below 0.2 of its volume
+    rng = np.random.default_rng(seed)
+    d = rng.uniform(-jitter_frac * h, jitter_frac * h, size=xyz.shape)
+    v0 = h ** 3 / 6.0
+    for _ in range(20):
+        x = xyz + d
+        p = x[tets]
+        vol = np.abs(np.einsum("ij,ij->i", p[:, 1] - p[:, 0], np.cross(p[:, 2] - p[:, 0], p[:, 3] - p[:, 0]))) / 6
+        bad = vol < 0.2 * v0
+        if not bad.any():
+            break
+        d[np.unique(tets[bad])] = 0.0
+    xyz = xyz + d
+    # rule-based fibres from the element centroid
+    c = xyz[tets].mean(1)
+    isr = region == 1
+    cx = np.where(isr, RV_SHIFT, 0.0)
+    rad = np.where(isr, _radial(c, RV_ENDO, RV_SHIFT), _radial(c, LV_ENDO))
+    rad_epi = np.where(isr, _radial(c, RV_EPI, RV_SHIFT), _radial(c, LV_EPI))
+    # transmural coordinate: 0 on the endo ellipsoid, 1 on the epi ellipsoid
+    e = np.clip((rad - 1.0) / np.maximum(rad - rad_epi, 1e-12), 0.0, 1.0)
+    ang = np.deg2rad(60.0 - 120.0 * e)
+    circ = np.stack([-c[:, 1], c[:, 0] - cx, np.zeros(len(c))], 1)
+    circ /= np.maximum(np.linalg.norm(circ, axis=1, keepdims=True), 1e-12)
+    fib = np.cos(ang)[:, None] * circ + np.sin(ang)[:, None] * np.array([0.0, 0.0, 1.0])
+    # endocardial nodes of the LV (for stimulus sites)
+    endo = np.nonzero(_radial(xyz, LV_ENDO) < 1.0 + 1.5 * h / LV_ENDO[0])[0].astype(np.int32)
+    out = dict(xyz=xyz, tets=tets, region=region, fibre=fib, endo_nodes=endo)
+    if permute:
+        xyz2, tets2, perm = permute_nodes(xyz, tets, seed=seed + 1)
+        invp = np.empty(len(perm), np.int64)
+        invp[perm] = np.arange(len(perm))
+        out.update(xyz=xyz2, tets=tets2, endo_nodes=invp[endo].astype(np.int32))
+    return out
+
+
+def biv_stimuli(mesh, n_sites=5, radius=1.5, seed=SEED):
+    """Five spheres of radius 1.5 mm around seeded LV endocardial nodes (P:320 'five initial stimuli')."""
+    rng = np.random.default_rng(seed + 7)
+    xyz = mesh["xyz"]
+    sites = rng.choice(mesh["endo_nodes"], size=n_sites, replace=False)
+    out = []
+    for s in sites:
+        nodes = np.nonzero(np.sum((xyz - xyz[s]) ** 2, axis=1) <= radius ** 2)[0].astype(np.int32)
+        out.append(nodes)
+    return out

@@ -187,6 +187,29 @@ def test_nccl_path_world1_parity(T, peer):
         sim.close()
 
 
+@pytest.mark.parametrize("peer_parts", [1, 3])
+def test_biv_mesh_trajectory_parity(T, peer_parts):
+    """Synthetic BiV recipe (configs[3]) at coarse h: unstructured (jittered, randomly
+    relabelled) mesh, two regions, rule-based rotating fibres, five stimulus spheres."""
+    m = G.biv(2.5)
+    stims = [O.Stimulus(nodes, 0.0, 2.0, 50.0) for nodes in G.biv_stimuli(m, radius=3.0)]
+    cond = {0: (0.1334177, 0.0173515), 1: (0.1334177, 0.0173515)}
+    dt = 0.05
+    ref = O.Monodomain(m["xyz"], m["tets"], m["region"], m["fibre"], cond,
+                       O.Config(dt=dt, abs_tol=1e-8, rel_tol=0.0), stims)
+    cfg = T.tc_config_default(dt=dt, abs_tol=1e-8, rel_tol=0.0, partitions=peer_parts)
+    sim = T.Monodomain(m["xyz"], m["tets"], m["region"], m["fibre"], cond, cfg, stims)
+    try:
+        for k in range(60):
+            sim.step(1)
+            ref.step()
+            assert np.linalg.norm(sim.V - ref.Vk) / np.linalg.norm(ref.Vk) <= 1e-8, k
+        lat, _ = sim.activation()
+        assert np.abs(lat - ref.lat).max() <= dt + 1e-12
+    finally:
+        sim.close()
+
+
 def test_state_injection_one_step(T):
     """One step from an injected mid-upstroke state: GPU == oracle (any size path)."""
     xyz, tets, region, fib, cond, stims = _slab_case("tt2006", 31, 12, 7, 0.5, permute=True, seed=5)
