@@ -19,7 +19,10 @@ namespace tcb {
 // Padding slots point at the row itself with value 0.
 // ---------------------------------------------------------------------------
 constexpr int kSellC = 32;
-constexpr int kCgThreads = 256;           // 8 warps per CTA
+#ifndef TCB_CG_THREADS
+#define TCB_CG_THREADS 512
+#endif
+constexpr int kCgThreads = TCB_CG_THREADS;  // threads per CTA of the PCG kernels (16 warps; measured best of 256/512/1024)
 constexpr int kCgWarps = kCgThreads / 32;
 
 struct HostSell {

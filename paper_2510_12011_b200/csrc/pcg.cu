@@ -27,7 +27,7 @@ namespace tcb {
 
 // ------------------------------------------------------------------ kernels
 // VAR 0: direct loads, int32 indices (default), 1: TMA-staged, 2: direct loads + 16-bit indices
-#define TCB_MINB(VAR) ((VAR) == 1 ? 2 : TCB_DIRECT_MINB)
+#define TCB_MINB(VAR) ((VAR) == 1 ? (512 / TCB_CG_THREADS > 0 ? 512 / TCB_CG_THREADS : 1) : TCB_DIRECT_MINB)
 
 __device__ __forceinline__ void setup_pipe(SlicePipe& P, char* smem, uint64_t* bars, int warp, int lane) {
   P.buf = smem + warp * kWarpSmem;
@@ -45,7 +45,7 @@ __device__ __forceinline__ void setup_pipe(SlicePipe& P, char* smem, uint64_t* b
 // DESIGN.md "RHS"), z_0 = r_0 / diag(A), and per-CTA partials of r.z, z.z.
 // Same grid as the PCG kernel that consumes the partials.
 template <int MODE, int VAR>
-__global__ void __launch_bounds__(kCgThreads, VAR == 1 ? 2 : 4) rhs_kernel(CgArgs a) {
+__global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : (1024 / TCB_CG_THREADS > 0 ? 1024 / TCB_CG_THREADS : 1)) rhs_kernel(CgArgs a) {
   constexpr bool TMA = VAR == 1;
   constexpr bool COMP = VAR == 2;
   extern __shared__ __align__(128) char smem[];

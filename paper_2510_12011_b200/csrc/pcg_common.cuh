@@ -14,14 +14,14 @@ namespace tcb {
 
 
 #ifndef TCB_DIRECT_MINB
-#define TCB_DIRECT_MINB 8   // CTAs/SM of the direct variant: 8 -> 32 registers, 64 warps/SM
+#define TCB_DIRECT_MINB (2048 / TCB_CG_THREADS)  // CTAs/SM of the direct variant: 32 registers, 64 warps/SM
 #endif
 constexpr int kWMax = 16;                               // widest TMA-staged slice
 constexpr int kValBytes = kWMax * kSellC * 8;           // 4 KB of values
 constexpr int kStageBytes = kWMax * kSellC * (8 + 4);   // + 2 KB of column indices
 constexpr int kStages = 2;
 constexpr int kWarpSmem = kStages * kStageBytes;        // 12 KB per warp
-constexpr int kCgSmem = kCgWarps * kWarpSmem;           // 96 KB per CTA (2 CTAs / SM)
+constexpr int kCgSmem = kCgWarps * kWarpSmem;           // 12 KB per warp: 16 warps per SM
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -78,8 +78,8 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* sh) {
   if (lane == 0) sh[warp] = v;
   __syncthreads();
   double2 t = make_double2(0.0, 0.0);
-  if (lane < kCgWarps) t = sh[lane];
-  t = warp_sum2(t);  // every warp reduces the 8 values identically
+  if (lane < (int)(blockDim.x >> 5)) t = sh[lane];
+  t = warp_sum2(t);  // every warp reduces the per-warp values identically
   return t;
 }
 

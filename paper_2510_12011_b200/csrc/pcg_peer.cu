@@ -25,6 +25,7 @@
 namespace tcb {
 
 constexpr int kPeerThreads = 256;
+constexpr int kPeerWarps = kPeerThreads / 32;
 constexpr long long kWaitCycles = 4000000000LL;  // ~2 s at 1.9 GHz
 
 constexpr int kMaxGroups = 8;  // partitions of one GPU in a peer launch (kernel-parameter space)
@@ -179,7 +180,7 @@ __device__ __forceinline__ void halo_wait(const XPart& X, unsigned long long epo
 // sums rho_0, ||z_0||^2 -> X.red0.  Own launch (64 registers); cooperative so
 // that every group's CTAs are resident while they wait for their neighbours.
 __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_constant__ PeerRun R) {
-  __shared__ double2 sh[kCgWarps];
+  __shared__ double2 sh[kPeerWarps];
   __shared__ double2 sh1;
   const int group = blockIdx.x / R.bpg;
   const int lb = blockIdx.x - group * R.bpg;
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_
   const XPart& X = R.parts[group];
   if (R.flags[0]) return;
   const int lane = threadIdx.x & 31;
-  const int gw = lb * kCgWarps + (threadIdx.x >> 5), nw = nb * kCgWarps;
+  const int gw = lb * kPeerWarps + (threadIdx.x >> 5), nw = nb * kPeerWarps;
   unsigned long long ep = X.epoch[0];
   unsigned long long nrx = X.epoch[1];
   ++ep;
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_
 
 // Algorithm 1's loop on the partitioned system (after rhs_peer_kernel).
 __global__ void __launch_bounds__(kPeerThreads, 8) pcg_peer_kernel(const __grid_constant__ PeerRun R) {
-  __shared__ double2 sh[kCgWarps];
+  __shared__ double2 sh[kPeerWarps];
   __shared__ double2 sh1;
   const int group = blockIdx.x / R.bpg;
   const int lb = blockIdx.x - group * R.bpg;  // CTA index inside the group
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kPeerThreads, 8) pcg_peer_kernel(const __grid_
   const XPart& X = R.parts[group];
   if (R.flags[0]) return;  // aborted earlier: uniform over the launch
   const int lane = threadIdx.x & 31;
-  const int gw = lb * kCgWarps + (threadIdx.x >> 5), nw = nb * kCgWarps;
+  const int gw = lb * kPeerWarps + (threadIdx.x >> 5), nw = nb * kPeerWarps;
   const int ns = X.nslices;
   double* __restrict__ x = X.V[R.iX];
   unsigned long long ep = X.epoch[0];   // epoch counter (halos and reductions), same in every CTA

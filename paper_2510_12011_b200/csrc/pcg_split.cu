@@ -19,6 +19,7 @@
 namespace tcb {
 
 constexpr int kSplitThreads = 256;
+constexpr int kSplitWarps = kSplitThreads / 32;
 
 // CTA partial -> part[blockIdx]; the last CTA to finish sums all partials in
 // index order (deterministic) into *out and re-arms the ticket.
@@ -50,10 +51,10 @@ __device__ __forceinline__ void reduce_to_rank(double2 acc, double2* part, unsig
 
 template <int MODE>
 __global__ void __launch_bounds__(kSplitThreads, 4) split_rhs_kernel(SplitArgs a) {
-  __shared__ double2 sh[kCgWarps];
+  __shared__ double2 sh[kSplitWarps];
   if (a.flags[0]) return;
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kCgWarps + (threadIdx.x >> 5), nw = gridDim.x * kCgWarps;
+  const int gw = blockIdx.x * kSplitWarps + (threadIdx.x >> 5), nw = gridDim.x * kSplitWarps;
   double2 acc = make_double2(0.0, 0.0);
   for (int s = gw; s < a.nslices; s += nw) {
     const int64_t base = __ldg(a.slice_ptr + s);
@@ -108,11 +109,11 @@ __global__ void pack_gather_kernel(int64_t m, const int32_t* __restrict__ idx,
 }
 
 __global__ void __launch_bounds__(kSplitThreads, 8) split_S_kernel(SplitArgs a) {
-  __shared__ double2 sh[kCgWarps];
+  __shared__ double2 sh[kSplitWarps];
   const Scalars s = *a.sc;
   if (s.done) return;
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kCgWarps + (threadIdx.x >> 5), nw = gridDim.x * kCgWarps;
+  const int gw = blockIdx.x * kSplitWarps + (threadIdx.x >> 5), nw = gridDim.x * kSplitWarps;
   double* __restrict__ pnew = (s.it & 1) ? a.p1 : a.p0;
   const double* __restrict__ pold = (s.it & 1) ? a.p0 : a.p1;
   const bool first = s.it == 0;
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(kSplitThreads, 8) split_S_kernel(SplitArgs a) 
 }
 
 __global__ void __launch_bounds__(kSplitThreads, 8) split_U_kernel(SplitArgs a) {
-  __shared__ double2 sh[kCgWarps];
+  __shared__ double2 sh[kSplitWarps];
   const Scalars s = *a.sc;
   if (s.done) return;
   const double alpha = s.rho / a.red[1].x;   // alpha_k = rho_k / p.q (all-reduced)
@@ -237,7 +238,7 @@ int split_grid(int32_t nslices) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, split_S_kernel, kSplitThreads, 0);
     if (per_sm < 1) per_sm = 1;
   }
-  int need = (nslices + kCgWarps - 1) / kCgWarps;
+  int need = (nslices + kSplitWarps - 1) / kSplitWarps;
   int cap = sm_count_split() * per_sm;
   return need < 1 ? 1 : (need < cap ? need : cap);
 }
