@@ -330,19 +330,23 @@ static TTDerived tt_derived(const TTParams& P) {
 }
 
 // ------------------------------------------------------------------ Mitchell-Schaeffer
-__global__ void ionic_ms_kernel(IonArgs a, MSParams P) {
+struct MSDerived {  // reciprocals of the time constants (host-computed)
+  double span, inv_open, inv_close, inv_in, inv_out;
+};
+
+__global__ void ionic_ms_kernel(IonArgs a, MSParams P, MSDerived D) {
   if (a.flags[0]) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   const double V = a.Vk[i];
   const double Vp = a.has_prev ? a.Vkm1[i] : V;
   if (a.do_lat) activation_update(a, i, V, Vp);
-  const double span = P.V_max - P.V_min;
-  const double v = (V - P.V_min) / span;
+  // the gate decision uses the same correctly rounded division as the oracle
+  const double v = (V - P.V_min) / D.span;
   double h = a.U[i];
-  h = (v < P.v_gate) ? h + a.dt * ((1.0 - h) / P.tau_open) : h + a.dt * (-h / P.tau_close);
+  h = (v < P.v_gate) ? h + a.dt * ((1.0 - h) * D.inv_open) : h + a.dt * (-h * D.inv_close);
   a.U[i] = h;
-  const double In = -span * (h * v * v * (1.0 - v) / P.tau_in - v / P.tau_out);
+  const double In = -D.span * (h * v * v * (1.0 - v) * D.inv_in - v * D.inv_out);
   write_rhs(a, i, V, Vp, In);
 }
 
@@ -409,7 +413,9 @@ cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s)
 }
 cudaError_t launch_ionic_ms(const IonArgs& a, const MSParams& p, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  ionic_ms_kernel<<<nblk(a.n, 256), 256, 0, s>>>(a, p);
+  const MSDerived D{p.V_max - p.V_min, 1.0 / p.tau_open, 1.0 / p.tau_close, 1.0 / p.tau_in,
+                    1.0 / p.tau_out};
+  ionic_ms_kernel<<<nblk(a.n, 256), 256, 0, s>>>(a, p, D);
   return cudaGetLastError();
 }
 cudaError_t launch_ionic_mms(const IonArgs& a, const MMSParams& p, cudaStream_t s) {
