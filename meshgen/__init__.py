@@ -247,3 +247,69 @@ def biv_stimuli(mesh, n_sites=5, radius=1.5, seed=SEED):
         nodes = np.nonzero(np.sum((xyz - xyz[s]) ** 2, axis=1) <= radius ** 2)[0].astype(np.int32)
         out.append(nodes)
     return out
+
+
+# --------------------------------------------------------------------------
+# Surface (triangle) meshes embedded in 3-D ("surface meshes")
+# --------------------------------------------------------------------------
+def tri_grid(nx: int, ny: int, dx: float, origin=(0.0, 0.0, 0.0)):
+    """nx*ny-node planar grid in z = origin[2], each square cut into 2 triangles
+    along its (0,0)-(1,1) diagonal.  Returns xyz (n,3), tris (E,3)."""
+    i = np.arange(nx)
+    j = np.arange(ny)
+    J, I = np.meshgrid(j, i, indexing="ij")
+    xyz = np.zeros((nx * ny, 3))
+    xyz[:, 0] = I.reshape(-1) * dx + origin[0]
+    xyz[:, 1] = J.reshape(-1) * dx + origin[1]
+    xyz[:, 2] = origin[2]
+    ci, cj = np.meshgrid(np.arange(nx - 1), np.arange(ny - 1), indexing="xy")
+    v00 = (ci + nx * cj).reshape(-1)
+    v10, v01, v11 = v00 + 1, v00 + nx, v00 + nx + 1
+    tris = np.concatenate([np.stack([v00, v10, v11], 1), np.stack([v00, v11, v01], 1)])
+    return xyz, tris.astype(np.int32)
+
+
+def unit_square(N: int):
+    """[0,1]^2 (z = 0) with N cells per side, 2 triangles per cell (the MMS domain of P:250)."""
+    return tri_grid(N + 1, N + 1, 1.0 / N)
+
+
+def rotate(xyz, seed=SEED):
+    """A seeded rigid rotation of the coordinates (surface meshes must not care)."""
+    q, _ = np.linalg.qr(np.random.default_rng(seed).normal(size=(3, 3)))
+    if np.linalg.det(q) < 0:
+        q[:, 0] = -q[:, 0]
+    return xyz @ q.T, q
+
+
+def sphere(level: int, radius: float = 10.0):
+    """Icosphere surface (subdivided icosahedron, `level` 2x refinements) of the
+    given radius (a closed surface: no boundary)."""
+    t = (1.0 + 5 ** 0.5) / 2.0
+    v = np.array([[-1, t, 0], [1, t, 0], [-1, -t, 0], [1, -t, 0], [0, -1, t], [0, 1, t], [0, -1, -t],
+                  [0, 1, -t], [t, 0, -1], [t, 0, 1], [-t, 0, -1], [-t, 0, 1]], float)
+    f = np.array([[0, 11, 5], [0, 5, 1], [0, 1, 7], [0, 7, 10], [0, 10, 11], [1, 5, 9], [5, 11, 4],
+                  [11, 10, 2], [10, 7, 6], [7, 1, 8], [3, 9, 4], [3, 4, 2], [3, 2, 6], [3, 6, 8],
+                  [3, 8, 9], [4, 9, 5], [2, 4, 11], [6, 2, 10], [8, 6, 7], [9, 8, 1]])
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    for _ in range(level):
+        e = np.sort(np.concatenate([f[:, [0, 1]], f[:, [1, 2]], f[:, [2, 0]]]), axis=1)
+        ue, inv = np.unique(e, axis=0, return_inverse=True)
+        mid = v[ue[:, 0]] + v[ue[:, 1]]
+        mid /= np.linalg.norm(mid, axis=1, keepdims=True)
+        m = len(v) + inv.reshape(3, -1).T            # midpoints of edges 01, 12, 20
+        v = np.concatenate([v, mid])
+        a, b, c = f[:, 0], f[:, 1], f[:, 2]
+        m01, m12, m20 = m[:, 0], m[:, 1], m[:, 2]
+        f = np.concatenate([np.stack([a, m01, m20], 1), np.stack([b, m12, m01], 1),
+                            np.stack([c, m20, m12], 1), np.stack([m01, m12, m20], 1)])
+    return v * radius, f.astype(np.int32)
+
+
+def sphere_fibres(xyz, tris):
+    """Per-triangle fibre along the local 'latitude' direction (tangent, rule-based)."""
+    c = xyz[tris].mean(1)
+    f = np.stack([-c[:, 1], c[:, 0], np.zeros(len(c))], 1)
+    bad = np.linalg.norm(f, axis=1) < 1e-9 * np.linalg.norm(c, axis=1)
+    f[bad] = [1.0, 0.0, 0.0]
+    return f / np.linalg.norm(f, axis=1, keepdims=True)

@@ -54,6 +54,10 @@ def _lib():
         L.or_tet_local.argtypes = [P, P, P, P, P]
         L.or_pattern.argtypes = [I64, I64, P, P, P]
         L.or_pattern.restype = I64
+        L.or_pattern_k.argtypes = [I64, I64, C.c_int, P, P, P]
+        L.or_pattern_k.restype = I64
+        L.or_assemble_k.argtypes = [I64, P, I64, C.c_int, P, P, P, I32, P, P, P, P, P, P, P]
+        L.or_tri_local.argtypes = [P, P, P, P, P]
         L.or_assemble.argtypes = [I64, P, I64, P, P, P, I32, P, P, P, P, P, P, P]
         L.or_rcm.argtypes = [I32, P, P, P]
         L.or_spmv.argtypes = [I32, P, P, P, P, P]
@@ -126,21 +130,32 @@ def tet_local(x, sigma):
     return Me.reshape(4, 4), Ke.reshape(4, 4), float(vol[0])
 
 
+def tri_local(x, sigma):
+    """Local P1 mass / stiffness matrices of one triangle in 3-D; returns (Me, Ke, |e|)."""
+    x = _f64(x).reshape(9)
+    s = _f64(sigma).reshape(9)
+    Me, Ke, area = np.zeros(9), np.zeros(9), np.zeros(1)
+    _check(_lib().or_tri_local(_p(x), _p(s), _p(Me), _p(Ke), _p(area)), "tri_local")
+    return Me.reshape(3, 3), Ke.reshape(3, 3), float(area[0])
+
+
 def pattern(n: int, tets):
-    """CSR pattern of M u K: (i,j) iff an element holds both."""
+    """CSR pattern of M u K: (i,j) iff an element holds both.
+    tets: (E, 4) tetrahedra or (E, 3) surface triangles."""
     tets = _i32(tets)
-    E = tets.shape[0]
+    E, k = tets.shape
     rowptr = np.zeros(n + 1, np.int32)
-    nnz = _lib().or_pattern(n, E, _p(tets), _p(rowptr), None)
+    nnz = _lib().or_pattern_k(n, E, k, _p(tets), _p(rowptr), None)
     if nnz < 0:
         raise OracleError("pattern: connectivity index out of range")
     col = np.zeros(nnz, np.int32)
-    _lib().or_pattern(n, E, _p(tets), _p(rowptr), _p(col))
+    _lib().or_pattern_k(n, E, k, _p(tets), _p(rowptr), _p(col))
     return rowptr, col
 
 
 def assemble(xyz, tets, region, fibre, conductivities: dict):
-    """Global (rowptr, col, M, K) by element-order scatter-add.
+    """Global (rowptr, col, M, K) by element-order scatter-add (S:133-141);
+    tets (E,4) tetrahedra or (E,3) triangles embedded in 3-D.
 
     ``conductivities`` maps region tag -> (sigma_l, sigma_t) in S/m."""
     xyz, tets, region, fibre = _f64(xyz), _i32(tets), _i32(region), _f64(fibre)
@@ -151,9 +166,9 @@ def assemble(xyz, tets, region, fibre, conductivities: dict):
     st = _f64([conductivities[int(i)][1] for i in ids])
     M = np.zeros(col.shape[0])
     K = np.zeros(col.shape[0])
-    _check(_lib().or_assemble(n, _p(xyz), tets.shape[0], _p(tets), _p(region), _p(fibre),
-                              len(ids), _p(ids), _p(sl), _p(st), _p(rowptr), _p(col),
-                              _p(M), _p(K)), "assemble")
+    _check(_lib().or_assemble_k(n, _p(xyz), tets.shape[0], tets.shape[1], _p(tets), _p(region),
+                                _p(fibre), len(ids), _p(ids), _p(sl), _p(st), _p(rowptr),
+                                _p(col), _p(M), _p(K)), "assemble")
     return rowptr, col, M, K
 
 

@@ -93,6 +93,47 @@ int or_tet_local(const double x[12], const double sig[9], double Me[16],
   return OR_OK;
 }
 
+/* Local P1 matrices of one triangle embedded in 3-D (surface meshes, P:68
+ * "triangular or tetrahedral elements"; "gradients are taken in the
+ * element's tangent plane").  With e1 = x1-x0, e2 = x2-x0, n = e1 x e2:
+ *   |e| = |n|/2,  grad phi_1 = (e2 x n)/|n|^2,  grad phi_2 = (n x e1)/|n|^2,
+ *   grad phi_0 = -(grad phi_1 + grad phi_2)   (in-plane vectors)
+ *   M_e[a][b] = |e|/12 (1 + delta_ab)
+ *   K_e[a][b] = |e| grad phi_a^T sigma grad phi_b (only the in-plane part of
+ *   sigma acts, since the gradients lie in the plane).                      */
+int or_tri_local(const double x[9], const double sig[9], double Me[9], double Ke[9],
+                 double* area_out) {
+  double e1[3], e2[3], nv[3];
+  for (int c = 0; c < 3; ++c) {
+    e1[c] = x[3 + c] - x[c];
+    e2[c] = x[6 + c] - x[c];
+  }
+  nv[0] = e1[1] * e2[2] - e1[2] * e2[1];
+  nv[1] = e1[2] * e2[0] - e1[0] * e2[2];
+  nv[2] = e1[0] * e2[1] - e1[1] * e2[0];
+  double nn = nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2];
+  if (nn == 0.0 || !isfinite(nn)) return OR_EDEGEN;
+  double area = sqrt(nn) / 2.0;
+  double G[3][3];
+  G[1][0] = (e2[1] * nv[2] - e2[2] * nv[1]) / nn;
+  G[1][1] = (e2[2] * nv[0] - e2[0] * nv[2]) / nn;
+  G[1][2] = (e2[0] * nv[1] - e2[1] * nv[0]) / nn;
+  G[2][0] = (nv[1] * e1[2] - nv[2] * e1[1]) / nn;
+  G[2][1] = (nv[2] * e1[0] - nv[0] * e1[2]) / nn;
+  G[2][2] = (nv[0] * e1[1] - nv[1] * e1[0]) / nn;
+  for (int c = 0; c < 3; ++c) G[0][c] = -(G[1][c] + G[2][c]);
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      double sum = 0.0;
+      for (int c = 0; c < 3; ++c)
+        for (int d = 0; d < 3; ++d) sum += G[a][c] * sig[3 * c + d] * G[b][d];
+      Ke[3 * a + b] = area * sum;
+      Me[3 * a + b] = area / 12.0 * (a == b ? 2.0 : 1.0);
+    }
+  if (area_out) *area_out = area;
+  return OR_OK;
+}
+
 /* ======================================================================== */
 /* 2. Sparsity pattern and global assembly           */
 /*    Pattern: (i,j) stored iff some element contains both i and j (i==j    */
@@ -106,24 +147,25 @@ static int cmp_i32(const void* a, const void* b) {
 
 /* Two calls: col == NULL -> fills rowptr (n+1) and returns nnz;
  * col != NULL -> fills col (rowptr must be the result of the first call).
+ * k = nodes per element (3 triangles, 4 tetrahedra).
  * Returns -1 on an out-of-range index. */
-int64_t or_pattern(int64_t n, int64_t E, const int32_t* tets, int32_t* rowptr,
-                   int32_t* col) {
-  for (int64_t e = 0; e < 4 * E; ++e)
+int64_t or_pattern_k(int64_t n, int64_t E, int k, const int32_t* tets, int32_t* rowptr,
+                     int32_t* col) {
+  for (int64_t e = 0; e < (int64_t)k * E; ++e)
     if (tets[e] < 0 || tets[e] >= n) return -1;
   /* node -> element incidence */
   int64_t* cnt = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
-  int64_t* inc = (int64_t*)malloc(sizeof(int64_t) * (size_t)(4 * E + 1));
+  int64_t* inc = (int64_t*)malloc(sizeof(int64_t) * (size_t)(k * E + 1));
   int32_t* mark = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
-  int32_t* buf = (int32_t*)malloc(sizeof(int32_t) * (size_t)(4 * E + 4));
+  int32_t* buf = (int32_t*)malloc(sizeof(int32_t) * (size_t)(k * E + 4));
   if (!cnt || !inc || !mark || !buf) { free(cnt); free(inc); free(mark); free(buf); return -1; }
   for (int64_t e = 0; e < E; ++e)
-    for (int a = 0; a < 4; ++a) cnt[tets[4 * e + a] + 1]++;
+    for (int a = 0; a < k; ++a) cnt[tets[k * e + a] + 1]++;
   for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
   int64_t* pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
   memcpy(pos, cnt, sizeof(int64_t) * (size_t)(n + 1));
   for (int64_t e = 0; e < E; ++e)
-    for (int a = 0; a < 4; ++a) inc[pos[tets[4 * e + a]]++] = e;
+    for (int a = 0; a < k; ++a) inc[pos[tets[k * e + a]]++] = e;
   for (int64_t i = 0; i < n; ++i) mark[i] = -1;
   int64_t nnz = 0;
   for (int64_t i = 0; i < n; ++i) {
@@ -132,8 +174,8 @@ int64_t or_pattern(int64_t n, int64_t E, const int32_t* tets, int32_t* rowptr,
     mark[i] = (int32_t)i;
     for (int64_t t = cnt[i]; t < cnt[i + 1]; ++t) {
       int64_t e = inc[t];
-      for (int a = 0; a < 4; ++a) {
-        int32_t j = tets[4 * e + a];
+      for (int a = 0; a < k; ++a) {
+        int32_t j = tets[k * e + a];
         if (mark[j] != (int32_t)i) { mark[j] = (int32_t)i; buf[m++] = j; }
       }
     }
@@ -150,6 +192,10 @@ int64_t or_pattern(int64_t n, int64_t E, const int32_t* tets, int32_t* rowptr,
   return nnz;
 }
 
+int64_t or_pattern(int64_t n, int64_t E, const int32_t* tets, int32_t* rowptr, int32_t* col) {
+  return or_pattern_k(n, E, 4, tets, rowptr, col);
+}
+
 /* slot of column j in row i (binary search over the sorted row), or -1 */
 static int64_t find_slot(const int32_t* rowptr, const int32_t* col, int32_t i, int32_t j) {
   int64_t lo = rowptr[i], hi = (int64_t)rowptr[i + 1] - 1;
@@ -163,12 +209,13 @@ static int64_t find_slot(const int32_t* rowptr, const int32_t* col, int32_t i, i
 
 /* Global M and K by scatter-add in ELEMENT ORDER ("global scatter-add").
  * Region r of element e picks (sigma_l, sigma_t) from the (reg_ids -> sl, st)
- * table; fibre[e] is normalised here. */
-int or_assemble(int64_t n, const double* xyz, int64_t E, const int32_t* tets,
-                const int32_t* region, const double* fibre, int32_t nreg,
-                const int32_t* reg_ids, const double* sig_l, const double* sig_t,
-                const int32_t* rowptr, const int32_t* col, double* Mval,
-                double* Kval) {
+ * table; fibre[e] is normalised here.  k = 4 for
+ * tetrahedra, 3 for surface triangles. */
+int or_assemble_k(int64_t n, const double* xyz, int64_t E, int k, const int32_t* tets,
+                  const int32_t* region, const double* fibre, int32_t nreg,
+                  const int32_t* reg_ids, const double* sig_l, const double* sig_t,
+                  const int32_t* rowptr, const int32_t* col, double* Mval, double* Kval) {
+  if (k != 3 && k != 4) return OR_EINVAL;
   int64_t nnz = rowptr[n];
   for (int64_t s = 0; s < nnz; ++s) { Mval[s] = 0.0; Kval[s] = 0.0; }
   for (int64_t e = 0; e < E; ++e) {
@@ -180,22 +227,31 @@ int or_assemble(int64_t n, const double* xyz, int64_t E, const int32_t* tets,
     if (or_conductivity_tensor(fibre + 3 * e, sig_l[r], sig_t[r], sig) != OR_OK)
       return OR_EFIBRE;
     double xl[12], Me[16], Ke[16];
-    for (int a = 0; a < 4; ++a) {
-      int32_t v = tets[4 * e + a];
+    for (int a = 0; a < k; ++a) {
+      int32_t v = tets[k * e + a];
       if (v < 0 || v >= n) return OR_EINVAL;
       for (int c = 0; c < 3; ++c) xl[3 * a + c] = xyz[3 * (int64_t)v + c];
     }
-    int st = or_tet_local(xl, sig, Me, Ke, NULL);
+    int st = (k == 4) ? or_tet_local(xl, sig, Me, Ke, NULL) : or_tri_local(xl, sig, Me, Ke, NULL);
     if (st != OR_OK) return st;
-    for (int a = 0; a < 4; ++a)
-      for (int b = 0; b < 4; ++b) {
-        int64_t s = find_slot(rowptr, col, tets[4 * e + a], tets[4 * e + b]);
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) {
+        int64_t s = find_slot(rowptr, col, tets[k * e + a], tets[k * e + b]);
         if (s < 0) return OR_EINVAL;
-        Mval[s] += Me[4 * a + b];
-        Kval[s] += Ke[4 * a + b];
+        Mval[s] += Me[k * a + b];
+        Kval[s] += Ke[k * a + b];
       }
   }
   return OR_OK;
+}
+
+int or_assemble(int64_t n, const double* xyz, int64_t E, const int32_t* tets,
+                const int32_t* region, const double* fibre, int32_t nreg,
+                const int32_t* reg_ids, const double* sig_l, const double* sig_t,
+                const int32_t* rowptr, const int32_t* col, double* Mval,
+                double* Kval) {
+  return or_assemble_k(n, xyz, E, 4, tets, region, fibre, nreg, reg_ids, sig_l, sig_t, rowptr,
+                       col, Mval, Kval);
 }
 
 /* ======================================================================== */
