@@ -125,6 +125,17 @@ const char* tc_last_error(const tc_ctx* ctx);
 tc_status tc_set_mesh(tc_ctx* ctx, int64_t n_nodes, const double* xyz, int64_t n_tets,
                       const int32_t* tets, const int32_t* region, const double* fibre);
 
+/* Mesh with `nodes_per_elem` nodes per element ("triangular or tetrahedral
+ * elements"): 4 = tetrahedra (exactly tc_set_mesh), 3 = P1 triangles embedded in
+ * 3-D (surface meshes, e.g. atria or the paper's MMS unit square).  elems:
+ * n_elems*nodes_per_elem node indices.  For triangles the gradients are taken in
+ * the element plane, so a fibre component normal to it does not act;
+ * M_e = |e|/12 (1 + delta_ab).  Same ownership and errors as tc_set_mesh, plus
+ * TC_EINVAL for nodes_per_elem not in {3, 4} and TC_EDEGEN for zero area. */
+tc_status tc_set_mesh_elems(tc_ctx* ctx, int64_t n_nodes, const double* xyz, int64_t n_elems,
+                            int32_t nodes_per_elem, const int32_t* elems, const int32_t* region,
+                            const double* fibre);
+
 /* Region conductivities: sigma = sigma_t I + (sigma_l - sigma_t) f f^T
  * (reading A13).  S/m, both > 0.  Replaces any previous table. */
 tc_status tc_set_conductivity(tc_ctx* ctx, int32_t n_regions, const int32_t* ids,

@@ -17,7 +17,7 @@ from . import _build
 
 __all__ = [
     "TcError", "tc_config", "tc_step_stat", "tc_config_default", "tc_create", "tc_destroy",
-    "tc_last_error", "tc_set_mesh", "tc_set_conductivity", "tc_set_ionic_param",
+    "tc_last_error", "tc_set_mesh", "tc_set_mesh_elems", "tc_set_conductivity", "tc_set_ionic_param",
     "tc_get_ionic_param", "tc_add_stimulus", "tc_set_mms", "tc_assemble", "tc_step",
     "tc_num_nodes", "tc_current_step", "tc_get_v", "tc_get_activation", "tc_state_len",
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
@@ -72,6 +72,7 @@ def _load():
         "tc_destroy": ([P], I32),
         "tc_last_error": ([P], C.c_char_p),
         "tc_set_mesh": ([P, I64, P, I64, P, P, P], I32),
+        "tc_set_mesh_elems": ([P, I64, P, I64, I32, P, P, P], I32),
         "tc_set_conductivity": ([P, I32, P, P, P], I32),
         "tc_set_ionic_param": ([P, C.c_char_p, D], I32),
         "tc_get_ionic_param": ([P, C.c_char_p, P], I32),
@@ -159,9 +160,21 @@ def tc_last_error(ctx) -> str:
 
 
 def tc_set_mesh(ctx, xyz, tets, region=None, fibre=None) -> None:
-    xyz, tets, region, fibre = _f64(xyz), _i32(tets), _i32(region), _f64(fibre)
+    """Tetrahedra (n_tets, 4); a (n_elems, 3) array is routed to tc_set_mesh_elems."""
+    tets = _i32(tets)
+    if tets.ndim == 2 and tets.shape[1] == 3:
+        return tc_set_mesh_elems(ctx, xyz, tets, region, fibre)
+    xyz, region, fibre = _f64(xyz), _i32(region), _f64(fibre)
     _check(ctx, _L.tc_set_mesh(ctx, xyz.shape[0], _ptr(xyz), tets.shape[0], _ptr(tets),
                                _ptr(region), _ptr(fibre)))
+
+
+def tc_set_mesh_elems(ctx, xyz, elems, region=None, fibre=None) -> None:
+    """Elements with 3 (surface triangles) or 4 (tetrahedra) nodes: (n_elems, k)."""
+    xyz, elems, region, fibre = _f64(xyz), _i32(elems), _i32(region), _f64(fibre)
+    k = elems.shape[1] if elems.ndim == 2 else 0
+    _check(ctx, _L.tc_set_mesh_elems(ctx, xyz.shape[0], _ptr(xyz), elems.shape[0], k,
+                                     _ptr(elems), _ptr(region), _ptr(fibre)))
 
 
 def tc_set_conductivity(ctx, ids, sigma_l, sigma_t) -> None:

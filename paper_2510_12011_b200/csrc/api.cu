@@ -80,6 +80,7 @@ struct tc_ctx {
   std::string err;
   // host mesh
   int64_t n = 0, E = 0;
+  int kel = 4;  // nodes per element (4 tetrahedra, 3 surface triangles)
   bool have_mesh = false;
   std::vector<double> xyz, fibre;
   std::vector<int32_t> tets, region;
@@ -280,17 +281,19 @@ tc_status tc_comm_init(tc_ctx* c, int rank, int world, const uint8_t id[128]) {
   return TC_OK;
 }
 
-tc_status tc_set_mesh(tc_ctx* c, int64_t n, const double* xyz, int64_t E, const int32_t* tets,
-                      const int32_t* region, const double* fibre) {
+tc_status tc_set_mesh_elems(tc_ctx* c, int64_t n, const double* xyz, int64_t E, int32_t k,
+                            const int32_t* tets, const int32_t* region, const double* fibre) {
   if (!c) return TC_EINVAL;
   if (c->have_mesh || c->csr_mode) return fail(c, TC_ESTATE, "tc_set_mesh: mesh already set");
+  if (k != 3 && k != 4) return fail(c, TC_EINVAL, "tc_set_mesh_elems: nodes_per_elem must be 3 or 4");
   if (n <= 0 || E <= 0 || !xyz || !tets) return fail(c, TC_EINVAL, "tc_set_mesh: empty mesh");
   if (n >= (1ll << 31) - 64 || 4 * E >= (1ll << 31))
     return fail(c, TC_EINVAL, "tc_set_mesh: mesh too large for int32 indices");
   c->n = n;
   c->E = E;
+  c->kel = k;
   c->xyz.assign(xyz, xyz + 3 * n);
-  c->tets.assign(tets, tets + 4 * E);
+  c->tets.assign(tets, tets + (int64_t)k * E);
   if (region) c->region.assign(region, region + E); else c->region.assign(E, 0);
   if (fibre) {
     c->fibre.assign(fibre, fibre + 3 * E);
@@ -298,13 +301,13 @@ tc_status tc_set_mesh(tc_ctx* c, int64_t n, const double* xyz, int64_t E, const 
       const double* f = fibre + 3 * e;
       double nn = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
       if (!(nn > 0) || !std::isfinite(nn))
-        return fail(c, TC_EINVAL, "tc_set_mesh: zero or non-finite fibre at tet " + std::to_string(e));
+        return fail(c, TC_EINVAL, "tc_set_mesh: zero or non-finite fibre at element " + std::to_string(e));
     }
   } else {
     c->fibre.assign(3 * E, 0.0);
     for (int64_t e = 0; e < E; ++e) c->fibre[3 * e] = 1.0;
   }
-  std::string m = orient_and_validate(n, E, c->tets.data(), c->xyz.data());
+  std::string m = orient_and_validate(n, E, k, c->tets.data(), c->xyz.data());
   if (!m.empty()) {
     tc_status st = m.rfind("EDEGEN", 0) == 0 ? TC_EDEGEN : TC_EINVAL;
     c->tets.clear();
@@ -312,6 +315,11 @@ tc_status tc_set_mesh(tc_ctx* c, int64_t n, const double* xyz, int64_t E, const 
   }
   c->have_mesh = true;
   return TC_OK;
+}
+
+tc_status tc_set_mesh(tc_ctx* c, int64_t n, const double* xyz, int64_t E, const int32_t* tets,
+                      const int32_t* region, const double* fibre) {
+  return tc_set_mesh_elems(c, n, xyz, E, 4, tets, region, fibre);
 }
 
 tc_status tc_set_conductivity(tc_ctx* c, int32_t nr, const int32_t* ids, const double* sl,
@@ -655,8 +663,9 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
   // pattern and RCM, identical on every rank
   std::vector<int64_t> iptr, rp;
   std::vector<int32_t> inc, col;
-  build_incidence(n, E, c->tets.data(), iptr, inc);
-  build_pattern(n, c->tets.data(), iptr, inc, rp, col);
+  const int k = c->kel;
+  build_incidence(n, E, k, c->tets.data(), iptr, inc);
+  build_pattern(n, k, c->tets.data(), iptr, inc, rp, col);
   c->perm.resize(n);
   if (c->cfg.use_rcm) {
     rcm_order(n, rp, col, c->perm);
@@ -670,12 +679,12 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
   permute_csr(n, rp, col, c->perm, c->inv, rp2, col2);
   rp.clear(); rp.shrink_to_fit(); col.clear(); col.shrink_to_fit();
   c->nnz = rp2[n];
-  std::vector<int32_t> tets2(4 * E);
-  for (int64_t t = 0; t < 4 * E; ++t) tets2[t] = c->inv[c->tets[t]];
+  std::vector<int32_t> tets2((int64_t)k * E);
+  for (int64_t t = 0; t < (int64_t)k * E; ++t) tets2[t] = c->inv[c->tets[t]];
   std::vector<double> xyz2(3 * n);
   for (int64_t i = 0; i < n; ++i)
     for (int q = 0; q < 3; ++q) xyz2[3 * i + q] = c->xyz[3 * (int64_t)c->perm[i] + q];
-  build_incidence(n, E, tets2.data(), iptr, inc);
+  build_incidence(n, E, k, tets2.data(), iptr, inc);
   // partitions
   std::vector<PartPlan> plans;
   plan_partitions(n, rp2.data(), col2.data(), c->nparts, plans);
@@ -693,7 +702,7 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
   const size_t nr = c->reg_ids.size();
   bool ok = cudaMalloc(&d_xyz, 3 * n * 8) == cudaSuccess && cudaMalloc(&d_fib, 3 * E * 8) == cudaSuccess &&
             cudaMalloc(&d_sl, nr * 8) == cudaSuccess && cudaMalloc(&d_st, nr * 8) == cudaSuccess &&
-            cudaMalloc(&d_tets, 4 * E * 4) == cudaSuccess && cudaMalloc(&d_ereg, E * 4) == cudaSuccess &&
+            cudaMalloc(&d_tets, (size_t)k * E * 4) == cudaSuccess && cudaMalloc(&d_ereg, E * 4) == cudaSuccess &&
             cudaMalloc(&d_err, 4) == cudaSuccess;
   auto free_setup = [&]() {
     cudaFree(d_xyz); cudaFree(d_fib); cudaFree(d_sl); cudaFree(d_st); cudaFree(d_tets);
@@ -707,7 +716,7 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
   cudaMemcpyAsync(d_fib, c->fibre.data(), 3 * E * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_sl, c->sig_l.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_st, c->sig_t.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
-  cudaMemcpyAsync(d_tets, tets2.data(), 4 * E * 4, cudaMemcpyHostToDevice, c->stream);
+  cudaMemcpyAsync(d_tets, tets2.data(), (size_t)k * E * 4, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_ereg, ereg.data(), E * 4, cudaMemcpyHostToDevice, c->stream);
   cudaMemsetAsync(d_err, 0, 4, c->stream);
   std::vector<uint8_t> dir_all;
@@ -772,7 +781,7 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
     cudaMemcpyAsync(d_rowlen, hs.rowlen.data(), P.n * 4, cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(d_colg, colg.data(), colg.size() * 4, cudaMemcpyHostToDevice, c->stream);
     AsmArgs a{};
-    a.n = (int32_t)P.n; a.row0 = (int32_t)g0; a.xyz = d_xyz; a.tets = d_tets; a.ereg = d_ereg;
+    a.n = (int32_t)P.n; a.row0 = (int32_t)g0; a.k = k; a.xyz = d_xyz; a.tets = d_tets; a.ereg = d_ereg;
     a.fibre = d_fib; a.sig_l = d_sl; a.sig_t = d_st; a.inc_ptr = d_iptr; a.inc = d_inc;
     a.slice_ptr = P.d_sp; a.col = d_colg; a.rowlen = d_rowlen;
     a.A = P.d_A; a.K = P.d_K; a.dinv = P.d_dinv; a.dirichlet = P.d_dir;
@@ -1381,8 +1390,8 @@ tc_status tc_mesh_pattern(int64_t n, int64_t E, const int32_t* tets, int64_t* ro
     if (tets[t] < 0 || tets[t] >= n) return TC_EINVAL;
   std::vector<int64_t> iptr, rp;
   std::vector<int32_t> inc, cl;
-  build_incidence(n, E, tets, iptr, inc);
-  build_pattern(n, tets, iptr, inc, rp, cl);
+  build_incidence(n, E, 4, tets, iptr, inc);
+  build_pattern(n, 4, tets, iptr, inc, rp, cl);
   std::copy(rp.begin(), rp.end(), rowptr);
   if (col) std::copy(cl.begin(), cl.end(), col);
   return TC_OK;

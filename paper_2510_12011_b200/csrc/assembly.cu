@@ -5,8 +5,10 @@
 // entry is summed in the same order as an element-order scatter-add, without
 // atomics (deterministic).  Boundary (one-time) work, not on the step path.
 //
-//   |e| = |det J| / 6,  grad phi_a from the adjugate of J (columns x_a - x_0),
-//   M_e = |e|/20 (1 + delta_ab),  K_e = |e| grad phi_a . sigma grad phi_b,
+//   tets:      |e| = |det J| / 6,  grad phi_a from the adjugate of J (columns
+//              x_a - x_0),  M_e = |e|/20 (1 + delta_ab);
+//   triangles: |e| = |n|/2 with n = e1 x e2, in-plane gradients, M_e = |e|/12 (1 + delta_ab);
+//   K_e = |e| grad phi_a . sigma grad phi_b,
 //   sigma = sigma_t I + (sigma_l - sigma_t) f f^T   (reading A13),
 //   A = chi Cm M + theta dt K (Eq. 3),  dinv = 1 / A_ii (Jacobi).
 #include <cstring>
@@ -36,29 +38,54 @@ __global__ void assemble_kernel(AsmArgs a) {
     const int32_t code = a.inc[t];
     const int64_t e = code >> 2;
     const int la = code & 3;
-    const int32_t* v = a.tets + 4 * e;
+    const int kel = a.k;
+    const int32_t* v = a.tets + (int64_t)kel * e;
     double X[4][3];
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < kel; ++q)
       for (int c = 0; c < 3; ++c) X[q][c] = a.xyz[3 * (int64_t)v[q] + c];
-    double d1[3], d2[3], d3[3];
-    for (int c = 0; c < 3; ++c) {
-      d1[c] = X[1][c] - X[0][c];
-      d2[c] = X[2][c] - X[0][c];
-      d3[c] = X[3][c] - X[0][c];
-    }
     double g[4][3];
-    cross3(d2, d3, g[1]);
-    cross3(d3, d1, g[2]);
-    cross3(d1, d2, g[3]);
-    const double det = d1[0] * g[1][0] + d1[1] * g[1][1] + d1[2] * g[1][2];
-    if (det == 0.0) { atomicExch(a.err, 1); return; }
-    for (int c = 0; c < 3; ++c) {
-      g[1][c] /= det;
-      g[2][c] /= det;
-      g[3][c] /= det;
-      g[0][c] = -(g[1][c] + g[2][c] + g[3][c]);
+    double vol, mass_w;  // |e| and the mass weight: |e|/20 (tet), |e|/12 (triangle)
+    if (kel == 4) {
+      double d1[3], d2[3], d3[3];
+      for (int c = 0; c < 3; ++c) {
+        d1[c] = X[1][c] - X[0][c];
+        d2[c] = X[2][c] - X[0][c];
+        d3[c] = X[3][c] - X[0][c];
+      }
+      cross3(d2, d3, g[1]);
+      cross3(d3, d1, g[2]);
+      cross3(d1, d2, g[3]);
+      const double det = d1[0] * g[1][0] + d1[1] * g[1][1] + d1[2] * g[1][2];
+      if (det == 0.0) { atomicExch(a.err, 1); return; }
+      for (int c = 0; c < 3; ++c) {
+        g[1][c] /= det;
+        g[2][c] /= det;
+        g[3][c] /= det;
+        g[0][c] = -(g[1][c] + g[2][c] + g[3][c]);
+      }
+      vol = fabs(det) / 6.0;
+      mass_w = vol / 20.0;
+    } else {
+      // triangle embedded in 3-D: n = e1 x e2, |e| = |n|/2,
+      // grad phi_1 = (e2 x n)/|n|^2, grad phi_2 = (n x e1)/|n|^2 (in-plane).
+      double e1[3], e2[3], nv[3];
+      for (int c = 0; c < 3; ++c) {
+        e1[c] = X[1][c] - X[0][c];
+        e2[c] = X[2][c] - X[0][c];
+      }
+      cross3(e1, e2, nv);
+      const double nn = nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2];
+      if (nn == 0.0) { atomicExch(a.err, 1); return; }
+      cross3(e2, nv, g[1]);
+      cross3(nv, e1, g[2]);
+      for (int c = 0; c < 3; ++c) {
+        g[1][c] /= nn;
+        g[2][c] /= nn;
+        g[0][c] = -(g[1][c] + g[2][c]);
+      }
+      vol = sqrt(nn) / 2.0;
+      mass_w = vol / 12.0;
     }
-    const double vol = fabs(det) / 6.0;
     // conductivity tensor of the element
     const int r = a.ereg[e];
     const double sl = a.sig_l[r], st = a.sig_t[r];
@@ -72,13 +99,13 @@ __global__ void assemble_kernel(AsmArgs a) {
       double fd = f[0] * g[la][0] + f[1] * g[la][1] + f[2] * g[la][2];
       sg[c] = acc + (sl - st) * f[c] * fd;
     }
-    for (int lb = 0; lb < 4; ++lb) {
+    for (int lb = 0; lb < kel; ++lb) {
       const int32_t j = v[lb];
       int k = 0;
       while (k < len && a.col[base + (int64_t)k * kSellC] != j) ++k;
       if (k == len) { atomicExch(a.err, 2); return; }
       const double Kab = vol * (sg[0] * g[lb][0] + sg[1] * g[lb][1] + sg[2] * g[lb][2]);
-      const double Mab = vol / 20.0 * (la == lb ? 2.0 : 1.0);
+      const double Mab = mass_w * (la == lb ? 2.0 : 1.0);
       a.A[base + (int64_t)k * kSellC] += Mab;
       a.K[base + (int64_t)k * kSellC] += Kab;
     }

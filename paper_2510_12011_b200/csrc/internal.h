@@ -189,6 +189,7 @@ struct IonArgs {
 struct AsmArgs {
   int32_t n;
   int32_t row0;        // global (internal) index of local row 0
+  int32_t k;           // nodes per element: 4 tetrahedra, 3 surface triangles
   const double* xyz;
   const int32_t* tets;
   const int32_t* ereg;
@@ -246,10 +247,10 @@ cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs
 
 // ---- host setup (setup_host.cpp) --------------------------------------------
 struct HostMesh;
-std::string orient_and_validate(int64_t n, int64_t E, int32_t* tets, const double* xyz);
-void build_incidence(int64_t n, int64_t E, const int32_t* tets, std::vector<int64_t>& ptr,
+std::string orient_and_validate(int64_t n, int64_t E, int k, int32_t* tets, const double* xyz);
+void build_incidence(int64_t n, int64_t E, int k, const int32_t* tets, std::vector<int64_t>& ptr,
                      std::vector<int32_t>& inc);
-void build_pattern(int64_t n, const int32_t* tets, const std::vector<int64_t>& ptr,
+void build_pattern(int64_t n, int k, const int32_t* tets, const std::vector<int64_t>& ptr,
                    const std::vector<int32_t>& inc, std::vector<int64_t>& rowptr,
                    std::vector<int32_t>& col);
 void rcm_order(int64_t n, const std::vector<int64_t>& rowptr, const std::vector<int32_t>& col,

@@ -13,18 +13,31 @@
 
 namespace tcb {
 
-// Swap tet vertices 1,2 when the signed volume is negative; report the first
-// zero-volume or out-of-range element.
-std::string orient_and_validate(int64_t n, int64_t E, int32_t* tets, const double* xyz) {
+// k = 4: swap tet vertices 1,2 when the signed volume is negative; k = 3
+// (surface triangles in 3-D): no orientation.  Reports the first zero-measure
+// or out-of-range element.
+std::string orient_and_validate(int64_t n, int64_t E, int k, int32_t* tets, const double* xyz) {
   int64_t bad_idx = -1, bad_vol = -1;
 #pragma omp parallel for schedule(static) reduction(max : bad_idx, bad_vol)
   for (int64_t e = 0; e < E; ++e) {
-    int32_t* t = tets + 4 * e;
+    int32_t* t = tets + (int64_t)k * e;
     bool ok = true;
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < k; ++a)
       if (t[a] < 0 || t[a] >= n) ok = false;
     if (!ok) {
       bad_idx = std::max(bad_idx, e);
+      continue;
+    }
+    if (k == 3) {
+      double e1[3], e2[3];
+      for (int c = 0; c < 3; ++c) {
+        e1[c] = xyz[3 * (int64_t)t[1] + c] - xyz[3 * (int64_t)t[0] + c];
+        e2[c] = xyz[3 * (int64_t)t[2] + c] - xyz[3 * (int64_t)t[0] + c];
+      }
+      const double nx = e1[1] * e2[2] - e1[2] * e2[1], ny = e1[2] * e2[0] - e1[0] * e2[2],
+                   nz = e1[0] * e2[1] - e1[1] * e2[0];
+      const double nn = nx * nx + ny * ny + nz * nz;
+      if (!(nn > 0.0) || !std::isfinite(nn)) bad_vol = std::max(bad_vol, e);
       continue;
     }
     const double* p0 = xyz + 3 * (int64_t)t[0];
@@ -45,20 +58,21 @@ std::string orient_and_validate(int64_t n, int64_t E, int32_t* tets, const doubl
   return "";
 }
 
-// node -> (4*e + a) incidence; entries of a node in ascending element order.
-void build_incidence(int64_t n, int64_t E, const int32_t* tets, std::vector<int64_t>& ptr,
+// node -> (4*e + a) incidence (k nodes per element, a < k); entries of a node
+// in ascending element order.
+void build_incidence(int64_t n, int64_t E, int k, const int32_t* tets, std::vector<int64_t>& ptr,
                      std::vector<int32_t>& inc) {
   ptr.assign(n + 1, 0);
-  for (int64_t e = 0; e < 4 * E; ++e) ptr[tets[e] + 1]++;
+  for (int64_t e = 0; e < (int64_t)k * E; ++e) ptr[tets[e] + 1]++;
   for (int64_t i = 0; i < n; ++i) ptr[i + 1] += ptr[i];
   std::vector<int64_t> pos(ptr.begin(), ptr.end() - 1);
-  inc.resize(4 * E);
+  inc.resize((int64_t)k * E);
   for (int64_t e = 0; e < E; ++e)
-    for (int a = 0; a < 4; ++a) inc[pos[tets[4 * e + a]]++] = (int32_t)(4 * e + a);
+    for (int a = 0; a < k; ++a) inc[pos[tets[(int64_t)k * e + a]]++] = (int32_t)(4 * e + a);
 }
 
 // Row i holds i and every node sharing an element with i, ascending.
-void build_pattern(int64_t n, const int32_t* tets, const std::vector<int64_t>& ptr,
+void build_pattern(int64_t n, int k, const int32_t* tets, const std::vector<int64_t>& ptr,
                    const std::vector<int32_t>& inc, std::vector<int64_t>& rowptr,
                    std::vector<int32_t>& col) {
   rowptr.assign(n + 1, 0);
@@ -67,7 +81,7 @@ void build_pattern(int64_t n, const int32_t* tets, const std::vector<int64_t>& p
     buf.push_back((int32_t)i);
     for (int64_t t = ptr[i]; t < ptr[i + 1]; ++t) {
       int64_t e = inc[t] >> 2;
-      for (int a = 0; a < 4; ++a) buf.push_back(tets[4 * e + a]);
+      for (int a = 0; a < k; ++a) buf.push_back(tets[(int64_t)k * e + a]);
     }
     std::sort(buf.begin(), buf.end());
     buf.erase(std::unique(buf.begin(), buf.end()), buf.end());

@@ -270,6 +270,84 @@ def test_mms_on_gpu_matches_oracle_and_converges(T):
     assert 1.7 < order < 2.3
 
 
+@pytest.mark.parametrize("model,parts,rot", [("ms", 1, False), ("tt2006", 1, True), ("tt2006", 3, False),
+                                             ("ms", 2, True)])
+def test_surface_sphere_trajectory_parity(T, model, parts, rot):
+    """Surface (triangle) meshes: an icosphere with tangent
+    fibres, two regions, stimulus at one pole; V per step within rel-L2 1e-8,
+    LAT within one dt, also under a rigid rotation and on row-block partitions."""
+    xyz, tris = G.sphere(3)
+    xyz, tris, _ = G.permute_nodes(xyz, tris, seed=11)
+    if rot:
+        xyz, _ = G.rotate(xyz)
+    E = tris.shape[0]
+    fib = G.sphere_fibres(xyz, tris)
+    c = xyz[tris].mean(1)
+    region = (c[:, 0] > 3.0).astype(np.int32)
+    cond = {0: (0.1334177, 0.0173515), 1: (0.3, 0.05)}
+    top = np.argmax(xyz @ np.array([0.3, 0.2, 0.93]))
+    d = np.linalg.norm(xyz - xyz[top], axis=1)
+    stims = [O.Stimulus(np.nonzero(d < 2.5)[0], 0.0, 2.0, 50.0)]
+    dt = 0.05
+    ref = O.Monodomain(xyz, tris, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0),
+                       stims)
+    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, partitions=parts)
+    sim = T.Monodomain(xyz, tris, region, fib, cond, cfg, stims)
+    try:
+        for k in range(150):
+            st = sim.step(1)
+            rep = ref.step()
+            rel = np.linalg.norm(sim.V - ref.Vk) / np.linalg.norm(ref.Vk)
+            assert rel <= 1e-8, (k, rel)
+            assert abs(int(st["iters"][0]) - rep.iters) <= 1
+        lat, _ = sim.activation()
+        assert np.all((lat < 0) == (ref.lat < 0))
+        assert np.abs(lat - ref.lat).max() <= dt + 1e-12
+        assert (ref.lat >= 0).sum() > 10      # the wave actually propagated
+    finally:
+        sim.close()
+
+
+def test_surface_mms_unit_square_on_gpu(T):
+    """The paper's own MMS setup: [0,1]^2 triangulated, Dirichlet w on the
+    perimeter, Crank-Nicolson; GPU V equals the oracle's, L2 order ~2."""
+    errs = []
+    for N in (8, 16):
+        xyz, tris = G.unit_square(N)
+        B = G.box_boundary(xyz[:, :2])
+        dt = 0.01 * 8 / N
+        out = O.run_mms(xyz, tris, B, dt=dt, T=0.5, tol=1e-10)
+        E = tris.shape[0]
+        cfg = T.tc_config_default(dt=dt, model="mms", chi=1.0, cm=1.0, abs_tol=1e-10, rel_tol=1e-10,
+                                  max_iters=1000)
+        sim = T.Monodomain(xyz, tris, np.zeros(E, np.int32), G.uniform_fibres(E), {0: (1.0, 1.0)}, cfg,
+                           mms=(1.0, np.pi, np.pi, np.pi, B))
+        try:
+            sim.step(int(round(0.5 / dt)))
+            v = sim.V
+        finally:
+            sim.close()
+        assert np.abs(v - out["V"]).max() <= 1e-8
+        errs.append(out["err_M"])
+    order = np.log2(errs[0] / errs[1])
+    assert 1.7 < order < 2.3
+
+
+def test_surface_mesh_errors(T):
+    xyz, tris = G.unit_square(2)
+    ctx = T.tc_create(T.tc_config_default())
+    try:
+        bad = tris.copy()
+        bad[0] = [0, 1, 2]          # collinear nodes on the bottom edge -> zero area
+        with pytest.raises(T.TcError) as ei:
+            T.tc_set_mesh_elems(ctx, xyz, bad)
+        assert ei.value.status == T.TC_EDEGEN
+        with pytest.raises(T.TcError):
+            T.tc_set_mesh_elems(ctx, xyz, np.zeros((2, 5), np.int32))
+    finally:
+        T.tc_destroy(ctx)
+
+
 def test_errors_are_reported(T):
     xyz, tets = G.kuhn_box(3, 3, 3, 1.0)
     ctx = T.tc_create(T.tc_config_default())
