@@ -49,6 +49,10 @@ WORKLOADS = {
     # configs[0]: N-version dx = 0.5 mm (4305 nodes), TT2006 epi, dt 0.05, 40 ms
     "nversion_dx0.5_tt": dict(cfg=0, dims=(41, 15, 7), dx=0.5, model="tt2006", dt=0.05,
                               stim="corner", preroll=0, sample_dims=(41, 15, 7)),
+    # a cohort of 100 configs[0]-sized slabs (seeded sizes,
+    # numbering, fibres, conductivities, TT2006 parameter resets), one cluster each
+    "cohort100_nversion05_tt": dict(cfg="f1 cohort", cohort=100, dims=None, dx=0.5, model="tt2006",
+                                    dt=0.05, stim="corner", preroll=40),
 }
 DEFAULT_WORKLOAD = "slab20M_ms"
 
@@ -219,6 +223,8 @@ def main():
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     rank, world, local = dist_env()
+    if w.get("cohort"):
+        return run_cohort(args, w)
     if world > 1 or args.dist:
         import bench_dist
         return bench_dist.main(args, w)
@@ -240,6 +246,7 @@ def main():
     t_setup = time.perf_counter() - t0
     del tets
     info = T.tc_matrix_info(sim.ctx)
+    eng = T.tc_engine_info(sim.ctx)
     preroll = w["preroll"] if args.preroll is None else args.preroll
     if preroll:
         sim.step(preroll)                   # move into the timing window (propagating front)
@@ -266,7 +273,9 @@ def main():
     cg_s = prof["pcg_ms"] / 1e3
     achieved = b_cg / cg_s / 1e9 if cg_s > 0 else None
     traffic = ncu_traffic(args.workload, iters / args.steps)
-    roof = {"kernel": "PCG path per step: rhs_kernel + cooperative pcg_kernel (Eq. 3 RHS + Alg. 1)",
+    kname = ("PCG path per step: rhs_kernel + cooperative pcg_kernel (Eq. 3 RHS + Alg. 1)" if eng["engine"] == "grid"
+             else "cohort_kernel (cluster engine: the whole step, ionic + RHS + Alg. 1, one launch per call)")
+    roof = {"kernel": kname,
             "bound": "hbm",
             "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"] if achieved else None,
@@ -314,6 +323,7 @@ def main():
                    "tets": int(E), "model": w["model"], "dt_ms": w["dt"], "dx_mm": w["dx"],
                    "grid": list(w["dims"]) if w["dims"] else f"BiV h={w['h']} mm", "tol": "abs=rel=1e-5, max 100 (P:316)",
                    "rcm": not args.no_rcm, "preroll_steps": preroll, "pcg_variant": args.pcg_variant,
+                   "engine": eng,
                    "wide_slices": info.get("wide_slices"),
                    "l2": f"inputs larger than L2 (A+K+col {(20 * info['nnz_pad']) / 1e9:.2f} GB >> 126 MB)"
                          if n > 1_000_000 else "small problem: L2-resident",
@@ -326,6 +336,136 @@ def main():
         "e2e": e2e,
         "gpu_launches": prof["launches"],
         "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_cohort(args, w):
+    """f1: every member advanced by one tc_cohort_step launch per timed call."""
+    import torch
+    import paper_2510_12011_b200 as T
+    rank, world, local = dist_env()
+    if world > 1:   # replicas only (DESIGN.md "Cohorts"): every rank runs its own cohort
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+    members = G.cohort_members(w["cohort"], seed=G.SEED + rank)
+    sims = []
+    t0 = time.perf_counter()
+    for m in members:
+        cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5,
+                                  max_iters=100)
+        sims.append(T.Monodomain(m["xyz"], m["tets"], None, m["fibre"],
+                                 {0: (SIGMA[0] * m["sigma_scale"], SIGMA[1] * m["sigma_scale"])}, cfg,
+                                 [(m["stim_nodes"], 0.0, 2.0, 50.0)], device=local,
+                                 stream=stream.cuda_stream))
+        for name, f in m["param_factors"].items():
+            T.tc_set_ionic_param(sims[-1].ctx, name, T.tc_get_ionic_param(sims[-1].ctx, name) * f)
+    co = T.Cohort(sims)
+    t_setup = time.perf_counter() - t0
+    info = co.info()
+    n_nodes = [T.tc_num_nodes(s.ctx) for s in sims]
+    nnz = [T.tc_matrix_info(s.ctx)["nnz"] for s in sims]
+    N = int(sum(n_nodes))
+    co.step(w["preroll"], want_stats=False)
+    co.step(args.warmup, want_stats=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        stats = co.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = N * world * args.steps / (ms / 1e3)
+    b_cg = b_ion = 0.0
+    for mi in range(len(sims)):
+        bc, bi = bytes_per_step(n_nodes[mi], nnz[mi], int(stats["iters"][mi].sum()), w["model"], args.steps)
+        b_cg += bc
+        b_ion += bi
+    peaks, which = measured_peaks()
+    achieved = (b_cg + b_ion) / (ms / 1e3) / 1e9
+    roof = {"kernel": "cohort_kernel (cluster engine, one cluster per member, whole step per launch)",
+            "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": which,
+            "bytes_model": "per member and step: B_ion + 20nnz+4(n+1)+44n + iters*(12nnz+4(n+1)+72n) (SURVEY 8d)",
+            "note": "members are shared-memory / L2 resident: latency-bound (cluster barriers, DSMEM), "
+                    "the HBM fraction is the algorithmic-byte rate, not a bandwidth claim"}
+    # end to end through the C ABI with host buffers: every member's state H2D, one cohort step, V D2H
+    hin = []
+    for s_ in sims:
+        st_ = s_.get_state()
+        h = torch.empty(st_.shape[0], dtype=torch.float64, pin_memory=True).numpy()
+        h[:] = st_
+        hin.append(h)
+    hout = [torch.empty(n_, dtype=torch.float64, pin_memory=True).numpy() for n_ in n_nodes]
+    ke = max(1, args.e2e_steps)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        for s_, h in zip(sims, hin):
+            T.tc_set_state(s_.ctx, h)
+        co.step(1, want_stats=False)
+        for s_, h in zip(sims, hout):
+            T.tc_get_v(s_.ctx, h)
+    e2e_s = time.perf_counter() - t0
+    e2e = {"value": N * world * ke / e2e_s, "unit": "node-steps/s",
+           "h2d_bytes_per_step": int(sum(h.nbytes for h in hin)), "d2h_bytes_per_step": int(sum(h.nbytes for h in hout)),
+           "what": "per step: tc_set_state of every member (pinned host) + tc_cohort_step(1) + tc_get_v of every member"}
+    iters = float(stats["iters"].mean())
+    co.close()
+    for s_ in sims:
+        s_.close()
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            import oracle as O
+            m = members[0]
+            E = m["tets"].shape[0]
+            names = O.tt_param_names()
+            prm = O.tt_default_params().copy()
+            for k_, f_ in m["param_factors"].items():
+                prm[names.index(k_)] *= f_
+            cfg = O.Config(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5,
+                           max_iters=100, params=prm)
+            osim = O.Monodomain(m["xyz"], m["tets"], np.zeros(E, np.int32), m["fibre"],
+                                {0: (SIGMA[0] * m["sigma_scale"], SIGMA[1] * m["sigma_scale"])}, cfg,
+                                [O.Stimulus(m["stim_nodes"], 0.0, 2.0, 50.0)])
+            k_, t1 = 0, time.perf_counter()
+            while time.perf_counter() - t1 < 15.0 and k_ < 800:
+                osim.step()
+                k_ += 1
+            el = time.perf_counter() - t1
+            cpu = dict(value=n_nodes[0] * k_ / el, unit="node-steps/s", cores=1, kind="oracle",
+                       sample=f"member 0 ({n_nodes[0]} nodes), first {k_} steps from rest, {el:.1f} s single-thread")
+        except Exception as ex:
+            cpu = {"error": str(ex)}
+    line = {
+        "metric": "node-steps/s", "value": value, "unit": "node-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "baseline_config": w["cfg"], "members": len(sims),
+                   "nodes_total": N, "nodes_min": int(min(n_nodes)), "nodes_max": int(max(n_nodes)),
+                   "model": w["model"], "dt_ms": w["dt"], "dx_mm": w["dx"], "tol": "abs=rel=1e-5, max 100 (P:316)",
+                   "preroll_steps": w["preroll"], "cohort": info,
+                   "l2": "small problems: L2 / shared-memory resident by design (cluster engine)",
+                   "parallelism": "replicas only" if world > 1 else "1 GPU"},
+        "sim_ms_per_wall_s": args.steps * w["dt"] / (ms / 1e3),
+        "pcg_iters_per_step": iters, "setup_s": t_setup, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": 1, "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
 

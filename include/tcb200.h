@@ -57,6 +57,21 @@ typedef enum {
   TC_ION_MMS = 2         /* no ionic model: manufactured source r of Eq. 8 */
 } tc_ionic;
 
+/* Execution engine of tc_step for a single-partition context (DESIGN.md
+ * "Cluster engine").  Both compute the same step; they differ in how the work
+ * is laid out on the GPU. */
+typedef enum {
+  TC_ENGINE_AUTO = 0,    /* cluster engine for small systems, grid engine otherwise */
+  TC_ENGINE_GRID = 1,    /* per step: ionic kernel + RHS kernel + one cooperative PCG
+                            kernel over all SMs (grid barriers) */
+  TC_ENGINE_CLUSTER = 2, /* every step of the tc_step call in ONE launch on one
+                            thread-block cluster (<= 16 CTAs; cluster barriers, DSMEM
+                            reductions); matrix and own-row vectors resident in shared
+                            memory when they fit.  TT2006 / MS only. */
+  TC_ENGINE_CLUSTER_STREAMING = 3 /* the cluster engine with everything streamed from
+                            global memory (measurement; what large systems get) */
+} tc_engine;
+
 typedef enum {
   TC_REL_CONSECUTIVE = 0, /* ||z_{k+1}|| / ||z_k||  (Alg. 1 literal, reading C1) */
   TC_REL_INITIAL = 1      /* ||z_{k+1}|| / ||z_0|| */
@@ -90,7 +105,7 @@ typedef struct {
                             doing halos and reductions itself over peer memory (NVLink via
                             CUDA IPC between ranks, plain device memory between the parts of
                             one GPU); 0 = split-phase kernels + NCCL / device copies */
-  int32_t reserved;
+  int32_t engine;        /* tc_engine (TC_ENGINE_AUTO) */
 } tc_config;
 
 /* Per-step PCG report. */
@@ -234,6 +249,45 @@ tc_status tc_pcg(tc_ctx* ctx, const double* b, const double* x0, double* x_out,
  * (NCCL is loaded at run time; without it tc_comm_init fails with TC_ENCCL). */
 tc_status tc_nccl_unique_id(uint8_t id[128]);
 tc_status tc_comm_init(tc_ctx* ctx, int rank, int world, const uint8_t id[128]);
+
+/* Engine tc_step uses for this context: out[0] TC_ENGINE_GRID or
+ * TC_ENGINE_CLUSTER, out[1] CTAs per cluster, out[2] dynamic shared memory per
+ * CTA (0 = streaming), out[3] clusters of that shape resident at once. */
+tc_status tc_engine_info(tc_ctx* ctx, int64_t out[4]);
+
+/* ---- Cohorts: many independent simulations per GPU ------------
+ * A cohort batches assembled single-partition contexts ("members": different
+ * meshes, conductivities, stimuli, ionic parameters, time steps, tolerances)
+ * that share the device and the ionic model (TT2006 or MS).  tc_cohort_step
+ * advances EVERY member by n_steps in ONE launch: one thread-block cluster per
+ * member runs its steps (the cluster engine), each member with its own PCG
+ * stopping test (per-replica stopping).  Each member's results equal what
+ * tc_step(member, n_steps) gives (same arithmetic; inner-product partial sums
+ * grouped per cluster), and afterwards every tc_get_* call on a member works as
+ * usual.  The members stay owned by the caller and must outlive the cohort;
+ * members must not be stepped concurrently with tc_cohort_step. */
+typedef struct tc_cohort tc_cohort;
+/* members: host array of `count` context pointers (copied).  cluster_size: CTAs
+ * per member cluster (1, 2, 4, 8, 16) or 0 = chosen from the largest member.
+ * resident: 1 = keep each CTA's matrix block and own-row vectors in shared
+ * memory for the whole launch when the largest member's block fits, 0 = stream
+ * from global memory.
+ * TC_ESTATE if a member is not assembled or is partitioned / multi-GPU;
+ * TC_EINVAL on mixed devices or models, MMS members, or a bad cluster size. */
+tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluster_size,
+                           int32_t resident, tc_cohort** out);
+/* Advance every member n_steps.  stats (nullable): count * n_steps reports,
+ * member-major (member m's step s at [m * n_steps + s]).  The work runs on
+ * member 0's stream, ordered after and before the other members' streams.
+ * A member that exceeds its fail budget or hits a NaN stops (its context
+ * reports the error on its next tc_step); the call then returns TC_ESOLVER /
+ * TC_ENAN naming the first such member, after all members were advanced. */
+tc_status tc_cohort_step(tc_cohort* cohort, int64_t n_steps, tc_step_stat* stats);
+/* out[0] members, out[1] CTAs per cluster, out[2] clusters resident at once,
+ * out[3] dynamic shared memory per CTA (0 = streaming). */
+tc_status tc_cohort_info(const tc_cohort* cohort, int32_t out[4]);
+const char* tc_cohort_last_error(const tc_cohort* cohort);
+tc_status tc_cohort_destroy(tc_cohort* cohort);
 
 /* ---- Host-only helpers (no GPU needed; used by the CPU tests) ------------- */
 /* CSR pattern of a tet mesh: (i,j) iff an element holds both.  Call

@@ -313,3 +313,35 @@ def sphere_fibres(xyz, tris):
     bad = np.linalg.norm(f, axis=1) < 1e-9 * np.linalg.norm(c, axis=1)
     f[bad] = [1.0, 0.0, 0.0]
     return f / np.linalg.norm(f, axis=1, keepdims=True)
+
+
+def cohort_members(count: int, seed=SEED, base=(41, 15, 7), dx=0.5):
+    """Seeded cohort of `count` N-version-like slabs (SURVEY 8f f1, P:349-353:
+    many patient meshes with per-patient settings).  Member m: Kuhn slab of
+    (nx, ny, nz) = base + (U{-6..6}, U{-3..3}, U{-2..2}) nodes at spacing dx,
+    node numbering randomly permuted, one fibre direction in the x-y plane at
+    U[-30, 30] degrees, conductivity scale U[0.8, 1.2], TT2006 parameter resets
+    GKr, GKs x U[0.7, 1.3] and GCaL x U[0.8, 1.2] (factors, applied by the
+    caller to its defaults), corner stimulus box <= 1.5 mm.  Returns a list of
+    dicts: xyz, tets, fibre, sigma_scale, param_factors, stim_nodes."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for m in range(count):
+        nx = base[0] + int(rng.integers(-6, 7))
+        ny = base[1] + int(rng.integers(-3, 4))
+        nz = base[2] + int(rng.integers(-2, 3))
+        xyz, tets = kuhn_box(nx, ny, nz, dx)
+        stim = nodes_in_box(xyz, (0, 0, 0), (1.5, 1.5, 1.5))
+        perm_seed = int(rng.integers(1 << 31))
+        xyz, tets, perm = permute_nodes(xyz, tets, seed=perm_seed)   # perm: new -> old
+        inv = np.empty(perm.shape[0], np.int64)
+        inv[perm] = np.arange(perm.shape[0])
+        stim = np.sort(inv[stim]).astype(np.int32)
+        ang = np.deg2rad(rng.uniform(-30.0, 30.0))
+        fib = uniform_fibres(tets.shape[0], (np.cos(ang), np.sin(ang), 0.0))
+        out.append(dict(xyz=xyz, tets=tets, fibre=fib, sigma_scale=float(rng.uniform(0.8, 1.2)),
+                        param_factors={"GKr": float(rng.uniform(0.7, 1.3)),
+                                       "GKs": float(rng.uniform(0.7, 1.3)),
+                                       "GCaL": float(rng.uniform(0.8, 1.2))},
+                        stim_nodes=stim))
+    return out

@@ -23,6 +23,8 @@ __all__ = [
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
     "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "tc_nccl_unique_id", "tc_comm_init",
     "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "Monodomain", "LIB_PATH",
+    "tc_engine_info", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
+    "TC_ENGINE_AUTO", "TC_ENGINE_GRID", "TC_ENGINE_CLUSTER",
     "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS",
 ]
 
@@ -32,6 +34,9 @@ STATUS_NAMES = ["TC_OK", "TC_EINVAL", "TC_ENOMEM", "TC_ECUDA", "TC_ENCCL", "TC_E
                 "TC_ESTATE", "TC_EDEGEN", "TC_EREGION"]
 TC_ION_TT2006_EPI, TC_ION_MS, TC_ION_MMS = 0, 1, 2
 MODELS = {"tt2006": TC_ION_TT2006_EPI, "ms": TC_ION_MS, "mms": TC_ION_MMS}
+TC_ENGINE_AUTO, TC_ENGINE_GRID, TC_ENGINE_CLUSTER, TC_ENGINE_CLUSTER_STREAMING = 0, 1, 2, 3
+ENGINES = {"auto": TC_ENGINE_AUTO, "grid": TC_ENGINE_GRID, "cluster": TC_ENGINE_CLUSTER,
+           "cluster_streaming": TC_ENGINE_CLUSTER_STREAMING}
 
 
 class tc_config(C.Structure):
@@ -41,7 +46,7 @@ class tc_config(C.Structure):
                 ("lat_threshold", C.c_double), ("lrt_threshold", C.c_double),
                 ("use_rcm", C.c_int32), ("pcg_variant", C.c_int32),
                 ("partitions", C.c_int32), ("check_every", C.c_int32),
-                ("peer", C.c_int32), ("reserved", C.c_int32)]
+                ("peer", C.c_int32), ("engine", C.c_int32)]
 
 
 class tc_step_stat(C.Structure):
@@ -96,6 +101,12 @@ def _load():
         "tc_abi_version": ([], I32),
         "tc_nccl_unique_id": ([P], I32),
         "tc_comm_init": ([P, C.c_int, C.c_int, P], I32),
+        "tc_engine_info": ([P, P], I32),
+        "tc_cohort_create": ([P, I32, I32, I32, P], I32),
+        "tc_cohort_step": ([P, I64, P], I32),
+        "tc_cohort_info": ([P, P], I32),
+        "tc_cohort_last_error": ([P], C.c_char_p),
+        "tc_cohort_destroy": ([P], I32),
         "tc_mesh_pattern": ([I64, I64, P, P, P], I32),
         "tc_rcm": ([I64, P, P, P], I32),
         "tc_partition_plan": ([I64, P, P, I32, I32, P, P, P, P, P, P, P], I32),
@@ -138,6 +149,8 @@ def tc_config_default(**overrides) -> tc_config:
     for k, v in overrides.items():
         if k == "model" and isinstance(v, str):
             v = MODELS[v]
+        if k == "engine" and isinstance(v, str):
+            v = ENGINES[v]
         setattr(cfg, k, v)
     return cfg
 
@@ -283,6 +296,56 @@ def tc_comm_init(ctx, rank: int, world: int, unique_id: bytes) -> None:
     _check(ctx, _L.tc_comm_init(ctx, rank, world, buf))
 
 
+def tc_engine_info(ctx) -> dict:
+    out = np.zeros(4, np.int64)
+    _check(ctx, _L.tc_engine_info(ctx, _ptr(out)))
+    return dict(engine={1: "grid", 2: "cluster"}[int(out[0])], cluster_size=int(out[1]),
+                smem_per_cta=int(out[2]), resident_clusters=int(out[3]))
+
+
+# ---------------------------------------------------------------- cohorts
+def tc_cohort_create(members, cluster_size: int = 0, resident: bool = True):
+    """members: contexts (assembled, single partition, same device and model)."""
+    arr = (C.c_void_p * len(members))(*[m.value if isinstance(m, C.c_void_p) else m for m in members])
+    out = C.c_void_p()
+    st = _L.tc_cohort_create(arr, len(members), cluster_size, int(resident), C.byref(out))
+    if st != TC_OK:
+        raise TcError(st, tc_last_error(members[0]) if members else "tc_cohort_create")
+    return out
+
+
+def tc_cohort_step(co, n_steps: int, count: int | None = None, want_stats: bool = True):
+    """-> stats (count, n_steps) structured array, member-major (or None)."""
+    stats = None
+    if want_stats:
+        if count is None:
+            count = tc_cohort_info(co)["members"]
+        stats = np.zeros((count, n_steps), STAT_DTYPE)
+    st = _L.tc_cohort_step(co, n_steps, _ptr(stats))
+    if st != TC_OK:
+        m = _L.tc_cohort_last_error(co)
+        raise TcError(st, m.decode() if m else "")
+    return stats
+
+
+def tc_cohort_info(co) -> dict:
+    out = np.zeros(4, np.int32)
+    st = _L.tc_cohort_info(co, _ptr(out))
+    if st != TC_OK:
+        raise TcError(st, "tc_cohort_info")
+    return dict(members=int(out[0]), cluster_size=int(out[1]), resident_clusters=int(out[2]),
+                smem_per_cta=int(out[3]))
+
+
+def tc_cohort_last_error(co) -> str:
+    m = _L.tc_cohort_last_error(co)
+    return m.decode() if m else ""
+
+
+def tc_cohort_destroy(co) -> None:
+    _L.tc_cohort_destroy(co)
+
+
 # ---------------------------------------------------------------- host-only helpers
 def tc_mesh_pattern(n: int, tets):
     tets = _i32(tets)
@@ -403,6 +466,32 @@ class Monodomain:
         if self.ctx is not None:
             tc_destroy(self.ctx)
             self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Cohort:
+    """Owning wrapper over tc_cohort_*: ``Cohort([Monodomain, ...])``; the members
+    stay usable (``m.V``, ``m.activation()``) and must outlive the cohort."""
+
+    def __init__(self, members, cluster_size: int = 0, resident: bool = True):
+        self.members = list(members)
+        self.co = tc_cohort_create([m.ctx for m in self.members], cluster_size, resident)
+
+    def step(self, n: int = 1, want_stats: bool = True):
+        return tc_cohort_step(self.co, n, len(self.members), want_stats)
+
+    def info(self) -> dict:
+        return tc_cohort_info(self.co)
+
+    def close(self):
+        if self.co is not None:
+            tc_cohort_destroy(self.co)
+            self.co = None
 
     def __del__(self):
         try:

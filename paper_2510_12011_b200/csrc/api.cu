@@ -28,10 +28,7 @@ struct Stim {
   std::vector<int32_t> nodes;
   double t0, dur, amp;
 };
-struct Epoch {
-  int64_t k0, k1;  // step window [k0, k1)
-  int32_t off, m;  // slice of the part's (local index, s) list
-};
+using Epoch = StimEpoch;  // step window [k0, k1) + slice of the part's (local index, s) list
 
 struct Part {
   PartPlan plan;
@@ -62,6 +59,8 @@ struct Part {
   std::vector<Epoch> epochs;
   int32_t* d_stim_idx = nullptr;
   double* d_stim_s = nullptr;
+  StimEpoch* d_ep = nullptr;      // epochs on the device (cluster engine)
+  std::vector<int64_t> h_sp;      // host copy of the slice pointers (cluster engine sizing)
   // persistent peer-memory PCG (pcg_peer.cu)
   char* d_inbox = nullptr;        // RedSlot[2 world] + uint64 halo flags[world]
   int32_t* d_send_nbr = nullptr;
@@ -124,6 +123,12 @@ struct tc_ctx {
   int iVk = 0, iVkm1 = 1, iX = 2;
   int64_t k = 0;
   bool has_prev = false;
+  // cluster engine (cohort.cu): descriptor, packed ionic parameters, epochs
+  CoRep* d_corep = nullptr;
+  double* d_params = nullptr;
+  uint64_t param_version = 1, params_uploaded = 0;
+  int co_csize = -1;               // cluster size for this context alone (-1 = not chosen yet)
+  size_t co_smem = 0;              // its dynamic shared memory (0 = streaming launch)
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> evs;
@@ -210,7 +215,7 @@ void tc_config_default(tc_config* c) {
   c->partitions = 1;
   c->check_every = 4;
   c->peer = 1;
-  c->reserved = 0;
+  c->engine = TC_ENGINE_AUTO;
 }
 
 tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx** out) {
@@ -219,7 +224,7 @@ tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx*
   if (!(cfg->dt > 0) || !(cfg->theta >= 0 && cfg->theta <= 1) || !(cfg->chi > 0) || !(cfg->cm > 0) ||
       cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 ||
       cfg->model > 2 || cfg->pcg_variant < 0 || cfg->pcg_variant > 2 || cfg->partitions < 1 ||
-      cfg->partitions > 4096 || cfg->check_every < 1)
+      cfg->partitions > 4096 || cfg->check_every < 1 || cfg->engine < 0 || cfg->engine > 3)
     return TC_EINVAL;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0) return TC_ECUDA;
@@ -343,6 +348,7 @@ tc_status tc_set_ionic_param(tc_ctx* c, const char* name, double v) {
   if (c->cfg.model == TC_ION_MS) p = ms_param_slot(&c->ms, name);
   if (!p) return fail(c, TC_EINVAL, std::string("unknown ionic parameter ") + name);
   *p = v;
+  c->param_version += 1;
   return TC_OK;
 }
 
@@ -738,6 +744,7 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
     P.n_vec = P.n_pad + P.n_ghost;
     P.nnz = rp2[g1] - rp2[g0];
     P.nnz_pad = hs.slice_ptr[hs.nslices];
+    P.h_sp = hs.slice_ptr;
     CUDA_TRY(c, upload(c, &P.d_sp, hs.slice_ptr));
     CUDA_TRY(c, upload(c, &P.d_col, hs.col));
     CUDA_TRY(c, dalloc(c, &P.d_A, P.nnz_pad));
@@ -840,6 +847,7 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
       }
       CUDA_TRY(c, upload(c, &P.d_stim_idx, idx));
       CUDA_TRY(c, upload(c, &P.d_stim_s, sv));
+      CUDA_TRY(c, upload(c, &P.d_ep, P.epochs));
     }
   }
   CUDA_TRY(c, upload(c, &c->d_perm_g, c->perm));
@@ -1061,6 +1069,109 @@ static tc_status pcg_split(tc_ctx* c) {
   return TC_OK;
 }
 
+// ------------------------------------------------------------------ cluster engine
+static bool cluster_capable(const tc_ctx* c) {
+  return c->assembled && !c->csr_mode && !split_mode(c) && c->parts.size() == 1 &&
+         (c->cfg.model == TC_ION_TT2006_EPI || c->cfg.model == TC_ION_MS);
+}
+
+// CTAs per cluster for a system of `nslices` warp slices: one slice per warp
+// where possible (power of two, <= 16, what the device can co-schedule).
+static int cluster_want(int64_t nslices) {
+  const int64_t need = (nslices + (kCoThreads / 32) - 1) / (kCoThreads / 32);
+  int c = 1;
+  while (c < need && c < kCoMaxCluster) c <<= 1;
+  return c;
+}
+
+static bool use_cluster(tc_ctx* c) {
+  if (!cluster_capable(c) || c->cfg.engine == TC_ENGINE_GRID) return false;
+  if (c->co_csize < 0) {
+    const Part& P = c->parts[0];
+    c->co_csize = cohort_cluster_size(c->cfg.model, cluster_want(P.nslices));
+    c->co_smem = 0;
+    if (c->co_csize > 0 && c->cfg.engine != TC_ENGINE_CLUSTER_STREAMING) {
+      const size_t need = cohort_smem_bytes(P.h_sp.data(), P.nslices, c->co_csize);
+      if (need <= cohort_smem_limit(c->cfg.model) && cohort_active_clusters(c->cfg.model, c->co_csize, need) > 0)
+        c->co_smem = need;
+    }
+  }
+  if (c->co_csize == 0) return false;
+  if (c->cfg.engine == TC_ENGINE_CLUSTER || c->cfg.engine == TC_ENGINE_CLUSTER_STREAMING) return true;
+  return c->parts[0].nslices <= kClusterAutoSlices;
+}
+
+// Descriptor of this context for a cluster-engine launch starting at step c->k;
+// uploads the packed ionic parameters when they changed.
+static tc_status make_corep(tc_ctx* c, CoRep& R, tc_step_stat* stats) {
+  Part& P = c->parts[0];
+  if (!c->d_params) CUDA_TRY(c, dalloc(c, &c->d_params, cohort_param_doubles()));
+  if (c->params_uploaded != c->param_version) {
+    std::vector<double> h(cohort_param_doubles());
+    cohort_pack_params(c->cfg.model, c->tt, c->ms, h.data());
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_params, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->params_uploaded = c->param_version;
+  }
+  R = CoRep{};
+  R.slice_ptr = P.d_sp;
+  R.col = P.d_col;
+  R.A = P.d_A;
+  R.K = P.d_K;
+  R.dinv = P.d_dinv;
+  R.nslices = P.nslices;
+  R.n = (int32_t)P.n;
+  R.stride = P.n_pad;
+  for (int b = 0; b < 3; ++b) R.V[b] = P.d_V[b];
+  R.U = P.d_U;
+  R.r = P.d_r;
+  R.z = P.d_z;
+  R.q = P.d_q;
+  R.p0 = P.d_p0;
+  R.p1 = P.d_p1;
+  R.up = P.d_up;
+  R.vp = P.d_vp;
+  R.act = P.d_act;
+  R.lat = P.d_lat;
+  R.lrt = P.d_lrt;
+  R.flags = c->d_flags;
+  R.stats = stats;
+  R.ep = P.d_ep;
+  R.stim_idx = P.d_stim_idx;
+  R.stim_s = P.d_stim_s;
+  R.n_ep = (int32_t)P.epochs.size();
+  R.iVk = c->iVk;
+  R.iVkm1 = c->iVkm1;
+  R.iX = c->iX;
+  R.has_prev = c->has_prev ? 1 : 0;
+  R.max_iters = c->cfg.max_iters;
+  R.rel_mode = c->cfg.rel_mode;
+  R.k0 = c->k;
+  R.dt = c->cfg.dt;
+  R.theta = c->cfg.theta;
+  R.eps_a = c->cfg.abs_tol;
+  R.eps_r = c->cfg.rel_tol;
+  R.lat_thr = c->cfg.lat_threshold;
+  R.lrt_thr = c->cfg.lrt_threshold;
+  R.params = c->d_params;
+  return TC_OK;
+}
+
+// Host bookkeeping of n steps taken by the cluster engine (the kernel rotated
+// the same three buffers the same way).
+static void advance_host(tc_ctx* c, int64_t nsteps) {
+  for (int64_t st = 0; st < nsteps; ++st) {
+    const int old = c->iVkm1;
+    c->iVkm1 = c->iVk;
+    c->iVk = c->iX;
+    c->iX = old;
+  }
+  c->k += nsteps;
+  c->has_prev = true;
+}
+
+static tc_status finish_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* stats, size_t evi, bool cluster);
+
 extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
   if (!c) return TC_EINVAL;
   if (!c->assembled || c->csr_mode) return fail(c, TC_ESTATE, "tc_step before tc_assemble");
@@ -1070,6 +1181,18 @@ extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
   TC_TRY(ensure_stats(c, nsteps));
   const int model = c->cfg.model;
   size_t evi = 0;
+  if (use_cluster(c)) {  // the whole call as one cluster-engine launch
+    CoRep R;
+    TC_TRY(make_corep(c, R, c->d_stats));
+    if (!c->d_corep) CUDA_TRY(c, dalloc(c, &c->d_corep, 1));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_corep, &R, sizeof(CoRep), cudaMemcpyHostToDevice, c->stream));
+    if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+    CUDA_TRY(c, launch_cohort(model, c->d_corep, 1, c->co_csize, c->co_smem, nsteps, c->stream));
+    c->launches += 1;
+    if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+    advance_host(c, nsteps);
+    return finish_steps(c, nsteps, stats, evi, true);
+  }
   for (int64_t st = 0; st < nsteps; ++st) {
     if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (1) ionic step + LAT/LRT of V^k + x0, u', v'; (2) stimulus of the epoch of step k
@@ -1126,13 +1249,24 @@ extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
       c->launches += 1;
     }
   if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+  return finish_steps(c, nsteps, stats, evi, false);
+}
+
+static tc_status finish_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* stats, size_t evi, bool cluster) {
+  (void)evi;
   std::vector<tc_step_stat> hst(nsteps);
   int32_t flags[8];
   CUDA_TRY(c, cudaMemcpyAsync(hst.data(), c->d_stats, nsteps * sizeof(tc_step_stat), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(flags, c->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   if (stats) std::memcpy(stats, hst.data(), nsteps * sizeof(tc_step_stat));
-  if (c->prof) {
+  if (c->prof && cluster) {  // one launch: the whole step is attributed to the PCG path
+    float a = 0;
+    cudaEventElapsedTime(&a, c->evs[0], c->evs[1]);
+    c->t_cg += a;
+    for (int64_t s = 0; s < nsteps; ++s) c->prof_iters += hst[s].iters;
+    c->prof_steps += nsteps;
+  } else if (c->prof) {
     for (int64_t s = 0; s < nsteps; ++s) {
       float a = 0, b = 0;
       cudaEventElapsedTime(&a, c->evs[3 * s], c->evs[3 * s + 1]);
@@ -1427,6 +1561,184 @@ tc_status tc_partition_plan(int64_t n, const int64_t* rowptr, const int32_t* col
   if (recv_off) std::copy(P.recv_off.begin(), P.recv_off.end(), recv_off);
   if (send_off) std::copy(P.send_off.begin(), P.send_off.end(), send_off);
   if (send_g) std::copy(P.send_g.begin(), P.send_g.end(), send_g);
+  return TC_OK;
+}
+
+}  // extern "C"
+
+extern "C" tc_status tc_engine_info(tc_ctx* c, int64_t out[4]) {
+  if (!c || !out) return TC_EINVAL;
+  if (!c->assembled || c->csr_mode) return fail(c, TC_ESTATE, "tc_engine_info before tc_assemble");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const bool cl = use_cluster(c);
+  out[0] = cl ? TC_ENGINE_CLUSTER : TC_ENGINE_GRID;
+  out[1] = cl ? c->co_csize : 0;
+  out[2] = cl ? (int64_t)c->co_smem : 0;
+  out[3] = cl ? cohort_active_clusters(c->cfg.model, c->co_csize, c->co_smem) : 0;
+  return TC_OK;
+}
+
+// ------------------------------------------------------------------ cohorts
+struct tc_cohort {
+  std::vector<tc_ctx*> m;
+  int device = 0, model = 0, csize = 1;
+  size_t smem = 0;                 // dynamic shared memory per CTA (0 = streaming)
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev = nullptr;
+  std::string err;
+  std::vector<void*> allocs;
+  CoRep* d_reps = nullptr;
+  tc_step_stat* d_stats = nullptr;
+  int64_t stats_cap = 0;
+  int32_t* d_status = nullptr;
+  std::vector<CoRep> h;
+};
+
+static tc_status cfail(tc_cohort* co, tc_status st, const std::string& msg) {
+  if (co) co->err = msg;
+  return st;
+}
+#define CO_CUDA(co, expr)                                                              \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return cfail((co), TC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+static cudaError_t co_alloc(tc_cohort* co, T** p, int64_t count) {
+  void* v = nullptr;
+  cudaError_t e = cudaMalloc(&v, (size_t)std::max<int64_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) return e;
+  co->allocs.push_back(v);
+  *p = (T*)v;
+  return cudaSuccess;
+}
+
+extern "C" {
+
+tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluster_size,
+                           int32_t resident, tc_cohort** out) {
+  if (!members || count <= 0 || !out) return TC_EINVAL;
+  *out = nullptr;
+  if (cluster_size < 0 || cluster_size > kCoMaxCluster || (cluster_size & (cluster_size - 1)))
+    return TC_EINVAL;
+  tc_ctx* m0 = members[0];
+  if (!m0) return TC_EINVAL;
+  int64_t max_slices = 0;
+  for (int32_t i = 0; i < count; ++i) {
+    tc_ctx* c = members[i];
+    if (!c) return TC_EINVAL;
+    if (!c->assembled || c->csr_mode) return fail(m0, TC_ESTATE, "cohort member " + std::to_string(i) + " is not assembled");
+    if (!cluster_capable(c))
+      return fail(m0, c->cfg.model == TC_ION_MMS ? TC_EINVAL : TC_ESTATE,
+                  "cohort member " + std::to_string(i) + " is partitioned, multi-GPU or MMS");
+    if (c->device != m0->device || c->cfg.model != m0->cfg.model)
+      return fail(m0, TC_EINVAL, "cohort member " + std::to_string(i) + ": device or ionic model differs from member 0");
+    for (int32_t j = 0; j < i; ++j)
+      if (members[j] == c) return fail(m0, TC_EINVAL, "cohort member " + std::to_string(i) + " repeats member " + std::to_string(j));
+    max_slices = std::max<int64_t>(max_slices, c->parts[0].nslices);
+  }
+  if (cudaSetDevice(m0->device) != cudaSuccess) return TC_ECUDA;
+  tc_cohort* co = new tc_cohort();
+  co->m.assign(members, members + count);
+  co->device = m0->device;
+  co->model = m0->cfg.model;
+  co->stream = m0->stream;
+  // auto: one slice per warp where possible; when the members outnumber the clusters of
+  // that size that fit at once, halve the size (more members in flight; measured on the
+  // configs[0] cohort: 16 CTAs 0.39, 8 CTAs 0.69 G node-steps/s at 74 members)
+  int want = cluster_size ? cluster_size : cluster_want(max_slices);
+  if (!cluster_size && want > 8 && count > cohort_active_clusters(co->model, want, 0)) want = 8;
+  co->csize = cohort_cluster_size(co->model, want);
+  if (co->csize == 0 || (cluster_size && co->csize != cluster_size)) {
+    delete co;
+    return fail(m0, TC_EINVAL, "cohort: the device cannot run clusters of the requested size");
+  }
+  if (resident) {  // cluster-resident when the largest member block fits
+    size_t need = 0;
+    for (tc_ctx* c : co->m)
+      need = std::max(need, cohort_smem_bytes(c->parts[0].h_sp.data(), c->parts[0].nslices, co->csize));
+    if (need <= cohort_smem_limit(co->model) && cohort_active_clusters(co->model, co->csize, need) > 0)
+      co->smem = need;
+  }
+  if (cudaEventCreateWithFlags(&co->ev, cudaEventDisableTiming) != cudaSuccess ||
+      co_alloc(co, &co->d_reps, count) != cudaSuccess || co_alloc(co, &co->d_status, count) != cudaSuccess) {
+    tc_cohort_destroy(co);
+    return TC_ENOMEM;
+  }
+  co->h.resize(count);
+  *out = co;
+  return TC_OK;
+}
+
+tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
+  if (!co) return TC_EINVAL;
+  if (nsteps < 0) return cfail(co, TC_EINVAL, "tc_cohort_step: negative step count");
+  if (nsteps == 0) return TC_OK;
+  CO_CUDA(co, cudaSetDevice(co->device));
+  const int64_t cnt = (int64_t)co->m.size();
+  if (co->stats_cap < cnt * nsteps) {
+    if (co->d_stats) {
+      cudaStreamSynchronize(co->stream);
+      cudaFree(co->d_stats);
+      co->allocs.erase(std::find(co->allocs.begin(), co->allocs.end(), (void*)co->d_stats));
+    }
+    CO_CUDA(co, co_alloc(co, &co->d_stats, cnt * nsteps));
+    co->stats_cap = cnt * nsteps;
+  }
+  for (int64_t i = 0; i < cnt; ++i) {
+    tc_ctx* c = co->m[i];
+    if (make_corep(c, co->h[i], co->d_stats + i * nsteps) != TC_OK)
+      return cfail(co, TC_ECUDA, "cohort member " + std::to_string(i) + ": " + c->err);
+    co->h[i].status = co->d_status + i;
+  }
+  // order after every member's pending work
+  for (int64_t i = 1; i < cnt; ++i)
+    if (co->m[i]->stream != co->stream) {
+      CO_CUDA(co, cudaEventRecord(co->ev, co->m[i]->stream));
+      CO_CUDA(co, cudaStreamWaitEvent(co->stream, co->ev, 0));
+    }
+  CO_CUDA(co, cudaMemcpyAsync(co->d_reps, co->h.data(), cnt * sizeof(CoRep), cudaMemcpyHostToDevice, co->stream));
+  CO_CUDA(co, launch_cohort(co->model, co->d_reps, (int)cnt, co->csize, co->smem, nsteps, co->stream));
+  CO_CUDA(co, cudaEventRecord(co->ev, co->stream));
+  for (int64_t i = 1; i < cnt; ++i)
+    if (co->m[i]->stream != co->stream) CO_CUDA(co, cudaStreamWaitEvent(co->m[i]->stream, co->ev, 0));
+  for (tc_ctx* c : co->m) {
+    advance_host(c, nsteps);
+    c->launches += 1.0 / (double)cnt;
+  }
+  std::vector<int32_t> status(cnt);
+  CO_CUDA(co, cudaMemcpyAsync(status.data(), co->d_status, cnt * 4, cudaMemcpyDeviceToHost, co->stream));
+  if (stats)
+    CO_CUDA(co, cudaMemcpyAsync(stats, co->d_stats, cnt * nsteps * sizeof(tc_step_stat), cudaMemcpyDeviceToHost, co->stream));
+  CO_CUDA(co, cudaStreamSynchronize(co->stream));
+  for (int64_t i = 0; i < cnt; ++i)
+    if (status[i])
+      return cfail(co, status[i] == 2 ? TC_ENAN : TC_ESOLVER,
+                   "cohort member " + std::to_string(i) +
+                       (status[i] == 2 ? ": NaN in a PCG inner product" : ": PCG fail budget exhausted"));
+  return TC_OK;
+}
+
+tc_status tc_cohort_info(const tc_cohort* co, int32_t out[4]) {
+  if (!co || !out) return TC_EINVAL;
+  out[0] = (int32_t)co->m.size();
+  out[1] = co->csize;
+  out[2] = cohort_active_clusters(co->model, co->csize, co->smem);
+  out[3] = (int32_t)co->smem;
+  return TC_OK;
+}
+
+const char* tc_cohort_last_error(const tc_cohort* co) { return co ? co->err.c_str() : "null cohort"; }
+
+tc_status tc_cohort_destroy(tc_cohort* co) {
+  if (!co) return TC_OK;
+  cudaSetDevice(co->device);
+  if (co->stream) cudaStreamSynchronize(co->stream);
+  for (void* p : co->allocs) cudaFree(p);
+  if (co->ev) cudaEventDestroy(co->ev);
+  delete co;
   return TC_OK;
 }
 

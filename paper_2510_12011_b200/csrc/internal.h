@@ -209,6 +209,50 @@ struct AsmArgs {
   int32_t* err;
 };
 
+// ---- cluster engine / cohorts (cohort.cu) ------------------------------------
+constexpr int kCoThreads = 256;     // threads per CTA of the cluster engine
+constexpr int kCoMaxCluster = 16;   // CTAs per cluster (non-portable size 16 where allowed)
+constexpr int kClusterAutoSlices = 256;   // TC_ENGINE_AUTO: cluster engine up to 8 192 rows (measured crossover between 4.3k and 30k nodes)
+struct StimEpoch {
+  int64_t k0, k1;  // step window [k0, k1)
+  int32_t off, m;  // slice of the (local index, s) list
+};
+// Device descriptor of one replica: a single-partition context's buffers and
+// settings at the start of a cluster-engine launch.
+struct CoRep {
+  const int64_t* slice_ptr;
+  const int32_t* col;
+  const double* A;
+  const double* K;
+  const double* dinv;
+  int32_t nslices, n;
+  int64_t stride;                // n_pad (SoA state stride)
+  double* V[3];
+  double *U, *r, *z, *q, *p0, *p1, *up, *vp;
+  uint8_t* act;
+  double *lat, *lrt;
+  int32_t* flags;
+  tc_step_stat* stats;           // nsteps entries
+  int32_t* status;               // nullable: 0 ran, 1 stopped by the fail budget, 2 NaN
+  const StimEpoch* ep;
+  const int32_t* stim_idx;
+  const double* stim_s;
+  int32_t n_ep;
+  int32_t iVk, iVkm1, iX, has_prev, max_iters, rel_mode, pad;
+  int64_t k0;
+  double dt, theta, eps_a, eps_r, lat_thr, lrt_thr;
+  const double* params;          // cohort_pack_params block (device)
+};
+int cohort_param_doubles();
+void cohort_pack_params(int model, const TTParams& tp, const MSParams& mp, double* out);
+int cohort_cluster_size(int model, int want);
+int cohort_active_clusters(int model, int csize, size_t smem);  // smem 0 = streaming launch
+size_t cohort_smem_bytes(const int64_t* sp, int32_t ns, int C);
+size_t cohort_smem_limit(int model);
+// smem > 0: cluster-resident launch with that much dynamic shared memory per CTA
+cudaError_t launch_cohort(int model, const CoRep* d_reps, int nrep, int csize, size_t smem,
+                          int64_t nsteps, cudaStream_t s);
+
 // ---- launchers (return cudaError_t of the launch) --------------------------
 cudaError_t launch_assemble(const AsmArgs& a, cudaStream_t s);
 cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s);

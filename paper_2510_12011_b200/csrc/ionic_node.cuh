@@ -1,0 +1,289 @@
+// ionic_node.cuh -- per-node device code of the ionic step (Eq. 2 row 1, P:128;
+// P:139), the LAT/LRT test and the RHS vectors x0, u', v' (P:200-203,
+// DESIGN.md "RHS"), shared by the per-step kernels (ionic.cu) and the cohort
+// engine (cohort.cu), so both paths run the same arithmetic per node.
+#pragma once
+
+#include "fp64math.cuh"
+#include "internal.h"
+
+namespace tcb {
+
+
+// ------------------------------------------------------------------ LAT / LRT
+__device__ __forceinline__ void activation_update(const IonArgs& a, int64_t i, double Vnow,
+                                                  double Vprev) {
+  const uint8_t st = a.act[i];
+  if (st == 0) {
+    if (Vnow > a.lat_thr) { a.lat[i] = a.t_k; a.act[i] = 1; }      // first V > 0
+  } else if (st == 1) {
+    if (Vnow < a.lrt_thr && Vnow - Vprev < 0.0) { a.lrt[i] = a.t_k; a.act[i] = 2; }
+  }
+}
+
+__device__ __forceinline__ void write_rhs(const IonArgs& a, int64_t i, double V, double Vp,
+                                          double In) {
+  const double x0 = 2.0 * V - Vp;
+  const double dv = -a.dt * In;            // y - V^k
+  a.x0[i] = x0;
+  a.up[i] = (V + dv) - x0;
+  a.vp[i] = a.dt * (V + a.theta * dv);
+}
+
+// ------------------------------------------------------------------ TT2006 epi
+// ten Tusscher & Panfilov 2006 (cited P:98), epicardial cell; states in the
+// order Ki Nai Cai CaSS CaSR Rbar m h j xr1 xr2 xs r s d f f2 fCass.
+//
+// Arithmetic layout: exact in exact arithmetic to
+// the model equations, rearranged for the FP64 pipe -- branch-free exp /
+// reciprocal (fp64math.cuh), division by constants as multiplication by
+// their reciprocals, parameter-only factors folded on the host (TTDerived),
+// and voltage exponentials that share a slope computed from one exponential,
+// e.g. exp((V+35)/5) = e^7 exp(V/5), exp((-60-V)/5) = e^-12 / exp(V/5).
+enum { sKi, sNai, sCai, sCaSS, sCaSR, sRbar, sm, sh, sj, sxr1, sxr2, sxs, sr, ss, sd, sf, sf2, sfc };
+
+struct TTDerived {      // parameter-only factors (host-computed per launch)
+  double frt, rtf;      // F/RT, RT/F
+  double sq_ko;         // sqrt(Ko / 5.4)
+  double ecal0;         // exp(-30 F/RT)
+  double gcal4;         // 4 GCaL F^2/RT
+  double inaca_k;       // kNaCa / ((KmNai^3 + Nao^3)(KmCa + Cao))
+  double nao3_alpha;    // Nao^3 alpha
+  double inak_k;        // PNaK Ko / (Ko + KmK)
+  double eks_num;       // Ko + pKNa Nao
+  double vc_vss, vsr_vss, vsr_vc;
+  double cap_2vssf, cap_2vcf, cap_vcf;
+  double kup2;          // Kup^2
+  // e^c of the constant offsets of the shared-slope voltage exponentials
+  double x_m12, x_7, x_m3_2, x_m26_7, x_m4_5, x_m3, x_5_6, x_20_6, x_4, x_m4, x_1, x_2_5, x_3,
+      x_20_7, x_1_3, x_5, x_m1;
+};
+
+struct TTVolt {         // factors that depend on V only (shared by both current evaluations)
+  double ecal;          // exp(2 (V-15) F/RT)
+  double enaca_a;       // exp(gamma V F/RT)
+  double enaca_b;       // exp((gamma-1) V F/RT)
+  double fnak;          // 1 / (1 + 0.1245 exp(-0.1 V F/RT) + 0.0353 exp(-V F/RT))
+  double fpk;           // 1 / (1 + exp((25 - V)/5.98))
+};
+
+struct TTCur {
+  double ina, ik1, ito, ikr, iks, ical, inaca, inak, ipca, ipk, ibna, ibca;
+};
+
+#define EXP(x) tc_exp((x), T)
+
+__device__ __forceinline__ double sig(double x, const Exp2Table* T) {  // 1 / (1 + e^x)
+  return tc_rcp(1.0 + EXP(x));
+}
+
+__device__ __forceinline__ TTVolt tt_volt(double V, const TTParams& P, const TTDerived& D,
+                                          const Exp2Table* T) {
+  TTVolt f;
+  const double E = EXP(V * D.frt);          // exp(V F/RT)
+  const double iE = tc_rcp(E);
+  f.ecal = E * E * D.ecal0;                 // exp(2 (V - 15) F/RT)
+  f.enaca_a = EXP(P.gamma * V * D.frt);
+  f.enaca_b = f.enaca_a * iE;               // exp((gamma - 1) V F/RT)
+  f.fnak = tc_rcp(1.0 + 0.1245 * EXP(-0.1 * V * D.frt) + 0.0353 * iE);
+  f.fpk = tc_rcp(1.0 + EXP((25.0 - V) * (1.0 / 5.98)));
+  return f;
+}
+
+__device__ __forceinline__ TTCur tt_cur(double V, const double* u, const TTParams& P,
+                                        const TTDerived& D, const TTVolt& f, const Exp2Table* T) {
+  const double ek = D.rtf * log(P.Ko * tc_rcp(u[sKi]));
+  const double ena = D.rtf * log(P.Nao * tc_rcp(u[sNai]));
+  const double eks = D.rtf * log(D.eks_num * tc_rcp(u[sKi] + P.pKNa * u[sNai]));
+  const double eca = 0.5 * D.rtf * log(P.Cao * tc_rcp(u[sCai]));
+  TTCur c;
+  c.ina = P.GNa * u[sm] * u[sm] * u[sm] * u[sh] * u[sj] * (V - ena);
+  {
+    const double dvk = V - ek;
+    const double a1 = 0.1 * tc_rcp(1.0 + EXP(0.06 * (dvk - 200.0)));
+    const double e1 = EXP(0.1 * dvk);                 // exp(0.1 (V - EK))
+    const double e2 = e1 * e1, e5 = e2 * e2 * e1;     // exp(0.5 (V - EK))
+    const double b1 = (3.0 * EXP(0.0002 * (dvk + 100.0)) + e1 * D.x_m1) *
+                      tc_rcp(1.0 + tc_rcp(e5));
+    c.ik1 = P.GK1 * (a1 * tc_rcp(a1 + b1)) * dvk;
+  }
+  c.ito = P.Gto * u[sr] * u[ss] * (V - ek);
+  c.ikr = P.GKr * D.sq_ko * u[sxr1] * u[sxr2] * (V - ek);
+  c.iks = P.GKs * u[sxs] * u[sxs] * (V - eks);
+  c.ical = D.gcal4 * u[sd] * u[sf] * u[sf2] * u[sfc] * (V - 15.0) *
+           (0.25 * u[sCaSS] * f.ecal - P.Cao) * tc_rcp(f.ecal - 1.0);
+  {
+    const double nai3 = u[sNai] * u[sNai] * u[sNai];
+    c.inaca = D.inaca_k * (f.enaca_a * nai3 * P.Cao - f.enaca_b * D.nao3_alpha * u[sCai]) *
+              tc_rcp(1.0 + P.ksat * f.enaca_b);
+  }
+  c.inak = D.inak_k * u[sNai] * f.fnak * tc_rcp(u[sNai] + P.KmNa);
+  c.ipca = P.GpCa * u[sCai] * tc_rcp(P.KpCa + u[sCai]);
+  c.ipk = P.GpK * f.fpk * (V - ek);
+  c.ibna = P.GbNa * (V - ena);
+  c.ibca = P.GbCa * (V - eca);
+  return c;
+}
+
+__device__ __forceinline__ double tt_total(const TTCur& c) {
+  return c.ina + c.ik1 + c.ito + c.ikr + c.iks + c.ical + c.inaca + c.inak + c.ipca + c.ipk +
+         c.ibna + c.ibca;
+}
+
+// c_new of a rapidly buffered pool: c + B c/(c+K) grows by delta.
+__device__ __forceinline__ double buffered(double c, double delta, double B, double K) {
+  const double bound = B * c * tc_rcp(c + K);
+  const double bb = B - bound - delta - c + K;
+  const double cc = K * (bound + delta + c);
+  return 0.5 * (sqrt(bb * bb + 4.0 * cc) - bb);
+}
+
+// Rush-Larsen with the rate 1/tau given
+__device__ __forceinline__ double rl_rate(double y, double yinf, double inv_tau, double dt,
+                                          const Exp2Table* T) {
+  return yinf - (yinf - y) * EXP(-dt * inv_tau);
+}
+
+// Advances u in place; returns I_n(V, u^{k+1}).
+__device__ __forceinline__ double tt_advance(double V, double* u, double dt, const TTParams& P,
+                                             const TTDerived& D, const Exp2Table* T) {
+  const TTVolt f = tt_volt(V, P, D, T);
+  const TTCur c = tt_cur(V, u, P, D, f, T);
+  // -- calcium dynamics (currents and fluxes at (V^k, u^k)) --
+  const double casr = u[sCaSR], cass = u[sCaSS], cai = u[sCai];
+  const double ec = P.EC * tc_rcp(casr);
+  const double kcasr = P.maxsr - (P.maxsr - P.minsr) * tc_rcp(1.0 + ec * ec);
+  const double k1 = P.k1p * tc_rcp(kcasr), k2 = P.k2p * kcasr;
+  const double rbar = u[sRbar] + dt * (P.k4 * (1.0 - u[sRbar]) - k2 * cass * u[sRbar]);
+  const double oo = k1 * cass * cass * rbar * tc_rcp(P.k3 + k1 * cass * cass);
+  const double irel = P.Vrel * oo * (casr - cass);
+  const double ileak = P.Vleak * (casr - cai);
+  const double iup = P.Vmaxup * tc_rcp(1.0 + D.kup2 * tc_rcp(cai * cai));
+  const double ixfer = P.Vxfer * (cass - cai);
+  const double nu_sr = dt * (iup - irel - ileak);
+  const double nu_ss = dt * (-ixfer * D.vc_vss + irel * D.vsr_vss - c.ical * D.cap_2vssf);
+  const double nu_i = dt * (-(c.ibca + c.ipca - 2.0 * c.inaca) * D.cap_2vcf -
+                            (iup - ileak) * D.vsr_vc + ixfer);
+  u[sRbar] = rbar;
+  u[sCaSR] = buffered(casr, nu_sr, P.Bufsr, P.Kbufsr);
+  u[sCaSS] = buffered(cass, nu_ss, P.Bufss, P.Kbufss);
+  u[sCai] = buffered(cai, nu_i, P.Bufc, P.Kbufc);
+  u[sNai] = u[sNai] - dt * (c.ina + c.ibna + 3.0 * c.inak + 3.0 * c.inaca) * D.cap_vcf;
+  u[sKi] = u[sKi] - dt * (c.ik1 + c.ito + c.ikr + c.iks - 2.0 * c.inak + c.ipk) * D.cap_vcf;
+
+  // -- gates, Rush-Larsen at V^k (fCass with the new CaSS) --
+  // shared-slope exponentials
+  const double e5 = EXP(V * (1.0 / 5.0)), ie5 = tc_rcp(e5);
+  const double e7 = EXP(V * (1.0 / 7.0)), ie7 = tc_rcp(e7);
+  const double e10 = EXP(V * (1.0 / 10.0)), ie10 = tc_rcp(e10);
+  const double e20 = EXP(V * (1.0 / 20.0)), ie20 = tc_rcp(e20);
+  const double e6 = EXP(V * (1.0 / 6.0)), ie6 = tc_rcp(e6);
+  {
+    const double am = tc_rcp(1.0 + D.x_m12 * ie5);     // (-60-V)/5: e^-12
+    const double bm = 0.1 * tc_rcp(1.0 + D.x_7 * e5)    // (V+35)/5: e^7
+                      + 0.1 * sig((V - 50.0) * (1.0 / 200.0), T);
+    const double mi = sig((-56.86 - V) * (1.0 / 9.03), T);
+    u[sm] = rl_rate(u[sm], mi * mi, tc_rcp(am * bm), dt, T);
+  }
+  {
+    const double hi = sig((V + 71.55) * (1.0 / 7.43), T);
+    const double hinf = hi * hi;
+    double ah, bh, aj, bj;
+    if (V >= -40.0) {
+      ah = 0.0;
+      bh = 0.77 * tc_rcp(0.13 * (1.0 + EXP(-(V + 10.66) * (1.0 / 11.1))));
+      aj = 0.0;
+      bj = 0.6 * EXP(0.057 * V) * tc_rcp(1.0 + D.x_m3_2 * ie10);   // e^-3.2
+    } else {
+      ah = 0.057 * EXP(-(V + 80.0) * (1.0 / 6.8));
+      bh = 2.7 * EXP(0.079 * V) + 3.1e5 * EXP(0.3485 * V);
+      aj = (-2.5428e4 * EXP(0.2444 * V) - 6.948e-6 * EXP(-0.04391 * V)) * (V + 37.78) *
+           tc_rcp(1.0 + EXP(0.311 * (V + 79.23)));
+      bj = 0.02424 * EXP(-0.01052 * V) * tc_rcp(1.0 + EXP(-0.1378 * (V + 40.14)));
+    }
+    u[sh] = rl_rate(u[sh], hinf, ah + bh, dt, T);
+    u[sj] = rl_rate(u[sj], hinf, aj + bj, dt, T);
+  }
+  {
+    const double xr1_inf = tc_rcp(1.0 + D.x_m26_7 * ie7);       // (-26-V)/7: e^(-26/7)
+    const double a = 450.0 * tc_rcp(1.0 + D.x_m4_5 * ie10);    // (-45-V)/10: e^-4.5
+    const double b = 6.0 * sig((V + 30.0) * (1.0 / 11.5), T);
+    u[sxr1] = rl_rate(u[sxr1], xr1_inf, tc_rcp(a * b), dt, T);
+  }
+  {
+    const double xr2_inf = sig((V + 88.0) * (1.0 / 24.0), T);
+    const double a = 3.0 * tc_rcp(1.0 + D.x_m3 * ie20);      // (-60-V)/20: e^-3
+    const double b = 1.12 * tc_rcp(1.0 + D.x_m3 * e20);      // (V-60)/20: e^-3
+    u[sxr2] = rl_rate(u[sxr2], xr2_inf, tc_rcp(a * b), dt, T);
+  }
+  {
+    const double xs_inf = sig((-5.0 - V) * (1.0 / 14.0), T);
+    const double tau = 1400.0 * tc_rcp(sqrt(1.0 + D.x_5_6 * ie6))  // (5-V)/6: e^(5/6)
+                       * sig((V - 35.0) * (1.0 / 15.0), T) + 80.0;
+    u[sxs] = rl_rate(u[sxs], xs_inf, tc_rcp(tau), dt, T);
+  }
+  {
+    const double r_inf = tc_rcp(1.0 + D.x_20_6 * ie6);              // (20-V)/6: e^(10/3)
+    const double d40 = V + 40.0;
+    const double tau = 9.5 * EXP(-d40 * d40 * (1.0 / 1800.0)) + 0.8;
+    u[sr] = rl_rate(u[sr], r_inf, tc_rcp(tau), dt, T);
+  }
+  {
+    const double s_inf = tc_rcp(1.0 + D.x_4 * e5);              // (V+20)/5: e^4
+    const double d45 = V + 45.0;
+    const double tau = 85.0 * EXP(-d45 * d45 * (1.0 / 320.0)) +
+                       5.0 * tc_rcp(1.0 + D.x_m4 * e5) + 3.0;   // (V-20)/5: e^-4
+    u[ss] = rl_rate(u[ss], s_inf, tc_rcp(tau), dt, T);
+  }
+  {
+    const double d_inf = sig((-8.0 - V) * (1.0 / 7.5), T);
+    const double tau = (1.4 * sig((-35.0 - V) * (1.0 / 13.0), T) + 0.25) *
+                           (1.4 * tc_rcp(1.0 + D.x_1 * e5)) +     // (V+5)/5: e
+                       tc_rcp(1.0 + D.x_2_5 * ie20);               // (50-V)/20: e^2.5
+    u[sd] = rl_rate(u[sd], d_inf, tc_rcp(tau), dt, T);
+  }
+  const double s30 = tc_rcp(1.0 + D.x_3 * e10);                 // (V+30)/10: e^3
+  {
+    const double f_inf = tc_rcp(1.0 + D.x_20_7 * e7);                // (V+20)/7: e^(20/7)
+    const double d27 = V + 27.0;
+    const double tau = 1102.5 * EXP(-d27 * d27 * (1.0 / 225.0)) +
+                       200.0 * tc_rcp(1.0 + D.x_1_3 * ie10) +      // (13-V)/10: e^1.3
+                       180.0 * s30 + 20.0;
+    u[sf] = rl_rate(u[sf], f_inf, tc_rcp(tau), dt, T);
+  }
+  {
+    const double f2_inf = 0.67 * tc_rcp(1.0 + D.x_5 * e7) + 0.33; // (V+35)/7: e^5
+    const double d25 = V + 25.0;
+    const double tau = 600.0 * EXP(-d25 * d25 * (1.0 / 170.0)) +
+                       31.0 * tc_rcp(1.0 + D.x_2_5 * ie10) +        // (25-V)/10: e^2.5
+                       16.0 * s30;
+    u[sf2] = rl_rate(u[sf2], f2_inf, tc_rcp(tau), dt, T);
+  }
+  {
+    const double q = u[sCaSS] * (1.0 / 0.05);
+    const double den = tc_rcp(1.0 + q * q);
+    u[sfc] = rl_rate(u[sfc], 0.6 * den + 0.4, tc_rcp(80.0 * den + 2.0), dt, T);
+  }
+  return tt_total(tt_cur(V, u, P, D, f, T));  // I_ion(V^k, u^{k+1}) (reading I2)
+}
+
+// ------------------------------------------------------------------ Mitchell-Schaeffer
+struct MSDerived {  // reciprocals of the time constants (host-computed)
+  double span, inv_open, inv_close, inv_in, inv_out;
+};
+
+// Advances the gate h in place (forward Euler at V^k); returns I_n(V^k, h^{k+1}).
+__device__ __forceinline__ double ms_advance(double V, double* h_io, double dt, const MSParams& P,
+                                             const MSDerived& D) {
+  // the gate decision uses the same correctly rounded division as the oracle
+  const double v = (V - P.V_min) / D.span;
+  double h = *h_io;
+  h = (v < P.v_gate) ? h + dt * ((1.0 - h) * D.inv_open) : h + dt * (-h * D.inv_close);
+  *h_io = h;
+  return -D.span * (h * v * v * (1.0 - v) * D.inv_in - v * D.inv_out);
+}
+
+TTDerived tt_derived(const TTParams& P);
+MSDerived ms_derived(const MSParams& P);
+
+}  // namespace tcb

@@ -1,0 +1,250 @@
+"""GPU parity of the cluster engine and of cohorts.
+
+The cluster engine runs every step of a tc_step call inside one thread-block
+cluster; a cohort runs many independent members
+in one launch, one cluster each, with per-member PCG stopping.  Each member is
+checked against its own CPU oracle run (same seeded inputs) with the
+north_star tolerances: V per step within rel-L2 1e-8, LAT within one dt,
+per-step PCG iteration counts within 1."""
+import numpy as np
+import pytest
+
+import meshgen as G
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SIG = (0.1334177, 0.0173515)   # Table 3
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2510_12011_b200 as T
+    return T
+
+
+def _member(spec):
+    """spec -> (xyz, tets, region, fibre, cond, stimuli, oracle Config kwargs, params dict)."""
+    kind = spec.get("mesh", "slab")
+    if kind == "biv":
+        m = G.biv(spec.get("h", 2.5))
+        xyz, tets, region, fib = m["xyz"], m["tets"], m["region"], m["fibre"]
+        stims = [O.Stimulus(nodes, 0.0, 2.0, 50.0) for nodes in G.biv_stimuli(m, radius=3.0)]
+        cond = {0: SIG, 1: SIG}
+    else:
+        nx, ny, nz = spec["dims"]
+        dx = spec.get("dx", 0.5)
+        xyz, tets = G.kuhn_box(nx, ny, nz, dx)
+        if spec.get("permute"):
+            xyz, tets, _ = G.permute_nodes(xyz, tets, seed=spec["permute"])
+        E = tets.shape[0]
+        region = np.zeros(E, np.int32)
+        fib = G.random_fibres(E, spec["fib_seed"]) if spec.get("fib_seed") else G.uniform_fibres(E)
+        sl, st = SIG
+        s = spec.get("sigma_scale", 1.0)
+        cond = {0: (sl * s, st * s)}
+        hi = spec.get("stim_box", 1.5)
+        stims = [O.Stimulus(G.nodes_in_box(xyz, (0, 0, 0), (hi, hi, hi)), spec.get("t0", 0.0),
+                            2.0, spec.get("amp", 50.0))]
+    return xyz, tets, region, fib, cond, stims
+
+
+def _oracle(spec, xyz, tets, region, fib, cond, stims):
+    model = spec.get("model", "tt2006")
+    params = None
+    if spec.get("params"):
+        if model == "tt2006":
+            names, params = O.tt_param_names(), O.tt_default_params().copy()
+        else:
+            names, params = list(O.MS_PARAM_NAMES), O.ms_default_params().copy()
+        for k, v in spec["params"].items():
+            params[names.index(k)] = v
+    cfg = O.Config(dt=spec.get("dt", 0.05), model=model, abs_tol=spec.get("tol", 1e-8), rel_tol=0.0,
+                   max_iters=spec.get("max_iters", 100), fail_budget=spec.get("fail_budget", 3),
+                   params=params)
+    return O.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+
+
+def _gpu(T, spec, xyz, tets, region, fib, cond, stims, engine="cluster"):
+    cfg = T.tc_config_default(dt=spec.get("dt", 0.05), model=spec.get("model", "tt2006"),
+                              abs_tol=spec.get("tol", 1e-8), rel_tol=0.0,
+                              max_iters=spec.get("max_iters", 100),
+                              fail_budget=spec.get("fail_budget", 3), engine=engine)
+    return T.Monodomain(xyz, tets, region, fib, cond, cfg, stims, params=spec.get("params"))
+
+
+def _check(sim, ref, stats_row, reps, dt, what):
+    v = sim.V
+    rel = np.linalg.norm(v - ref.Vk) / np.linalg.norm(ref.Vk)
+    assert rel <= 1e-8, (what, rel)
+    if stats_row is not None:
+        for a, b in zip(stats_row, reps):
+            assert abs(int(a["iters"]) - b.iters) <= 1, (what, int(a["iters"]), b.iters)
+    lat, _ = sim.activation()
+    assert np.all((lat < 0) == (ref.lat < 0)), what
+    assert np.abs(lat - ref.lat).max() <= dt + 1e-12, what
+
+
+@pytest.mark.parametrize("model,permute,chunk,engine", [("tt2006", 0, 1, "cluster"), ("tt2006", 7, 9, "cluster"),
+                                                        ("ms", 0, 5, "cluster"), ("ms", 3, 1, "cluster"),
+                                                        ("tt2006", 7, 9, "cluster_streaming"),
+                                                        ("ms", 3, 4, "cluster_streaming")])
+def test_cluster_engine_trajectory_parity(T, model, permute, chunk, engine):
+    """One context on the cluster engine (shared-memory resident or streaming),
+    `chunk` steps per tc_step call (the in-kernel rotation, the V write-back and
+    the LAT epilogue across call boundaries)."""
+    spec = dict(dims=(21, 8, 5), model=model, permute=permute, fib_seed=3 if permute else 0)
+    args = _member(spec)
+    ref = _oracle(spec, *args)
+    sim = _gpu(T, spec, *args, engine=engine)
+    try:
+        info = T.tc_engine_info(sim.ctx)
+        assert info["engine"] == "cluster"
+        assert (info["smem_per_cta"] > 0) == (engine == "cluster")
+        for c in range(120 // chunk):
+            st = sim.step(chunk)
+            reps = [ref.step() for _ in range(chunk)]
+            _check(sim, ref, st, reps, 0.05, f"chunk {c}")
+        s = sim.get_state()
+        n = args[0].shape[0]
+        U = s[2 * n:-2].reshape(-1, n)
+        assert np.allclose(U, ref.U, rtol=1e-8, atol=1e-14)
+    finally:
+        sim.close()
+
+
+def test_cluster_engine_equals_grid_engine(T):
+    """Both engines compute the same step (only inner-product grouping differs)."""
+    spec = dict(dims=(41, 15, 7), model="tt2006", permute=11, fib_seed=2)
+    args = _member(spec)
+    a = _gpu(T, spec, *args, engine="cluster")
+    b = _gpu(T, spec, *args, engine="grid")
+    try:
+        for _ in range(8):
+            sa = a.step(10)
+            sb = b.step(10)
+            assert np.abs(sa["iters"] - sb["iters"]).max() <= 1
+            va, vb = a.V, b.V
+            assert np.linalg.norm(va - vb) / np.linalg.norm(vb) <= 1e-10
+        la, _ = a.activation()
+        lb, _ = b.activation()
+        assert np.array_equal(la, lb)
+    finally:
+        a.close()
+        b.close()
+
+
+COHORT = [
+    dict(dims=(21, 8, 5)),                                                  # small slab
+    dict(dims=(41, 15, 7), permute=5, fib_seed=4),                          # configs[0] mesh, relabelled
+    dict(dims=(13, 6, 4), sigma_scale=2.0, params={"GKr": 0.0765, "GNa": 11.0}),  # parameter reset
+    dict(dims=(2, 2, 2), stim_box=0.6),                                     # 8 nodes, 6 tets, one slice
+    dict(mesh="biv", h=2.5, dt=0.02),                                       # unstructured, 2 regions, other dt
+    dict(dims=(17, 9, 6), tol=1e-10, t0=1.0, amp=80.0),                     # other tolerance / stimulus
+]
+
+
+@pytest.mark.parametrize("cluster_size,resident", [(0, True), (1, False), (4, True), (4, False), (16, True)])
+def test_cohort_parity(T, cluster_size, resident):
+    """A heterogeneous cohort (meshes of 8 .. ~5k nodes, structured and BiV, other
+    dt / tolerances / conductivities / ionic parameters / stimuli) advanced in
+    chunks of 10 steps per launch; every member against its own oracle run."""
+    members, refs, dts = [], [], []
+    try:
+        for spec in COHORT:
+            args = _member(spec)
+            refs.append(_oracle(spec, *args))
+            members.append(_gpu(T, spec, *args))
+            dts.append(spec.get("dt", 0.05))
+        co = T.Cohort(members, cluster_size, resident)
+        try:
+            info = co.info()
+            assert info["members"] == len(COHORT)
+            if not resident:
+                assert info["smem_per_cta"] == 0
+            if cluster_size:
+                assert info["cluster_size"] == cluster_size
+            assert info["resident_clusters"] >= 1
+            for c in range(6):
+                stats = co.step(10)
+                assert stats.shape == (len(COHORT), 10)
+                for m, (sim, ref) in enumerate(zip(members, refs)):
+                    reps = [ref.step() for _ in range(10)]
+                    _check(sim, ref, stats[m], reps, dts[m], f"member {m} chunk {c}")
+                    assert T.tc_current_step(sim.ctx) == 10 * (c + 1)
+        finally:
+            co.close()
+        # members stay usable on their own after the cohort
+        for sim, ref in zip(members, refs):
+            st = sim.step(3)
+            reps = [ref.step() for _ in range(3)]
+            _check(sim, ref, st, reps, 0.05, "after cohort")
+    finally:
+        for s in members:
+            s.close()
+
+
+def test_cohort_of_identical_members_is_bitwise_uniform(T):
+    """Identical members give bitwise-identical results (no cross-member coupling)."""
+    spec = dict(dims=(21, 8, 5), model="ms")
+    members = [_gpu(T, spec, *_member(spec)) for _ in range(40)]
+    try:
+        co = T.Cohort(members)
+        st = co.step(50)
+        co.close()
+        v0 = members[0].V
+        for s in members[1:]:
+            assert np.array_equal(s.V, v0)
+        assert np.all(st["iters"] == st["iters"][0])
+    finally:
+        for s in members:
+            s.close()
+
+
+def test_cohort_per_member_failure(T):
+    """A member that exhausts its fail budget stops alone; the call reports it by
+    index; the other members advance exactly as their oracle runs."""
+    good = dict(dims=(21, 8, 5))
+    bad = dict(dims=(21, 8, 5), max_iters=1, fail_budget=2, tol=1e-14)
+    ga, ba = _member(good), _member(bad)
+    ref = _oracle(good, *ga)
+    members = [_gpu(T, good, *ga), _gpu(T, bad, *ba)]
+    try:
+        co = T.Cohort(members)
+        with pytest.raises(T.TcError) as ei:
+            co.step(5)
+        assert ei.value.status == T.TC_ESOLVER and "member 1" in str(ei.value)
+        reps = [ref.step() for _ in range(5)]
+        _check(members[0], ref, None, reps, 0.05, "good member")
+        with pytest.raises(T.TcError):   # the failed member's context stays failed
+            members[1].step(1)
+        co.close()
+    finally:
+        for s in members:
+            s.close()
+
+
+def test_cohort_errors(T):
+    spec = dict(dims=(9, 5, 4))
+    a = _gpu(T, spec, *_member(spec))
+    b = _gpu(T, dict(spec, model="ms"), *_member(spec))
+    cfg = T.tc_config_default(dt=0.05, partitions=2)
+    xyz, tets, region, fib, cond, stims = _member(spec)
+    p = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+    try:
+        with pytest.raises(T.TcError) as ei:
+            T.Cohort([a, b])                       # mixed ionic models
+        assert ei.value.status == T.TC_EINVAL
+        with pytest.raises(T.TcError) as ei:
+            T.Cohort([a, p])                       # partitioned member
+        assert ei.value.status == T.TC_ESTATE
+        with pytest.raises(T.TcError):
+            T.Cohort([a, a])                       # repeated member
+        with pytest.raises(T.TcError):
+            T.Cohort([a], cluster_size=3)          # not a power of two
+    finally:
+        for s in (a, b, p):
+            s.close()

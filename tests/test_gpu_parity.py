@@ -110,7 +110,7 @@ def test_step_trajectory_parity(T, model, permute, rcm, variant):
     dt = 0.05
     ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0), stims)
     cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, use_rcm=rcm,
-                              pcg_variant=variant)
+                              pcg_variant=variant, engine="grid")
     sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
     try:
         for k in range(120):
@@ -187,8 +187,8 @@ def test_nccl_path_world1_parity(T, peer):
         sim.close()
 
 
-@pytest.mark.parametrize("peer_parts", [1, 3])
-def test_biv_mesh_trajectory_parity(T, peer_parts):
+@pytest.mark.parametrize("peer_parts,engine", [(1, "grid"), (1, "cluster"), (3, "auto")])
+def test_biv_mesh_trajectory_parity(T, peer_parts, engine):
     """Synthetic BiV recipe (configs[3]) at coarse h: unstructured (jittered, randomly
     relabelled) mesh, two regions, rule-based rotating fibres, five stimulus spheres."""
     m = G.biv(2.5)
@@ -197,7 +197,7 @@ def test_biv_mesh_trajectory_parity(T, peer_parts):
     dt = 0.05
     ref = O.Monodomain(m["xyz"], m["tets"], m["region"], m["fibre"], cond,
                        O.Config(dt=dt, abs_tol=1e-8, rel_tol=0.0), stims)
-    cfg = T.tc_config_default(dt=dt, abs_tol=1e-8, rel_tol=0.0, partitions=peer_parts)
+    cfg = T.tc_config_default(dt=dt, abs_tol=1e-8, rel_tol=0.0, partitions=peer_parts, engine=engine)
     sim = T.Monodomain(m["xyz"], m["tets"], m["region"], m["fibre"], cond, cfg, stims)
     try:
         for k in range(60):
@@ -210,7 +210,8 @@ def test_biv_mesh_trajectory_parity(T, peer_parts):
         sim.close()
 
 
-def test_state_injection_one_step(T):
+@pytest.mark.parametrize("engine", ["grid", "cluster"])
+def test_state_injection_one_step(T, engine):
     """One step from an injected mid-upstroke state: GPU == oracle (any size path)."""
     xyz, tets, region, fib, cond, stims = _slab_case("tt2006", 31, 12, 7, 0.5, permute=True, seed=5)
     dt = 0.02
@@ -218,7 +219,7 @@ def test_state_injection_one_step(T):
     ref.run(300)                       # 6 ms: front is propagating
     n = xyz.shape[0]
     buf = np.concatenate([ref.Vk, ref.Vkm1, ref.U.reshape(-1), [ref.k, 1.0]])
-    cfg = T.tc_config_default(dt=dt, abs_tol=1e-9, rel_tol=0.0)
+    cfg = T.tc_config_default(dt=dt, abs_tol=1e-9, rel_tol=0.0, engine=engine)
     sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
     try:
         sim.set_state(buf)
@@ -270,9 +271,10 @@ def test_mms_on_gpu_matches_oracle_and_converges(T):
     assert 1.7 < order < 2.3
 
 
-@pytest.mark.parametrize("model,parts,rot", [("ms", 1, False), ("tt2006", 1, True), ("tt2006", 3, False),
-                                             ("ms", 2, True)])
-def test_surface_sphere_trajectory_parity(T, model, parts, rot):
+@pytest.mark.parametrize("model,parts,rot,engine", [("ms", 1, False, "grid"), ("tt2006", 1, True, "cluster"),
+                                                    ("tt2006", 3, False, "auto"), ("ms", 2, True, "auto"),
+                                                    ("ms", 1, True, "cluster")])
+def test_surface_sphere_trajectory_parity(T, model, parts, rot, engine):
     """Surface (triangle) meshes: an icosphere with tangent
     fibres, two regions, stimulus at one pole; V per step within rel-L2 1e-8,
     LAT within one dt, also under a rigid rotation and on row-block partitions."""
@@ -291,7 +293,7 @@ def test_surface_sphere_trajectory_parity(T, model, parts, rot):
     dt = 0.05
     ref = O.Monodomain(xyz, tris, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0),
                        stims)
-    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, partitions=parts)
+    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, partitions=parts, engine=engine)
     sim = T.Monodomain(xyz, tris, region, fib, cond, cfg, stims)
     try:
         for k in range(150):
