@@ -106,6 +106,10 @@ typedef struct {
                             CUDA IPC between ranks, plain device memory between the parts of
                             one GPU); 0 = split-phase kernels + NCCL / device copies */
   int32_t engine;        /* tc_engine (TC_ENGINE_AUTO) */
+  int32_t device_setup;  /* 1 (default): single-partition systems build their pattern, RCM,
+                            SELL layout and element incidence on the GPU (
+                            identical result to the host path); 0: host setup */
+  int32_t reserved;
 } tc_config;
 
 /* Per-step PCG report. */
@@ -117,7 +121,8 @@ typedef struct {
 
 /* Fills the defaults: theta 0.5, dt 0.01, chi 140, cm 0.01, tolerances 1e-5,
  * max_iters 100, consecutive rel-mode, TT2006 epi, fail_budget 3,
- * thresholds 0 / -70 mV, use_rcm 1, pcg_variant 0, partitions 1, check_every 4, peer 1. */
+ * thresholds 0 / -70 mV, use_rcm 1, pcg_variant 0, partitions 1, check_every 4, peer 1,
+ * engine auto, device_setup 1. */
 void tc_config_default(tc_config* cfg);
 
 /* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
@@ -249,6 +254,11 @@ tc_status tc_pcg(tc_ctx* ctx, const double* b, const double* x0, double* x_out,
  * (NCCL is loaded at run time; without it tc_comm_init fails with TC_ENCCL). */
 tc_status tc_nccl_unique_id(uint8_t id[128]);
 tc_status tc_comm_init(tc_ctx* ctx, int rank, int world, const uint8_t id[128]);
+
+/* Internal row order of the assembled system: perm[i] = original index of
+ * internal row i (n_nodes entries; the RCM order of P:135 when use_rcm, the
+ * identity otherwise).  Host and device setup give the same order. */
+tc_status tc_node_order(const tc_ctx* ctx, int32_t* perm);
 
 /* Engine tc_step uses for this context: out[0] TC_ENGINE_GRID or
  * TC_ENGINE_CLUSTER, out[1] CTAs per cluster, out[2] dynamic shared memory per

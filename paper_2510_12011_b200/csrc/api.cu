@@ -13,6 +13,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <climits>
 #include <cstring>
 #include <map>
 #include <set>
@@ -195,7 +196,7 @@ static unsigned long long* inbox_flags(char* inbox, int world) {
 
 extern "C" {
 
-int32_t tc_abi_version(void) { return 2; }
+int32_t tc_abi_version(void) { return 3; }
 
 void tc_config_default(tc_config* c) {
   c->theta = 0.5;
@@ -216,6 +217,8 @@ void tc_config_default(tc_config* c) {
   c->check_every = 4;
   c->peer = 1;
   c->engine = TC_ENGINE_AUTO;
+  c->device_setup = 1;
+  c->reserved = 0;
 }
 
 tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx** out) {
@@ -300,17 +303,25 @@ tc_status tc_set_mesh_elems(tc_ctx* c, int64_t n, const double* xyz, int64_t E, 
   c->xyz.assign(xyz, xyz + 3 * n);
   c->tets.assign(tets, tets + (int64_t)k * E);
   if (region) c->region.assign(region, region + E); else c->region.assign(E, 0);
+  c->fibre.resize(3 * E);
   if (fibre) {
-    c->fibre.assign(fibre, fibre + 3 * E);
+    int64_t bad = INT64_MAX;  // first offending element
+#pragma omp parallel for schedule(static) reduction(min : bad)
     for (int64_t e = 0; e < E; ++e) {
       const double* f = fibre + 3 * e;
-      double nn = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
-      if (!(nn > 0) || !std::isfinite(nn))
-        return fail(c, TC_EINVAL, "tc_set_mesh: zero or non-finite fibre at element " + std::to_string(e));
+      for (int q = 0; q < 3; ++q) c->fibre[3 * e + q] = f[q];
+      const double nn = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+      if (!(nn > 0) || !std::isfinite(nn)) bad = std::min(bad, e);
     }
+    if (bad != INT64_MAX)
+      return fail(c, TC_EINVAL, "tc_set_mesh: zero or non-finite fibre at element " + std::to_string(bad));
   } else {
-    c->fibre.assign(3 * E, 0.0);
-    for (int64_t e = 0; e < E; ++e) c->fibre[3 * e] = 1.0;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e) {
+      c->fibre[3 * e] = 1.0;
+      c->fibre[3 * e + 1] = 0.0;
+      c->fibre[3 * e + 2] = 0.0;
+    }
   }
   std::string m = orient_and_validate(n, E, k, c->tets.data(), c->xyz.data());
   if (!m.empty()) {
@@ -647,25 +658,11 @@ static tc_status setup_peer(tc_ctx* c, const std::vector<PartPlan>& plans) {
   return TC_OK;
 }
 
-extern "C" tc_status tc_assemble(tc_ctx* c) {
-  if (!c) return TC_EINVAL;
-  if (!c->have_mesh) return fail(c, TC_ESTATE, "tc_assemble before tc_set_mesh");
-  if (c->assembled) return fail(c, TC_ESTATE, "tc_assemble called twice");
-  if (c->reg_ids.empty()) return fail(c, TC_EREGION, "tc_assemble: no conductivity table");
-  CUDA_TRY(c, cudaSetDevice(c->device));
+// Host setup path (partitioned systems, the 16-bit index variant, or
+// device_setup = 0): pattern, RCM, partition plan, SELL on the host; assembly
+// on the GPU.
+static tc_status assemble_host(tc_ctx* c, const std::vector<int32_t>& ereg, std::vector<PartPlan>& plans) {
   const int64_t n = c->n, E = c->E;
-  if (c->nparts > n) return fail(c, TC_EINVAL, "more partitions than nodes");
-  // region tag -> table index
-  std::map<int32_t, int32_t> rmap;
-  for (size_t r = 0; r < c->reg_ids.size(); ++r) rmap[c->reg_ids[r]] = (int32_t)r;
-  std::vector<int32_t> ereg(E);
-  for (int64_t e = 0; e < E; ++e) {
-    auto it = rmap.find(c->region[e]);
-    if (it == rmap.end())
-      return fail(c, TC_EREGION, "tet " + std::to_string(e) + " has region " +
-                                     std::to_string(c->region[e]) + " without conductivity");
-    ereg[e] = it->second;
-  }
   // pattern and RCM, identical on every rank
   std::vector<int64_t> iptr, rp;
   std::vector<int32_t> inc, col;
@@ -692,7 +689,6 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
     for (int q = 0; q < 3; ++q) xyz2[3 * i + q] = c->xyz[3 * (int64_t)c->perm[i] + q];
   build_incidence(n, E, k, tets2.data(), iptr, inc);
   // partitions
-  std::vector<PartPlan> plans;
   plan_partitions(n, rp2.data(), col2.data(), c->nparts, plans);
   c->bounds.resize(c->nparts + 1);
   for (int p = 0; p < c->nparts; ++p) c->bounds[p] = plans[p].g0;
@@ -701,7 +697,6 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
   if (c->use_comm) c->part_ids.push_back(c->comm.rank);
   else for (int p = 0; p < c->nparts; ++p) c->part_ids.push_back(p);
   c->parts.resize(c->part_ids.size());
-  c->nstates = c->cfg.model == TC_ION_TT2006_EPI ? kTTStates : (c->cfg.model == TC_ION_MS ? 1 : 0);
   // element data shared by all parts of this device (setup only)
   double *d_xyz = nullptr, *d_fib = nullptr, *d_sl = nullptr, *d_st = nullptr;
   int32_t *d_tets = nullptr, *d_ereg = nullptr, *d_err = nullptr;
@@ -815,6 +810,152 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
   free_setup();
   if (herr == 1) return fail(c, TC_EDEGEN, "assembly: zero-volume element");
   if (herr == 2) return fail(c, TC_EINVAL, "assembly: pattern slot missing (internal)");
+  return TC_OK;
+}
+
+// Device setup path (single partition): pattern, RCM, SELL and
+// incidence built on the GPU by dev_setup (setup_dev.cu) from the element
+// list; only the permutation and the slice pointers come back to the host.
+static tc_status assemble_device(tc_ctx* c, const std::vector<int32_t>& ereg) {
+  const int64_t n = c->n, E = c->E;
+  const int k = c->kel;
+  const size_t nr = c->reg_ids.size();
+  double *d_xyz = nullptr, *d_xyz2 = nullptr, *d_fib = nullptr, *d_sl = nullptr, *d_st = nullptr;
+  int32_t *d_tets = nullptr, *d_ereg = nullptr, *d_err = nullptr;
+  DevPattern dp;
+  auto cleanup = [&]() {
+    cudaFree(d_xyz); cudaFree(d_xyz2); cudaFree(d_fib); cudaFree(d_sl); cudaFree(d_st);
+    cudaFree(d_tets); cudaFree(d_ereg); cudaFree(d_err);
+    dev_setup_free(dp);
+  };
+  bool ok = cudaMalloc(&d_xyz, 3 * n * 8) == cudaSuccess && cudaMalloc(&d_xyz2, 3 * n * 8) == cudaSuccess &&
+            cudaMalloc(&d_fib, std::max<int64_t>(3 * E, 1) * 8) == cudaSuccess &&
+            cudaMalloc(&d_sl, nr * 8) == cudaSuccess && cudaMalloc(&d_st, nr * 8) == cudaSuccess &&
+            cudaMalloc(&d_tets, std::max<int64_t>((int64_t)k * E, 1) * 4) == cudaSuccess &&
+            cudaMalloc(&d_ereg, std::max<int64_t>(E, 1) * 4) == cudaSuccess && cudaMalloc(&d_err, 4) == cudaSuccess;
+  if (!ok) {
+    cleanup();
+    return fail(c, TC_ENOMEM, "tc_assemble: device allocation failed");
+  }
+  cudaMemcpyAsync(d_xyz, c->xyz.data(), 3 * n * 8, cudaMemcpyHostToDevice, c->stream);
+  if (E > 0) {
+    cudaMemcpyAsync(d_fib, c->fibre.data(), 3 * E * 8, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_tets, c->tets.data(), (size_t)k * E * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_ereg, ereg.data(), E * 4, cudaMemcpyHostToDevice, c->stream);
+  }
+  cudaMemcpyAsync(d_sl, c->sig_l.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
+  cudaMemcpyAsync(d_st, c->sig_t.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
+  cudaMemsetAsync(d_err, 0, 4, c->stream);
+  cudaError_t e = dev_setup(n, E, k, d_tets, c->cfg.use_rcm, dp, c->stream);
+  if (e == cudaSuccess) e = dev_gather3(n, dp.perm, d_xyz, d_xyz2, c->stream);
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(c, e == cudaErrorMemoryAllocation ? TC_ENOMEM : TC_ECUDA,
+                std::string("device setup: ") + cudaGetErrorString(e));
+  }
+  c->perm.resize(n);
+  c->inv.resize(n);
+  CUDA_TRY(c, cudaMemcpyAsync(c->perm.data(), dp.perm, n * 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int64_t i = 0; i < n; ++i) c->inv[c->perm[i]] = (int32_t)i;
+  c->nnz = dp.nnz;
+  c->bounds = {0, n};
+  c->part_ids = {0};
+  c->parts.resize(1);
+  Part& P = c->parts[0];
+  P.plan = PartPlan{};
+  P.plan.g0 = 0;
+  P.plan.g1 = n;
+  P.plan.recv_off = {0};
+  P.plan.send_off = {0};
+  P.n = n;
+  P.nslices = dp.nslices;
+  P.n_pad = (int64_t)dp.nslices * kSellC;
+  P.n_ghost = 0;
+  P.n_vec = P.n_pad;
+  P.nnz = dp.nnz;
+  P.nnz_pad = dp.nnz_pad;
+  P.h_sp.resize(dp.nslices + 1);
+  CUDA_TRY(c, cudaMemcpyAsync(P.h_sp.data(), dp.slice_ptr, (dp.nslices + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+  P.d_sp = dp.slice_ptr;  // adopted: freed with the context
+  P.d_col = dp.col;
+  c->allocs.push_back(dp.slice_ptr);
+  c->allocs.push_back(dp.col);
+  dp.slice_ptr = nullptr;
+  dp.col = nullptr;
+  CUDA_TRY(c, dalloc(c, &P.d_A, P.nnz_pad));
+  CUDA_TRY(c, dalloc(c, &P.d_K, P.nnz_pad));
+  TC_TRY(alloc_part_vectors(c, P));
+  CUDA_TRY(c, dalloc(c, &P.d_U, (int64_t)std::max(c->nstates, 1) * P.n_pad));
+  CUDA_TRY(c, dalloc(c, &P.d_act, P.n_pad));
+  CUDA_TRY(c, dalloc(c, &P.d_lat, P.n_pad));
+  CUDA_TRY(c, dalloc(c, &P.d_lrt, P.n_pad));
+  CUDA_TRY(c, dalloc(c, &P.d_send_idx, 0));
+  CUDA_TRY(c, dalloc(c, &P.d_send_buf, 0));
+  if (c->cfg.model == TC_ION_MMS) {
+    std::vector<uint8_t> dir(P.n_pad, 0);
+    for (int32_t o : c->dirichlet_nodes) dir[c->inv[o]] = 1;
+    CUDA_TRY(c, upload(c, &P.d_dir, dir));
+    CUDA_TRY(c, dalloc(c, &P.d_xyz, 3 * P.n_pad));
+    CUDA_TRY(c, cudaMemcpyAsync(P.d_xyz, d_xyz2, 3 * n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  AsmArgs a{};
+  a.n = (int32_t)n; a.row0 = 0; a.k = k; a.xyz = d_xyz2; a.tets = dp.tets2; a.ereg = d_ereg;
+  a.fibre = d_fib; a.sig_l = d_sl; a.sig_t = d_st; a.inc_ptr = dp.iptr; a.inc = dp.inc;
+  a.slice_ptr = P.d_sp; a.col = P.d_col; a.rowlen = dp.rowlen;
+  a.A = P.d_A; a.K = P.d_K; a.dinv = P.d_dinv; a.dirichlet = P.d_dir;
+  a.c_mass = c->cfg.chi * c->cfg.cm; a.c_stiff = c->cfg.theta * c->cfg.dt; a.err = d_err;
+  cudaError_t le = launch_assemble(a, c->stream);
+  cudaError_t ss = cudaStreamSynchronize(c->stream);
+  int32_t herr = 0;
+  if (le == cudaSuccess && ss == cudaSuccess) {
+    cudaMemcpy(&herr, d_err, 4, cudaMemcpyDeviceToHost);
+  }
+  cleanup();
+  if (le != cudaSuccess || ss != cudaSuccess)
+    return fail(c, TC_ECUDA, std::string("assembly kernel: ") + cudaGetErrorString(le != cudaSuccess ? le : ss));
+  if (herr == 1) return fail(c, TC_EDEGEN, "assembly: zero-volume element");
+  if (herr == 2) return fail(c, TC_EINVAL, "assembly: pattern slot missing (internal)");
+  P.grid = cg_grid_size(1, c->cfg.pcg_variant, P.nslices, c->device);
+  CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
+  return TC_OK;
+}
+
+extern "C" tc_status tc_assemble(tc_ctx* c) {
+  if (!c) return TC_EINVAL;
+  if (!c->have_mesh) return fail(c, TC_ESTATE, "tc_assemble before tc_set_mesh");
+  if (c->assembled) return fail(c, TC_ESTATE, "tc_assemble called twice");
+  if (c->reg_ids.empty()) return fail(c, TC_EREGION, "tc_assemble: no conductivity table");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int64_t n = c->n, E = c->E;
+  if (c->nparts > n) return fail(c, TC_EINVAL, "more partitions than nodes");
+  // region tag -> table index (sorted ids, binary search; parallel over elements)
+  std::vector<std::pair<int32_t, int32_t>> rids;
+  for (size_t r = 0; r < c->reg_ids.size(); ++r) rids.push_back({c->reg_ids[r], (int32_t)r});
+  std::sort(rids.begin(), rids.end());
+  std::vector<int32_t> ereg(E);
+  int64_t bad = INT64_MAX;  // first offending element
+#pragma omp parallel for schedule(static) reduction(min : bad)
+  for (int64_t e = 0; e < E; ++e) {
+    auto it = std::lower_bound(rids.begin(), rids.end(), std::make_pair(c->region[e], INT32_MIN));
+    if (it == rids.end() || it->first != c->region[e]) {
+      bad = std::min(bad, e);
+      ereg[e] = 0;
+    } else {
+      ereg[e] = it->second;
+    }
+  }
+  if (bad != INT64_MAX)
+    return fail(c, TC_EREGION, "tet " + std::to_string(bad) + " has region " +
+                                   std::to_string(c->region[bad]) + " without conductivity");
+  std::vector<PartPlan> plans;
+  c->nstates = c->cfg.model == TC_ION_TT2006_EPI ? kTTStates : (c->cfg.model == TC_ION_MS ? 1 : 0);
+  const bool on_dev = c->cfg.device_setup && c->nparts == 1 && !c->use_comm && c->cfg.pcg_variant != 2;
+  if (on_dev) {
+    TC_TRY(assemble_device(c, ereg));
+  } else {
+    TC_TRY(assemble_host(c, ereg, plans));
+  }
   // stimulus epochs: step windows [round(t0/dt), round((t0+dur)/dt)) (reading T1)
   {
     std::set<int64_t> cuts;
@@ -1565,6 +1706,13 @@ tc_status tc_partition_plan(int64_t n, const int64_t* rowptr, const int32_t* col
 }
 
 }  // extern "C"
+
+extern "C" tc_status tc_node_order(const tc_ctx* c, int32_t* perm) {
+  if (!c || !perm) return TC_EINVAL;
+  if (!c->assembled || c->csr_mode) return TC_ESTATE;
+  std::copy(c->perm.begin(), c->perm.end(), perm);
+  return TC_OK;
+}
 
 extern "C" tc_status tc_engine_info(tc_ctx* c, int64_t out[4]) {
   if (!c || !out) return TC_EINVAL;

@@ -306,6 +306,24 @@ void csr_to_sell(int32_t n, const int64_t* rowptr, const int32_t* col, HostSell&
                  std::vector<int64_t>* csr_slot = nullptr);
 void compress_sell(HostSell& s);
 
+// ---- device-side setup (setup_dev.cu): single-partition pattern, RCM, SELL, incidence
+struct DevPattern {         // device arrays, cudaMalloc'ed by dev_setup (dev_setup_free)
+  int64_t n = 0, nnz = 0, nnz_pad = 0;
+  int32_t nslices = 0;
+  int32_t* perm = nullptr;      // [n] internal -> original
+  int32_t* inv = nullptr;       // [n] original -> internal
+  int64_t* slice_ptr = nullptr; // [nslices + 1]
+  int32_t* col = nullptr;       // [nnz_pad] SELL columns (internal numbering)
+  int32_t* rowlen = nullptr;    // [n]
+  int64_t* iptr = nullptr;      // [n + 1] incidence of the permuted elements
+  int32_t* inc = nullptr;       // [k E] 4 e + a, ascending e per node
+  int32_t* tets2 = nullptr;     // [k E] element nodes in internal numbering
+};
+cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int use_rcm, DevPattern& out,
+                      cudaStream_t s);
+void dev_setup_free(DevPattern& p);
+cudaError_t dev_gather3(int64_t n, const int32_t* perm, const double* in, double* out, cudaStream_t s);
+
 // Row-block partition of a system in internal (RCM) order: part p owns the
 // contiguous rows [g0, g1); ghosts = columns of owned rows outside the block.
 struct PartPlan {

@@ -218,11 +218,34 @@ __device__ __forceinline__ ColIdx col_of(const CgArgs& a, int64_t i, int64_t bas
   return ci;
 }
 
+#ifndef TCB_ROW_BATCH
+#define TCB_ROW_BATCH 0   // 0: unroll-4 loop; N > 0: slots in batches of N with clamped indices
+#endif
 template <bool FIRST>
 __device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, const ColIdx& ci,
                                                 const double* A, const double* z, const double* pold,
                                                 double beta) {
   double sum = 0.0;
+#if TCB_ROW_BATCH > 0
+  // every load of a batch in flight together; slots past the row end reload its
+  // last slot (no remainder loop), accumulation in slot order
+  constexpr int NB = TCB_ROW_BATCH;
+#pragma unroll 1
+  for (int k0 = 0; k0 < w; k0 += NB) {
+    double av[NB], g[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int kk = min(k0 + j, w - 1);
+      const int64_t t = base + (int64_t)kk * kSellC + lane;
+      const int c = ci(t, kk);
+      av[j] = __ldcs(A + t);
+      g[j] = FIRST ? z[c] : z[c] + beta * pold[c];
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (k0 + j < w) sum += av[j] * g[j];
+  }
+#else
 #pragma unroll 4
   for (int k = 0; k < w; ++k) {
     const int64_t t = base + (int64_t)k * kSellC + lane;
@@ -230,6 +253,7 @@ __device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, c
     const double g = FIRST ? z[c] : z[c] + beta * pold[c];
     sum += __ldcs(A + t) * g;
   }
+#endif
   return sum;
 }
 
