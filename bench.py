@@ -40,6 +40,9 @@ WORKLOADS = {
     # north-star target: ~10M-node TT2006 slab
     "slab10M_tt": dict(cfg="north_star", dims=(250, 200, 200), dx=0.1, model="tt2006", dt=0.01,
                        stim="face", preroll=500, sample_dims=(48, 48, 48)),
+    # the north-star slab with the CRN atrial model
+    "slab10M_crn": dict(cfg="f4 (north-star slab, CRN)", dims=(250, 200, 200), dx=0.1, model="crn", dt=0.01,
+                        stim="face", preroll=500, sample_dims=(48, 48, 48)),
     # configs[2]: N-version dx = 0.1 mm (~442k nodes), TT2006 epi, dt 0.01
     "nversion_dx0.1_tt": dict(cfg=2, dims=(201, 71, 31), dx=0.1, model="tt2006", dt=0.01,
                               stim="corner", preroll=500, sample_dims=(48, 48, 31)),
@@ -90,7 +93,7 @@ def bytes_per_step(n, nnz, iters, model, steps):
     """Algorithmic bytes: B_rhs + iters B_it per PCG launch; ionic per node."""
     b_it = 12 * nnz + 4 * (n + 1) + 72 * n
     b_rhs = 20 * nnz + 4 * (n + 1) + 44 * n
-    b_ion = (352 if model == "tt2006" else 80) * n
+    b_ion = {"tt2006": 352, "crn": 376}.get(model, 80) * n
     return b_rhs * steps + b_it * iters, b_ion * steps
 
 

@@ -54,7 +54,9 @@ typedef enum {
 typedef enum {
   TC_ION_TT2006_EPI = 0, /* ten Tusscher-Panfilov 2006, epicardial */
   TC_ION_MS = 1,         /* Mitchell-Schaeffer 2003 (reading I5) */
-  TC_ION_MMS = 2         /* no ionic model: manufactured source r of Eq. 8 */
+  TC_ION_MMS = 2,        /* no ionic model: manufactured source r of Eq. 8 */
+  TC_ION_CRN = 3         /* Courtemanche-Ramirez-Nattel 1998 human atrial cell (
+                            DESIGN.md reading I6), 20 states */
 } tc_ionic;
 
 /* Execution engine of tc_step for a single-partition context (DESIGN.md

@@ -85,6 +85,20 @@ def _lib():
         L.or_tt_param_name.restype = C.c_char_p
         L.or_tt_state_name.argtypes = [I32]
         L.or_tt_state_name.restype = C.c_char_p
+        L.or_crn_default_params.argtypes = [P]
+        L.or_crn_default_params.restype = None
+        L.or_crn_initial_state.argtypes = [P]
+        L.or_crn_initial_state.restype = D
+        L.or_crn_step.argtypes = [I64, P, P, D, P, P]
+        L.or_crn_step.restype = None
+        L.or_crn_current.argtypes = [D, P, P]
+        L.or_crn_current.restype = D
+        L.or_crn_nparams.restype = I32
+        L.or_crn_nstates.restype = I32
+        L.or_crn_param_name.argtypes = [I32]
+        L.or_crn_param_name.restype = C.c_char_p
+        L.or_crn_state_name.argtypes = [I32]
+        L.or_crn_state_name.restype = C.c_char_p
         _L = L
     return _L
 
@@ -282,6 +296,44 @@ def tt_current(V: float, u, params=None) -> float:
     return _lib().or_tt_current(V, _p(_f64(u)), _p(p))
 
 
+def crn_param_names() -> list[str]:
+    """Courtemanche-Ramirez-Nattel 1998 (reading I6)."""
+    L = _lib()
+    return [L.or_crn_param_name(k).decode() for k in range(L.or_crn_nparams())]
+
+
+def crn_state_names() -> list[str]:
+    L = _lib()
+    return [L.or_crn_state_name(k).decode() for k in range(L.or_crn_nstates())]
+
+
+def crn_default_params() -> np.ndarray:
+    p = np.zeros(_lib().or_crn_nparams())
+    _lib().or_crn_default_params(_p(p))
+    return p
+
+
+def crn_initial_state(n: int):
+    """-> V0 (n,), U0 (20, n) state-major."""
+    u = np.zeros(_lib().or_crn_nstates())
+    v0 = _lib().or_crn_initial_state(_p(u))
+    return np.full(n, v0), np.repeat(u[:, None], n, axis=1).copy()
+
+
+def crn_step(V, U, dt: float, params=None) -> np.ndarray:
+    """Advance U (20, n) in place (RL gates, FE concentrations); -> I_n(V, U^{k+1})."""
+    V = _f64(V)
+    p = crn_default_params() if params is None else _f64(params)
+    In = np.zeros(V.shape[0])
+    _lib().or_crn_step(V.shape[0], _p(V), _p(U), dt, _p(p), _p(In))
+    return In
+
+
+def crn_current(V: float, u, params=None) -> float:
+    p = crn_default_params() if params is None else _f64(params)
+    return _lib().or_crn_current(V, _p(_f64(u)), _p(p))
+
+
 def tt_buffer(c_old, delta, B, K) -> float:
     return _lib().or_tt_buffer(c_old, delta, B, K)
 
@@ -367,7 +419,7 @@ class Config:
     max_iters: int = 100
     rel_mode: int = 0         # reading C1: 0 literal consecutive, 1 initial
     fail_budget: int = 3
-    model: str = "tt2006"     # "tt2006" | "ms"
+    model: str = "tt2006"     # "tt2006" | "ms" | "crn"
     params: np.ndarray | None = None
 
 
@@ -394,6 +446,9 @@ class Monodomain:
         elif cfg.model == "ms":
             self.params = ms_default_params() if cfg.params is None else _f64(cfg.params)
             v, u = ms_initial_state(self.n, self.params)
+        elif cfg.model == "crn":
+            self.params = crn_default_params() if cfg.params is None else _f64(cfg.params)
+            v, u = crn_initial_state(self.n)
         else:
             raise ValueError(cfg.model)
         self.Vk = v if V0 is None else _f64(V0).copy()
@@ -408,6 +463,8 @@ class Monodomain:
     def ionic(self, V, U):
         if self.cfg.model == "tt2006":
             return tt_step(V, U, self.cfg.dt, self.params)
+        if self.cfg.model == "crn":
+            return crn_step(V, U, self.cfg.dt, self.params)
         return ms_step(V, U, self.cfg.dt, self.params)
 
     def step(self) -> SolveReport:

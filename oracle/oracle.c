@@ -658,3 +658,223 @@ void or_tt_step(int64_t n, const double* V, double* U, double dt, const double* 
     for (int s = 0; s < TT_NS; ++s) U[(int64_t)s * n + i] = u[s];
   }
 }
+
+/* ---- 6c. Courtemanche-Ramirez-Nattel 1998 human atrial cell ("CRN",      */
+/*      named among the supported models).           */
+/* The paper gives no equations; they are the published model (Am J Physiol */
+/* 275:H301, 1998; the CellML transcription), reading I6:          */
+/* "parity unpinned" for the biological constants, pinned for quiescence,   */
+/* the action potential, Nernst potentials and the integrator.               */
+/* Integrator (as TT2006, readings I1/I2/I3): Rush-Larsen for the 15 gates,  */
+/* forward Euler for the 5 concentrations with the instantaneous-buffer      */
+/* factor of Ca_i and Ca_rel, all at (V^k, u^k); I_n = I_ion(V^k, u^{k+1}).  */
+/* 20 states, state-major: */
+enum { CR_Nai, CR_Ki, CR_Cai, CR_Caup, CR_Carel, CR_m, CR_h, CR_j, CR_oa, CR_oi,
+       CR_ua, CR_ui, CR_xr, CR_xs, CR_d, CR_f, CR_fCa, CR_u, CR_v, CR_w, CR_NS };
+enum { Q_R, Q_T, Q_F, Q_Cm, Q_Vi, Q_Vup, Q_Vrel, Q_Ko, Q_Nao, Q_Cao, Q_gNa, Q_gK1,
+       Q_gto, Q_gKr, Q_gKs, Q_gCaL, Q_gbNa, Q_gbCa, Q_INaKmax, Q_KmNai, Q_KmKo,
+       Q_INaCamax, Q_KmNa, Q_KmCa, Q_ksat, Q_gamma, Q_IpCamax, Q_Krel, Q_tautr,
+       Q_Iupmax, Q_Kup, Q_Caupmax, Q_CMDNmax, Q_TRPNmax, Q_CSQNmax, Q_KmCMDN,
+       Q_KmTRPN, Q_KmCSQN, Q_tauu, Q_KQ10, Q_N };
+static const char* CR_PNAMES[Q_N] = {
+    "R", "T", "F", "Cm", "Vi", "Vup", "Vrel", "Ko", "Nao", "Cao", "gNa", "gK1",
+    "gto", "gKr", "gKs", "gCaL", "gbNa", "gbCa", "INaKmax", "KmNai", "KmKo",
+    "INaCamax", "KmNa", "KmCa", "ksat", "gamma", "IpCamax", "Krel", "tautr",
+    "Iupmax", "Kup", "Caupmax", "CMDNmax", "TRPNmax", "CSQNmax", "KmCMDN",
+    "KmTRPN", "KmCSQN", "tauu", "KQ10"};
+static const char* CR_SNAMES[CR_NS] = {"Nai", "Ki", "Cai", "Caup", "Carel", "m", "h", "j",
+                                       "oa", "oi", "ua", "ui", "xr", "xs", "d", "f",
+                                       "fCa", "u", "v", "w"};
+int32_t or_crn_nparams(void) { return Q_N; }
+int32_t or_crn_nstates(void) { return CR_NS; }
+const char* or_crn_param_name(int32_t k) { return (k >= 0 && k < Q_N) ? CR_PNAMES[k] : 0; }
+const char* or_crn_state_name(int32_t k) { return (k >= 0 && k < CR_NS) ? CR_SNAMES[k] : 0; }
+
+void or_crn_default_params(double* p) {
+  p[Q_R] = 8.3143; p[Q_T] = 310.0; p[Q_F] = 96.4867; p[Q_Cm] = 100.0;
+  p[Q_Vi] = 13668.0; p[Q_Vup] = 1109.52; p[Q_Vrel] = 96.48;
+  p[Q_Ko] = 5.4; p[Q_Nao] = 140.0; p[Q_Cao] = 1.8;
+  p[Q_gNa] = 7.8; p[Q_gK1] = 0.09; p[Q_gto] = 0.1652; p[Q_gKr] = 0.029411765;
+  p[Q_gKs] = 0.12941176; p[Q_gCaL] = 0.12375; p[Q_gbNa] = 6.744375e-4; p[Q_gbCa] = 1.131e-3;
+  p[Q_INaKmax] = 0.59933874; p[Q_KmNai] = 10.0; p[Q_KmKo] = 1.5;
+  p[Q_INaCamax] = 1600.0; p[Q_KmNa] = 87.5; p[Q_KmCa] = 1.38; p[Q_ksat] = 0.1;
+  p[Q_gamma] = 0.35; p[Q_IpCamax] = 0.275; p[Q_Krel] = 30.0; p[Q_tautr] = 180.0;
+  p[Q_Iupmax] = 0.005; p[Q_Kup] = 0.00092; p[Q_Caupmax] = 15.0;
+  p[Q_CMDNmax] = 0.05; p[Q_TRPNmax] = 0.07; p[Q_CSQNmax] = 10.0;
+  p[Q_KmCMDN] = 0.00238; p[Q_KmTRPN] = 0.0005; p[Q_KmCSQN] = 0.8;
+  p[Q_tauu] = 8.0; p[Q_KQ10] = 3.0;
+}
+/* Published initial conditions (resting cell). */
+double or_crn_initial_state(double* u) {
+  u[CR_Nai] = 11.17; u[CR_Ki] = 139.0; u[CR_Cai] = 1.013e-4; u[CR_Caup] = 1.488;
+  u[CR_Carel] = 1.488; u[CR_m] = 2.908e-3; u[CR_h] = 0.9649; u[CR_j] = 0.9775;
+  u[CR_oa] = 3.043e-2; u[CR_oi] = 0.9992; u[CR_ua] = 4.966e-3; u[CR_ui] = 0.9986;
+  u[CR_xr] = 3.296e-5; u[CR_xs] = 1.869e-2; u[CR_d] = 1.367e-4; u[CR_f] = 0.9996;
+  u[CR_fCa] = 0.7755; u[CR_u] = 2.35e-112; u[CR_v] = 1.0; u[CR_w] = 0.9992;
+  return -81.18;
+}
+
+/* membrane currents per unit capacitance (pA/pF = mV/ms) at (V, u) */
+typedef struct {
+  double INa, IK1, Ito, IKur, IKr, IKs, ICaL, INaK, INaCa, IbNa, IbCa, IpCa;
+} crn_currents;
+
+static crn_currents crn_eval_currents(double V, const double* u, const double* p) {
+  crn_currents c;
+  const double RTF = p[Q_R] * p[Q_T] / p[Q_F], FRT = p[Q_F] / (p[Q_R] * p[Q_T]);
+  const double Nai = u[CR_Nai], Ki = u[CR_Ki], Cai = u[CR_Cai];
+  const double Ko = p[Q_Ko], Nao = p[Q_Nao], Cao = p[Q_Cao];
+  const double ENa = RTF * log(Nao / Nai), EK = RTF * log(Ko / Ki);
+  const double ECa = RTF / 2.0 * log(Cao / Cai);
+  const double m = u[CR_m], oa = u[CR_oa], ua = u[CR_ua], xs = u[CR_xs];
+  c.INa = p[Q_gNa] * m * m * m * u[CR_h] * u[CR_j] * (V - ENa);
+  c.IK1 = p[Q_gK1] * (V - EK) / (1.0 + exp(0.07 * (V + 80.0)));
+  c.Ito = p[Q_gto] * oa * oa * oa * u[CR_oi] * (V - EK);
+  const double gKur = 0.005 + 0.05 / (1.0 + exp((V - 15.0) / -13.0));
+  c.IKur = gKur * ua * ua * ua * u[CR_ui] * (V - EK);
+  c.IKr = p[Q_gKr] * u[CR_xr] * (V - EK) / (1.0 + exp((V + 15.0) / 22.4));
+  c.IKs = p[Q_gKs] * xs * xs * (V - EK);
+  c.ICaL = p[Q_gCaL] * u[CR_d] * u[CR_f] * u[CR_fCa] * (V - 65.0);
+  const double sigma = (exp(Nao / 67.3) - 1.0) / 7.0;
+  const double fNaK = 1.0 / (1.0 + 0.1245 * exp(-0.1 * V * FRT) + 0.0365 * sigma * exp(-V * FRT));
+  c.INaK = p[Q_INaKmax] * fNaK / (1.0 + pow(p[Q_KmNai] / Nai, 1.5)) * Ko / (Ko + p[Q_KmKo]);
+  const double g = p[Q_gamma];
+  c.INaCa = p[Q_INaCamax] *
+            (exp(g * V * FRT) * Nai * Nai * Nai * Cao - exp((g - 1.0) * V * FRT) * Nao * Nao * Nao * Cai) /
+            ((p[Q_KmNa] * p[Q_KmNa] * p[Q_KmNa] + Nao * Nao * Nao) * (p[Q_KmCa] + Cao) *
+             (1.0 + p[Q_ksat] * exp((g - 1.0) * V * FRT)));
+  c.IbNa = p[Q_gbNa] * (V - ENa);
+  c.IbCa = p[Q_gbCa] * (V - ECa);
+  c.IpCa = p[Q_IpCamax] * Cai / (0.0005 + Cai);
+  return c;
+}
+
+static double crn_sum(const crn_currents* c) {
+  return c->INa + c->IK1 + c->Ito + c->IKur + c->IKr + c->IKs + c->ICaL + c->INaK +
+         c->INaCa + c->IbNa + c->IbCa + c->IpCa;
+}
+
+double or_crn_current(double V, const double* u, const double* p) {
+  crn_currents c = crn_eval_currents(V, u, p);
+  return crn_sum(&c);
+}
+
+/* steady states and time constants of the 15 gates at (V, u) */
+typedef struct { double inf[15], tau[15]; } crn_gates;
+enum { G_m, G_h, G_j, G_oa, G_oi, G_ua, G_ui, G_xr, G_xs, G_d, G_f, G_fCa, G_u, G_v, G_w };
+
+static void crn_eval_gates(double V, const double* u, const double* p, const crn_currents* c,
+                           double Irel, crn_gates* G) {
+  double a, b;
+  /* I_Na gates */
+  a = (V == -47.13) ? 3.2 : 0.32 * (V + 47.13) / (1.0 - exp(-0.1 * (V + 47.13)));
+  b = 0.08 * exp(-V / 11.0);
+  G->inf[G_m] = a / (a + b); G->tau[G_m] = 1.0 / (a + b);
+  if (V < -40.0) {
+    a = 0.135 * exp((V + 80.0) / -6.8);
+    b = 3.56 * exp(0.079 * V) + 3.1e5 * exp(0.35 * V);
+  } else {
+    a = 0.0;
+    b = 1.0 / (0.13 * (1.0 + exp((V + 10.66) / -11.1)));
+  }
+  G->inf[G_h] = a / (a + b); G->tau[G_h] = 1.0 / (a + b);
+  if (V < -40.0) {
+    a = (-127140.0 * exp(0.2444 * V) - 3.474e-5 * exp(-0.04391 * V)) * (V + 37.78) /
+        (1.0 + exp(0.311 * (V + 79.23)));
+    b = 0.1212 * exp(-0.01052 * V) / (1.0 + exp(-0.1378 * (V + 40.14)));
+  } else {
+    a = 0.0;
+    b = 0.3 * exp(-2.535e-7 * V) / (1.0 + exp(-0.1 * (V + 32.0)));
+  }
+  G->inf[G_j] = a / (a + b); G->tau[G_j] = 1.0 / (a + b);
+  /* I_to, I_Kur gates (time constants divided by K_Q10) */
+  const double KQ = p[Q_KQ10];
+  a = 0.65 / (exp((V + 10.0) / -8.5) + exp((V - 30.0) / -59.0));
+  b = 0.65 / (2.5 + exp((V + 82.0) / 17.0));
+  G->tau[G_oa] = 1.0 / (a + b) / KQ;
+  G->inf[G_oa] = 1.0 / (1.0 + exp((V + 20.47) / -17.54));
+  a = 1.0 / (18.53 + exp((V + 113.7) / 10.95));
+  b = 1.0 / (35.56 + exp((V + 1.26) / -7.44));
+  G->tau[G_oi] = 1.0 / (a + b) / KQ;
+  G->inf[G_oi] = 1.0 / (1.0 + exp((V + 43.1) / 5.3));
+  a = 0.65 / (exp((V + 10.0) / -8.5) + exp((V - 30.0) / -59.0));
+  b = 0.65 / (2.5 + exp((V + 82.0) / 17.0));
+  G->tau[G_ua] = 1.0 / (a + b) / KQ;
+  G->inf[G_ua] = 1.0 / (1.0 + exp((V + 30.3) / -9.6));
+  a = 1.0 / (21.0 + exp((V - 185.0) / -28.0));
+  b = exp((V - 158.0) / 16.0);
+  G->tau[G_ui] = 1.0 / (a + b) / KQ;
+  G->inf[G_ui] = 1.0 / (1.0 + exp((V - 99.45) / 27.48));
+  /* I_Kr, I_Ks */
+  a = (V == -14.1) ? 0.0015 : 0.0003 * (V + 14.1) / (1.0 - exp((V + 14.1) / -5.0));
+  b = (V == 3.3328) ? 3.7836118e-4 : 7.3898e-5 * (V - 3.3328) / (exp((V - 3.3328) / 5.1237) - 1.0);
+  G->tau[G_xr] = 1.0 / (a + b);
+  G->inf[G_xr] = 1.0 / (1.0 + exp((V + 14.1) / -6.5));
+  a = (V == 19.9) ? 0.00068 : 4e-5 * (V - 19.9) / (1.0 - exp((V - 19.9) / -17.0));
+  b = (V == 19.9) ? 0.000315 : 3.5e-5 * (V - 19.9) / (exp((V - 19.9) / 9.0) - 1.0);
+  G->tau[G_xs] = 0.5 / (a + b);
+  G->inf[G_xs] = 1.0 / sqrt(1.0 + exp((V - 19.9) / -12.7));
+  /* I_CaL */
+  G->inf[G_d] = 1.0 / (1.0 + exp((V + 10.0) / -8.0));
+  G->tau[G_d] = (V == -10.0) ? 4.579 / (1.0 + exp((V + 10.0) / -6.24))
+                             : (1.0 - exp((V + 10.0) / -6.24)) /
+                                   (0.035 * (V + 10.0) * (1.0 + exp((V + 10.0) / -6.24)));
+  G->inf[G_f] = exp(-(V + 28.0) / 6.9) / (1.0 + exp(-(V + 28.0) / 6.9));
+  G->tau[G_f] = 9.0 / (0.0197 * exp(-0.0337 * 0.0337 * (V + 10.0) * (V + 10.0)) + 0.02);
+  G->inf[G_fCa] = 1.0 / (1.0 + u[CR_Cai] / 0.00035);
+  G->tau[G_fCa] = 2.0;
+  /* SR release gates: flux Fn in the release junction (pA -> femtomoles) */
+  const double Cm = p[Q_Cm];
+  const double Fn = 1000.0 * (1e-15 * p[Q_Vrel] * Irel -
+                              1e-15 / (2.0 * p[Q_F]) * (0.5 * c->ICaL * Cm - 0.2 * c->INaCa * Cm));
+  G->inf[G_u] = 1.0 / (1.0 + exp(-(Fn - 3.4175e-13) / 13.67e-16));
+  G->tau[G_u] = p[Q_tauu];
+  G->tau[G_v] = 1.91 + 2.09 / (1.0 + exp(-(Fn - 3.4175e-13) / 13.67e-16));
+  G->inf[G_v] = 1.0 - 1.0 / (1.0 + exp(-(Fn - 6.835e-14) / 13.67e-16));
+  G->tau[G_w] = (V == 7.9) ? 6.0 * 0.2 / 1.3
+                           : 6.0 * (1.0 - exp(-(V - 7.9) / 5.0)) /
+                                 ((1.0 + 0.3 * exp(-(V - 7.9) / 5.0)) * (V - 7.9));
+  G->inf[G_w] = 1.0 - 1.0 / (1.0 + exp(-(V - 40.0) / 17.0));
+}
+
+/* One CRN step of one cell: u -> u^{k+1}; returns I_n(V, u^{k+1}). */
+static double crn_cell_step(double V, double* u, double dt, const double* p) {
+  crn_currents c = crn_eval_currents(V, u, p);
+  const double F = p[Q_F], Cm = p[Q_Cm], Vi = p[Q_Vi], Vup = p[Q_Vup], Vrel = p[Q_Vrel];
+  const double Cai = u[CR_Cai], Caup = u[CR_Caup], Carel = u[CR_Carel];
+  /* SR fluxes (mM/ms) */
+  const double Irel = p[Q_Krel] * u[CR_u] * u[CR_u] * u[CR_v] * u[CR_w] * (Carel - Cai);
+  const double Itr = (Caup - Carel) / p[Q_tautr];
+  const double Iupleak = p[Q_Iupmax] * Caup / p[Q_Caupmax];
+  const double Iup = p[Q_Iupmax] / (1.0 + p[Q_Kup] / Cai);
+  crn_gates G;
+  crn_eval_gates(V, u, p, &c, Irel, &G);
+  /* concentrations: forward Euler (currents in pA = per-capacitance x Cm) */
+  const double dNai = (-3.0 * c.INaK - 3.0 * c.INaCa - c.IbNa - c.INa) * Cm / (Vi * F);
+  const double dKi = (2.0 * c.INaK - c.IK1 - c.Ito - c.IKur - c.IKr - c.IKs) * Cm / (Vi * F);
+  const double B1 = (2.0 * c.INaCa - c.IpCa - c.ICaL - c.IbCa) * Cm / (2.0 * Vi * F) +
+                    (Vup * (Iupleak - Iup) + Irel * Vrel) / Vi;
+  const double B2 = 1.0 + p[Q_TRPNmax] * p[Q_KmTRPN] / ((Cai + p[Q_KmTRPN]) * (Cai + p[Q_KmTRPN])) +
+                    p[Q_CMDNmax] * p[Q_KmCMDN] / ((Cai + p[Q_KmCMDN]) * (Cai + p[Q_KmCMDN]));
+  const double dCaup = Iup - Iupleak - Itr * Vrel / Vup;
+  const double dCarel = (Itr - Irel) /
+                        (1.0 + p[Q_CSQNmax] * p[Q_KmCSQN] / ((Carel + p[Q_KmCSQN]) * (Carel + p[Q_KmCSQN])));
+  u[CR_Nai] += dt * dNai;
+  u[CR_Ki] += dt * dKi;
+  u[CR_Cai] += dt * (B1 / B2);
+  u[CR_Caup] += dt * dCaup;
+  u[CR_Carel] += dt * dCarel;
+  /* gates: Rush-Larsen at (V^k, u^k) */
+  for (int g = 0; g < 15; ++g)
+    u[CR_m + g] = or_rush_larsen(u[CR_m + g], G.inf[g], G.tau[g], dt);
+  return or_crn_current(V, u, p);   /* I_ion(V^k, u^{k+1}) (reading I2) */
+}
+
+void or_crn_step(int64_t n, const double* V, double* U, double dt, const double* p, double* In) {
+  double u[CR_NS];
+  for (int64_t i = 0; i < n; ++i) {
+    for (int s = 0; s < CR_NS; ++s) u[s] = U[(int64_t)s * n + i];
+    In[i] = crn_cell_step(V[i], u, dt, p);
+    for (int s = 0; s < CR_NS; ++s) U[(int64_t)s * n + i] = u[s];
+  }
+}

@@ -25,15 +25,15 @@ __all__ = [
     "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "Monodomain", "LIB_PATH",
     "tc_engine_info", "tc_node_order", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
     "TC_ENGINE_AUTO", "TC_ENGINE_GRID", "TC_ENGINE_CLUSTER",
-    "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS",
+    "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS", "TC_ION_CRN",
 ]
 
 LIB_PATH = os.environ.get("TCB200_LIB") or _build.LIB   # override: experiment variants only
 TC_OK, TC_EINVAL, TC_ENOMEM, TC_ECUDA, TC_ENCCL, TC_ESOLVER, TC_ENAN, TC_ESTATE, TC_EDEGEN, TC_EREGION = range(10)
 STATUS_NAMES = ["TC_OK", "TC_EINVAL", "TC_ENOMEM", "TC_ECUDA", "TC_ENCCL", "TC_ESOLVER", "TC_ENAN",
                 "TC_ESTATE", "TC_EDEGEN", "TC_EREGION"]
-TC_ION_TT2006_EPI, TC_ION_MS, TC_ION_MMS = 0, 1, 2
-MODELS = {"tt2006": TC_ION_TT2006_EPI, "ms": TC_ION_MS, "mms": TC_ION_MMS}
+TC_ION_TT2006_EPI, TC_ION_MS, TC_ION_MMS, TC_ION_CRN = 0, 1, 2, 3
+MODELS = {"tt2006": TC_ION_TT2006_EPI, "ms": TC_ION_MS, "mms": TC_ION_MMS, "crn": TC_ION_CRN}
 TC_ENGINE_AUTO, TC_ENGINE_GRID, TC_ENGINE_CLUSTER, TC_ENGINE_CLUSTER_STREAMING = 0, 1, 2, 3
 ENGINES = {"auto": TC_ENGINE_AUTO, "grid": TC_ENGINE_GRID, "cluster": TC_ENGINE_CLUSTER,
            "cluster_streaming": TC_ENGINE_CLUSTER_STREAMING}

@@ -89,6 +89,9 @@ struct tc_ctx {
   TTParams tt;
   double tt_V0;
   double tt_u0[kTTStates];
+  CRNParams crn;
+  double crn_V0;
+  double crn_u0[kCRNStates];
   MSParams ms;
   MMSParams mms{1.0, M_PI, M_PI, M_PI};
   std::vector<Stim> stims;
@@ -226,7 +229,7 @@ tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx*
   *out = nullptr;
   if (!(cfg->dt > 0) || !(cfg->theta >= 0 && cfg->theta <= 1) || !(cfg->chi > 0) || !(cfg->cm > 0) ||
       cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 ||
-      cfg->model > 2 || cfg->pcg_variant < 0 || cfg->pcg_variant > 2 || cfg->partitions < 1 ||
+      cfg->model > 3 || cfg->pcg_variant < 0 || cfg->pcg_variant > 2 || cfg->partitions < 1 ||
       cfg->partitions > 4096 || cfg->check_every < 1 || cfg->engine < 0 || cfg->engine > 3)
     return TC_EINVAL;
   int ndev = 0;
@@ -237,6 +240,7 @@ tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx*
   c->device = device;
   c->nparts = cfg->partitions;
   tt_defaults(&c->tt, &c->tt_V0, c->tt_u0);
+  crn_defaults(&c->crn, &c->crn_V0, c->crn_u0);
   ms_defaults(&c->ms);
   if (cuda_stream) {
     c->stream = (cudaStream_t)cuda_stream;
@@ -356,6 +360,7 @@ tc_status tc_set_ionic_param(tc_ctx* c, const char* name, double v) {
   if (!c || !name) return TC_EINVAL;
   double* p = nullptr;
   if (c->cfg.model == TC_ION_TT2006_EPI) p = tt_param_slot(&c->tt, name);
+  if (c->cfg.model == TC_ION_CRN) p = crn_param_slot(&c->crn, name);
   if (c->cfg.model == TC_ION_MS) p = ms_param_slot(&c->ms, name);
   if (!p) return fail(c, TC_EINVAL, std::string("unknown ionic parameter ") + name);
   *p = v;
@@ -368,6 +373,7 @@ tc_status tc_get_ionic_param(const tc_ctx* c, const char* name, double* v) {
   tc_ctx* m = const_cast<tc_ctx*>(c);
   double* p = nullptr;
   if (c->cfg.model == TC_ION_TT2006_EPI) p = tt_param_slot(&m->tt, name);
+  if (c->cfg.model == TC_ION_CRN) p = crn_param_slot(&m->crn, name);
   if (c->cfg.model == TC_ION_MS) p = ms_param_slot(&m->ms, name);
   if (!p) return TC_EINVAL;
   *v = *p;
@@ -450,6 +456,13 @@ static tc_status init_state(tc_ctx* c) {
       std::vector<double> u((size_t)kTTStates * np, 0.0);
       for (int s = 0; s < kTTStates; ++s)
         for (int64_t i = 0; i < n; ++i) u[s * np + i] = c->tt_u0[s];
+      CUDA_TRY(c, cudaMemcpyAsync(P.d_U, u.data(), u.size() * 8, cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    } else if (c->cfg.model == TC_ION_CRN) {
+      for (int64_t i = 0; i < n; ++i) v[i] = c->crn_V0;
+      std::vector<double> u((size_t)kCRNStates * np, 0.0);
+      for (int s = 0; s < kCRNStates; ++s)
+        for (int64_t i = 0; i < n; ++i) u[s * np + i] = c->crn_u0[s];
       CUDA_TRY(c, cudaMemcpyAsync(P.d_U, u.data(), u.size() * 8, cudaMemcpyHostToDevice, c->stream));
       CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     } else if (c->cfg.model == TC_ION_MS) {
@@ -949,7 +962,10 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
     return fail(c, TC_EREGION, "tet " + std::to_string(bad) + " has region " +
                                    std::to_string(c->region[bad]) + " without conductivity");
   std::vector<PartPlan> plans;
-  c->nstates = c->cfg.model == TC_ION_TT2006_EPI ? kTTStates : (c->cfg.model == TC_ION_MS ? 1 : 0);
+  c->nstates = c->cfg.model == TC_ION_TT2006_EPI ? kTTStates
+               : c->cfg.model == TC_ION_CRN   ? kCRNStates
+               : c->cfg.model == TC_ION_MS    ? 1
+                                              : 0;
   const bool on_dev = c->cfg.device_setup && c->nparts == 1 && !c->use_comm && c->cfg.pcg_variant != 2;
   if (on_dev) {
     TC_TRY(assemble_device(c, ereg));
@@ -1213,7 +1229,7 @@ static tc_status pcg_split(tc_ctx* c) {
 // ------------------------------------------------------------------ cluster engine
 static bool cluster_capable(const tc_ctx* c) {
   return c->assembled && !c->csr_mode && !split_mode(c) && c->parts.size() == 1 &&
-         (c->cfg.model == TC_ION_TT2006_EPI || c->cfg.model == TC_ION_MS);
+         (c->cfg.model == TC_ION_TT2006_EPI || c->cfg.model == TC_ION_MS || c->cfg.model == TC_ION_CRN);
 }
 
 // CTAs per cluster for a system of `nslices` warp slices: one slice per warp
@@ -1249,7 +1265,7 @@ static tc_status make_corep(tc_ctx* c, CoRep& R, tc_step_stat* stats) {
   if (!c->d_params) CUDA_TRY(c, dalloc(c, &c->d_params, cohort_param_doubles()));
   if (c->params_uploaded != c->param_version) {
     std::vector<double> h(cohort_param_doubles());
-    cohort_pack_params(c->cfg.model, c->tt, c->ms, h.data());
+    cohort_pack_params(c->cfg.model, c->tt, c->ms, c->crn, h.data());
     CUDA_TRY(c, cudaMemcpyAsync(c->d_params, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->params_uploaded = c->param_version;
@@ -1341,6 +1357,7 @@ extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
       IonArgs ia = ion_args(c, P, (st > 0 && c->has_prev) ? 1 : 0);
       cudaError_t e;
       if (model == TC_ION_TT2006_EPI) e = launch_ionic_tt(ia, c->tt, c->stream);
+      else if (model == TC_ION_CRN) e = launch_ionic_crn(ia, c->crn, c->stream);
       else if (model == TC_ION_MS) e = launch_ionic_ms(ia, c->ms, c->stream);
       else e = launch_ionic_mms(ia, c->mms, c->stream);
       CUDA_TRY(c, e);
@@ -1883,7 +1900,9 @@ const char* tc_cohort_last_error(const tc_cohort* co) { return co ? co->err.c_st
 tc_status tc_cohort_destroy(tc_cohort* co) {
   if (!co) return TC_OK;
   cudaSetDevice(co->device);
-  if (co->stream) cudaStreamSynchronize(co->stream);
+  // wait for the last launch through the cohort's own event: the members (and
+  // member 0's stream) may already be gone
+  if (co->ev) cudaEventSynchronize(co->ev);
   for (void* p : co->allocs) cudaFree(p);
   if (co->ev) cudaEventDestroy(co->ev);
   delete co;

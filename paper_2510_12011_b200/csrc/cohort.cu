@@ -31,7 +31,9 @@ namespace tcb {
 namespace {
 
 constexpr int kCoWarps = kCoThreads / 32;
-constexpr int kParamDoubles = (sizeof(TTParams) + sizeof(TTDerived) + 7) / 8;
+constexpr size_t kTTBytes = sizeof(TTParams) + sizeof(TTDerived);
+constexpr size_t kCRNBytes = sizeof(CRNParams) + sizeof(CRNDerived);
+constexpr int kParamDoubles = (int)(((kTTBytes > kCRNBytes ? kTTBytes : kCRNBytes) + 7) / 8);
 
 struct CoShared {
   CoRep R;
@@ -135,12 +137,14 @@ __global__ void __launch_bounds__(kCoThreads, 1)
   __syncthreads();
   const CoRep& R = S.R;
   for (int j = threadIdx.x; j < kParamDoubles; j += blockDim.x) S.prm[j] = R.params[j];
-  if (MODEL == TC_ION_TT2006_EPI) exp2_table_init(&T);  // includes __syncthreads
+  if (MODEL != TC_ION_MS) exp2_table_init(&T);  // includes __syncthreads
   __syncthreads();
   const TTParams& TP = *reinterpret_cast<const TTParams*>(S.prm);
   const TTDerived& TD = *reinterpret_cast<const TTDerived*>(S.prm + sizeof(TTParams) / 8);
   const MSParams& MP = *reinterpret_cast<const MSParams*>(S.prm);
   const MSDerived& MD = *reinterpret_cast<const MSDerived*>(S.prm + sizeof(MSParams) / 8);
+  const CRNParams& CP = *reinterpret_cast<const CRNParams*>(S.prm);
+  const CRNDerived& CD = *reinterpret_cast<const CRNDerived*>(S.prm + sizeof(CRNParams) / 8);
 
   // every CTA reads the same flags before any CTA can change them (the first
   // write follows a cluster barrier), so the early exit is cluster-uniform
@@ -284,6 +288,13 @@ __global__ void __launch_bounds__(kCoThreads, 1)
         In = tt_advance(V, u, R.dt, TP, TD, &T);
 #pragma unroll
         for (int q2 = 0; q2 < kTTStates; ++q2) R.U[q2 * R.stride + i] = u[q2];
+      } else if (MODEL == TC_ION_CRN) {
+        double u[kCRNStates];
+#pragma unroll
+        for (int q2 = 0; q2 < kCRNStates; ++q2) u[q2] = R.U[q2 * R.stride + i];
+        In = crn_advance(V, u, R.dt, CP, CD, &T);
+#pragma unroll
+        for (int q2 = 0; q2 < kCRNStates; ++q2) R.U[q2 * R.stride + i] = u[q2];
       } else {
         In = ms_advance(V, R.U + i, R.dt, MP, MD);
       }
@@ -530,14 +541,21 @@ __global__ void __launch_bounds__(kCoThreads, 1)
 static const void* cohort_fn(int model, bool res) {
   if (model == TC_ION_TT2006_EPI)
     return res ? (const void*)cohort_kernel<TC_ION_TT2006_EPI, true> : (const void*)cohort_kernel<TC_ION_TT2006_EPI, false>;
+  if (model == TC_ION_CRN)
+    return res ? (const void*)cohort_kernel<TC_ION_CRN, true> : (const void*)cohort_kernel<TC_ION_CRN, false>;
   return res ? (const void*)cohort_kernel<TC_ION_MS, true> : (const void*)cohort_kernel<TC_ION_MS, false>;
 }
 
 int cohort_param_doubles() { return kParamDoubles; }
 
-void cohort_pack_params(int model, const TTParams& tp, const MSParams& mp, double* out) {
+void cohort_pack_params(int model, const TTParams& tp, const MSParams& mp, const CRNParams& cp,
+                        double* out) {
   for (int j = 0; j < kParamDoubles; ++j) out[j] = 0.0;
-  if (model == TC_ION_TT2006_EPI) {
+  if (model == TC_ION_CRN) {
+    const CRNDerived d = crn_derived(cp);
+    std::memcpy(out, &cp, sizeof(CRNParams));
+    std::memcpy(out + sizeof(CRNParams) / 8, &d, sizeof(CRNDerived));
+  } else if (model == TC_ION_TT2006_EPI) {
     const TTDerived d = tt_derived(tp);
     std::memcpy(out, &tp, sizeof(TTParams));
     std::memcpy(out + sizeof(TTParams) / 8, &d, sizeof(TTDerived));

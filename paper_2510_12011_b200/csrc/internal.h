@@ -55,9 +55,18 @@ struct MSParams {
 struct MMSParams {
   double k, w1, w2, lam;
 };
+// ---- CRN 1998 atrial model parameters (names for tc_set_ionic_param, oracle order)
+struct CRNParams {
+  double R, T, F, Cm, Vi, Vup, Vrel, Ko, Nao, Cao, gNa, gK1, gto, gKr, gKs, gCaL, gbNa, gbCa;
+  double INaKmax, KmNai, KmKo, INaCamax, KmNa, KmCa, ksat, gamma, IpCamax, Krel, tautr;
+  double Iupmax, Kup, Caupmax, CMDNmax, TRPNmax, CSQNmax, KmCMDN, KmTRPN, KmCSQN, tauu, KQ10;
+};
+constexpr int kCRNStates = 20;
 
 void tt_defaults(TTParams* p, double* V0, double u0[kTTStates]);
 void ms_defaults(MSParams* p);
+void crn_defaults(CRNParams* p, double* V0, double u0[kCRNStates]);
+double* crn_param_slot(CRNParams* p, const char* name);
 double* tt_param_slot(TTParams* p, const char* name);
 double* ms_param_slot(MSParams* p, const char* name);
 
@@ -244,7 +253,8 @@ struct CoRep {
   const double* params;          // cohort_pack_params block (device)
 };
 int cohort_param_doubles();
-void cohort_pack_params(int model, const TTParams& tp, const MSParams& mp, double* out);
+void cohort_pack_params(int model, const TTParams& tp, const MSParams& mp, const CRNParams& cp,
+                        double* out);
 int cohort_cluster_size(int model, int want);
 int cohort_active_clusters(int model, int csize, size_t smem);  // smem 0 = streaming launch
 size_t cohort_smem_bytes(const int64_t* sp, int32_t ns, int C);
@@ -258,6 +268,7 @@ cudaError_t launch_assemble(const AsmArgs& a, cudaStream_t s);
 cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s);
 cudaError_t launch_ionic_ms(const IonArgs& a, const MSParams& p, cudaStream_t s);
 cudaError_t launch_ionic_mms(const IonArgs& a, const MMSParams& p, cudaStream_t s);
+cudaError_t launch_ionic_crn(const IonArgs& a, const CRNParams& p, cudaStream_t s);
 cudaError_t launch_stimulus(int32_t m, const int32_t* idx, const double* s, double* up, double* vp,
                             double dt, double theta, const int32_t* flags, cudaStream_t st);
 cudaError_t launch_lat_epilogue(const IonArgs& a, cudaStream_t s);

@@ -160,6 +160,51 @@ cudaError_t launch_ionic_mms(const IonArgs& a, const MMSParams& p, cudaStream_t 
   ionic_mms_kernel<<<nblk(a.n, 256), 256, 0, s>>>(a, p);
   return cudaGetLastError();
 }
+// ------------------------------------------------------------------ CRN 1998
+CRNDerived crn_derived(const CRNParams& P) {
+  CRNDerived D;
+  D.rtf = P.R * P.T / P.F;
+  D.frt = P.F / (P.R * P.T);
+  D.sigma_k = 0.0365 * (std::exp(P.Nao / 67.3) - 1.0) / 7.0;
+  D.cm_vif = P.Cm / (P.Vi * P.F);
+  D.cm_2vif = P.Cm / (2.0 * P.Vi * P.F);
+  D.inak_k = P.INaKmax * P.Ko / (P.Ko + P.KmKo);
+  D.inaca_k = P.INaCamax / ((P.KmNa * P.KmNa * P.KmNa + P.Nao * P.Nao * P.Nao) * (P.KmCa + P.Cao));
+  D.nao3 = P.Nao * P.Nao * P.Nao;
+  D.inv_tautr = 1.0 / P.tautr;
+  D.iupleak_k = P.Iupmax / P.Caupmax;
+  D.vup_vi = P.Vup / P.Vi;
+  D.vrel_vi = P.Vrel / P.Vi;
+  D.vrel_vup = P.Vrel / P.Vup;
+  D.inv_kq10 = 1.0 / P.KQ10;
+  D.fn_c = 1e-15 / (2.0 * P.F) * P.Cm;  // currents per capacitance -> pA
+  return D;
+}
+
+__global__ void __launch_bounds__(128) ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D) {
+  __shared__ Exp2Table T;
+  exp2_table_init(&T);
+  if (a.flags[0]) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const double V = a.Vk[i];
+  const double Vp = a.has_prev ? a.Vkm1[i] : V;
+  if (a.do_lat) activation_update(a, i, V, Vp);
+  double u[kCRNStates];
+#pragma unroll
+  for (int s = 0; s < kCRNStates; ++s) u[s] = a.U[s * a.stride + i];
+  const double In = crn_advance(V, u, a.dt, P, D, &T);
+#pragma unroll
+  for (int s = 0; s < kCRNStates; ++s) a.U[s * a.stride + i] = u[s];
+  write_rhs(a, i, V, Vp, In);
+}
+
+cudaError_t launch_ionic_crn(const IonArgs& a, const CRNParams& p, cudaStream_t s) {
+  if (a.n == 0) return cudaSuccess;
+  ionic_crn_kernel<<<nblk(a.n, 128), 128, 0, s>>>(a, p, crn_derived(p));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stimulus(int32_t m, const int32_t* idx, const double* sv, double* up, double* vp,
                             double dt, double theta, const int32_t* flags, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
@@ -200,6 +245,18 @@ void tt_defaults(TTParams* p, double* V0, double u0[kTTStates]) {
 
 void ms_defaults(MSParams* p) { *p = MSParams{0.3, 6.0, 120.0, 150.0, 0.13, -80.0, 20.0}; }
 
+void crn_defaults(CRNParams* p, double* V0, double u0[kCRNStates]) {
+  *p = CRNParams{8.3143, 310.0, 96.4867, 100.0, 13668.0, 1109.52, 96.48, 5.4, 140.0, 1.8,
+                 7.8, 0.09, 0.1652, 0.029411765, 0.12941176, 0.12375, 6.744375e-4, 1.131e-3,
+                 0.59933874, 10.0, 1.5, 1600.0, 87.5, 1.38, 0.1, 0.35, 0.275, 30.0, 180.0,
+                 0.005, 0.00092, 15.0, 0.05, 0.07, 10.0, 0.00238, 0.0005, 0.8, 8.0, 3.0};
+  *V0 = -81.18;
+  const double ic[kCRNStates] = {11.17, 139.0, 1.013e-4, 1.488, 1.488, 2.908e-3, 0.9649, 0.9775,
+                                 3.043e-2, 0.9992, 4.966e-3, 0.9986, 3.296e-5, 1.869e-2, 1.367e-4,
+                                 0.9996, 0.7755, 2.35e-112, 1.0, 0.9992};
+  for (int s = 0; s < kCRNStates; ++s) u0[s] = ic[s];
+}
+
 static const char* kTTNames[] = {
     "R", "T", "F", "CAP", "Vc", "Vsr", "Vss", "Ko", "Nao", "Cao", "GNa", "GK1", "Gto", "GKr", "GKs",
     "pKNa", "GCaL", "GbNa", "GbCa", "GpCa", "KpCa", "GpK", "PNaK", "KmK", "KmNa", "kNaCa", "KmNai",
@@ -214,6 +271,19 @@ double* tt_param_slot(TTParams* p, const char* name) {
     if (!strcmp(kTTNames[k], name)) return reinterpret_cast<double*>(p) + k;
   return nullptr;
 }
+static const char* kCRNNames[] = {
+    "R", "T", "F", "Cm", "Vi", "Vup", "Vrel", "Ko", "Nao", "Cao", "gNa", "gK1", "gto", "gKr",
+    "gKs", "gCaL", "gbNa", "gbCa", "INaKmax", "KmNai", "KmKo", "INaCamax", "KmNa", "KmCa", "ksat",
+    "gamma", "IpCamax", "Krel", "tautr", "Iupmax", "Kup", "Caupmax", "CMDNmax", "TRPNmax",
+    "CSQNmax", "KmCMDN", "KmTRPN", "KmCSQN", "tauu", "KQ10"};
+
+double* crn_param_slot(CRNParams* p, const char* name) {
+  static_assert(sizeof(CRNParams) == sizeof(kCRNNames) / sizeof(kCRNNames[0]) * sizeof(double), "");
+  for (size_t k = 0; k < sizeof(kCRNNames) / sizeof(kCRNNames[0]); ++k)
+    if (!strcmp(kCRNNames[k], name)) return reinterpret_cast<double*>(p) + k;
+  return nullptr;
+}
+
 double* ms_param_slot(MSParams* p, const char* name) {
   for (size_t k = 0; k < sizeof(kMSNames) / sizeof(kMSNames[0]); ++k)
     if (!strcmp(kMSNames[k], name)) return reinterpret_cast<double*>(p) + k;

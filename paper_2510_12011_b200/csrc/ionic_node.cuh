@@ -283,7 +283,172 @@ __device__ __forceinline__ double ms_advance(double V, double* h_io, double dt, 
   return -D.span * (h * v * v * (1.0 - v) * D.inv_in - v * D.inv_out);
 }
 
+
+// ------------------------------------------------------------------ CRN 1998 (atrial)
+// Courtemanche, Ramirez & Nattel 1998 (named among the paper's models, P:98;
+// SURVEY 8f row f4; reading I6), the same equations as the oracle
+// (oracle.c 6c): Rush-Larsen for the 15 gates, forward Euler for Na_i, K_i,
+// Ca_i (instantaneous TRPN/CMDN buffering factor), Ca_up, Ca_rel -- all at
+// (V^k, u^k); I_n = I_ion(V^k, u^{k+1}) (reading I2).  20 states in the order
+// Nai Ki Cai Caup Carel m h j oa oi ua ui xr xs d f fCa u v w.
+enum { cNai, cKi, cCai, cCaup, cCarel, cm, chh, cj, coa, coi, cua, cui, cxr, cxs, cd, cf, cfCa,
+       cu, cv, cw };
+
+struct CRNDerived {   // parameter-only factors (host-computed)
+  double rtf, frt, sigma_k;   // RT/F, F/RT, 0.0365 sigma
+  double cm_vif, cm_2vif;     // Cm / (Vi F), Cm / (2 Vi F)
+  double inak_k;              // INaK_max Ko / (Ko + KmKo)
+  double inaca_k;             // INaCa_max / ((KmNa^3 + Nao^3)(KmCa + Cao))
+  double nao3, inv_tautr, iupleak_k, vup_vi, vrel_vi, vrel_vup, inv_kq10, fn_c;
+};
+
+struct CRNCur {
+  double ina, ik1, ito, ikur, ikr, iks, ical, inak, inaca, ibna, ibca, ipca;
+};
+
+__device__ __forceinline__ CRNCur crn_cur(double V, const double* u, const CRNParams& P,
+                                          const CRNDerived& D, const Exp2Table* T) {
+  CRNCur c;
+  const double nai = u[cNai], ki = u[cKi], cai = u[cCai];
+  const double ena = D.rtf * log(P.Nao / nai), ek = D.rtf * log(P.Ko / ki);
+  const double eca = 0.5 * D.rtf * log(P.Cao / cai);
+  const double m = u[cm], oa = u[coa], ua = u[cua], xs = u[cxs];
+  c.ina = P.gNa * m * m * m * u[chh] * u[cj] * (V - ena);
+  c.ik1 = P.gK1 * (V - ek) * tc_rcp(1.0 + EXP(0.07 * (V + 80.0)));
+  c.ito = P.gto * oa * oa * oa * u[coi] * (V - ek);
+  const double gkur = 0.005 + 0.05 * tc_rcp(1.0 + EXP((V - 15.0) * (1.0 / -13.0)));
+  c.ikur = gkur * ua * ua * ua * u[cui] * (V - ek);
+  c.ikr = P.gKr * u[cxr] * (V - ek) * tc_rcp(1.0 + EXP((V + 15.0) * (1.0 / 22.4)));
+  c.iks = P.gKs * xs * xs * (V - ek);
+  c.ical = P.gCaL * u[cd] * u[cf] * u[cfCa] * (V - 65.0);
+  const double e = EXP(-V * D.frt);                         // exp(-F V / RT)
+  const double fnak = tc_rcp(1.0 + 0.1245 * EXP(-0.1 * V * D.frt) + D.sigma_k * e);
+  const double q = P.KmNai / nai;
+  c.inak = D.inak_k * fnak * tc_rcp(1.0 + q * sqrt(q));
+  const double eg = EXP(P.gamma * V * D.frt), eg1 = eg * e;  // exp((gamma-1) F V / RT)
+  c.inaca = D.inaca_k * (eg * nai * nai * nai * P.Cao - eg1 * D.nao3 * cai) *
+            tc_rcp(1.0 + P.ksat * eg1);
+  c.ibna = P.gbNa * (V - ena);
+  c.ibca = P.gbCa * (V - eca);
+  c.ipca = P.IpCamax * cai * tc_rcp(0.0005 + cai);
+  return c;
+}
+
+__device__ __forceinline__ double crn_total(const CRNCur& c) {
+  return c.ina + c.ik1 + c.ito + c.ikur + c.ikr + c.iks + c.ical + c.inak + c.inaca + c.ibna +
+         c.ibca + c.ipca;
+}
+
+// 1 / (1 + e^x) for the release-flux sigmoids, whose arguments (Fn / 1.367e-15)
+// reach |x| ~ 1e4: outside |x| <= 700 (the range of tc_exp) the value is 0 or 1
+// to double precision (what 1/(1 + exp(x)) gives with libm: inf -> 0, 0 -> 1).
+__device__ __forceinline__ double crn_sig(double x, const Exp2Table* T) {
+  if (x > 700.0) return 0.0;
+  if (x < -700.0) return 1.0;
+  return tc_rcp(1.0 + EXP(x));
+}
+
+__device__ __forceinline__ double rl_tau(double y, double yinf, double tau, double dt,
+                                         const Exp2Table* T) {
+  return yinf - (yinf - y) * EXP(-dt * tc_rcp(tau));
+}
+
+// Advances u in place; returns I_n(V, u^{k+1}).
+__device__ __forceinline__ double crn_advance(double V, double* u, double dt, const CRNParams& P,
+                                              const CRNDerived& D, const Exp2Table* T) {
+  const CRNCur c = crn_cur(V, u, P, D, T);
+  const double cai = u[cCai], caup = u[cCaup], carel = u[cCarel];
+  const double irel = P.Krel * u[cu] * u[cu] * u[cv] * u[cw] * (carel - cai);
+  const double itr = (caup - carel) * D.inv_tautr;
+  const double iupleak = D.iupleak_k * caup;
+  const double iup = P.Iupmax * tc_rcp(1.0 + P.Kup * tc_rcp(cai));
+  // gates at (V^k, u^k), each Rush-Larsen update applied as soon as its
+  // steady state and time constant are known (nothing below reads a gate)
+  {
+    double a, b, ti;
+    a = (V == -47.13) ? 3.2 : 0.32 * (V + 47.13) * tc_rcp(1.0 - EXP(-0.1 * (V + 47.13)));
+    b = 0.08 * EXP(V * (-1.0 / 11.0));
+    ti = tc_rcp(a + b);
+    u[cm] = rl_tau(u[cm], a * ti, ti, dt, T);
+    if (V < -40.0) {
+      a = 0.135 * EXP((V + 80.0) * (1.0 / -6.8));
+      b = 3.56 * EXP(0.079 * V) + 3.1e5 * EXP(0.35 * V);
+    } else {
+      a = 0.0;
+      b = tc_rcp(0.13 * (1.0 + EXP((V + 10.66) * (1.0 / -11.1))));
+    }
+    ti = tc_rcp(a + b);
+    u[chh] = rl_tau(u[chh], a * ti, ti, dt, T);
+    if (V < -40.0) {
+      a = (-127140.0 * EXP(0.2444 * V) - 3.474e-5 * EXP(-0.04391 * V)) * (V + 37.78) *
+          tc_rcp(1.0 + EXP(0.311 * (V + 79.23)));
+      b = 0.1212 * EXP(-0.01052 * V) * tc_rcp(1.0 + EXP(-0.1378 * (V + 40.14)));
+    } else {
+      a = 0.0;
+      b = 0.3 * EXP(-2.535e-7 * V) * tc_rcp(1.0 + EXP(-0.1 * (V + 32.0)));
+    }
+    ti = tc_rcp(a + b);
+    u[cj] = rl_tau(u[cj], a * ti, ti, dt, T);
+    // oa and ua share their rate functions
+    a = 0.65 * tc_rcp(EXP((V + 10.0) * (1.0 / -8.5)) + EXP((V - 30.0) * (1.0 / -59.0)));
+    b = 0.65 * tc_rcp(2.5 + EXP((V + 82.0) * (1.0 / 17.0)));
+    ti = tc_rcp(a + b) * D.inv_kq10;
+    u[coa] = rl_tau(u[coa], tc_rcp(1.0 + EXP((V + 20.47) * (1.0 / -17.54))), ti, dt, T);
+    u[cua] = rl_tau(u[cua], tc_rcp(1.0 + EXP((V + 30.3) * (1.0 / -9.6))), ti, dt, T);
+    a = tc_rcp(18.53 + EXP((V + 113.7) * (1.0 / 10.95)));
+    b = tc_rcp(35.56 + EXP((V + 1.26) * (1.0 / -7.44)));
+    u[coi] = rl_tau(u[coi], tc_rcp(1.0 + EXP((V + 43.1) * (1.0 / 5.3))), tc_rcp(a + b) * D.inv_kq10, dt, T);
+    a = tc_rcp(21.0 + EXP((V - 185.0) * (1.0 / -28.0)));
+    b = EXP((V - 158.0) * (1.0 / 16.0));
+    u[cui] = rl_tau(u[cui], tc_rcp(1.0 + EXP((V - 99.45) * (1.0 / 27.48))), tc_rcp(a + b) * D.inv_kq10, dt, T);
+    a = (V == -14.1) ? 0.0015 : 0.0003 * (V + 14.1) * tc_rcp(1.0 - EXP((V + 14.1) * (1.0 / -5.0)));
+    b = (V == 3.3328) ? 3.7836118e-4
+                      : 7.3898e-5 * (V - 3.3328) * tc_rcp(EXP((V - 3.3328) * (1.0 / 5.1237)) - 1.0);
+    u[cxr] = rl_tau(u[cxr], tc_rcp(1.0 + EXP((V + 14.1) * (1.0 / -6.5))), tc_rcp(a + b), dt, T);
+    a = (V == 19.9) ? 0.00068 : 4e-5 * (V - 19.9) * tc_rcp(1.0 - EXP((V - 19.9) * (1.0 / -17.0)));
+    b = (V == 19.9) ? 0.000315 : 3.5e-5 * (V - 19.9) * tc_rcp(EXP((V - 19.9) * (1.0 / 9.0)) - 1.0);
+    u[cxs] = rl_tau(u[cxs], tc_rcp(sqrt(1.0 + EXP((V - 19.9) * (1.0 / -12.7)))), 0.5 * tc_rcp(a + b), dt, T);
+    {
+      const double ed = EXP((V + 10.0) * (1.0 / -6.24));
+      const double td = (V == -10.0) ? 4.579 * tc_rcp(1.0 + ed)
+                                     : (1.0 - ed) * tc_rcp(0.035 * (V + 10.0) * (1.0 + ed));
+      u[cd] = rl_tau(u[cd], tc_rcp(1.0 + EXP((V + 10.0) * (1.0 / -8.0))), td, dt, T);
+    }
+    {
+      const double ef = EXP(-(V + 28.0) * (1.0 / 6.9));
+      const double v10 = V + 10.0;
+      u[cf] = rl_tau(u[cf], ef * tc_rcp(1.0 + ef),
+                     9.0 * tc_rcp(0.0197 * EXP(-0.0337 * 0.0337 * v10 * v10) + 0.02), dt, T);
+    }
+    u[cfCa] = rl_tau(u[cfCa], tc_rcp(1.0 + cai * (1.0 / 0.00035)), 2.0, dt, T);
+    const double fn = 1000.0 * (1e-15 * P.Vrel * irel - D.fn_c * (0.5 * c.ical - 0.2 * c.inaca));
+    const double su = crn_sig(-(fn - 3.4175e-13) * (1.0 / 13.67e-16), T);
+    u[cu] = rl_tau(u[cu], su, P.tauu, dt, T);
+    u[cv] = rl_tau(u[cv], 1.0 - crn_sig(-(fn - 6.835e-14) * (1.0 / 13.67e-16), T), 1.91 + 2.09 * su, dt, T);
+    const double ew = EXP(-(V - 7.9) * (1.0 / 5.0));
+    const double tw = (V == 7.9) ? 6.0 * 0.2 / 1.3 : 6.0 * (1.0 - ew) * tc_rcp((1.0 + 0.3 * ew) * (V - 7.9));
+    u[cw] = rl_tau(u[cw], 1.0 - tc_rcp(1.0 + EXP(-(V - 40.0) * (1.0 / 17.0))), tw, dt, T);
+  }
+  // concentrations: forward Euler at (V^k, u^k)
+  const double dnai = (-3.0 * c.inak - 3.0 * c.inaca - c.ibna - c.ina) * D.cm_vif;
+  const double dki = (2.0 * c.inak - c.ik1 - c.ito - c.ikur - c.ikr - c.iks) * D.cm_vif;
+  const double b1 = (2.0 * c.inaca - c.ipca - c.ical - c.ibca) * D.cm_2vif +
+                    (iupleak - iup) * D.vup_vi + irel * D.vrel_vi;
+  const double t1 = cai + P.KmTRPN, t2 = cai + P.KmCMDN;
+  const double b2 = 1.0 + P.TRPNmax * P.KmTRPN * tc_rcp(t1 * t1) + P.CMDNmax * P.KmCMDN * tc_rcp(t2 * t2);
+  const double dcaup = iup - iupleak - itr * D.vrel_vup;
+  const double t3 = carel + P.KmCSQN;
+  const double dcarel = (itr - irel) * tc_rcp(1.0 + P.CSQNmax * P.KmCSQN * tc_rcp(t3 * t3));
+  u[cNai] += dt * dnai;
+  u[cKi] += dt * dki;
+  u[cCai] += dt * (b1 * tc_rcp(b2));
+  u[cCaup] += dt * dcaup;
+  u[cCarel] += dt * dcarel;
+  return crn_total(crn_cur(V, u, P, D, T));  // I_ion(V^k, u^{k+1}) (reading I2)
+}
+
 TTDerived tt_derived(const TTParams& P);
 MSDerived ms_derived(const MSParams& P);
+CRNDerived crn_derived(const CRNParams& P);
 
 }  // namespace tcb

@@ -58,6 +58,8 @@ def _oracle(spec, xyz, tets, region, fib, cond, stims):
     if spec.get("params"):
         if model == "tt2006":
             names, params = O.tt_param_names(), O.tt_default_params().copy()
+        elif model == "crn":
+            names, params = O.crn_param_names(), O.crn_default_params().copy()
         else:
             names, params = list(O.MS_PARAM_NAMES), O.ms_default_params().copy()
         for k, v in spec["params"].items():
@@ -91,7 +93,8 @@ def _check(sim, ref, stats_row, reps, dt, what):
 @pytest.mark.parametrize("model,permute,chunk,engine", [("tt2006", 0, 1, "cluster"), ("tt2006", 7, 9, "cluster"),
                                                         ("ms", 0, 5, "cluster"), ("ms", 3, 1, "cluster"),
                                                         ("tt2006", 7, 9, "cluster_streaming"),
-                                                        ("ms", 3, 4, "cluster_streaming")])
+                                                        ("ms", 3, 4, "cluster_streaming"),
+                                                        ("crn", 0, 6, "cluster"), ("crn", 5, 3, "cluster_streaming")])
 def test_cluster_engine_trajectory_parity(T, model, permute, chunk, engine):
     """One context on the cluster engine (shared-memory resident or streaming),
     `chunk` steps per tc_step call (the in-kernel rotation, the V write-back and
@@ -182,6 +185,30 @@ def test_cohort_parity(T, cluster_size, resident):
             st = sim.step(3)
             reps = [ref.step() for _ in range(3)]
             _check(sim, ref, st, reps, 0.05, "after cohort")
+    finally:
+        for s in members:
+            s.close()
+
+
+def test_cohort_crn_members(T):
+    """CRN atrial members in one cohort, each against its oracle."""
+    specs = [dict(dims=(21, 8, 5), model="crn"), dict(dims=(13, 6, 4), model="crn", params={"gto": 0.08}),
+             dict(dims=(17, 9, 6), model="crn", permute=2, fib_seed=5)]
+    members, refs = [], []
+    try:
+        for spec in specs:
+            args = _member(spec)
+            refs.append(_oracle(spec, *args))
+            members.append(_gpu(T, spec, *args))
+        co = T.Cohort(members)
+        try:
+            for c in range(4):
+                stats = co.step(15)
+                for m, (sim, ref) in enumerate(zip(members, refs)):
+                    reps = [ref.step() for _ in range(15)]
+                    _check(sim, ref, stats[m], reps, 0.05, f"crn member {m} chunk {c}")
+        finally:
+            co.close()
     finally:
         for s in members:
             s.close()

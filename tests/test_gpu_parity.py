@@ -102,7 +102,8 @@ def _slab_case(model, nx=21, ny=8, nz=5, dx=0.5, permute=False, seed=0):
 @pytest.mark.parametrize("model,permute,rcm,variant", [("ms", False, 1, 0), ("tt2006", False, 1, 0),
                                                         ("tt2006", True, 1, 0), ("tt2006", True, 0, 1),
                                                         ("ms", True, 0, 1), ("tt2006", False, 1, 1),
-                                                        ("tt2006", True, 1, 2)])
+                                                        ("tt2006", True, 1, 2), ("crn", False, 1, 0),
+                                                        ("crn", True, 1, 1)])
 def test_step_trajectory_parity(T, model, permute, rcm, variant):
     """Multi-step trajectory through the real stimulus window (upstroke), V per
     step within rel-L2 1e-8, LAT within one dt, per-step iteration counts equal."""
@@ -235,7 +236,8 @@ def test_state_injection_one_step(T, engine):
 def test_ionic_params_match_oracle_transcription(T):
     """Two independent transcriptions of TT2006 / MS constants agree."""
     for model, names, vals in (("tt2006", O.tt_param_names(), O.tt_default_params()),
-                               ("ms", O.MS_PARAM_NAMES, O.ms_default_params())):
+                               ("ms", O.MS_PARAM_NAMES, O.ms_default_params()),
+                               ("crn", O.crn_param_names(), O.crn_default_params())):
         ctx = T.tc_create(T.tc_config_default(model=model))
         try:
             for nme, v in zip(names, vals):

@@ -176,3 +176,105 @@ def test_tt_stimulated_action_potential():
     assert (Vs[up:] < -70).any()
     down = up + np.argmax(Vs[up:] < -70)
     assert 150 < (down - up) * dt < 450     # a ventricular-length action potential
+
+
+# ---------------------------------------------------------------- CRN 1998
+def _crn_only(keep):
+    """CRN parameters with every membrane conductance / pump maximum zeroed except `keep`."""
+    names = O.crn_param_names()
+    p = O.crn_default_params()
+    for g in ("gNa", "gK1", "gto", "gKr", "gKs", "gCaL", "gbNa", "gbCa", "INaKmax", "INaCamax",
+              "IpCamax"):
+        if g not in keep:
+            p[names.index(g)] = 0.0
+    return p, names
+
+
+def test_crn_reversal_potentials_nernst():
+    """I_Kur has no conductance parameter; with every other current off, the
+    model current is I_Kur alone: zero at E_K.  Each K, Na, Ca channel current
+    vanishes at its Nernst potential computed here from R, T, F and the
+    concentrations only, and is linear in V with the conductance as slope."""
+    _, U = O.crn_initial_state(1)
+    u = U[:, 0].copy()
+    sn = O.crn_state_names()
+    R, T, F = 8.3143, 310.0, 96.4867
+    RTF = R * T / F
+    EK = RTF * math.log(5.4 / u[sn.index("Ki")])
+    ENa = RTF * math.log(140.0 / u[sn.index("Nai")])
+    ECa = 0.5 * RTF * math.log(1.8 / u[sn.index("Cai")])
+    assert EK == pytest.approx(-86.765, abs=2e-3) and ENa == pytest.approx(67.5, abs=0.2)
+    # I_Kur alone (every parameterised current off)
+    p, _ = _crn_only(set())
+    assert O.crn_current(EK, u, p) == pytest.approx(0.0, abs=1e-14)
+    assert O.crn_current(EK + 5.0, u, p) > 0 > O.crn_current(EK - 5.0, u, p)
+    # open every gate fully so that each channel current is g (V - E) x rectification
+    for g in ("m", "h", "j", "oa", "oi", "xr", "xs", "d", "f", "fCa"):
+        u[sn.index(g)] = 1.0
+    u[sn.index("ua")] = 0.0                       # I_Kur off
+    for g, E in (("gK1", EK), ("gto", EK), ("gKr", EK), ("gKs", EK), ("gNa", ENa), ("gbNa", ENa),
+                 ("gbCa", ECa)):
+        p, _ = _crn_only({g})
+        assert O.crn_current(E, u, p) == pytest.approx(0.0, abs=1e-12), g
+        assert O.crn_current(E + 5.0, u, p) > 0 > O.crn_current(E - 5.0, u, p), g
+    for g, slope in (("gNa", 7.8), ("gbNa", 6.744375e-4), ("gbCa", 1.131e-3), ("gto", 0.1652),
+                     ("gKs", 0.12941176)):
+        p, _ = _crn_only({g})
+        E = ENa if g in ("gNa", "gbNa") else (ECa if g == "gbCa" else EK)
+        assert O.crn_current(E + 10.0, u, p) == pytest.approx(10.0 * slope, rel=1e-12), g
+
+
+def test_crn_rush_larsen_gates_and_dt0():
+    """dt = 0 leaves the state unchanged and returns I_ion(V, u); at a held V a
+    gate follows the exact solution of its linear ODE: two half steps == one
+    full step (Rush-Larsen is exact for frozen V and frozen other states)."""
+    V, U = O.crn_initial_state(5)
+    rng = np.random.default_rng(3)
+    V = V + rng.uniform(-10, 80, 5)
+    U0 = U.copy()
+    In = O.crn_step(V, U, 0.0)
+    assert np.allclose(U, U0, rtol=1e-14, atol=1e-15)   # RL: yinf - (yinf - y) rounds (gates in [0, 1])
+    for i in range(5):
+        assert In[i] == pytest.approx(O.crn_current(V[i], U0[:, i]), rel=1e-14)
+    sn = O.crn_state_names()
+    voltage_only = ["m", "h", "j", "oa", "oi", "ua", "ui", "xr", "xs", "d", "f", "w"]
+    Ua, Ub = U0.copy(), U0.copy()
+    O.crn_step(V, Ua, 0.2)
+    O.crn_step(V, Ub, 0.1)
+    O.crn_step(V, Ub, 0.1)
+    for g in voltage_only:
+        k = sn.index(g)
+        assert np.allclose(Ua[k], Ub[k], rtol=1e-12, atol=1e-15), g
+
+
+def _crn_single_cell(dt, T, stim_amp=0.0, stim_dur=2.0):
+    V, U = O.crn_initial_state(1)
+    Vs = np.empty(int(round(T / dt)))
+    for k in range(Vs.shape[0]):
+        In = O.crn_step(V, U, dt)
+        s = stim_amp if k * dt < stim_dur else 0.0
+        V = V - dt * In + dt * s
+        Vs[k] = V[0]
+    return Vs, U
+
+
+def test_crn_quiescence():
+    """No stimulus: the published resting state stays within 0.1 mV for 300 ms."""
+    Vs, U = _crn_single_cell(0.02, 300.0)
+    assert np.abs(Vs + 81.18).max() < 0.1
+
+
+def test_crn_stimulated_action_potential():
+    """A 2 ms, 20 pA/pF stimulus: overshoot, then repolarisation to rest with an
+    atrial-length APD90 (the model's published ~300 ms at this pacing)."""
+    dt = 0.02
+    Vs, U = _crn_single_cell(dt, 700.0, stim_amp=20.0, stim_dur=2.0)
+    pk = int(np.argmax(Vs))
+    assert 10.0 < Vs[pk] < 40.0
+    up = int(np.argmax(Vs > -40.0))
+    v90 = Vs[pk] - 0.9 * (Vs[pk] + 81.18)
+    down = pk + int(np.argmax(Vs[pk:] < v90))
+    assert 250.0 < (down - up) * dt < 360.0
+    assert abs(Vs[-1] + 81.18) < 1.5
+    sn = O.crn_state_names()
+    assert U[sn.index("Cai"), 0] > 0 and U[sn.index("Carel"), 0] > 0
