@@ -219,7 +219,10 @@ struct AsmArgs {
 };
 
 // ---- cluster engine / cohorts (cohort.cu) ------------------------------------
-constexpr int kCoThreads = 256;     // threads per CTA of the cluster engine
+#ifndef TCB_CO_THREADS
+#define TCB_CO_THREADS 256
+#endif
+constexpr int kCoThreads = TCB_CO_THREADS;  // threads per CTA of the cluster engine
 constexpr int kCoMaxCluster = 16;   // CTAs per cluster (non-portable size 16 where allowed)
 constexpr int kClusterAutoSlices = 256;   // TC_ENGINE_AUTO: cluster engine up to 8 192 rows (measured crossover between 4.3k and 30k nodes)
 struct StimEpoch {
