@@ -203,6 +203,11 @@ int64_t tc_current_step(const tc_ctx* ctx);
 /* V^k (n_nodes doubles, original order). */
 tc_status tc_get_v(tc_ctx* ctx, double* v_out);
 
+/* y = A x (which = 0; A = chi Cm M + theta dt K, Eq. 3) or y = K x (which = 1)
+ * with the assembled matrices; x, y: n_nodes doubles in the original order.
+ * Single-partition contexts (TC_ESTATE otherwise).  Inspection / parity. */
+tc_status tc_apply(tc_ctx* ctx, int32_t which, const double* x, double* y);
+
 /* LAT and LRT (n_nodes doubles each, original order; -1.0 = unset). */
 tc_status tc_get_activation(tc_ctx* ctx, double* lat, double* lrt);
 

@@ -23,7 +23,7 @@ __all__ = [
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
     "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "tc_nccl_unique_id", "tc_comm_init",
     "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "Monodomain", "LIB_PATH",
-    "tc_engine_info", "tc_node_order", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
+    "tc_engine_info", "tc_node_order", "tc_apply", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
     "TC_ENGINE_AUTO", "TC_ENGINE_GRID", "TC_ENGINE_CLUSTER",
     "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS", "TC_ION_CRN",
 ]
@@ -103,6 +103,7 @@ def _load():
         "tc_nccl_unique_id": ([P], I32),
         "tc_comm_init": ([P, C.c_int, C.c_int, P], I32),
         "tc_engine_info": ([P, P], I32),
+        "tc_apply": ([P, I32, P, P], I32),
         "tc_node_order": ([P, P], I32),
         "tc_cohort_create": ([P, I32, I32, I32, P], I32),
         "tc_cohort_step": ([P, I64, P], I32),
@@ -296,6 +297,14 @@ def tc_nccl_unique_id() -> bytes:
 def tc_comm_init(ctx, rank: int, world: int, unique_id: bytes) -> None:
     buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
     _check(ctx, _L.tc_comm_init(ctx, rank, world, buf))
+
+
+def tc_apply(ctx, which: int, x):
+    """A x (which 0) or K x (which 1), original node order."""
+    x = _f64(x)
+    y = np.empty_like(x)
+    _check(ctx, _L.tc_apply(ctx, which, _ptr(x), _ptr(y)))
+    return y
 
 
 def tc_node_order(ctx):

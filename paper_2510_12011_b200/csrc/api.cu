@@ -1538,6 +1538,24 @@ tc_status tc_get_v(tc_ctx* c, double* v) {
   return gather_field(c, per_part(c, [iv](Part& P) { return P.d_V[iv]; }).data(), v);
 }
 
+// y = A x (which 0) or K x (which 1) with the assembled system, host vectors in
+// the original node order (inspection: full-size parity checks).
+tc_status tc_apply(tc_ctx* c, int32_t which, const double* x, double* y) {
+  if (!c || !x || !y || (which != 0 && which != 1)) return TC_EINVAL;
+  if (!c->assembled || c->csr_mode) return fail(c, TC_ESTATE, "tc_apply before tc_assemble");
+  if (c->parts.size() != 1 || c->use_comm) return fail(c, TC_ESTATE, "tc_apply: single-partition contexts only");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  Part& P = c->parts[0];
+  CUDA_TRY(c, cudaMemsetAsync(P.d_r, 0, P.n_vec * 8, c->stream));  // padding rows of x stay 0
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_io, x, c->n * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, launch_gather(P.n, c->d_perm_g, c->d_io, P.d_r, c->stream));
+  CUDA_TRY(c, launch_spmv(P.d_sp, P.d_col, which == 0 ? P.d_A : P.d_K, P.nslices, P.d_r, P.d_q, c->stream));
+  CUDA_TRY(c, launch_scatter(P.n, c->d_perm_g, P.d_q, c->d_io, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(y, c->d_io, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TC_OK;
+}
+
 tc_status tc_get_activation(tc_ctx* c, double* lat, double* lrt) {
   if (!c) return TC_EINVAL;
   if (!c->assembled) return fail(c, TC_ESTATE, "tc_get_activation before tc_assemble");

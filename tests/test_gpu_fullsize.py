@@ -1,0 +1,175 @@
+"""Parity at BASELINE.json's FULL sizes, in the launch configuration bench.py
+times (same inputs, config, engine and preroll):
+
+* sampled outputs the oracle computes one by one: rows of the assembled
+  A = chi Cm M + theta dt K and K (element by element, oracle `tet_local`),
+  and the per-node ionic update u^{k+1} (oracle `tt_step` / `ms_step` /
+  `crn_step` on the sampled nodes);
+* a property that holds at any size: the V^{k+1} the GPU returns solves
+  Eq. 3 to Algorithm 1's tolerance, with b built on the host from
+  the literal Eq. 3 formula and the oracle's ionic currents;
+* configs[2] (442 k nodes) is small enough for the whole oracle step.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import bench
+import meshgen as G
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2510_12011_b200 as T
+    return T
+
+
+def _bench_sim(T, name, preroll=None):
+    """The context exactly as bench.py builds and prerolls it."""
+    w = bench.WORKLOADS[name]
+    xyz, tets, stims, region, fibre = bench.make_inputs(w)
+    cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=bench.CHI, cm=bench.CM, abs_tol=1e-5,
+                              rel_tol=1e-5, max_iters=100, use_rcm=1, pcg_variant=0, partitions=1)
+    sim = T.Monodomain(xyz, tets, region, fibre, {0: bench.SIGMA, 1: bench.SIGMA}, cfg, stims)
+    sim.step(w["preroll"] if preroll is None else preroll)
+    return w, sim, xyz, tets, region, fibre
+
+
+def _split_state(s, n, ns):
+    return s[:n].copy(), s[n:2 * n].copy(), s[2 * n:(2 + ns) * n].reshape(ns, n).copy()
+
+
+@pytest.mark.parametrize("name", ["slab20M_ms", "biv3M_tt"])
+def test_fullsize_assembly_rows_sampled(T, name):
+    w, sim, xyz, tets, region, fibre = _bench_sim(T, name, preroll=0)
+    try:
+        n = xyz.shape[0]
+        rng = np.random.default_rng(11)
+        sample = np.unique(np.concatenate([rng.choice(n, 48, replace=False), [0, n - 1]]))
+        x = rng.uniform(-1.0, 1.0, n)
+        yA = T.tc_apply(sim.ctx, 0, x)
+        yK = T.tc_apply(sim.ctx, 1, x)
+        hit = np.nonzero(np.isin(tets, sample).any(axis=1))[0]
+        accA = {int(i): [0.0, 0.0] for i in sample}      # value, sum of |terms|
+        accK = {int(i): [0.0, 0.0] for i in sample}
+        cm, st = w.get("chi", bench.CHI) * bench.CM, 0.5 * w["dt"]
+        for e in hit:
+            nodes = tets[e]
+            f = (1.0, 0.0, 0.0) if fibre is None else fibre[e]
+            sig = O.conductivity_tensor(f, *bench.SIGMA)
+            Me, Ke, _ = O.tet_local(xyz[nodes], sig)
+            for a, i in enumerate(nodes):
+                if int(i) in accA:
+                    ta = (cm * Me[a] + st * Ke[a]) * x[nodes]
+                    tk = Ke[a] * x[nodes]
+                    accA[int(i)][0] += ta.sum()
+                    accA[int(i)][1] += np.abs(ta).sum()
+                    accK[int(i)][0] += tk.sum()
+                    accK[int(i)][1] += np.abs(tk).sum()
+        for i in sample:
+            a, sa = accA[int(i)]
+            k, sk = accK[int(i)]
+            assert abs(yA[i] - a) <= 1e-12 * sa + 1e-300, (i, yA[i], a)
+            assert abs(yK[i] - k) <= 1e-12 * sk + 1e-300, (i, yK[i], k)
+    finally:
+        sim.close()
+
+
+@pytest.mark.parametrize("name", ["slab10M_tt", "slab10M_crn", "slab20M_ms", "biv3M_tt"])
+def test_fullsize_ionic_update_sampled(T, name):
+    """u^{k+1} at sampled nodes after one full-size step equals the oracle's
+    per-node update of (V^k, u^k) read back from the GPU."""
+    w, sim, xyz, tets, region, fibre = _bench_sim(T, name)
+    try:
+        n = xyz.shape[0]
+        ns = {"tt2006": 18, "crn": 20, "ms": 1}[w["model"]]
+        Vk, _, U0 = _split_state(sim.get_state(), n, ns)
+        sim.step(1)
+        _, _, U1 = _split_state(sim.get_state(), n, ns)
+        rng = np.random.default_rng(5)
+        # sampled nodes, biased to the propagating front (largest |dV| states)
+        front = np.argsort(-np.abs(Vk - np.median(Vk)))[:256]
+        sample = np.unique(np.concatenate([rng.choice(n, 256, replace=False), front]))
+        u = np.ascontiguousarray(U0[:, sample])
+        step = {"tt2006": O.tt_step, "crn": O.crn_step, "ms": O.ms_step}[w["model"]]
+        step(Vk[sample], u, w["dt"])
+        assert np.allclose(U1[:, sample], u, rtol=1e-10, atol=1e-14)
+    finally:
+        sim.close()
+
+
+def _kuhn_diag(T, sim, dims):
+    """diag(A) of a Kuhn-grid system with 8 probes: nodes coloured by the parity
+    of their grid indices never share a row (every stencil offset changes some
+    index by one)."""
+    nx, ny, nz = dims
+    idx = np.arange(nx * ny * nz)
+    i, j, k = idx % nx, (idx // nx) % ny, idx // (nx * ny)
+    colour = (i % 2) + 2 * (j % 2) + 4 * (k % 2)
+    d = np.zeros(idx.shape[0])
+    for c in range(8):
+        e = (colour == c).astype(np.float64)
+        y = T.tc_apply(sim.ctx, 0, e)
+        d[colour == c] = y[colour == c]
+    return d
+
+
+def test_fullsize_step_solves_eq3_to_tolerance(T):
+    """20 M-node MS slab, one step in the timing window: with b from the literal
+    Eq. 3 (oracle ionic currents, M x = (A x - theta dt K x)/(chi Cm)) and
+    z = D^-1 (b - A V^{k+1}), ||z|| meets Algorithm 1's absolute test and agrees
+    with the norm the GPU reported."""
+    name = "slab20M_ms"
+    w, sim, xyz, tets, region, fibre = _bench_sim(T, name)
+    try:
+        n = xyz.shape[0]
+        Vk, _, U0 = _split_state(sim.get_state(), n, 1)
+        st = sim.step(1)
+        Vn = sim.V
+        dt, th, chicm = w["dt"], 0.5, bench.CHI * bench.CM
+        In = O.ms_step(Vk, np.ascontiguousarray(U0), dt)
+        y = Vk - dt * In                                     # stimulus has ended (t > 2 ms)
+        b = (T.tc_apply(sim.ctx, 0, y) - th * dt * T.tc_apply(sim.ctx, 1, y)
+             - (1.0 - th) * dt * T.tc_apply(sim.ctx, 1, Vk))
+        r = b - T.tc_apply(sim.ctx, 0, Vn)
+        d = _kuhn_diag(T, sim, w["dims"])
+        z = np.linalg.norm(r / d)
+        assert bool(st["converged"][0])
+        assert z < 1e-5 * 1.01, z
+        assert z == pytest.approx(float(st["znorm"][0]), rel=1e-3, abs=1e-9)
+    finally:
+        sim.close()
+
+
+def test_configs2_full_oracle_step(T):
+    """configs[2] (N-version dx 0.1 mm, 442 401 nodes, TT2006, dt 0.01) at full
+    size: one step from the GPU state after the bench preroll, GPU vs the whole
+    oracle step (rel-L2 of V <= 1e-8, states to 1e-9)."""
+    name = "nversion_dx0.1_tt"
+    w, sim, xyz, tets, region, fibre = _bench_sim(T, name)
+    try:
+        n = xyz.shape[0]
+        s = sim.get_state()
+        Vk, Vkm1, U = _split_state(s, n, 18)
+        k = int(round(s[-2]))
+        E = tets.shape[0]
+        ref = O.Monodomain(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: bench.SIGMA},
+                           O.Config(dt=w["dt"], abs_tol=1e-5, rel_tol=1e-5, max_iters=100),
+                           [O.Stimulus(*st_) for st_ in bench.make_inputs(w)[2]])
+        ref.set_state(Vk, Vkm1, U, k)
+        rep = ref.step()
+        stg = sim.step(1)
+        v = sim.V
+        assert abs(int(stg["iters"][0]) - rep.iters) <= 1
+        assert np.linalg.norm(v - ref.Vk) / np.linalg.norm(ref.Vk) <= 1e-8
+        _, _, U1 = _split_state(sim.get_state(), n, 18)
+        assert np.allclose(U1, ref.U, rtol=1e-9, atol=1e-14)
+    finally:
+        sim.close()
