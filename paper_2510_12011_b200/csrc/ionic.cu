@@ -16,7 +16,12 @@
 namespace tcb {
 
 
-__global__ void __launch_bounds__(128) ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D) {
+#ifndef TCB_ION_THREADS
+#define TCB_ION_THREADS 128   // measured: 128 / 256
+#endif
+constexpr int kIonThreads = TCB_ION_THREADS;
+
+__global__ void __launch_bounds__(kIonThreads) ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D) {
   __shared__ Exp2Table T;
   exp2_table_init(&T);
   if (a.flags[0]) return;
@@ -147,7 +152,7 @@ static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  ionic_tt_kernel<<<nblk(a.n, 128), 128, 0, s>>>(a, p, tt_derived(p));
+  ionic_tt_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, tt_derived(p));
   return cudaGetLastError();
 }
 cudaError_t launch_ionic_ms(const IonArgs& a, const MSParams& p, cudaStream_t s) {
@@ -181,7 +186,7 @@ CRNDerived crn_derived(const CRNParams& P) {
   return D;
 }
 
-__global__ void __launch_bounds__(128) ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D) {
+__global__ void __launch_bounds__(kIonThreads) ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D) {
   __shared__ Exp2Table T;
   exp2_table_init(&T);
   if (a.flags[0]) return;
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(128) ionic_crn_kernel(IonArgs a, CRNParams P, 
 
 cudaError_t launch_ionic_crn(const IonArgs& a, const CRNParams& p, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  ionic_crn_kernel<<<nblk(a.n, 128), 128, 0, s>>>(a, p, crn_derived(p));
+  ionic_crn_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, crn_derived(p));
   return cudaGetLastError();
 }
 

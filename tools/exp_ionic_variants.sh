@@ -1,8 +1,10 @@
 #!/bin/bash
-# FP64 ionic kernel launch shapes: registers per
-# thread (TCB_ION_MINB CTAs of 128 threads per SM) x grid-stride persistence.
+# FP64 ionic kernels: CTA size sweep (TCB_ION_THREADS), one node per thread.
+# (An earlier sweep of grid-stride / register-capped shapes measured slower;
+# DESIGN.md "Ionic kernel".)  Libraries are built here (tools/ion_*.so) and
+# selected with TCB200_LIB.
 cd "$(dirname "$0")/.."
-VARS="p1m4:-DTCB_ION_MINB=4 p1m3:-DTCB_ION_MINB=3 p1m5:-DTCB_ION_MINB=5 p0m4:-DTCB_ION_MINB=4+-DTCB_ION_PERSIST=0"
+VARS="t128:-DTCB_ION_THREADS=128 t256:-DTCB_ION_THREADS=256 t64:-DTCB_ION_THREADS=64"
 if [ "$1" == "build" ]; then
   for v in $VARS; do n=${v%%:*}; f=$(echo ${v#*:} | tr + ' ')
     [ -f tools/ion_$n.so ] || /usr/local/cuda/bin/nvcc -O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a \
