@@ -173,3 +173,31 @@ def test_configs2_full_oracle_step(T):
         assert np.allclose(U1, ref.U, rtol=1e-9, atol=1e-14)
     finally:
         sim.close()
+
+
+@pytest.mark.parametrize("name", ["slab20M_ms", "slab10M_tt"])
+def test_fullsize_activation_front_is_planar_and_ordered(T, name):
+    """The bench's planar stimulus (x <= 0.3 mm) on a fibre-aligned slab drives a
+    front along x: every activated node's LAT is non-decreasing in x
+    along each grid line, the activated region is a prefix of every line, the
+    front position varies by at most one node across (y, z), and the front
+    moves (LAT grows along x).  (LAT at one x is NOT equal across (y, z): the
+    boundary nodes' smaller mass rows bend the front by ~0.1 ms.)"""
+    w, sim, xyz, tets, region, fibre = _bench_sim(T, name, preroll=0)
+    try:
+        sim.step(700)                                   # 7 ms: the front is well inside the slab
+        lat, _ = sim.activation()
+        nx, ny, nz = w["dims"]
+        L = lat.reshape(nz, ny, nx)
+        act = L >= 0
+        assert act[:, :, 0].all() and not act[:, :, -1].any()
+        first_off = act.argmin(axis=2)                  # first non-activated x index on every line
+        assert np.all(act.sum(axis=2) == first_off)     # activated set is a prefix along x
+        assert first_off.max() - first_off.min() <= 1   # planar front (within one node)
+        dt = w["dt"]
+        m = int(first_off.min())
+        sub = L[:, :, :m]
+        assert np.all(np.diff(sub, axis=2) >= -1e-12)   # ordered along x
+        assert sub[:, :, m - 1].min() > sub[:, :, 0].max() + 10 * dt   # the front travelled
+    finally:
+        sim.close()
