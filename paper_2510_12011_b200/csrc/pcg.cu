@@ -290,6 +290,9 @@ int cg_grid_size(int mode, int variant, int32_t nslices, int device) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_fn(mode, variant), kCgThreads, pcg_smem(variant));
   if (per_sm < 1) per_sm = 1;
+#ifdef TCB_CG_PER_SM_CAP
+  if (per_sm > TCB_CG_PER_SM_CAP) per_sm = TCB_CG_PER_SM_CAP;
+#endif
   int maxg = per_sm * sm_count(device);
   int need = (nslices + kCgWarps - 1) / kCgWarps;
   if (need < 1) need = 1;
