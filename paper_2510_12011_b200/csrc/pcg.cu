@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : (1024 / T
                  for (int k = 0; k < w; ++k) {
                    const int64_t t = base + (int64_t)k * kSellC + lane;
                    const int c = staged ? Cs[k * kSellC + lane] : ci(t, k);
-                   const double av = staged ? As[k * kSellC + lane] : __ldcs(Av + t);
-                   sum += av * a.up[c] - __ldcs(Kv + t) * a.vp[c];
+                   const double av = staged ? As[k * kSellC + lane] : ld_mat(Av + t);
+                   sum += av * a.up[c] - ld_mat(Kv + t) * a.vp[c];
                  }
                } else {
                  const double ax = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.x, nullptr, 0.0)

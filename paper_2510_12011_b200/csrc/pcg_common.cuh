@@ -193,6 +193,21 @@ __device__ __forceinline__ double row_Ap_staged(int w, int lane, const double* A
   return sum;
 }
 
+// Streamed matrix loads: evict-first (default: the matrix of a large system
+// is read once per iteration and never fits in L2) or cached (experiment:
+// TCB_MATRIX_LOAD = 1, __ldg) for systems whose matrix could stay in L2.
+#ifndef TCB_MATRIX_LOAD
+#define TCB_MATRIX_LOAD 0
+#endif
+template <class T>
+__device__ __forceinline__ T ld_mat(const T* p) {
+#if TCB_MATRIX_LOAD == 1
+  return __ldg(p);
+#else
+  return __ldcs(p);
+#endif
+}
+
 // Column index of slot t (slot row k) of one slice: either the plain int32
 // array, or (compressed slices) a per-(slice, k) int32 base, broadcast to the
 // warp, plus a 16-bit offset per slot.
@@ -201,7 +216,7 @@ struct ColIdx {
   const uint16_t* c16;  // null: uncompressed slice
   const int* kb;
   __device__ __forceinline__ int operator()(int64_t t, int k) const {
-    return c16 ? __ldg(kb + k) + (int)__ldcs(c16 + t) : __ldcs(c32 + t);
+    return c16 ? __ldg(kb + k) + (int)ld_mat(c16 + t) : ld_mat(c32 + t);
   }
 };
 
@@ -238,7 +253,7 @@ __device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, c
       const int kk = min(k0 + j, w - 1);
       const int64_t t = base + (int64_t)kk * kSellC + lane;
       const int c = ci(t, kk);
-      av[j] = __ldcs(A + t);
+      av[j] = ld_mat(A + t);
       g[j] = FIRST ? z[c] : z[c] + beta * pold[c];
     }
 #pragma unroll
@@ -251,7 +266,7 @@ __device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, c
     const int64_t t = base + (int64_t)k * kSellC + lane;
     const int c = ci(t, k);
     const double g = FIRST ? z[c] : z[c] + beta * pold[c];
-    sum += __ldcs(A + t) * g;
+    sum += ld_mat(A + t) * g;
   }
 #endif
   return sum;
