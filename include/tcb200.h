@@ -275,10 +275,11 @@ tc_status tc_engine_info(tc_ctx* ctx, int64_t out[4]);
 /* ---- Cohorts: many independent simulations per GPU ------------
  * A cohort batches assembled single-partition contexts ("members": different
  * meshes, conductivities, stimuli, ionic parameters, time steps, tolerances)
- * that share the device and the ionic model (TT2006 or MS).  tc_cohort_step
- * advances EVERY member by n_steps in ONE launch: one thread-block cluster per
- * member runs its steps (the cluster engine), each member with its own PCG
- * stopping test (per-replica stopping).  Each member's results equal what
+ * that share the device and the ionic model (TT2006, MS or CRN).  tc_cohort_step
+ * advances EVERY member by n_steps: the small members (those TC_ENGINE_AUTO
+ * would give the cluster engine) in ONE launch, one thread-block cluster per
+ * member, each with its own PCG stopping test (per-replica stopping); larger
+ * members with their own grid-engine tc_step while that launch runs.  Each member's results equal what
  * tc_step(member, n_steps) gives (same arithmetic; inner-product partial sums
  * grouped per cluster), and afterwards every tc_get_* call on a member works as
  * usual.  The members stay owned by the caller and must outlive the cohort;

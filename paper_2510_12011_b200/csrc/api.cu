@@ -1775,6 +1775,8 @@ struct tc_cohort {
   int64_t stats_cap = 0;
   int32_t* d_status = nullptr;
   std::vector<CoRep> h;
+  std::vector<int> small;          // members on the cluster engine (index into m)
+  std::vector<int> big;            // members too large for it: grid engine, one tc_step each
 };
 
 static tc_status cfail(tc_cohort* co, tc_status st, const std::string& msg) {
@@ -1820,11 +1822,20 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
       return fail(m0, TC_EINVAL, "cohort member " + std::to_string(i) + ": device or ionic model differs from member 0");
     for (int32_t j = 0; j < i; ++j)
       if (members[j] == c) return fail(m0, TC_EINVAL, "cohort member " + std::to_string(i) + " repeats member " + std::to_string(j));
-    max_slices = std::max<int64_t>(max_slices, c->parts[0].nslices);
   }
   if (cudaSetDevice(m0->device) != cudaSuccess) return TC_ECUDA;
   tc_cohort* co = new tc_cohort();
   co->m.assign(members, members + count);
+  for (int32_t i = 0; i < count; ++i) {
+    // members the auto engine would give the grid engine run on it (overlapped
+    // with the cluster launch); the cluster engine only takes the small ones
+    if (members[i]->parts[0].nslices > kClusterAutoSlices) {
+      co->big.push_back(i);
+    } else {
+      co->small.push_back(i);
+      max_slices = std::max<int64_t>(max_slices, members[i]->parts[0].nslices);
+    }
+  }
   co->device = m0->device;
   co->model = m0->cfg.model;
   co->stream = m0->stream;
@@ -1832,7 +1843,7 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
   // that size that fit at once, halve the size (more members in flight; measured on the
   // configs[0] cohort: 16 CTAs 0.39, 8 CTAs 0.69 G node-steps/s at 74 members)
   int want = cluster_size ? cluster_size : cluster_want(max_slices);
-  if (!cluster_size && want > 8 && count > cohort_active_clusters(co->model, want, 0)) want = 8;
+  if (!cluster_size && want > 8 && (int64_t)co->small.size() > cohort_active_clusters(co->model, want, 0)) want = 8;
   co->csize = cohort_cluster_size(co->model, want);
   if (co->csize == 0 || (cluster_size && co->csize != cluster_size)) {
     delete co;
@@ -1840,8 +1851,10 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
   }
   if (resident) {  // cluster-resident when the largest member block fits
     size_t need = 0;
-    for (tc_ctx* c : co->m)
+    for (int i : co->small) {
+      const tc_ctx* c = co->m[i];
       need = std::max(need, cohort_smem_bytes(c->parts[0].h_sp.data(), c->parts[0].nslices, co->csize));
+    }
     if (need <= cohort_smem_limit(co->model) && cohort_active_clusters(co->model, co->csize, need) > 0)
       co->smem = need;
   }
@@ -1870,32 +1883,52 @@ tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
     CO_CUDA(co, co_alloc(co, &co->d_stats, cnt * nsteps));
     co->stats_cap = cnt * nsteps;
   }
-  for (int64_t i = 0; i < cnt; ++i) {
+  const int64_t ns_small = (int64_t)co->small.size();
+  for (int64_t j = 0; j < ns_small; ++j) {
+    const int i = co->small[j];
     tc_ctx* c = co->m[i];
-    if (make_corep(c, co->h[i], co->d_stats + i * nsteps) != TC_OK)
+    if (make_corep(c, co->h[j], co->d_stats + (int64_t)i * nsteps) != TC_OK)
       return cfail(co, TC_ECUDA, "cohort member " + std::to_string(i) + ": " + c->err);
-    co->h[i].status = co->d_status + i;
+    co->h[j].status = co->d_status + i;
   }
-  // order after every member's pending work
-  for (int64_t i = 1; i < cnt; ++i)
-    if (co->m[i]->stream != co->stream) {
-      CO_CUDA(co, cudaEventRecord(co->ev, co->m[i]->stream));
-      CO_CUDA(co, cudaStreamWaitEvent(co->stream, co->ev, 0));
+  if (ns_small > 0) {
+    // order after every member's pending work
+    for (int i : co->small)
+      if (co->m[i]->stream != co->stream) {
+        CO_CUDA(co, cudaEventRecord(co->ev, co->m[i]->stream));
+        CO_CUDA(co, cudaStreamWaitEvent(co->stream, co->ev, 0));
+      }
+    CO_CUDA(co, cudaMemsetAsync(co->d_status, 0, cnt * 4, co->stream));
+    CO_CUDA(co, cudaMemcpyAsync(co->d_reps, co->h.data(), ns_small * sizeof(CoRep), cudaMemcpyHostToDevice, co->stream));
+    CO_CUDA(co, launch_cohort(co->model, co->d_reps, (int)ns_small, co->csize, co->smem, nsteps, co->stream));
+    CO_CUDA(co, cudaEventRecord(co->ev, co->stream));
+    for (int i : co->small)
+      if (co->m[i]->stream != co->stream) CO_CUDA(co, cudaStreamWaitEvent(co->m[i]->stream, co->ev, 0));
+    for (int i : co->small) {
+      advance_host(co->m[i], nsteps);
+      co->m[i]->launches += 1.0 / (double)ns_small;
     }
-  CO_CUDA(co, cudaMemcpyAsync(co->d_reps, co->h.data(), cnt * sizeof(CoRep), cudaMemcpyHostToDevice, co->stream));
-  CO_CUDA(co, launch_cohort(co->model, co->d_reps, (int)cnt, co->csize, co->smem, nsteps, co->stream));
-  CO_CUDA(co, cudaEventRecord(co->ev, co->stream));
-  for (int64_t i = 1; i < cnt; ++i)
-    if (co->m[i]->stream != co->stream) CO_CUDA(co, cudaStreamWaitEvent(co->m[i]->stream, co->ev, 0));
-  for (tc_ctx* c : co->m) {
-    advance_host(c, nsteps);
-    c->launches += 1.0 / (double)cnt;
   }
-  std::vector<int32_t> status(cnt);
-  CO_CUDA(co, cudaMemcpyAsync(status.data(), co->d_status, cnt * 4, cudaMemcpyDeviceToHost, co->stream));
-  if (stats)
-    CO_CUDA(co, cudaMemcpyAsync(stats, co->d_stats, cnt * nsteps * sizeof(tc_step_stat), cudaMemcpyDeviceToHost, co->stream));
-  CO_CUDA(co, cudaStreamSynchronize(co->stream));
+  // large members: the grid engine, while the cluster launch runs
+  std::vector<tc_step_stat> hbig(co->big.size() * nsteps);
+  std::vector<tc_status> sbig(co->big.size(), TC_OK);
+  for (size_t b = 0; b < co->big.size(); ++b)
+    sbig[b] = tc_step(co->m[co->big[b]], nsteps, hbig.data() + b * nsteps);
+  std::vector<int32_t> status(cnt, 0);
+  if (ns_small > 0) {
+    CO_CUDA(co, cudaMemcpyAsync(status.data(), co->d_status, cnt * 4, cudaMemcpyDeviceToHost, co->stream));
+    if (stats)
+      CO_CUDA(co, cudaMemcpyAsync(stats, co->d_stats, cnt * nsteps * sizeof(tc_step_stat), cudaMemcpyDeviceToHost, co->stream));
+    CO_CUDA(co, cudaStreamSynchronize(co->stream));
+  }
+  for (size_t b = 0; b < co->big.size(); ++b) {
+    const int i = co->big[b];
+    if (stats) std::memcpy(stats + (int64_t)i * nsteps, hbig.data() + b * nsteps, nsteps * sizeof(tc_step_stat));
+    if (sbig[b] == TC_ENAN) status[i] = 2;
+    else if (sbig[b] == TC_ESOLVER) status[i] = 1;
+    else if (sbig[b] != TC_OK)
+      return cfail(co, sbig[b], "cohort member " + std::to_string(i) + ": " + co->m[i]->err);
+  }
   for (int64_t i = 0; i < cnt; ++i)
     if (status[i])
       return cfail(co, status[i] == 2 ? TC_ENAN : TC_ESOLVER,

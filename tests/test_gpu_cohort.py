@@ -275,3 +275,28 @@ def test_cohort_errors(T):
     finally:
         for s in (a, b, p):
             s.close()
+
+
+def test_cohort_mixes_small_and_large_members(T):
+    """A member above the cluster engine's size runs on the grid engine inside the
+    same tc_cohort_step; every member still matches its oracle run."""
+    specs = [dict(dims=(21, 8, 5)), dict(dims=(61, 23, 9), permute=3, fib_seed=2), dict(dims=(13, 6, 4))]
+    members, refs = [], []
+    try:
+        for spec in specs:
+            args = _member(spec)
+            refs.append(_oracle(spec, *args))
+            members.append(_gpu(T, spec, *args, engine="auto"))
+        assert T.tc_matrix_info(members[1].ctx)["nslices"] > 256     # grid-engine size
+        co = T.Cohort(members)
+        try:
+            for c in range(3):
+                stats = co.step(10)
+                for m, (sim, ref) in enumerate(zip(members, refs)):
+                    reps = [ref.step() for _ in range(10)]
+                    _check(sim, ref, stats[m], reps, 0.05, f"member {m} chunk {c}")
+        finally:
+            co.close()
+    finally:
+        for s in members:
+            s.close()
