@@ -90,7 +90,18 @@ __device__ __forceinline__ TTVolt tt_volt(double V, const TTParams& P, const TTD
   return f;
 }
 
-__device__ __forceinline__ TTCur tt_cur(double V, const double* u, const TTParams& P,
+// The current evaluation runs twice per step (at u^k and u^{k+1}); TCB_CUR_NOINLINE
+// keeps one copy of its code (instruction-cache experiment).
+#ifndef TCB_CUR_NOINLINE
+#define TCB_CUR_NOINLINE 0
+#endif
+#if TCB_CUR_NOINLINE
+#define TCB_CUR_ATTR static __device__ __noinline__
+#else
+#define TCB_CUR_ATTR __device__ __forceinline__
+#endif
+
+TCB_CUR_ATTR TTCur tt_cur(double V, const double* u, const TTParams& P,
                                         const TTDerived& D, const TTVolt& f, const Exp2Table* T) {
   const double ek = D.rtf * log(P.Ko * tc_rcp(u[sKi]));
   const double ena = D.rtf * log(P.Nao * tc_rcp(u[sNai]));
@@ -306,7 +317,7 @@ struct CRNCur {
   double ina, ik1, ito, ikur, ikr, iks, ical, inak, inaca, ibna, ibca, ipca;
 };
 
-__device__ __forceinline__ CRNCur crn_cur(double V, const double* u, const CRNParams& P,
+TCB_CUR_ATTR CRNCur crn_cur(double V, const double* u, const CRNParams& P,
                                           const CRNDerived& D, const Exp2Table* T) {
   CRNCur c;
   const double nai = u[cNai], ki = u[cKi], cai = u[cCai];
