@@ -187,6 +187,26 @@ def ncu_traffic(workload, iters_per_step):
         return None
 
 
+def ionic_roofline(workload, model, n, ionic_ms_per_step):
+    """FP64 roofline of the ionic kernel (FP64-ALU bound for TT2006 /
+    CRN): ncu-counted FP64 work per node (profiles/ncu_fp64.json) x nodes over the
+    live kernel time, against the measured DFMA rate."""
+    if model not in ("tt2006", "crn") or not ionic_ms_per_step:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_fp64.json")) as f:
+            d = json.load(f)
+        e = d.get(workload) or d["slab10M_tt" if model == "tt2006" else "slab10M_crn"]
+    except Exception:
+        return None
+    ach = e["flop_per_node"] * n / (ionic_ms_per_step / 1e3) / 1e12
+    return {"kernel": e["kernel"], "bound": "fp64", "achieved": ach, "peak": d["peak_tflops"],
+            "unit": "TFLOP/s", "frac": ach / d["peak_tflops"], "flop_per_node": e["flop_per_node"],
+            "fp64_pipe_active_ncu": e["fp64_pipe_active_ncu"],
+            "peak_source": "measured DFMA rate (profiles/r01_probe_fp64.txt)",
+            "work_source": "ncu FP64 instruction counts per node (profiles/ncu_fp64.json)"}
+
+
 def run_reference(args, w):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -335,6 +355,7 @@ def main():
         "pcg_iters_per_step": iters / args.steps,
         "setup_s": t_setup,
         "roofline": roof,
+        "ionic_roofline": ionic_roofline(args.workload, w["model"], n, prof["ionic_ms"] / args.steps),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": prof["launches"],
