@@ -511,7 +511,7 @@ static void local_sell(const PartPlan& pl, const int64_t* rp, const int32_t* col
     for (int l = 0; l < kSellC; ++l) {
       const int64_t i = sl * kSellC + l;
       for (int64_t k = 0; k < w; ++k) {
-        const int64_t t = base + k * kSellC + l;
+        const int64_t t = sell_slot(base, w, k, l);
         if (i >= n || k >= hs.rowlen[i]) {
           hs.col[t] = (int32_t)i;          // padding slot: own local row, value 0
           colg[t] = (int32_t)(pl.g0 + std::min<int64_t>(i, n - 1));

@@ -27,12 +27,12 @@ __global__ void assemble_kernel(AsmArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   const int64_t s = i / kSellC, lane = i % kSellC;
-  const int64_t base = a.slice_ptr[s] + lane;
+  const int64_t base = a.slice_ptr[s];
   const int len = a.rowlen[i];
   const int w = (int)((a.slice_ptr[s + 1] - a.slice_ptr[s]) / kSellC);
   for (int k = 0; k < w; ++k) {
-    a.A[base + (int64_t)k * kSellC] = 0.0;  // accumulates M first
-    a.K[base + (int64_t)k * kSellC] = 0.0;
+    a.A[sell_slot(base, w, k, lane)] = 0.0;  // accumulates M first
+    a.K[sell_slot(base, w, k, lane)] = 0.0;
   }
   for (int64_t t = a.inc_ptr[i]; t < a.inc_ptr[i + 1]; ++t) {
     const int32_t code = a.inc[t];
@@ -102,17 +102,18 @@ __global__ void assemble_kernel(AsmArgs a) {
     for (int lb = 0; lb < kel; ++lb) {
       const int32_t j = v[lb];
       int k = 0;
-      while (k < len && a.col[base + (int64_t)k * kSellC] != j) ++k;
+      while (k < len && a.col[sell_slot(base, w, k, lane)] != j) ++k;
       if (k == len) { atomicExch(a.err, 2); return; }
       const double Kab = vol * (sg[0] * g[lb][0] + sg[1] * g[lb][1] + sg[2] * g[lb][2]);
       const double Mab = mass_w * (la == lb ? 2.0 : 1.0);
-      a.A[base + (int64_t)k * kSellC] += Mab;
-      a.K[base + (int64_t)k * kSellC] += Kab;
+      const int64_t t = sell_slot(base, w, k, lane);
+      a.A[t] += Mab;
+      a.K[t] += Kab;
     }
   }
   double diag = 0.0;
   for (int k = 0; k < w; ++k) {
-    const int64_t t = base + (int64_t)k * kSellC;
+    const int64_t t = sell_slot(base, w, k, lane);
     const double Aval = a.c_mass * a.A[t] + a.c_stiff * a.K[t];
     a.A[t] = Aval;
     if (k < len && a.col[t] == (int32_t)(a.row0 + i)) diag = Aval;

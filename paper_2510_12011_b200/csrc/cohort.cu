@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kCoThreads, 1)
         double a[kB], b[kB], g1[kB], g2[kB];
 #pragma unroll
         for (int j = 0; j < kB; ++j) {  // slots past the row end reload its last slot
-          const int64_t t = base + (int64_t)min(k0 + j, w - 1) * kSellC + lane;
+          const int64_t t = sell_slot(base, w, min(k0 + j, w - 1), lane);
           a[j] = Av[t];
           b[j] = Kv[t];
           if (RES) {
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kCoThreads, 1)
               double a[kB], g1[kB];
 #pragma unroll
               for (int j = 0; j < kB; ++j) {
-                const int64_t t = base + (int64_t)min(k0 + j, w - 1) * kSellC + lane;
+                const int64_t t = sell_slot(base, w, min(k0 + j, w - 1), lane);
                 a[j] = Av[t];
                 g1[j] = RES ? ld_dsmem(gaddr(col[t]) + vZ * vstride) : z[col[t]];
               }
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kCoThreads, 1)
               double a[kB], g1[kB], g2[kB];
 #pragma unroll
               for (int j = 0; j < kB; ++j) {
-                const int64_t t = base + (int64_t)min(k0 + j, w - 1) * kSellC + lane;
+                const int64_t t = sell_slot(base, w, min(k0 + j, w - 1), lane);
                 a[j] = Av[t];
                 if (RES) {
                   const uint32_t g = gaddr(col[t]);

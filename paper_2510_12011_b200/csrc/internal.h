@@ -13,12 +13,31 @@
 namespace tcb {
 
 // ---------------------------------------------------------------------------
-// SELL-32 sparse layout (one warp = one slice of 32 consecutive rows; slot k of
-// row 32*s + lane at slice_ptr[s] + 32*k + lane).  Rows keep the ascending column
-// order of CSR, so the SpMV sums every row in the same order as a CSR loop.
+// SELL-32 sparse layout (one warp = one slice of 32 consecutive rows of width w).
+// Slot pairs (TCB_SELL_PAIRS=1, measured slower in situ: DESIGN.md): slots 2j and 2j+1 of a lane's row are
+// adjacent, so a warp reads a slot pair as one 16-byte value load and one
+// 8-byte index load per lane (measured: 16-byte streaming loads reach 7.1 TB/s
+// on B200, 8-byte loads 4.9 TB/s; tools/probe_bw.cu):
+//   slot k < (w & ~1) of row 32*s + lane at slice_ptr[s] + 64*(k/2) + 2*lane + k%2,
+//   the odd last slot (w odd)          at slice_ptr[s] + 32*(w-1) + lane.
+// TCB_SELL_PAIRS=0 (default): plain SELL, slot k at slice_ptr[s] + 32*k + lane.
+// Rows keep the ascending column order of CSR, and every kernel sums a row's
+// slots in that order, so the SpMV sums every row as a CSR loop does.
 // Padding slots point at the row itself with value 0.
 // ---------------------------------------------------------------------------
 constexpr int kSellC = 32;
+#ifndef TCB_SELL_PAIRS
+#define TCB_SELL_PAIRS 0
+#endif
+// Offset of slot k of lane `lane`'s row in a slice at `base` of width w.
+__host__ __device__ __forceinline__ int64_t sell_slot(int64_t base, int64_t w, int64_t k, int64_t lane) {
+#if TCB_SELL_PAIRS
+  return k < (w & ~(int64_t)1) ? base + 64 * (k >> 1) + 2 * lane + (k & 1) : base + 32 * k + lane;
+#else
+  (void)w;
+  return base + 32 * k + lane;
+#endif
+}
 #ifndef TCB_CG_THREADS
 #define TCB_CG_THREADS 512
 #endif

@@ -27,6 +27,9 @@ namespace tcb {
 
 // ------------------------------------------------------------------ kernels
 // VAR 0: direct loads, int32 indices (default), 1: TMA-staged, 2: direct loads + 16-bit indices
+#ifndef TCB_VEC_U
+#define TCB_VEC_U 0   // 1: U phase and final x update over 16-byte row pairs (measured slower)
+#endif
 #define TCB_MINB(VAR) ((VAR) == 1 ? (512 / TCB_CG_THREADS > 0 ? 512 / TCB_CG_THREADS : 1) : TCB_DIRECT_MINB)
 
 __device__ __forceinline__ void setup_pipe(SlicePipe& P, char* smem, uint64_t* bars, int warp, int lane) {
@@ -65,12 +68,32 @@ __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : (1024 / T
                if (MODE == 1) {
                  const double* __restrict__ Kv = a.K;
                  const ColIdx ci = col_of<COMP>(a, i, base);
+                 if (TCB_SELL_PAIRS && !staged && !ci.c16) {  // slot pairs: 16-byte value loads
+                   const double2* A2 = reinterpret_cast<const double2*>(Av + base) + lane;
+                   const double2* K2 = reinterpret_cast<const double2*>(Kv + base) + lane;
+                   const int2* C2 = reinterpret_cast<const int2*>(a.col + base) + lane;
+                   const int np = w >> 1;
+#pragma unroll 2
+                   for (int j = 0; j < np; ++j) {
+                     const double2 av = ld_mat(A2 + 32 * j), kv = ld_mat(K2 + 32 * j);
+                     const int2 c = ld_mat(C2 + 32 * j);
+                     sum += av.x * a.up[c.x] - kv.x * a.vp[c.x];
+                     sum += av.y * a.up[c.y] - kv.y * a.vp[c.y];
+                   }
+                   if (w & 1) {
+                     const int64_t t = base + (int64_t)kSellC * (w - 1) + lane;
+                     const int c = ld_mat(a.col + t);
+                     sum += ld_mat(Av + t) * a.up[c] - ld_mat(Kv + t) * a.vp[c];
+                   }
+                 } else {
 #pragma unroll 4
-                 for (int k = 0; k < w; ++k) {
-                   const int64_t t = base + (int64_t)k * kSellC + lane;
-                   const int c = staged ? Cs[k * kSellC + lane] : ci(t, k);
-                   const double av = staged ? As[k * kSellC + lane] : ld_mat(Av + t);
-                   sum += av * a.up[c] - ld_mat(Kv + t) * a.vp[c];
+                   for (int k = 0; k < w; ++k) {
+                     const int64_t t = sell_slot(base, w, k, lane);
+                     const int64_t ts = sell_slot(0, w, k, lane);
+                     const int c = staged ? Cs[ts] : ci(t, k);
+                     const double av = staged ? As[ts] : ld_mat(Av + t);
+                     sum += av * a.up[c] - ld_mat(Kv + t) * a.vp[c];
+                   }
                  }
                } else {
                  const double ax = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.x, nullptr, 0.0)
@@ -112,6 +135,11 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
 
   SlicePipe P;
   if (TMA) setup_pipe(P, smem, bars[TMA ? warp : 0], warp, lane);
+  // streaming phases over row pairs when every vector is 16-byte aligned
+  const int64_t n2 = (int64_t)ns * (kSellC / 2);
+  const bool vec2 = !TMA && TCB_VEC_U &&
+                    ((((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)dinv) |
+                      ((uintptr_t)a.x) | ((uintptr_t)a.p0) | ((uintptr_t)a.p1)) & 15) == 0;
 
   // ---- rho_0 = r.z, ||z_0|| from the RHS kernel's per-CTA partials ------------
   double2 tot;
@@ -172,6 +200,26 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
       alpha = rho / pq;                                   // alpha_k = rho_k / p.q
       // ---- U: r -= alpha q, z = r / d, partials of r.z and z.z (UU slices / warp pass)
       acc = make_double2(0.0, 0.0);
+      if (vec2) {  // row pairs: 16-byte loads and stores
+        double2* __restrict__ r2 = reinterpret_cast<double2*>(a.r);
+        double2* __restrict__ z2 = reinterpret_cast<double2*>(a.z);
+        const double2* __restrict__ q2 = reinterpret_cast<const double2*>(a.q);
+        const double2* __restrict__ d2 = reinterpret_cast<const double2*>(dinv);
+        for (int64_t j = (int64_t)gw * kSellC + lane; j < n2; j += (int64_t)nw * kSellC) {
+          const double2 rr = r2[j], qq = q2[j], dd = __ldg(d2 + j);
+          double2 rn, zn;
+          rn.x = rr.x - alpha * qq.x;
+          rn.y = rr.y - alpha * qq.y;
+          zn.x = dd.x * rn.x;
+          zn.y = dd.y * rn.y;
+          r2[j] = rn;
+          z2[j] = zn;
+          acc.x += rn.x * zn.x;
+          acc.x += rn.y * zn.y;
+          acc.y += zn.x * zn.x;
+          acc.y += zn.y * zn.y;
+        }
+      } else
       for (int s = gw; s < ns; s += UU * nw) {
         double rr[UU], qq[UU], dd[UU];
 #pragma unroll
@@ -211,6 +259,14 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
   // deferred x += alpha p of the last iteration (Alg. 1 updates x before the test)
   if (last_valid && !nan) {
     const double* __restrict__ plast = ((it - 1) & 1) ? a.p1 : a.p0;  // p of the last iteration
+    if (vec2) {
+      double2* __restrict__ x2 = reinterpret_cast<double2*>(a.x);
+      const double2* __restrict__ pl2 = reinterpret_cast<const double2*>(plast);
+      for (int64_t j = (int64_t)gw * kSellC + lane; j < n2; j += (int64_t)nw * kSellC) {
+        const double2 xx = x2[j], pp = pl2[j];
+        x2[j] = make_double2(xx.x + alpha * pp.x, xx.y + alpha * pp.y);
+      }
+    } else
     for (int s = gw; s < ns; s += UU * nw) {
       double xx[UU], pp[UU];
 #pragma unroll
@@ -251,7 +307,7 @@ __global__ void spmv_kernel(const int64_t* __restrict__ sp, const int* __restric
     double sum = 0.0;
 #pragma unroll 4
     for (int k = 0; k < w; ++k) {
-      const int64_t t = base + (int64_t)k * kSellC + lane;
+      const int64_t t = sell_slot(base, w, k, lane);
       sum += Av[t] * x[col[t]];
     }
     y[(int64_t)s * kSellC + lane] = sum;

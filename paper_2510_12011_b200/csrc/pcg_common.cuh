@@ -186,9 +186,10 @@ __device__ __forceinline__ double row_Ap_staged(int w, int lane, const double* A
   double sum = 0.0;
 #pragma unroll 8
   for (int k = 0; k < w; ++k) {
-    const int c = Cs[k * kSellC + lane];
+    const int64_t t = sell_slot(0, w, k, lane);
+    const int c = Cs[t];
     const double g = FIRST ? z[c] : z[c] + beta * pold[c];
-    sum += As[k * kSellC + lane] * g;
+    sum += As[t] * g;
   }
   return sum;
 }
@@ -251,7 +252,7 @@ __device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, c
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       const int kk = min(k0 + j, w - 1);
-      const int64_t t = base + (int64_t)kk * kSellC + lane;
+      const int64_t t = sell_slot(base, w, kk, lane);
       const int c = ci(t, kk);
       av[j] = ld_mat(A + t);
       g[j] = FIRST ? z[c] : z[c] + beta * pold[c];
@@ -261,12 +262,71 @@ __device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, c
       if (k0 + j < w) sum += av[j] * g[j];
   }
 #else
+#ifndef TCB_PAIRS_S
+#define TCB_PAIRS_S 1   // 16-byte pair loads in the q = A p product (else per-slot loads)
+#endif
+#if TCB_SELL_PAIRS && TCB_PAIRS_S
+  if (!ci.c16) {  // slot pairs: one 16-byte value load + one 8-byte index load per pair
+    const double2* A2 = reinterpret_cast<const double2*>(A + base) + lane;
+    const int2* C2 = reinterpret_cast<const int2*>(ci.c32 + base) + lane;
+    const int np = w >> 1;
+#pragma unroll 2
+    for (int j = 0; j < np; ++j) {
+      const double2 av = ld_mat(A2 + 32 * j);
+      const int2 c = ld_mat(C2 + 32 * j);
+      const double g0 = FIRST ? z[c.x] : z[c.x] + beta * pold[c.x];
+      const double g1 = FIRST ? z[c.y] : z[c.y] + beta * pold[c.y];
+      sum += av.x * g0;
+      sum += av.y * g1;
+    }
+    if (w & 1) {
+      const int64_t t = base + (int64_t)kSellC * (w - 1) + lane;
+      const int c = ld_mat(ci.c32 + t);
+      sum += ld_mat(A + t) * (FIRST ? z[c] : z[c] + beta * pold[c]);
+    }
+    return sum;
+  }
+#endif
 #pragma unroll 4
   for (int k = 0; k < w; ++k) {
-    const int64_t t = base + (int64_t)k * kSellC + lane;
+    const int64_t t = sell_slot(base, w, k, lane);
     const int c = ci(t, k);
     const double g = FIRST ? z[c] : z[c] + beta * pold[c];
     sum += ld_mat(A + t) * g;
+  }
+#endif
+  return sum;
+}
+
+// r_0 row of Eq. 3 as A u' - K v', slots in CSR order, plain
+// int32 indices, direct evict-first loads (slot pairs when TCB_SELL_PAIRS).
+__device__ __forceinline__ double row_rhs_direct(int64_t base, int w, int lane, const int* col,
+                                                 const double* A, const double* K, const double* up,
+                                                 const double* vp) {
+  double sum = 0.0;
+#if TCB_SELL_PAIRS
+  const double2* A2 = reinterpret_cast<const double2*>(A + base) + lane;
+  const double2* K2 = reinterpret_cast<const double2*>(K + base) + lane;
+  const int2* C2 = reinterpret_cast<const int2*>(col + base) + lane;
+  const int np = w >> 1;
+#pragma unroll 2
+  for (int j = 0; j < np; ++j) {
+    const double2 av = ld_mat(A2 + 32 * j), kv = ld_mat(K2 + 32 * j);
+    const int2 c = ld_mat(C2 + 32 * j);
+    sum += av.x * up[c.x] - kv.x * vp[c.x];
+    sum += av.y * up[c.y] - kv.y * vp[c.y];
+  }
+  if (w & 1) {
+    const int64_t t = base + (int64_t)kSellC * (w - 1) + lane;
+    const int c = ld_mat(col + t);
+    sum += ld_mat(A + t) * up[c] - ld_mat(K + t) * vp[c];
+  }
+#else
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const int64_t t = base + (int64_t)k * kSellC + lane;
+    const int c = ld_mat(col + t);
+    sum += ld_mat(A + t) * up[c] - ld_mat(K + t) * vp[c];
   }
 #endif
   return sum;

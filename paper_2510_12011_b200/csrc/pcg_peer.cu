@@ -201,13 +201,7 @@ __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_
     const int64_t base = __ldg(X.slice_ptr + s);
     const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
     const int64_t i = (int64_t)s * kSellC + lane;
-    double sum = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < w; ++k) {
-      const int64_t t = base + (int64_t)k * kSellC + lane;
-      const int c = __ldcs(X.col + t);
-      sum += __ldcs(X.A + t) * X.up[c] - __ldcs(X.K + t) * X.vp[c];
-    }
+    const double sum = row_rhs_direct(base, w, lane, X.col, X.A, X.K, X.up, X.vp);
     const double zi = __ldg(X.dinv + i) * sum;
     X.r[i] = sum;
     X.z[i] = zi;

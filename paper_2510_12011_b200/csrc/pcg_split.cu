@@ -60,13 +60,7 @@ __global__ void __launch_bounds__(kSplitThreads, 4) split_rhs_kernel(SplitArgs a
     const int64_t base = __ldg(a.slice_ptr + s);
     const int w = (int)((__ldg(a.slice_ptr + s + 1) - base) >> 5);
     const int64_t i = (int64_t)s * kSellC + lane;
-    double sum = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < w; ++k) {
-      const int64_t t = base + (int64_t)k * kSellC + lane;
-      const int c = __ldcs(a.col + t);
-      sum += __ldcs(a.A + t) * a.up[c] - __ldcs(a.K + t) * a.vp[c];   // r_0 = A u' - K v'
-    }
+    const double sum = row_rhs_direct(base, w, lane, a.col, a.A, a.K, a.up, a.vp);  // r_0 = A u' - K v'
     const double zi = __ldg(a.dinv + i) * sum;
     a.r[i] = sum;
     a.z[i] = zi;
@@ -128,14 +122,12 @@ __global__ void __launch_bounds__(kSplitThreads, 8) split_S_kernel(SplitArgs a) 
       pi += s.beta * po;
       a.x[i] += s.alpha * po;            // deferred x += alpha_{it-1} p_{it-1}
     }
-    double sum = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < w; ++k) {
-      const int64_t t = base + (int64_t)k * kSellC + lane;
-      const int c = __ldcs(a.col + t);
-      const double g = first ? a.z[c] : a.z[c] + s.beta * pold[c];
-      sum += __ldcs(a.A + t) * g;
-    }
+    ColIdx ci;
+    ci.c32 = a.col;
+    ci.c16 = nullptr;
+    ci.kb = nullptr;
+    const double sum = first ? row_Ap_direct<true>(base, w, lane, ci, a.A, a.z, nullptr, 0.0)
+                             : row_Ap_direct<false>(base, w, lane, ci, a.A, a.z, pold, s.beta);
     pnew[i] = pi;
     a.q[i] = sum;
     acc.x += pi * sum;

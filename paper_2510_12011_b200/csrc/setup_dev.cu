@@ -153,7 +153,7 @@ __global__ void k_fill_sell(int64_t n, int32_t nslices, const int64_t* __restric
   const int64_t base = sp[s], w = (sp[s + 1] - base) / kSellC;
   const int64_t len = i < n ? rowptr[i + 1] - rowptr[i] : 0;
   for (int64_t k = 0; k < w; ++k)
-    scol[base + k * kSellC + l] = k < len ? col[rowptr[i] + k] : (int32_t)i;  // padding: self
+    scol[sell_slot(base, w, k, l)] = k < len ? col[rowptr[i] + k] : (int32_t)i;  // padding: self
 }
 
 __global__ void k_tets_perm(int64_t m, const int32_t* __restrict__ tets, const int32_t* __restrict__ inv,

@@ -197,7 +197,7 @@ void csr_to_sell(int32_t n, const int64_t* rowptr, const int32_t* col, HostSell&
       int64_t len = (i < n) ? rowptr[i + 1] - rowptr[i] : 0;
       if (i < n) s.rowlen[i] = (int32_t)len;
       for (int64_t k = 0; k < w; ++k) {
-        int64_t slot = base + k * kSellC + l;
+        int64_t slot = sell_slot(base, w, k, l);
         if (k < len) {
           s.col[slot] = col[rowptr[i] + k];
           if (csr_slot) (*csr_slot)[rowptr[i] + k] = slot;
@@ -222,9 +222,9 @@ void compress_sell(HostSell& s) {
     const int64_t base = s.slice_ptr[sl], w = (s.slice_ptr[sl + 1] - base) / kSellC;
     bool ok = true;
     for (int64_t k = 0; k < w && ok; ++k) {
-      int32_t mn = s.col[base + k * kSellC], mx = mn;
+      int32_t mn = s.col[sell_slot(base, w, k, 0)], mx = mn;
       for (int l = 1; l < kSellC; ++l) {
-        const int32_t c = s.col[base + k * kSellC + l];
+        const int32_t c = s.col[sell_slot(base, w, k, l)];
         mn = std::min(mn, c);
         mx = std::max(mx, c);
       }
@@ -238,7 +238,7 @@ void compress_sell(HostSell& s) {
     }
     for (int64_t k = 0; k < w; ++k)
       for (int l = 0; l < kSellC; ++l) {
-        const int64_t t = base + k * kSellC + l;
+        const int64_t t = sell_slot(base, w, k, l);
         s.col16[t] = (uint16_t)(s.col[t] - s.kbase[base / kSellC + k]);
       }
   }
