@@ -234,7 +234,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-rcm", action="store_true")
     ap.add_argument("--partitions", type=int, default=1, help="row-block partitions on this GPU")
-    ap.add_argument("--pcg-variant", type=int, default=0, help="0 direct loads (default), 1 TMA-staged, 2 direct + 16-bit indices")
+    ap.add_argument("--pcg-variant", type=int, default=-1,
+                    help="-1 automatic (default), 0 direct loads, 1 TMA-staged, 2 direct + 16-bit indices, "
+                         "3 L2-resident matrix, 4 all slots of a row in flight")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--preroll", type=int, default=None)
@@ -345,7 +347,7 @@ def main():
         "config": {"workload": args.workload, "baseline_config": w["cfg"], "nodes": n, "nnz": nnz,
                    "tets": int(E), "model": w["model"], "dt_ms": w["dt"], "dx_mm": w["dx"],
                    "grid": list(w["dims"]) if w["dims"] else f"BiV h={w['h']} mm", "tol": "abs=rel=1e-5, max 100 (P:316)",
-                   "rcm": not args.no_rcm, "preroll_steps": preroll, "pcg_variant": args.pcg_variant,
+                   "rcm": not args.no_rcm, "preroll_steps": preroll, "pcg_variant": info["pcg_variant"],
                    "engine": eng,
                    "wide_slices": info.get("wide_slices"),
                    "l2": f"inputs larger than L2 (A+K+col {(20 * info['nnz_pad']) / 1e9:.2f} GB >> 126 MB)"

@@ -96,7 +96,12 @@ typedef struct {
   int32_t use_rcm;       /* 1: Reverse Cuthill-McKee reordering */
   int32_t pcg_variant;   /* PCG kernel memory pipeline: 0 direct
                             loads at full occupancy (default), 1 TMA-staged matrix stream,
-                            2 direct loads with 16-bit column offsets */
+                            2 direct loads with 16-bit column offsets, 3 direct loads with
+                            the matrix held in L2 (evict-last policy; for systems whose
+                            values + indices fit in L2), 4 every slot of a row in flight
+                            at once (latency-bound mid-size systems); -1 (default):
+                            automatic, 4 when the system has at most 4 slices per
+                            resident warp of variant 0, else 0 */
   int32_t partitions;    /* row-block partitions of the RCM order held by this context on
                             its GPU (1 = persistent single-kernel PCG; >1 = split-phase PCG
                             with device-copy halos).  Ignored after tc_comm_init (one
@@ -123,7 +128,7 @@ typedef struct {
 
 /* Fills the defaults: theta 0.5, dt 0.01, chi 140, cm 0.01, tolerances 1e-5,
  * max_iters 100, consecutive rel-mode, TT2006 epi, fail_budget 3,
- * thresholds 0 / -70 mV, use_rcm 1, pcg_variant 0, partitions 1, check_every 4, peer 1,
+ * thresholds 0 / -70 mV, use_rcm 1, pcg_variant -1, partitions 1, check_every 4, peer 1,
  * engine auto, device_setup 1. */
 void tc_config_default(tc_config* cfg);
 
@@ -232,9 +237,10 @@ tc_status tc_profile_read(tc_ctx* ctx, double out[6], int reset);
  * slices, out[4] PCG grid (CTAs) of the first part, out[5] slices kept at int32
  * indices (variant 2), out[6] partitions, out[7] ghost columns of the parts held,
  * out[8] PCG path (0 persistent single part, 1 split-phase, 2 persistent peer),
- * out[9] CTAs per partition of the peer kernel.
+ * out[9] CTAs per partition of the peer kernel, out[10] PCG kernel variant
+ * launched for the first part (tc_config.pcg_variant, or the automatic choice).
  * TC_ESTATE before tc_assemble/tc_csr_upload. */
-tc_status tc_matrix_info(const tc_ctx* ctx, int64_t out[10]);
+tc_status tc_matrix_info(const tc_ctx* ctx, int64_t out[11]);
 
 /* ---- Minimum-slice operators on an uploaded CSR (no mesh needed) ---------- */
 /* Upload an n x n CSR (rowptr n+1, col/val nnz, columns sorted per row, the

@@ -278,12 +278,12 @@ def tc_profile_read(ctx, reset: bool = False):
 
 
 def tc_matrix_info(ctx) -> dict:
-    out = np.zeros(10, np.int64)
+    out = np.zeros(11, np.int64)
     _check(ctx, _L.tc_matrix_info(ctx, _ptr(out)))
     return dict(n=int(out[0]), nnz=int(out[1]), nnz_pad=int(out[2]), nslices=int(out[3]),
                 pcg_grid=int(out[4]), wide_slices=int(out[5]), partitions=int(out[6]),
                 ghosts=int(out[7]), path=["persistent", "split", "peer"][int(out[8])],
-                peer_ctas=int(out[9]))
+                peer_ctas=int(out[9]), pcg_variant=int(out[10]))
 
 
 def tc_nccl_unique_id() -> bytes:

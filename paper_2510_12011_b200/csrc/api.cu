@@ -37,6 +37,7 @@ struct Part {
   int32_t nslices = 0;
   int64_t n_wide = 0;
   int grid = 1;  // persistent kernel grid (1 part) or split-kernel grid
+  int pcg_var = 0;  // PCG kernel variant launched for this part (cg_pick_variant)
   int64_t* d_sp = nullptr;
   int32_t* d_col = nullptr;
   uint16_t* d_col16 = nullptr;
@@ -215,7 +216,7 @@ void tc_config_default(tc_config* c) {
   c->lat_threshold = 0.0;
   c->lrt_threshold = -70.0;
   c->use_rcm = 1;
-  c->pcg_variant = 0;
+  c->pcg_variant = -1;
   c->partitions = 1;
   c->check_every = 4;
   c->peer = 1;
@@ -229,7 +230,7 @@ tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx*
   *out = nullptr;
   if (!(cfg->dt > 0) || !(cfg->theta >= 0 && cfg->theta <= 1) || !(cfg->chi > 0) || !(cfg->cm > 0) ||
       cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 ||
-      cfg->model > 3 || cfg->pcg_variant < 0 || cfg->pcg_variant > 2 || cfg->partitions < 1 ||
+      cfg->model > 3 || cfg->pcg_variant < -1 || cfg->pcg_variant > 4 || cfg->partitions < 1 ||
       cfg->partitions > 4096 || cfg->check_every < 1 || cfg->engine < 0 || cfg->engine > 3)
     return TC_EINVAL;
   int ndev = 0;
@@ -813,7 +814,8 @@ static tc_status assemble_host(tc_ctx* c, const std::vector<int32_t>& ereg, std:
     if (split_mode(c)) {
       P.grid = split_grid(P.nslices);
     } else {
-      P.grid = cg_grid_size(1, c->cfg.pcg_variant, P.nslices, c->device);
+      P.pcg_var = cg_pick_variant(c->cfg.pcg_variant, P.nslices, c->device);
+      P.grid = cg_grid_size(1, P.pcg_var, P.nslices, c->device);
     }
     CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
   }
@@ -929,7 +931,8 @@ static tc_status assemble_device(tc_ctx* c, const std::vector<int32_t>& ereg) {
     return fail(c, TC_ECUDA, std::string("assembly kernel: ") + cudaGetErrorString(le != cudaSuccess ? le : ss));
   if (herr == 1) return fail(c, TC_EDEGEN, "assembly: zero-volume element");
   if (herr == 2) return fail(c, TC_EINVAL, "assembly: pattern slot missing (internal)");
-  P.grid = cg_grid_size(1, c->cfg.pcg_variant, P.nslices, c->device);
+  P.pcg_var = cg_pick_variant(c->cfg.pcg_variant, P.nslices, c->device);
+  P.grid = cg_grid_size(1, P.pcg_var, P.nslices, c->device);
   CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
   return TC_OK;
 }
@@ -1388,7 +1391,7 @@ extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
       Part& P = c->parts[0];
       CgArgs ca = cg_args(c, P, P.d_V[c->iX]);
       ca.stat = c->d_stats + st;
-      CUDA_TRY(c, launch_pcg(1, c->cfg.pcg_variant, ca, P.grid, c->stream));
+      CUDA_TRY(c, launch_pcg(1, P.pcg_var, ca, P.grid, c->stream));
       c->launches += 2;  // RHS kernel + cooperative PCG kernel
     }
     if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
@@ -1467,7 +1470,7 @@ tc_status tc_profile_read(tc_ctx* c, double out[6], int reset) {
   return TC_OK;
 }
 
-tc_status tc_matrix_info(const tc_ctx* c, int64_t out[10]) {
+tc_status tc_matrix_info(const tc_ctx* c, int64_t out[11]) {
   if (!c || !out) return TC_EINVAL;
   if (!c->assembled && !c->csr_mode) return TC_ESTATE;
   const Part& P = c->parts[0];
@@ -1488,6 +1491,7 @@ tc_status tc_matrix_info(const tc_ctx* c, int64_t out[10]) {
   out[7] = ghosts;
   out[8] = c->peer ? 2 : (split_mode(c) ? 1 : 0);  // PCG path: 0 persistent, 1 split-phase, 2 peer persistent
   out[9] = c->peer_bpg;
+  out[10] = P.pcg_var;
   return TC_OK;
 }
 
@@ -1649,7 +1653,8 @@ tc_status tc_csr_upload(tc_ctx* c, int32_t n, int64_t nnz, const int32_t* rowptr
   for (int32_t i = 0; i < n; ++i) dinv[i] = diag[i] != 0.0 ? 1.0 / diag[i] : 0.0;
   CUDA_TRY(c, cudaMemcpyAsync(P.d_dinv, dinv.data(), dinv.size() * 8, cudaMemcpyHostToDevice, c->stream));
   TC_TRY(upload_compressed(c, P, hs));
-  P.grid = cg_grid_size(0, c->cfg.pcg_variant, P.nslices, c->device);
+  P.pcg_var = cg_pick_variant(c->cfg.pcg_variant, P.nslices, c->device);
+  P.grid = cg_grid_size(0, P.pcg_var, P.nslices, c->device);
   CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
   TC_TRY(ensure_stats(c, 1));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1682,7 +1687,7 @@ tc_status tc_pcg(tc_ctx* c, const double* b, const double* x0, double* x, tc_ste
   CUDA_TRY(c, cudaMemcpyAsync(P.d_V[0], x0, c->n * 8, cudaMemcpyHostToDevice, c->stream));
   CgArgs ca = cg_args(c, P, P.d_V[0]);
   ca.stat = c->d_stats;
-  CUDA_TRY(c, launch_pcg(0, c->cfg.pcg_variant, ca, P.grid, c->stream));
+  CUDA_TRY(c, launch_pcg(0, P.pcg_var, ca, P.grid, c->stream));
   tc_step_stat h;
   CUDA_TRY(c, cudaMemcpyAsync(&h, c->d_stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(x, P.d_V[0], c->n * 8, cudaMemcpyDeviceToHost, c->stream));

@@ -301,6 +301,7 @@ cudaError_t launch_spmv(const int64_t* slice_ptr, const int32_t* col, const doub
 // PCG: mode 0 = plain (r0 = b - A x0), 1 = monodomain RHS (r0 = A u' - K v')
 // variant 0 = direct loads at full occupancy, 1 = TMA-staged matrix stream
 int cg_grid_size(int mode, int variant, int32_t nslices, int device);
+int cg_pick_variant(int requested, int32_t nslices, int device);
 cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
 
 // split-phase PCG launchers (pcg_split.cu); grid = split_grid(nslices)

@@ -26,11 +26,21 @@
 namespace tcb {
 
 // ------------------------------------------------------------------ kernels
-// VAR 0: direct loads, int32 indices (default), 1: TMA-staged, 2: direct loads + 16-bit indices
+// VAR 0: direct loads, int32 indices (default), 1: TMA-staged, 2: direct loads + 16-bit indices,
+// 3: direct loads with the matrix kept in L2 (evict-last; systems whose A + col fit in L2),
+// 4: latency variant for systems with few slices per resident warp: every slot
+//    of a row in flight at once (row_Ap_batch), one 16-warp CTA per SM
 #ifndef TCB_VEC_U
 #define TCB_VEC_U 0   // 1: U phase and final x update over 16-byte row pairs (measured slower)
 #endif
-#define TCB_MINB(VAR) ((VAR) == 1 ? (512 / TCB_CG_THREADS > 0 ? 512 / TCB_CG_THREADS : 1) : TCB_DIRECT_MINB)
+#ifndef TCB_BATCH_NB
+#define TCB_BATCH_NB 16   // slots in flight per row in variant 4 (measured: 16 at 1 CTA/SM best)
+#endif
+#ifndef TCB_BATCH_UU
+#define TCB_BATCH_UU 1    // slices per warp pass in variant 4's U phase (measured 1 < 2 < 4)
+#endif
+#define TCB_MINB(VAR) ((VAR) == 1 ? (512 / TCB_CG_THREADS > 0 ? 512 / TCB_CG_THREADS : 1) : \
+                       (VAR) == 4 ? 1 : TCB_DIRECT_MINB)
 
 __device__ __forceinline__ void setup_pipe(SlicePipe& P, char* smem, uint64_t* bars, int warp, int lane) {
   P.buf = smem + warp * kWarpSmem;
@@ -51,6 +61,7 @@ template <int MODE, int VAR>
 __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : (1024 / TCB_CG_THREADS > 0 ? 1024 / TCB_CG_THREADS : 1)) rhs_kernel(CgArgs a) {
   constexpr bool TMA = VAR == 1;
   constexpr bool COMP = VAR == 2;
+  constexpr bool KEEP = VAR == 3;
   extern __shared__ __align__(128) char smem[];
   __shared__ double2 sh[kCgWarps];
   __shared__ __align__(8) uint64_t bars[TMA ? kCgWarps : 1][kStages];
@@ -68,7 +79,14 @@ __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : (1024 / T
                if (MODE == 1) {
                  const double* __restrict__ Kv = a.K;
                  const ColIdx ci = col_of<COMP>(a, i, base);
-                 if (TCB_SELL_PAIRS && !staged && !ci.c16) {  // slot pairs: 16-byte value loads
+                 if (KEEP) {
+#pragma unroll 4
+                   for (int k = 0; k < w; ++k) {
+                     const int64_t t = sell_slot(base, w, k, lane);
+                     const int c = ld_keep(a.col + t);
+                     sum += ld_keep(Av + t) * a.up[c] - ld_mat(Kv + t) * a.vp[c];
+                   }
+                 } else if (TCB_SELL_PAIRS && !staged && !ci.c16) {  // slot pairs: 16-byte value loads
                    const double2* A2 = reinterpret_cast<const double2*>(Av + base) + lane;
                    const double2* K2 = reinterpret_cast<const double2*>(Kv + base) + lane;
                    const int2* C2 = reinterpret_cast<const int2*>(a.col + base) + lane;
@@ -97,7 +115,7 @@ __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : (1024 / T
                  }
                } else {
                  const double ax = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.x, nullptr, 0.0)
-                                          : row_Ap_direct<true>(base, w, lane, col_of<COMP>(a, i, base), Av, a.x, nullptr, 0.0);
+                                          : row_Ap_direct<true, KEEP>(base, w, lane, col_of<COMP>(a, i, base), Av, a.x, nullptr, 0.0);
                  sum = a.b[i] - ax;
                }
                const double zi = __ldg(a.dinv + i) * sum;
@@ -115,13 +133,15 @@ template <int MODE, int VAR>
 __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a) {
   constexpr bool TMA = VAR == 1;
   constexpr bool COMP = VAR == 2;
+  constexpr bool KEEP = VAR == 3;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) char smem[];
   __shared__ double2 sh[kCgWarps];
   __shared__ __align__(8) uint64_t bars[TMA ? kCgWarps : 1][kStages];
   if (a.flags[0]) return;  // context aborted earlier: uniform across the grid
 
-  constexpr int UU = TMA ? 4 : 1;  // slices per warp pass in the streaming phases
+  constexpr bool BATCH = VAR == 4;
+  constexpr int UU = TMA ? 4 : BATCH ? TCB_BATCH_UU : 1;  // slices per warp pass in the streaming phases
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * kCgWarps + warp;
   const int nw = gridDim.x * kCgWarps;
@@ -174,7 +194,8 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
                    [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
                      const double pi = a.z[i];
                      const double sum = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.z, nullptr, 0.0)
-                                               : row_Ap_direct<true>(base, w, lane, col_of<COMP>(a, i, base), Av, a.z, nullptr, 0.0);
+                                      : BATCH ? row_Ap_batch<true, TCB_BATCH_NB>(base, w, lane, col, Av, a.z, nullptr, 0.0)
+                                               : row_Ap_direct<true, KEEP>(base, w, lane, col_of<COMP>(a, i, base), Av, a.z, nullptr, 0.0);
                      pnew[i] = pi;
                      a.q[i] = sum;
                      acc.x += pi * sum;
@@ -187,7 +208,8 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
                      const double pi = a.z[i] + beta * po;
                      a.x[i] = xi + alpha * po;
                      const double sum = staged ? row_Ap_staged<false>(w, lane, As, Cs, a.z, pold, beta)
-                                               : row_Ap_direct<false>(base, w, lane, col_of<COMP>(a, i, base), Av, a.z, pold, beta);
+                                      : BATCH ? row_Ap_batch<false, TCB_BATCH_NB>(base, w, lane, col, Av, a.z, pold, beta)
+                                               : row_Ap_direct<false, KEEP>(base, w, lane, col_of<COMP>(a, i, base), Av, a.z, pold, beta);
                      pnew[i] = pi;
                      a.q[i] = sum;
                      acc.x += pi * sum;
@@ -327,16 +349,32 @@ static int sm_count(int dev) {
 }
 
 static const void* rhs_fn(int mode, int variant) {
+  if (variant == 4) return mode == 1 ? (const void*)rhs_kernel<1, 4> : (const void*)rhs_kernel<0, 4>;
+  if (variant == 3) return mode == 1 ? (const void*)rhs_kernel<1, 3> : (const void*)rhs_kernel<0, 3>;
   if (variant == 1) return mode == 1 ? (const void*)rhs_kernel<1, 1> : (const void*)rhs_kernel<0, 1>;
   if (variant == 2) return mode == 1 ? (const void*)rhs_kernel<1, 2> : (const void*)rhs_kernel<0, 2>;
   return mode == 1 ? (const void*)rhs_kernel<1, 0> : (const void*)rhs_kernel<0, 0>;
 }
 static const void* pcg_fn(int mode, int variant) {
+  if (variant == 4) return mode == 1 ? (const void*)pcg_kernel<1, 4> : (const void*)pcg_kernel<0, 4>;
+  if (variant == 3) return mode == 1 ? (const void*)pcg_kernel<1, 3> : (const void*)pcg_kernel<0, 3>;
   if (variant == 1) return mode == 1 ? (const void*)pcg_kernel<1, 1> : (const void*)pcg_kernel<0, 1>;
   if (variant == 2) return mode == 1 ? (const void*)pcg_kernel<1, 2> : (const void*)pcg_kernel<0, 2>;
   return mode == 1 ? (const void*)pcg_kernel<1, 0> : (const void*)pcg_kernel<0, 0>;
 }
 static int pcg_smem(int variant) { return variant == 1 ? kCgSmem : 0; }
+
+// Variant actually launched: an explicit request, or (requested < 0, the
+// default) the latency variant 4 when the system has at most kAutoBatch slices
+// per resident warp of the direct variant (mid-size systems such as configs[2],
+// where each warp owns 1-3 slices and the S phase is one latency chain per
+// slot batch), else the direct variant 0 (measured crossover: DESIGN.md "PCG").
+constexpr int kAutoBatch = 4;
+int cg_pick_variant(int requested, int32_t nslices, int device) {
+  if (requested >= 0) return requested;
+  const int64_t warps = (int64_t)sm_count(device) * (2048 / 32);
+  return (int64_t)nslices <= kAutoBatch * warps ? 4 : 0;
+}
 
 // Grid: enough CTAs for one slice per warp, capped at the co-resident maximum
 // (cooperative launch); large problems get every SM x occupancy (2 CTAs / SM).

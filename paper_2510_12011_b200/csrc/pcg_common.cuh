@@ -209,6 +209,25 @@ __device__ __forceinline__ T ld_mat(const T* p) {
 #endif
 }
 
+// L2-resident matrix (variant 3, systems whose matrix fits in L2): values and
+// column indices loaded with an L2 evict-last policy so they survive the
+// vector traffic between iterations; everything else keeps its default policy.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_keep(const double* p) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy_evict_last()));
+  return v;
+}
+__device__ __forceinline__ int ld_keep(const int* p) {
+  int v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+  return v;
+}
+
 // Column index of slot t (slot row k) of one slice: either the plain int32
 // array, or (compressed slices) a per-(slice, k) int32 base, broadcast to the
 // warp, plus a 16-bit offset per slot.
@@ -238,7 +257,22 @@ __device__ __forceinline__ ColIdx col_of(const CgArgs& a, int64_t i, int64_t bas
 #define TCB_ROW_BATCH 0   // 0: unroll-4 loop; N > 0: slots in batches of N with clamped indices
 #endif
 template <bool FIRST>
-__device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, const ColIdx& ci,
+__device__ __forceinline__ double row_Ap_keep(int64_t base, int w, int lane, const ColIdx& ci,
+                                              const double* A, const double* z, const double* pold,
+                                              double beta) {
+  double sum = 0.0;  // variant 3: L2-resident matrix, plain int32 indices
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const int64_t t = sell_slot(base, w, k, lane);
+    const int c = ld_keep(ci.c32 + t);
+    const double g = FIRST ? z[c] : z[c] + beta * pold[c];
+    sum += ld_keep(A + t) * g;
+  }
+  return sum;
+}
+
+template <bool FIRST>
+__device__ __forceinline__ double row_Ap_stream(int64_t base, int w, int lane, const ColIdx& ci,
                                                 const double* A, const double* z, const double* pold,
                                                 double beta) {
   double sum = 0.0;
@@ -296,6 +330,40 @@ __device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, c
   }
 #endif
   return sum;
+}
+
+// Latency variant (VAR 4): all slots of a row in batches of NB loads in flight
+// (values, indices, then the gathers), slots past the row end reload its last
+// slot; accumulation in slot order.  Needs ~100 registers: one 16-warp CTA per SM.
+template <bool FIRST, int NB>
+__device__ __forceinline__ double row_Ap_batch(int64_t base, int w, int lane, const int* col,
+                                               const double* A, const double* z, const double* pold,
+                                               double beta) {
+  double sum = 0.0;
+#pragma unroll 1
+  for (int k0 = 0; k0 < w; k0 += NB) {
+    double av[NB], g[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int kk = min(k0 + j, w - 1);
+      const int64_t t = sell_slot(base, w, kk, lane);
+      const int c = ld_mat(col + t);
+      av[j] = ld_mat(A + t);
+      g[j] = FIRST ? z[c] : z[c] + beta * pold[c];
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (k0 + j < w) sum += av[j] * g[j];
+  }
+  return sum;
+}
+
+template <bool FIRST, bool KEEP = false>
+__device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, const ColIdx& ci,
+                                                const double* A, const double* z, const double* pold,
+                                                double beta) {
+  if constexpr (KEEP) return row_Ap_keep<FIRST>(base, w, lane, ci, A, z, pold, beta);
+  else return row_Ap_stream<FIRST>(base, w, lane, ci, A, z, pold, beta);
 }
 
 // r_0 row of Eq. 3 as A u' - K v', slots in CSR order, plain

@@ -36,7 +36,7 @@ def _bench_sim(T, name, preroll=None):
     w = bench.WORKLOADS[name]
     xyz, tets, stims, region, fibre = bench.make_inputs(w)
     cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=bench.CHI, cm=bench.CM, abs_tol=1e-5,
-                              rel_tol=1e-5, max_iters=100, use_rcm=1, pcg_variant=0, partitions=1)
+                              rel_tol=1e-5, max_iters=100, use_rcm=1, pcg_variant=-1, partitions=1)
     sim = T.Monodomain(xyz, tets, region, fibre, {0: bench.SIGMA, 1: bench.SIGMA}, cfg, stims)
     sim.step(w["preroll"] if preroll is None else preroll)
     return w, sim, xyz, tets, region, fibre

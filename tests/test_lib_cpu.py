@@ -44,6 +44,7 @@ def test_config_defaults_match_paper(lib):
     assert c.chi == 140.0 and c.cm == 0.01             # Table 3
     assert c.lat_threshold == 0.0 and c.lrt_threshold == -70.0
     assert c.use_rcm == 1
+    assert c.pcg_variant == -1       # automatic PCG kernel choice (include/tcb200.h)
 
 
 def test_no_cpu_fallback():
