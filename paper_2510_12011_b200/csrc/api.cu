@@ -107,6 +107,7 @@ struct tc_ctx {
   bool peer = false;             // persistent peer-memory PCG in use
   int peer_bpg = 0;              // CTAs per group (loop kernel)
   int peer_bpg_rhs = 0;          // CTAs per group (RHS kernel)
+  bool peer_batch = false;       // loop kernel with the latency row product (variant 4)
   std::vector<XPart> xparts;     // host copies, passed by value at launch
   std::vector<void*> ipc_opened; // peer mappings to close
   // assembled system
@@ -547,7 +548,18 @@ static tc_status setup_peer(tc_ctx* c, const std::vector<PartPlan>& plans) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   const int groups = (int)c->parts.size();
-  const int bpg = peer_blocks_per_sm(0) * sms / groups;
+  // latency variant when the one partition held here (one rank per GPU) has few
+  // slices per resident warp of the direct kernel (same rule as cg_pick_variant);
+  // several partitions emulated on one GPU keep the direct kernel unless asked
+  // (measured: tools/exp_peer_batch.py)
+  const int bpg0 = peer_blocks_per_sm(0) * sms / groups;
+  bool batch = c->cfg.pcg_variant == 4;
+  if (c->cfg.pcg_variant < 0 && bpg0 > 0 && groups == 1) {
+    batch = true;
+    for (Part& P : c->parts)
+      if ((int64_t)P.nslices > (int64_t)kAutoBatch * bpg0 * (kPeerThreadsHost / 32)) batch = false;
+  }
+  const int bpg = batch ? peer_blocks_per_sm(2) * sms / groups : bpg0;
   const int bpg_rhs = peer_blocks_per_sm(1) * sms / groups;
   if (bpg_rhs < 1) ok = false;
   if (bpg < 1) ok = false;
@@ -669,6 +681,8 @@ static tc_status setup_peer(tc_ctx* c, const std::vector<PartPlan>& plans) {
   c->peer = true;
   c->peer_bpg = bpg;
   c->peer_bpg_rhs = bpg_rhs;
+  c->peer_batch = batch;
+  for (Part& P : c->parts) P.pcg_var = batch ? 4 : 0;
   return TC_OK;
 }
 
@@ -1375,7 +1389,7 @@ extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
     if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (3) RHS + Algorithm 1
     if (c->peer) {
-      CUDA_TRY(c, launch_pcg_peer(c->xparts.data(), (int)c->parts.size(), c->peer_bpg, c->peer_bpg_rhs, c->iX, c->iVk,
+      CUDA_TRY(c, launch_pcg_peer(c->xparts.data(), (int)c->parts.size(), c->peer_bpg, c->peer_bpg_rhs, c->peer_batch, c->iX, c->iVk,
                                   c->cfg.abs_tol, c->cfg.rel_tol, c->cfg.max_iters, c->cfg.rel_mode,
                                   c->d_stats + st, c->d_flags, (int32_t)c->k, c->stream));
       c->launches += 2;  // RHS + loop kernels

@@ -26,6 +26,8 @@ namespace tcb {
 // Padding slots point at the row itself with value 0.
 // ---------------------------------------------------------------------------
 constexpr int kSellC = 32;
+constexpr int kAutoBatch = 4;          // PCG variant 4 up to this many slices per resident warp (pcg.cu)
+constexpr int kPeerThreadsHost = 256;  // threads per CTA of the peer-memory PCG kernels (pcg_peer.cu)
 #ifndef TCB_SELL_PAIRS
 #define TCB_SELL_PAIRS 0
 #endif
@@ -316,10 +318,10 @@ cudaError_t launch_split_U(const SplitArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_split_scalar(const SplitArgs& a, cudaStream_t s);
 cudaError_t launch_split_final(const SplitArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_sum_partials(double2* const* reds, int nparts, int slot, cudaStream_t s);
-int peer_blocks_per_sm(int which);  // 0 loop kernel, 1 RHS kernel
+int peer_blocks_per_sm(int which);  // 0 loop kernel, 1 RHS kernel, 2 loop kernel (batch variant)
 int peer_max_groups();
 // parts: HOST array of `groups` XParts (passed by value in kernel-parameter space)
-cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, int iX, int iVk, double eps_a,
+cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, bool batch, int iX, int iVk, double eps_a,
                             double eps_r, int32_t max_iters, int32_t rel_mode, tc_step_stat* stat,
                             int32_t* flags, int32_t step_tag, cudaStream_t s);
 

@@ -33,9 +33,6 @@ namespace tcb {
 #ifndef TCB_VEC_U
 #define TCB_VEC_U 0   // 1: U phase and final x update over 16-byte row pairs (measured slower)
 #endif
-#ifndef TCB_BATCH_NB
-#define TCB_BATCH_NB 16   // slots in flight per row in variant 4 (measured: 16 at 1 CTA/SM best)
-#endif
 #ifndef TCB_BATCH_UU
 #define TCB_BATCH_UU 1    // slices per warp pass in variant 4's U phase (measured 1 < 2 < 4)
 #endif
@@ -369,7 +366,6 @@ static int pcg_smem(int variant) { return variant == 1 ? kCgSmem : 0; }
 // per resident warp of the direct variant (mid-size systems such as configs[2],
 // where each warp owns 1-3 slices and the S phase is one latency chain per
 // slot batch), else the direct variant 0 (measured crossover: DESIGN.md "PCG").
-constexpr int kAutoBatch = 4;
 int cg_pick_variant(int requested, int32_t nslices, int device) {
   if (requested >= 0) return requested;
   const int64_t warps = (int64_t)sm_count(device) * (2048 / 32);

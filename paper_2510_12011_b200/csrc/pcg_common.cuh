@@ -332,6 +332,9 @@ __device__ __forceinline__ double row_Ap_stream(int64_t base, int w, int lane, c
   return sum;
 }
 
+#ifndef TCB_BATCH_NB
+#define TCB_BATCH_NB 16   // slots in flight per row in variant 4 (measured: 16 at 1 CTA/SM best)
+#endif
 // Latency variant (VAR 4): all slots of a row in batches of NB loads in flight
 // (values, indices, then the gathers), slots past the row end reload its last
 // slot; accumulation in slot order.  Needs ~100 registers: one 16-warp CTA per SM.

@@ -24,7 +24,7 @@
 
 namespace tcb {
 
-constexpr int kPeerThreads = 256;
+constexpr int kPeerThreads = kPeerThreadsHost;
 constexpr int kPeerWarps = kPeerThreads / 32;
 constexpr long long kWaitCycles = 4000000000LL;  // ~2 s at 1.9 GHz
 
@@ -220,7 +220,11 @@ __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_
 }
 
 // Algorithm 1's loop on the partitioned system (after rhs_peer_kernel).
-__global__ void __launch_bounds__(kPeerThreads, 8) pcg_peer_kernel(const __grid_constant__ PeerRun R) {
+// BATCH: the latency variant's row product (row_Ap_batch, every slot of a row in
+// flight; ~128 registers, 2 CTAs of 8 warps per SM) for partitions with few
+// slices per resident warp (variant 4).
+template <bool BATCH>
+__global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(const __grid_constant__ PeerRun R) {
   __shared__ double2 sh[kPeerWarps];
   __shared__ double2 sh1;
   const int group = blockIdx.x / R.bpg;
@@ -259,7 +263,8 @@ __global__ void __launch_bounds__(kPeerThreads, 8) pcg_peer_kernel(const __grid_
           const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
           const int64_t i = (int64_t)s * kSellC + lane;
           const double pi = X.z[i];
-          const double sum = row_Ap_direct<true>(base, w, lane, ci, X.A, X.z, nullptr, 0.0);
+          const double sum = BATCH ? row_Ap_batch<true, TCB_BATCH_NB>(base, w, lane, X.col, X.A, X.z, nullptr, 0.0)
+                                   : row_Ap_direct<true>(base, w, lane, ci, X.A, X.z, nullptr, 0.0);
           pnew[i] = pi;
           X.q[i] = sum;
           acc.x += pi * sum;
@@ -273,7 +278,8 @@ __global__ void __launch_bounds__(kPeerThreads, 8) pcg_peer_kernel(const __grid_
           const double xi = x[i];
           const double pi = X.z[i] + beta * po;
           x[i] = xi + alpha * po;
-          const double sum = row_Ap_direct<false>(base, w, lane, ci, X.A, X.z, pold, beta);
+          const double sum = BATCH ? row_Ap_batch<false, TCB_BATCH_NB>(base, w, lane, X.col, X.A, X.z, pold, beta)
+                                   : row_Ap_direct<false>(base, w, lane, ci, X.A, X.z, pold, beta);
           pnew[i] = pi;
           X.q[i] = sum;
           acc.x += pi * sum;
@@ -338,12 +344,15 @@ __global__ void __launch_bounds__(kPeerThreads, 8) pcg_peer_kernel(const __grid_
   }
 }
 
+static const void* peer_fn(int which) {
+  return which == 1 ? (const void*)rhs_peer_kernel
+                    : which == 2 ? (const void*)pcg_peer_kernel<true> : (const void*)pcg_peer_kernel<false>;
+}
+
 int peer_blocks_per_sm(int which) {
-  static int v[2] = {0, 0};
+  static int v[3] = {0, 0, 0};
   if (!v[which]) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v[which], which ? (const void*)rhs_peer_kernel
-                                                                   : (const void*)pcg_peer_kernel,
-                                                  kPeerThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v[which], peer_fn(which), kPeerThreads, 0);
     if (v[which] < 1) v[which] = 1;
   }
   return v[which];
@@ -351,7 +360,7 @@ int peer_blocks_per_sm(int which) {
 
 int peer_max_groups() { return kMaxGroups; }
 
-cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, int iX, int iVk, double eps_a,
+cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, bool batch, int iX, int iVk, double eps_a,
                             double eps_r, int32_t max_iters, int32_t rel_mode, tc_step_stat* stat,
                             int32_t* flags, int32_t step_tag, cudaStream_t s) {
   if (groups < 1 || groups > kMaxGroups) return cudaErrorInvalidValue;
@@ -367,7 +376,7 @@ cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs
                                   args, 0, s);
   if (e != cudaSuccess) return e;
   R.bpg = bpg;
-  return cudaLaunchCooperativeKernel((const void*)pcg_peer_kernel, dim3(groups * bpg), dim3(kPeerThreads),
+  return cudaLaunchCooperativeKernel(peer_fn(batch ? 2 : 0), dim3(groups * bpg), dim3(kPeerThreads),
                                      args, 0, s);
 }
 

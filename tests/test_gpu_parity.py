@@ -135,22 +135,25 @@ def test_step_trajectory_parity(T, model, permute, rcm, variant):
         sim.close()
 
 
-@pytest.mark.parametrize("peer", [1, 0])
+@pytest.mark.parametrize("peer,variant", [(1, -1), (1, 4), (0, -1)])
 @pytest.mark.parametrize("model,nparts,permute", [("ms", 2, False), ("tt2006", 3, True), ("tt2006", 2, False),
                                                   ("ms", 5, True)])
-def test_partitioned_trajectory_parity(T, model, nparts, permute, peer):
+def test_partitioned_trajectory_parity(T, model, nparts, permute, peer, variant):
     """Row-block partitions on one GPU (split-phase PCG, device-copy halos,
-    in-order scalar sums): same trajectory as the oracle and as 1 partition."""
+    in-order scalar sums; or the peer-memory kernels with the latency (auto, 4)
+    or direct (0) row product): same trajectory as the oracle and as 1 partition."""
     xyz, tets, region, fib, cond, stims = _slab_case(model, 25, 9, 5, permute=permute, seed=2 if permute else 0)
     dt = 0.05
     ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0), stims)
     cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, partitions=nparts, check_every=3,
-                              peer=peer)
+                              peer=peer, pcg_variant=variant)
     sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
     try:
         info = T.tc_matrix_info(sim.ctx)
         assert info["partitions"] == nparts and info["ghosts"] > 0
         assert info["path"] == ("peer" if peer else "split")
+        if peer:   # emulated partitions: direct kernel unless the latency variant is asked for
+            assert info["pcg_variant"] == (0 if variant < 0 else variant)
         for k in range(80):
             st = sim.step(1)
             rep = ref.step()
@@ -179,6 +182,8 @@ def test_nccl_path_world1_parity(T, peer):
         pytest.skip("NCCL not loadable")
     sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims, comm=(0, 1, uid))
     try:
+        if peer:   # one partition per process: the automatic choice takes the latency variant
+            assert T.tc_matrix_info(sim.ctx)["pcg_variant"] == 4
         for k in range(60):
             sim.step(1)
             ref.step()
