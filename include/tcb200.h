@@ -224,6 +224,21 @@ int64_t tc_state_len(const tc_ctx* ctx);
 tc_status tc_get_state(tc_ctx* ctx, double* buf, int64_t len);
 tc_status tc_set_state(tc_ctx* ctx, const double* buf, int64_t len);
 
+/* Pipelined host I/O: n_steps independent one-step problems.  For j = 0 ..
+ * n_steps-1: the state states[j*stride .. j*stride + tc_state_len) (host, the
+ * tc_set_state layout; pinned memory lets the copies overlap) is loaded, one
+ * step is taken (Eq. 2-3 and Algorithm 1, as tc_step), and V^{k+1}
+ * (n_nodes doubles, original order) is written to v_out[j*n_nodes ..].  The
+ * host->device copy of input j+1 and the device->host copy of output j-1 run
+ * on two copy streams while step j computes -- the result equals
+ * tc_set_state + tc_step(1) + tc_get_v for every j.  stats: nullable,
+ * n_steps entries.  After the call the context holds the state after the last
+ * problem.  Errors: TC_EINVAL (null pointers, stride < tc_state_len, a bad step
+ * index in an input), TC_ESTATE (before tc_assemble, or a multi-process
+ * context), and tc_step's errors.  Host buffers stay owned by the caller. */
+tc_status tc_step_io(tc_ctx* ctx, int64_t n_steps, const double* states, int64_t stride, double* v_out,
+                     tc_step_stat* stats);
+
 /* Device time (ms) spent per phase since the last reset, measured with CUDA
  * events on the context stream when profiling is enabled:
  * out[0] ionic + stimulus kernels, out[1] PCG kernel (RHS + Alg. 1),

@@ -93,6 +93,7 @@ def _load():
         "tc_state_len": ([P], I64),
         "tc_get_state": ([P, P, I64], I32),
         "tc_set_state": ([P, P, I64], I32),
+        "tc_step_io": ([P, I64, P, I64, P, P], I32),
         "tc_profile": ([P, C.c_int], I32),
         "tc_profile_read": ([P, P, C.c_int], I32),
         "tc_matrix_info": ([P, P], I32),
@@ -264,6 +265,21 @@ def tc_set_state(ctx, buf) -> None:
     if not (isinstance(buf, np.ndarray) and buf.dtype == np.float64 and buf.flags.c_contiguous):
         buf = _f64(buf)
     _check(ctx, _L.tc_set_state(ctx, _ptr(buf), buf.shape[0]))
+
+
+def tc_step_io(ctx, states, v_out, want_stats: bool = False):
+    """states: (n_steps, >= tc_state_len) float64 host array (pinned for overlap);
+    v_out: (n_steps, n_nodes) float64 host array, filled with V^{k+1} of each."""
+    if not (isinstance(states, np.ndarray) and states.dtype == np.float64 and states.ndim == 2
+            and states.strides[1] == 8):
+        raise ValueError("states: 2-D float64 array with contiguous rows")
+    if not (isinstance(v_out, np.ndarray) and v_out.dtype == np.float64 and v_out.flags.c_contiguous
+            and v_out.shape == (states.shape[0], tc_num_nodes(ctx))):
+        raise ValueError("v_out: C-contiguous float64 array (n_steps, n_nodes)")
+    m = states.shape[0]
+    stats = np.zeros(m, STAT_DTYPE) if want_stats else None
+    _check(ctx, _L.tc_step_io(ctx, m, _ptr(states), states.strides[0] // 8, _ptr(v_out), _ptr(stats)))
+    return stats
 
 
 def tc_profile(ctx, enable: bool = True) -> None:

@@ -119,6 +119,11 @@ struct tc_ctx {
   int32_t* d_perm_g = nullptr;     // perm on the device (internal -> original)
   int32_t* d_pos = nullptr;        // NCCL mode: original -> position in the padded all-gather
   double* d_io = nullptr;          // original-order staging for host I/O
+  // tc_step_io: copy streams, double-buffered device staging, events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  double* d_sin[2] = {nullptr, nullptr};   // staged input states (original order)
+  double* d_sout[2] = {nullptr, nullptr};  // staged outputs V^{k+1} (original order)
+  cudaEvent_t e_loaded[2] = {}, e_used[2] = {}, e_done[2] = {}, e_read[2] = {};
   double* d_all = nullptr;         // NCCL mode: all-gather buffer (nparts x max block)
   int64_t max_block = 0;
   int64_t nnz = 0;
@@ -265,6 +270,18 @@ tc_status tc_destroy(tc_ctx* c) {
   if (!c) return TC_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->s_in) {
+    cudaStreamSynchronize(c->s_in);
+    cudaStreamSynchronize(c->s_out);
+    cudaStreamDestroy(c->s_in);
+    cudaStreamDestroy(c->s_out);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(c->e_loaded[b]);
+      cudaEventDestroy(c->e_used[b]);
+      cudaEventDestroy(c->e_done[b]);
+      cudaEventDestroy(c->e_read[b]);
+    }
+  }
   free_all(c);
   c->comm.destroy();
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -1346,29 +1363,26 @@ static void advance_host(tc_ctx* c, int64_t nsteps) {
 
 static tc_status finish_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* stats, size_t evi, bool cluster);
 
-extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
-  if (!c) return TC_EINVAL;
-  if (!c->assembled || c->csr_mode) return fail(c, TC_ESTATE, "tc_step before tc_assemble");
-  if (nsteps < 0) return fail(c, TC_EINVAL, "tc_step: negative step count");
-  if (nsteps == 0) return TC_OK;
-  CUDA_TRY(c, cudaSetDevice(c->device));
-  TC_TRY(ensure_stats(c, nsteps));
+// Enqueue nsteps steps on c->stream (no host synchronisation); per-step reports
+// go to dstats[0 .. nsteps).  prof: record the profiling events (tc_step only).
+static tc_status enqueue_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* dstats, bool prof, size_t& evi,
+                               bool& cluster) {
   const int model = c->cfg.model;
-  size_t evi = 0;
-  if (use_cluster(c)) {  // the whole call as one cluster-engine launch
+  cluster = use_cluster(c);
+  if (cluster) {  // the whole call as one cluster-engine launch
     CoRep R;
-    TC_TRY(make_corep(c, R, c->d_stats));
+    TC_TRY(make_corep(c, R, dstats));
     if (!c->d_corep) CUDA_TRY(c, dalloc(c, &c->d_corep, 1));
     CUDA_TRY(c, cudaMemcpyAsync(c->d_corep, &R, sizeof(CoRep), cudaMemcpyHostToDevice, c->stream));
-    if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+    if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     CUDA_TRY(c, launch_cohort(model, c->d_corep, 1, c->co_csize, c->co_smem, nsteps, c->stream));
     c->launches += 1;
-    if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+    if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     advance_host(c, nsteps);
-    return finish_steps(c, nsteps, stats, evi, true);
+    return TC_OK;
   }
   for (int64_t st = 0; st < nsteps; ++st) {
-    if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+    if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (1) ionic step + LAT/LRT of V^k + x0, u', v'; (2) stimulus of the epoch of step k
     for (Part& P : c->parts) {
       IonArgs ia = ion_args(c, P, (st > 0 && c->has_prev) ? 1 : 0);
@@ -1386,29 +1400,29 @@ extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
           c->launches += 1;
         }
     }
-    if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+    if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (3) RHS + Algorithm 1
     if (c->peer) {
       CUDA_TRY(c, launch_pcg_peer(c->xparts.data(), (int)c->parts.size(), c->peer_bpg, c->peer_bpg_rhs, c->peer_batch, c->iX, c->iVk,
                                   c->cfg.abs_tol, c->cfg.rel_tol, c->cfg.max_iters, c->cfg.rel_mode,
-                                  c->d_stats + st, c->d_flags, (int32_t)c->k, c->stream));
+                                  dstats + st, c->d_flags, (int32_t)c->k, c->stream));
       c->launches += 2;  // RHS + loop kernels
     } else if (split_mode(c)) {
       TC_TRY(pcg_split(c));
       for (Part& P : c->parts) {
         SplitArgs sa = split_args(c, P);
-        sa.stat = c->d_stats + st;
+        sa.stat = dstats + st;
         CUDA_TRY(c, launch_split_final(sa, P.grid, c->stream));
         c->launches += 1;
       }
     } else {
       Part& P = c->parts[0];
       CgArgs ca = cg_args(c, P, P.d_V[c->iX]);
-      ca.stat = c->d_stats + st;
+      ca.stat = dstats + st;
       CUDA_TRY(c, launch_pcg(1, P.pcg_var, ca, P.grid, c->stream));
       c->launches += 2;  // RHS kernel + cooperative PCG kernel
     }
-    if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+    if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (4) V^{k-1} <- V^k <- x
     int old = c->iVkm1;
     c->iVkm1 = c->iVk;
@@ -1423,8 +1437,21 @@ extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
       CUDA_TRY(c, launch_lat_epilogue(ion_args(c, P, 1), c->stream));
       c->launches += 1;
     }
-  if (c->prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
-  return finish_steps(c, nsteps, stats, evi, false);
+  if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+  return TC_OK;
+}
+
+extern "C" tc_status tc_step(tc_ctx* c, int64_t nsteps, tc_step_stat* stats) {
+  if (!c) return TC_EINVAL;
+  if (!c->assembled || c->csr_mode) return fail(c, TC_ESTATE, "tc_step before tc_assemble");
+  if (nsteps < 0) return fail(c, TC_EINVAL, "tc_step: negative step count");
+  if (nsteps == 0) return TC_OK;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  TC_TRY(ensure_stats(c, nsteps));
+  size_t evi = 0;
+  bool cluster = false;
+  TC_TRY(enqueue_steps(c, nsteps, c->d_stats, c->prof, evi, cluster));
+  return finish_steps(c, nsteps, stats, evi, cluster);
 }
 
 static tc_status finish_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* stats, size_t evi, bool cluster) {
@@ -1619,6 +1646,92 @@ tc_status tc_set_state(tc_ctx* c, const double* buf, int64_t len) {
   c->k = (int64_t)kk;
   c->has_prev = hp != 0.0;
   return TC_OK;
+}
+
+// Pipelined host I/O: n_steps independent one-step
+// problems, each from a host state (tc_set_state layout) to a host V^{k+1};
+// the H2D copy of input j+1 (stream s_in) and the D2H copy of output j-1
+// (stream s_out) overlap the compute of step j on the context stream.  Device
+// staging is double-buffered; events order every reuse.  Same arithmetic as
+// tc_set_state + tc_step(1) + tc_get_v per input.
+static tc_status io_setup(tc_ctx* c) {
+  if (c->s_in) return TC_OK;
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->e_loaded[b], cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->e_used[b], cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->e_done[b], cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->e_read[b], cudaEventDisableTiming));
+    CUDA_TRY(c, dalloc(c, &c->d_sin[b], tc_state_len(c)));
+    CUDA_TRY(c, dalloc(c, &c->d_sout[b], c->n));
+  }
+  return TC_OK;
+}
+
+tc_status tc_step_io(tc_ctx* c, int64_t n_steps, const double* states, int64_t stride, double* v_out,
+                     tc_step_stat* stats) {
+  if (!c || n_steps < 0 || !states || !v_out) return TC_EINVAL;
+  if (!c->assembled || c->csr_mode) return fail(c, TC_ESTATE, "tc_step_io before tc_assemble");
+  if (c->use_comm) return fail(c, TC_ESTATE, "tc_step_io: single-process contexts only");
+  const int64_t len = tc_state_len(c), n = c->n;
+  if (stride < len) return fail(c, TC_EINVAL, "tc_step_io: stride shorter than the state");
+  if (n_steps == 0) return TC_OK;
+  for (int64_t j = 0; j < n_steps; ++j) {
+    const double kk = states[j * stride + (2 + c->nstates) * n];
+    if (!(kk >= 0) || kk != std::floor(kk)) return fail(c, TC_EINVAL, "tc_step_io: bad step index in input " + std::to_string(j));
+  }
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  TC_TRY(io_setup(c));
+  TC_TRY(ensure_stats(c, n_steps));
+  auto load = [&](int64_t j) -> tc_status {  // H2D of input j into staging j % 2
+    const int b = (int)(j & 1);
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s_in, c->e_used[b], 0));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_sin[b], states + j * stride, len * 8, cudaMemcpyHostToDevice, c->s_in));
+    CUDA_TRY(c, cudaEventRecord(c->e_loaded[b], c->s_in));
+    return TC_OK;
+  };
+  // every event starts "complete" so the first waits pass
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(c, cudaEventRecord(c->e_used[b], c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->e_read[b], c->s_out));
+  }
+  TC_TRY(load(0));
+  for (int64_t j = 0; j < n_steps; ++j) {
+    const int b = (int)(j & 1);
+    if (j + 1 < n_steps) TC_TRY(load(j + 1));
+    // state j: staging -> internal order (as tc_set_state)
+    CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->e_loaded[b], 0));
+    const double* in = c->d_sin[b];
+    const int iv = c->iVk, ip = c->iVkm1;
+    for (Part& P : c->parts) {
+      CUDA_TRY(c, launch_gather(P.n, c->d_perm_g + P.plan.g0, in, P.d_V[iv], c->stream));
+      CUDA_TRY(c, launch_gather(P.n, c->d_perm_g + P.plan.g0, in + n, P.d_V[ip], c->stream));
+      for (int q = 0; q < c->nstates; ++q)
+        CUDA_TRY(c, launch_gather(P.n, c->d_perm_g + P.plan.g0, in + (2 + q) * n, P.d_U + q * P.n_pad, c->stream));
+    }
+    CUDA_TRY(c, cudaEventRecord(c->e_used[b], c->stream));
+    c->k = (int64_t)states[j * stride + (2 + c->nstates) * n];
+    c->has_prev = states[j * stride + (2 + c->nstates) * n + 1] != 0.0;
+    size_t evi = 0;
+    bool cluster = false;
+    TC_TRY(enqueue_steps(c, 1, c->d_stats + j, false, evi, cluster));
+    // V^{k+1} -> staging (original order) -> host
+    CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->e_read[b], 0));
+    for (Part& P : c->parts)
+      CUDA_TRY(c, launch_scatter(P.n, c->d_perm_g + P.plan.g0, P.d_V[c->iVk], c->d_sout[b], c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->e_done[b], c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s_out, c->e_done[b], 0));
+    CUDA_TRY(c, cudaMemcpyAsync(v_out + j * n, c->d_sout[b], n * 8, cudaMemcpyDeviceToHost, c->s_out));
+    CUDA_TRY(c, cudaEventRecord(c->e_read[b], c->s_out));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->s_out));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s_in));
+  const bool prof = c->prof;
+  c->prof = false;  // the profiling events belong to tc_step
+  tc_status st = finish_steps(c, n_steps, stats, 0, false);
+  c->prof = prof;
+  return st;
 }
 
 // ------------------------------------------------------------------ minimum slice (CSR)

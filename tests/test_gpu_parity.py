@@ -239,6 +239,51 @@ def test_state_injection_one_step(T, engine):
         sim.close()
 
 
+@pytest.mark.parametrize("engine,nparts", [("grid", 1), ("cluster", 1), ("auto", 2)])
+def test_step_io_equals_serial_calls(T, engine, nparts):
+    """tc_step_io (pipelined H2D / step / D2H over copy streams) returns, for every
+    input state, exactly what tc_set_state + tc_step(1) + tc_get_v return; and
+    the first problem matches the oracle's step from the same state."""
+    xyz, tets, region, fib, cond, stims = _slab_case("tt2006", 31, 12, 7, 0.5, permute=True, seed=5)
+    dt = 0.02
+    ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, abs_tol=1e-9, rel_tol=0.0), stims)
+    states = []
+    for k in (100, 150, 200, 250, 300):          # distinct states along an upstroke, has_prev 1
+        ref.run(k - ref.k)
+        states.append(np.concatenate([ref.Vk, ref.Vkm1, ref.U.reshape(-1), [ref.k, 1.0]]))
+    states.append(states[0].copy())
+    states[-1][-1] = 0.0                         # has_prev 0: V^{k-1} := V^k
+    n = xyz.shape[0]
+    cfg = T.tc_config_default(dt=dt, abs_tol=1e-9, rel_tol=0.0, engine=engine, partitions=nparts)
+    sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+    try:
+        serial = []
+        for b in states:
+            sim.set_state(b)
+            sim.step(1)
+            serial.append(sim.V.copy())
+        pad = np.zeros((len(states), len(states[0]) + 3))   # stride > state length
+        pad[:, :len(states[0])] = np.array(states)
+        out = np.zeros((len(states), n))
+        st = T.tc_step_io(sim.ctx, pad, out, want_stats=True)
+        for j in range(len(states)):
+            assert np.array_equal(out[j], serial[j]), j
+        assert (st["iters"] > 0).all()
+        assert np.array_equal(sim.V, serial[-1])     # the context holds the last problem's result
+        ref2 = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, abs_tol=1e-9, rel_tol=0.0), stims)
+        ref2.run(100)
+        ref2.step()
+        assert np.linalg.norm(out[0] - ref2.Vk) / np.linalg.norm(ref2.Vk) <= 1e-8
+        with pytest.raises(ValueError):
+            T.tc_step_io(sim.ctx, pad, np.zeros((len(states), n + 1)))
+        bad = pad.copy()
+        bad[2, len(states[0]) - 2] = 1.5             # non-integer step index
+        with pytest.raises(T.TcError):
+            T.tc_step_io(sim.ctx, bad, out)
+    finally:
+        sim.close()
+
+
 def test_ionic_params_match_oracle_transcription(T):
     """Two independent transcriptions of TT2006 / MS constants agree."""
     for model, names, vals in (("tt2006", O.tt_param_names(), O.tt_default_params()),
