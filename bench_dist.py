@@ -17,7 +17,17 @@ import numpy as np
 
 
 def main(args, w):
+    # every rank runs the host setup (pattern, RCM, partition plan) with OpenMP:
+    # share the host cores between the ranks of this node instead of oversubscribing
+    # (torchrun sets OMP_NUM_THREADS=1 for nproc > 1; an explicit larger value is kept)
+    nloc = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+    nthr = max(1, (os.cpu_count() or 1) // max(1, nloc))
+    if os.environ.get("OMP_NUM_THREADS", "1") == "1":
+        os.environ["OMP_NUM_THREADS"] = str(nthr)
+    else:
+        nthr = int(os.environ["OMP_NUM_THREADS"])
     import torch
+    torch.set_num_threads(nthr)   # the process-wide OpenMP runtime is shared with libtcb200
     import torch.distributed as dist
 
     import bench
