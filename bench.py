@@ -108,23 +108,43 @@ class ClockSampler:
         self.p = None
 
     def __enter__(self):
+        import threading
+        self.lines, self.out = [], ""
+        self.first = threading.Event()
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
+            return self
+
+        def reader():
+            for line in self.p.stdout:
+                self.lines.append(line)
+                self.first.set()
+            self.first.set()
+
+        self.t = threading.Thread(target=reader, daemon=True)
+        self.t.start()
+        self.first.wait(timeout=10.0)   # nvidia-smi is up (its start-up can exceed a short timed region)
+        self.n0 = len(self.lines)       # samples from before the timed region are dropped
         return self
 
     def __exit__(self, *a):
-        self.out = ""
         if self.p is not None:
-            time.sleep(0.25)
+            n_end = len(self.lines)
+            t0 = time.time()
+            while len(self.lines) <= n_end and time.time() - t0 < 1.0:   # one sample after the region
+                time.sleep(0.02)
             self.p.terminate()
             try:
-                self.out, _ = self.p.communicate(timeout=5)
+                self.p.wait(timeout=5)
             except Exception:
                 self.p.kill()
+            self.t.join(timeout=2)
+            kept = self.lines[self.n0:] or self.lines[-1:]
+            self.out = "".join(kept)
 
     def summary(self):
         rows = [r.split(",") for r in self.out.strip().splitlines() if r.count(",") >= 8]

@@ -55,7 +55,10 @@ __device__ __forceinline__ void setup_pipe(SlicePipe& P, char* smem, uint64_t* b
 // DESIGN.md "RHS"), z_0 = r_0 / diag(A), and per-CTA partials of r.z, z.z.
 // Same grid as the PCG kernel that consumes the partials.
 template <int MODE, int VAR>
-__global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : (1024 / TCB_CG_THREADS > 0 ? 1024 / TCB_CG_THREADS : 1)) rhs_kernel(CgArgs a) {
+#ifndef TCB_RHS_BATCH_NB
+#define TCB_RHS_BATCH_NB 16  // slots in flight per row in variant 4's RHS (0: direct loop; measured 16 > 8 > 4 > 0)
+#endif
+__global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : VAR == 4 ? 1 : (1024 / TCB_CG_THREADS > 0 ? 1024 / TCB_CG_THREADS : 1)) rhs_kernel(CgArgs a) {
   constexpr bool TMA = VAR == 1;
   constexpr bool COMP = VAR == 2;
   constexpr bool KEEP = VAR == 3;
@@ -76,7 +79,10 @@ __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : (1024 / T
                if (MODE == 1) {
                  const double* __restrict__ Kv = a.K;
                  const ColIdx ci = col_of<COMP>(a, i, base);
-                 if (KEEP) {
+                 if (VAR == 4 && TCB_RHS_BATCH_NB > 0) {
+                   sum = row_rhs_batch<(TCB_RHS_BATCH_NB > 0 ? TCB_RHS_BATCH_NB : 1)>(base, w, lane, a.col, Av, Kv,
+                                                                                      a.up, a.vp);
+                 } else if (KEEP) {
 #pragma unroll 4
                    for (int k = 0; k < w; ++k) {
                      const int64_t t = sell_slot(base, w, k, lane);

@@ -361,6 +361,32 @@ __device__ __forceinline__ double row_Ap_batch(int64_t base, int w, int lane, co
   return sum;
 }
 
+// r_0 row (A u' - K v') of the latency variant: NB slots in flight at once.
+template <int NB>
+__device__ __forceinline__ double row_rhs_batch(int64_t base, int w, int lane, const int* col,
+                                                const double* A, const double* K, const double* up,
+                                                const double* vp) {
+  double sum = 0.0;
+#pragma unroll 1
+  for (int k0 = 0; k0 < w; k0 += NB) {
+    double av[NB], kv[NB], gu[NB], gv[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int kk = min(k0 + j, w - 1);
+      const int64_t t = sell_slot(base, w, kk, lane);
+      const int c = ld_mat(col + t);
+      av[j] = ld_mat(A + t);
+      kv[j] = ld_mat(K + t);
+      gu[j] = up[c];
+      gv[j] = vp[c];
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (k0 + j < w) sum += av[j] * gu[j] - kv[j] * gv[j];
+  }
+  return sum;
+}
+
 template <bool FIRST, bool KEEP = false>
 __device__ __forceinline__ double row_Ap_direct(int64_t base, int w, int lane, const ColIdx& ci,
                                                 const double* A, const double* z, const double* pold,
