@@ -52,12 +52,27 @@ WORKLOADS = {
     # configs[0]: N-version dx = 0.5 mm (4305 nodes), TT2006 epi, dt 0.05, 40 ms
     "nversion_dx0.5_tt": dict(cfg=0, dims=(41, 15, 7), dx=0.5, model="tt2006", dt=0.05,
                               stim="corner", preroll=0, sample_dims=(41, 15, 7)),
+    # SURVEY 8f row f2 (Fig. 8c/d): surface meshes (P1 triangles in 3-D) with
+    # Mitchell-Schaeffer -- an icosphere of the left-atrium surface's size (660,557 nodes)
+    # and one of the largest cube-surface size (~2 M nodes, Fig. 8c); tangent fibres, cap stimulus
+    "sphere655k_ms": dict(cfg="f2 surface (LA-surface-sized, P:389)", dims=None, level=8, radius=28.0,
+                          dx=0.13, model="ms", dt=0.01, stim="sphere", preroll=500, sample_level=7),
+    "sphere2.6M_ms": dict(cfg="f2 surface (Fig. 8c-sized)", dims=None, level=9, radius=56.0,
+                          dx=0.13, model="ms", dt=0.01, stim="sphere", preroll=500, sample_level=7),
     # a cohort of 100 configs[0]-sized slabs (seeded sizes,
     # numbering, fibres, conductivities, TT2006 parameter resets), one cluster each
     "cohort100_nversion05_tt": dict(cfg="f1 cohort", cohort=100, dims=None, dx=0.5, model="tt2006",
                                     dt=0.05, stim="corner", preroll=40),
 }
 DEFAULT_WORKLOAD = "slab20M_ms"
+
+
+def mesh_desc(w):
+    if w.get("dims"):
+        return list(w["dims"])
+    if w["stim"] == "sphere":
+        return f"icosphere level {w['level']} r={w['radius']} mm (P1 triangles)"
+    return f"BiV h={w['h']} mm"
 
 
 def dist_env():
@@ -71,6 +86,12 @@ def make_inputs(w, dims=None):
         m = G.biv(dims if dims is not None else w["h"])
         stims = [(nodes, 0.0, 2.0, 50.0) for nodes in G.biv_stimuli(m)]
         return m["xyz"], m["tets"], stims, m["region"], m["fibre"]
+    if w["stim"] == "sphere":    # surface mesh: icosphere triangles, stimulus on a 2 mm polar cap
+        level = dims if dims is not None else w["level"]
+        r = w["radius"] * 2.0 ** (level - w["level"])       # samples keep the edge length
+        xyz, tris = G.sphere(level, r)
+        nodes = np.nonzero(xyz[:, 2] >= r - 2.0 * r / w["radius"])[0].astype(np.int32)
+        return xyz, tris, [(nodes, 0.0, 2.0, 50.0)], None, G.sphere_fibres(xyz, tris)
     nx, ny, nz = dims or w["dims"]
     xyz, tets = G.kuhn_box(nx, ny, nz, w["dx"])
     if w["stim"] == "face":      # planar stimulus on x <= 0.3 mm (SURVEY 8d, C5 / C*)
@@ -162,7 +183,7 @@ def oracle_sample(w, max_seconds=20.0):
     """The CPU oracle (as it stands, single thread) on a bounded sample of the workload:
     same dx, dt, model, stimulus style and tolerances on a smaller slab."""
     import oracle as O
-    sample = w.get("sample_h") if w["stim"] == "biv" else w["sample_dims"]
+    sample = {"biv": w.get("sample_h"), "sphere": w.get("sample_level")}.get(w["stim"], w.get("sample_dims"))
     xyz, tets, stims, region, fibre = make_inputs(w, sample)
     E = tets.shape[0]
     cfg = O.Config(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5, max_iters=100)
@@ -180,6 +201,7 @@ def oracle_sample(w, max_seconds=20.0):
     iters = float(np.mean([r.iters for r in sim.reports]))
     return dict(value=n * steps / el, unit="node-steps/s", cores=1, kind="oracle",
                 sample=(f"BiV recipe at h={sample} mm" if w["stim"] == "biv" else
+                        f"icosphere level {sample} (same edge length)" if w["stim"] == "sphere" else
                         f"{sample[0]}x{sample[1]}x{sample[2]} grid") +
                        f" ({n} nodes, same dx/dt/model/stimulus style), first {steps} steps from rest, "
                        f"{el:.1f} s single-thread, mean PCG iters {iters:.1f}")
@@ -281,6 +303,7 @@ def main():
     stream = torch.cuda.current_stream()
     xyz, tets, stims, region, fibre = make_inputs(w)
     E = tets.shape[0]
+    elem_key = "triangles" if tets.shape[1] == 3 else "tets"
     n = xyz.shape[0]
     cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5,
                               max_iters=100, use_rcm=0 if args.no_rcm else 1,
@@ -365,8 +388,8 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.workload, "baseline_config": w["cfg"], "nodes": n, "nnz": nnz,
-                   "tets": int(E), "model": w["model"], "dt_ms": w["dt"], "dx_mm": w["dx"],
-                   "grid": list(w["dims"]) if w["dims"] else f"BiV h={w['h']} mm", "tol": "abs=rel=1e-5, max 100 (P:316)",
+                   elem_key: int(E), "model": w["model"], "dt_ms": w["dt"], "dx_mm": w["dx"],
+                   "grid": mesh_desc(w), "tol": "abs=rel=1e-5, max 100 (P:316)",
                    "rcm": not args.no_rcm, "preroll_steps": preroll, "pcg_variant": info["pcg_variant"],
                    "engine": eng,
                    "wide_slices": info.get("wide_slices"),

@@ -104,7 +104,7 @@ def main(args, w):
             "data": "synthetic",
             "config": {"workload": args.workload, "baseline_config": w["cfg"], "nodes": n,
                        "nnz": int(info["nnz"]), "model": w["model"], "dt_ms": w["dt"],
-                       "dx_mm": w["dx"], "grid": list(w["dims"]) if w["dims"] else f"BiV h={w['h']} mm",
+                       "dx_mm": w["dx"], "grid": bench.mesh_desc(w),
                        "rcm": not args.no_rcm,
                        "preroll_steps": preroll, "parallelism": f"row blocks x{world} ({info['path']} PCG: "
                                       + ("NVLink peer memory" if info["path"] == "peer" else "NCCL") + ")",

@@ -46,7 +46,7 @@ def _split_state(s, n, ns):
     return s[:n].copy(), s[n:2 * n].copy(), s[2 * n:(2 + ns) * n].reshape(ns, n).copy()
 
 
-@pytest.mark.parametrize("name", ["slab20M_ms", "biv3M_tt"])
+@pytest.mark.parametrize("name", ["slab20M_ms", "biv3M_tt", "sphere2.6M_ms"])
 def test_fullsize_assembly_rows_sampled(T, name):
     w, sim, xyz, tets, region, fibre = _bench_sim(T, name, preroll=0)
     try:
@@ -64,7 +64,7 @@ def test_fullsize_assembly_rows_sampled(T, name):
             nodes = tets[e]
             f = (1.0, 0.0, 0.0) if fibre is None else fibre[e]
             sig = O.conductivity_tensor(f, *bench.SIGMA)
-            Me, Ke, _ = O.tet_local(xyz[nodes], sig)
+            Me, Ke, _ = (O.tri_local if tets.shape[1] == 3 else O.tet_local)(xyz[nodes], sig)
             for a, i in enumerate(nodes):
                 if int(i) in accA:
                     ta = (cm * Me[a] + st * Ke[a]) * x[nodes]
@@ -82,7 +82,7 @@ def test_fullsize_assembly_rows_sampled(T, name):
         sim.close()
 
 
-@pytest.mark.parametrize("name", ["slab10M_tt", "slab10M_crn", "slab20M_ms", "biv3M_tt"])
+@pytest.mark.parametrize("name", ["slab10M_tt", "slab10M_crn", "slab20M_ms", "biv3M_tt", "sphere2.6M_ms"])
 def test_fullsize_ionic_update_sampled(T, name):
     """u^{k+1} at sampled nodes after one full-size step equals the oracle's
     per-node update of (V^k, u^k) read back from the GPU."""
