@@ -99,7 +99,9 @@ typedef struct {
                             2 direct loads with 16-bit column offsets, 3 direct loads with
                             the matrix held in L2 (evict-last policy; for systems whose
                             values + indices fit in L2), 4 every slot of a row in flight
-                            at once (latency-bound mid-size systems); -1 (default):
+                            at once (latency-bound mid-size systems), 5 the solve as a CUDA
+                            graph with a device-driven WHILE node (init, S, U, final
+                            kernels; tc_step only); -1 (default):
                             automatic, 4 when the system has at most 4 slices per
                             resident warp of variant 0, else 0 */
   int32_t partitions;    /* row-block partitions of the RCM order held by this context on

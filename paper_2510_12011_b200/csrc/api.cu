@@ -38,6 +38,12 @@ struct Part {
   int64_t n_wide = 0;
   int grid = 1;  // persistent kernel grid (1 part) or split-kernel grid
   int pcg_var = 0;  // PCG kernel variant launched for this part (cg_pick_variant)
+  // graph engine (variant 5)
+  cudaGraphExec_t gexec = nullptr;
+  double2* d_gpart = nullptr;    // S and U partials (2 x grid)
+  GScal* d_gsc = nullptr;
+  GStep* d_gstep = nullptr;
+  unsigned int* d_ticket = nullptr;
   int64_t* d_sp = nullptr;
   int32_t* d_col = nullptr;
   uint16_t* d_col16 = nullptr;
@@ -53,7 +59,7 @@ struct Part {
   double* d_xyz = nullptr;
   uint8_t* d_dir = nullptr;
   double2* d_part = nullptr;
-  unsigned int* d_ticket = nullptr;
+  unsigned int* d_gticket = nullptr;
   double2* d_red = nullptr;
   Scalars* d_sc = nullptr;
   int32_t* d_send_idx = nullptr;
@@ -188,6 +194,11 @@ static cudaError_t upload(tc_ctx* c, T** p, const std::vector<T>& h) {
 }
 
 static void free_all(tc_ctx* c) {
+  for (Part& P : c->parts)
+    if (P.gexec) {
+      cudaGraphExecDestroy(P.gexec);
+      P.gexec = nullptr;
+    }
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   c->ipc_opened.clear();
   for (void* p : c->allocs) cudaFree(p);
@@ -236,7 +247,7 @@ tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx*
   *out = nullptr;
   if (!(cfg->dt > 0) || !(cfg->theta >= 0 && cfg->theta <= 1) || !(cfg->chi > 0) || !(cfg->cm > 0) ||
       cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 ||
-      cfg->model > 3 || cfg->pcg_variant < -1 || cfg->pcg_variant > 4 || cfg->partitions < 1 ||
+      cfg->model > 3 || cfg->pcg_variant < -1 || cfg->pcg_variant > 5 || cfg->partitions < 1 ||
       cfg->partitions > 4096 || cfg->check_every < 1 || cfg->engine < 0 || cfg->engine > 3)
     return TC_EINVAL;
   int ndev = 0;
@@ -846,7 +857,7 @@ static tc_status assemble_host(tc_ctx* c, const std::vector<int32_t>& ereg, std:
       P.grid = split_grid(P.nslices);
     } else {
       P.pcg_var = cg_pick_variant(c->cfg.pcg_variant, P.nslices, c->device);
-      P.grid = cg_grid_size(1, P.pcg_var, P.nslices, c->device);
+      P.grid = P.pcg_var == 5 ? g_grid_size(c->device) : cg_grid_size(1, P.pcg_var, P.nslices, c->device);
     }
     CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
   }
@@ -963,8 +974,42 @@ static tc_status assemble_device(tc_ctx* c, const std::vector<int32_t>& ereg) {
   if (herr == 1) return fail(c, TC_EDEGEN, "assembly: zero-volume element");
   if (herr == 2) return fail(c, TC_EINVAL, "assembly: pattern slot missing (internal)");
   P.pcg_var = cg_pick_variant(c->cfg.pcg_variant, P.nslices, c->device);
-  P.grid = cg_grid_size(1, P.pcg_var, P.nslices, c->device);
+  P.grid = P.pcg_var == 5 ? g_grid_size(c->device) : cg_grid_size(1, P.pcg_var, P.nslices, c->device);
   CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
+  return TC_OK;
+}
+
+// Graph engine (variant 5): scalar block, partials and the instantiated solve graph.
+static tc_status setup_graph(tc_ctx* c, Part& P) {
+  CUDA_TRY(c, dalloc(c, &P.d_gpart, 2 * (int64_t)P.grid));
+  CUDA_TRY(c, dalloc(c, &P.d_gsc, 1));
+  CUDA_TRY(c, dalloc(c, &P.d_gstep, 1));
+  CUDA_TRY(c, dalloc(c, &P.d_gticket, 1));
+  CUDA_TRY(c, cudaMemsetAsync(P.d_gticket, 0, sizeof(unsigned int), c->stream));
+  GArgs a{};
+  a.slice_ptr = P.d_sp;
+  a.col = P.d_col;
+  a.A = P.d_A;
+  a.dinv = P.d_dinv;
+  a.nslices = P.nslices;
+  a.r = P.d_r;
+  a.z = P.d_z;
+  a.q = P.d_q;
+  a.p0 = P.d_p0;
+  a.p1 = P.d_p1;
+  a.part0 = P.d_part;
+  a.n_part0 = P.grid;
+  a.partS = P.d_gpart;
+  a.partU = P.d_gpart + P.grid;
+  a.sc = P.d_gsc;
+  a.gs = P.d_gstep;
+  a.ticket = P.d_gticket;
+  a.flags = c->d_flags;
+  a.eps_a = c->cfg.abs_tol;
+  a.eps_r = c->cfg.rel_tol;
+  a.max_iters = c->cfg.max_iters;
+  a.rel_mode = c->cfg.rel_mode;
+  CUDA_TRY(c, g_build(a, P.grid, &P.gexec));
   return TC_OK;
 }
 
@@ -1061,6 +1106,7 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
     CUDA_TRY(c, upload(c, &c->d_reds, reds));
   }
   if (split_mode(c)) TC_TRY(setup_peer(c, plans));
+  else if (c->parts[0].pcg_var == 5) TC_TRY(setup_graph(c, c->parts[0]));
   int32_t flags[8] = {0, 0, 0, c->cfg.fail_budget, -1, 0, 0, 0};
   CUDA_TRY(c, cudaMemcpyAsync(c->d_flags, flags, sizeof(flags), cudaMemcpyHostToDevice, c->stream));
   TC_TRY(ensure_stats(c, 1024));
@@ -1419,8 +1465,14 @@ static tc_status enqueue_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* dstats, 
       Part& P = c->parts[0];
       CgArgs ca = cg_args(c, P, P.d_V[c->iX]);
       ca.stat = dstats + st;
-      CUDA_TRY(c, launch_pcg(1, P.pcg_var, ca, P.grid, c->stream));
-      c->launches += 2;  // RHS kernel + cooperative PCG kernel
+      if (P.pcg_var == 5) {  // RHS kernel, then the solve graph (init, WHILE{S, U}, final)
+        CUDA_TRY(c, launch_rhs(1, 0, ca, P.grid, c->stream));
+        CUDA_TRY(c, g_launch(P.gexec, P.d_gstep, P.d_V[c->iX], dstats + st, (int32_t)c->k, c->stream));
+        c->launches += 2;    // setstep + RHS; the graph's init, final and S, U per iteration are added in finish_steps
+      } else {
+        CUDA_TRY(c, launch_pcg(1, P.pcg_var, ca, P.grid, c->stream));
+        c->launches += 2;  // RHS kernel + cooperative PCG kernel
+      }
     }
     if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (4) V^{k-1} <- V^k <- x
@@ -1462,6 +1514,8 @@ static tc_status finish_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* stats, si
   CUDA_TRY(c, cudaMemcpyAsync(flags, c->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   if (stats) std::memcpy(stats, hst.data(), nsteps * sizeof(tc_step_stat));
+  if (!cluster && !split_mode(c) && c->parts[0].pcg_var == 5)   // graph engine: init, final, setstep
+    for (int64_t s = 0; s < nsteps; ++s) c->launches += 2 * (int64_t)hst[s].iters + 2;  // + S, U per iteration
   if (c->prof && cluster) {  // one launch: the whole step is attributed to the PCG path
     float a = 0;
     cudaEventElapsedTime(&a, c->evs[0], c->evs[1]);
@@ -1781,6 +1835,7 @@ tc_status tc_csr_upload(tc_ctx* c, int32_t n, int64_t nnz, const int32_t* rowptr
   CUDA_TRY(c, cudaMemcpyAsync(P.d_dinv, dinv.data(), dinv.size() * 8, cudaMemcpyHostToDevice, c->stream));
   TC_TRY(upload_compressed(c, P, hs));
   P.pcg_var = cg_pick_variant(c->cfg.pcg_variant, P.nslices, c->device);
+  if (P.pcg_var == 5) P.pcg_var = 0;   // the graph engine serves tc_step only
   P.grid = cg_grid_size(0, P.pcg_var, P.nslices, c->device);
   CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
   TC_TRY(ensure_stats(c, 1));

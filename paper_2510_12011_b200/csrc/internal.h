@@ -303,7 +303,43 @@ cudaError_t launch_spmv(const int64_t* slice_ptr, const int32_t* col, const doub
 // PCG: mode 0 = plain (r0 = b - A x0), 1 = monodomain RHS (r0 = A u' - K v')
 // variant 0 = direct loads at full occupancy, 1 = TMA-staged matrix stream
 int cg_grid_size(int mode, int variant, int32_t nslices, int device);
+// ---- graph engine (pcg_graph.cu, variant 5): Algorithm 1 as a CUDA graph with a
+// device-driven WHILE node; scalars live in device memory between the kernels
+struct GScal {
+  double rho, zeta, zref, alpha, beta;
+  int32_t it, conv, nan, done, last_valid;
+};
+struct GStep {            // per-step arguments, written by a one-thread kernel before each launch
+  double* x;              // in: x0, out: V^{k+1}
+  tc_step_stat* stat;
+  int32_t tag;
+};
+struct GArgs {
+  const int64_t* slice_ptr;
+  const int32_t* col;
+  const double* A;
+  const double* dinv;
+  int32_t nslices;
+  double *r, *z, *q, *p0, *p1;
+  const double2* part0;   // RHS kernel partials (rho_0, ||z_0||^2)
+  int32_t n_part0;
+  double2* partS;         // S kernel partials (p.q)
+  double2* partU;         // U kernel partials (r.z, z.z)
+  int32_t n_part;         // S / U grid
+  GScal* sc;
+  GStep* gs;
+  unsigned int* ticket;
+  int32_t* flags;
+  double eps_a, eps_r;
+  int32_t max_iters, rel_mode;
+  cudaGraphConditionalHandle cond;
+};
+int g_grid_size(int device);
+cudaError_t g_build(GArgs a, int grid, cudaGraphExec_t* exec);
+cudaError_t g_launch(cudaGraphExec_t exec, GStep* gs, double* x, tc_step_stat* stat, int32_t tag, cudaStream_t s);
+
 int cg_pick_variant(int requested, int32_t nslices, int device);
+cudaError_t launch_rhs(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
 
 // split-phase PCG launchers (pcg_split.cu); grid = split_grid(nslices)

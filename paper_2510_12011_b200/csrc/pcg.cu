@@ -404,6 +404,11 @@ cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStr
                                      pcg_smem(variant), s);
 }
 
+cudaError_t launch_rhs(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s) {
+  void* args[] = {(void*)&a};
+  return cudaLaunchKernel(rhs_fn(mode, variant), dim3(grid), dim3(kCgThreads), args, pcg_smem(variant), s);
+}
+
 cudaError_t launch_spmv(const int64_t* sp, const int32_t* col, const double* A, int32_t ns,
                         const double* x, double* y, cudaStream_t s) {
   int threads = 256;

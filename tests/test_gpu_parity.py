@@ -57,7 +57,7 @@ def test_spmv_parity(T, case):
     assert np.all(np.abs(y - yref) <= 1e-13 * scale)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, -1])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, -1])
 @pytest.mark.parametrize("case,rel_mode", [("fem", 0), ("fem_perm", 1), ("spd", 0), ("big", 0)])
 def test_pcg_parity(T, case, rel_mode, variant):
     if case == "fem":
@@ -104,7 +104,8 @@ def _slab_case(model, nx=21, ny=8, nz=5, dx=0.5, permute=False, seed=0):
                                                         ("ms", True, 0, 1), ("tt2006", False, 1, 1),
                                                         ("tt2006", True, 1, 2), ("crn", False, 1, 0),
                                                         ("crn", True, 1, 1), ("tt2006", True, 1, 3),
-                                                        ("tt2006", True, 1, 4), ("crn", False, 1, 4)])
+                                                        ("tt2006", True, 1, 4), ("crn", False, 1, 4),
+                                                        ("tt2006", True, 1, 5), ("ms", False, 0, 5), ("crn", True, 1, 5)])
 def test_step_trajectory_parity(T, model, permute, rcm, variant):
     """Multi-step trajectory through the real stimulus window (upstroke), V per
     step within rel-L2 1e-8, LAT within one dt, per-step iteration counts equal."""

@@ -113,6 +113,62 @@ __global__ void __launch_bounds__(512, MINB) sell1(const double* __restrict__ A,
   }
 }
 
+// Full S phase of Algorithm 1 as a standalone kernel: per row p = z + beta pold,
+// deferred x += alpha pold, q = A p (gathers of z and pold), pnew / q / x
+// writes and a per-CTA p.q partial.  PAIRS: slot-pair layout (16-byte values).
+template <int MINB, bool PAIRS>
+__global__ void __launch_bounds__(512, MINB) sfull(const double* __restrict__ A, const int* __restrict__ col,
+    const double* __restrict__ z, const double* __restrict__ pold, double* __restrict__ pnew,
+    double* __restrict__ x, double* __restrict__ q, double* __restrict__ part, int nslices, int w,
+    double alpha, double beta) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  double acc = 0.0;
+  for (int s = gw; s < nslices; s += nw) {
+    const size_t base = (size_t)s * w * 32;
+    const size_t i = (size_t)s * 32 + lane;
+    const double po = pold[i];
+    const double pi = z[i] + beta * po;
+    x[i] = x[i] + alpha * po;
+    double sum = 0.0;
+    if (PAIRS) {
+      const double2* A2 = reinterpret_cast<const double2*>(A + base) + lane;
+      const int2* C2 = reinterpret_cast<const int2*>(col + base) + lane;
+#pragma unroll 2
+      for (int j = 0; j < (w >> 1); ++j) {
+        const double2 av = __ldcs(A2 + 32 * j);
+        const int2 c = __ldcs(C2 + 32 * j);
+        sum += av.x * (z[c.x] + beta * pold[c.x]);
+        sum += av.y * (z[c.y] + beta * pold[c.y]);
+      }
+      if (w & 1) {
+        const size_t t = base + 32 * (size_t)(w - 1) + lane;
+        const int c = __ldcs(col + t);
+        sum += __ldcs(A + t) * (z[c] + beta * pold[c]);
+      }
+    } else {
+#pragma unroll 4
+      for (int k = 0; k < w; ++k) {
+        const size_t t = base + (size_t)k * 32 + lane;
+        const int c = __ldcs(col + t);
+        sum += __ldcs(A + t) * (z[c] + beta * pold[c]);
+      }
+    }
+    pnew[i] = pi;
+    q[i] = sum;
+    acc += pi * sum;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double sh[16];
+  if (lane == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+    part[blockIdx.x] = t;
+  }
+}
+
 __global__ void fill_col(int* col, int nslices, int w, int n, int band) {
   size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   size_t tot = (size_t)nslices * w * 32;
@@ -180,14 +236,18 @@ int main() {
   cudaMemset(zp, 0, (size_t)nrows * 16);
   const double alg = (double)nsl * 32 * (w * 12.0 + 8 + 16);  // matrix + q write + z,p once
   auto rep = [&](const char* name, float t) { printf("%-28s %.3f ms  %.0f GB/s algorithmic\n", name, t, alg / t / 1e6); };
-  rep("sell1 unbounded g=4/SM", timeit([&] { sell<<<sms * 4, 512>>>(A, col, z, p, q, nsl, w); }, 10));
-  rep("sell1 minb4 (32 regs)", timeit([&] { sell1<4><<<sms * 4, 512>>>(A, col, z, p, q, nsl, w); }, 10));
-  rep("sell1 minb2 (64 regs)", timeit([&] { sell1<2><<<sms * 2, 512>>>(A, col, z, p, q, nsl, w); }, 10));
-  rep("sell2 minb4", timeit([&] { sell2<4, false><<<sms * 4, 512>>>(A, col, z, p, zp, q, nsl, w); }, 10));
-  rep("sell2 minb2", timeit([&] { sell2<2, false><<<sms * 2, 512>>>(A, col, z, p, zp, q, nsl, w); }, 10));
-  rep("sell2+zp minb4", timeit([&] { sell2<4, true><<<sms * 4, 512>>>(A, col, z, p, zp, q, nsl, w); }, 10));
-  rep("sell2+zp minb2", timeit([&] { sell2<2, true><<<sms * 2, 512>>>(A, col, z, p, zp, q, nsl, w); }, 10));
-  rep("sell2+zp minb3", timeit([&] { sell2<3, true><<<sms * 3, 512>>>(A, col, z, p, zp, q, nsl, w); }, 10));
+  double *pold, *pnew, *x, *part;
+  cudaMalloc(&pold, (size_t)nrows * 8); cudaMalloc(&pnew, (size_t)nrows * 8); cudaMalloc(&x, (size_t)nrows * 8);
+  cudaMalloc(&part, 8192 * 8);
+  cudaMemset(pold, 0, (size_t)nrows * 8); cudaMemset(x, 0, (size_t)nrows * 8);
+  const double algS = (double)nsl * 32 * (w * 12.0 + 48);  // matrix + z, pold, x r/w, pnew, q (S phase bytes)
+  auto repS = [&](const char* name, float t) { printf("%-28s %.3f ms  %.0f GB/s (S-phase bytes)\n", name, t, algS / t / 1e6); };
+  repS("S full plain minb4", timeit([&] { sfull<4, false><<<sms * 4, 512>>>(A, col, z, pold, pnew, x, q, part, nsl, w, 0.5, 0.25); }, 10));
+  repS("S full pairs minb4", timeit([&] { sfull<4, true><<<sms * 4, 512>>>(A, col, z, pold, pnew, x, q, part, nsl, w, 0.5, 0.25); }, 10));
+  repS("S full plain minb3", timeit([&] { sfull<3, false><<<sms * 3, 512>>>(A, col, z, pold, pnew, x, q, part, nsl, w, 0.5, 0.25); }, 10));
+  repS("S full pairs minb3", timeit([&] { sfull<3, true><<<sms * 3, 512>>>(A, col, z, pold, pnew, x, q, part, nsl, w, 0.5, 0.25); }, 10));
+  repS("S full plain minb2", timeit([&] { sfull<2, false><<<sms * 2, 512>>>(A, col, z, pold, pnew, x, q, part, nsl, w, 0.5, 0.25); }, 10));
+  repS("S full pairs minb2", timeit([&] { sfull<2, true><<<sms * 2, 512>>>(A, col, z, pold, pnew, x, q, part, nsl, w, 0.5, 0.25); }, 10));
   cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));
   return 0;
