@@ -2,7 +2,7 @@
 // large single-partition systems as a CUDA graph whose loop is a conditional
 // WHILE node (variant 5):
 //
-//   [init] -> WHILE(continue) { [S] -> [U] } -> [final]
+//   [init] -> [S first] -> [U] -> WHILE(continue) { [S] -> [U] } -> [final]
 //
 //   init : rho_0 = r_0.z_0 and ||z_0|| from the RHS kernel's per-CTA partials;
 //          early exit (reading C4); sets the loop condition.
@@ -81,9 +81,12 @@ __global__ void __launch_bounds__(kGThreads) g_init_kernel(GArgs a) {
   }
 }
 
+// FIRST: the peeled first iteration (p_0 = z_0), outside the WHILE node.
+template <bool FIRST>
 __global__ void __launch_bounds__(kGThreads, TCB_G_MINB) g_S_kernel(GArgs a) {
   __shared__ double2 sh[kGWarps];
   const GScal s = *a.sc;
+  if (s.done) return;   // converged / aborted before the first iteration (uniform)
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * kGWarps + (threadIdx.x >> 5), nw = gridDim.x * kGWarps;
   const int32_t ns = a.nslices;
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(kGThreads, TCB_G_MINB) g_S_kernel(GArgs a) {
   const double* __restrict__ pold = (s.it & 1) ? a.p0 : a.p1;  // p_{it-1}
   const ColIdx ci{a.col, nullptr, nullptr};
   double2 acc = make_double2(0.0, 0.0);
-  if (s.it == 0) {
+  if (FIRST) {
     for (int sl = gw; sl < ns; sl += nw) {
       const int64_t base = __ldg(a.slice_ptr + sl);
       const int w = (int)((__ldg(a.slice_ptr + sl + 1) - base) >> 5);
@@ -126,6 +129,7 @@ __global__ void __launch_bounds__(kGThreads, TCB_G_MINB) g_U_kernel(GArgs a) {
   __shared__ double2 sh[kGWarps];
   __shared__ bool last;
   const GScal s = *a.sc;
+  if (s.done) return;   // only after init's early exit (the peeled first iteration)
   const double pq = sum_parts(a.partS, a.n_part, sh).x;
   const double alpha = s.rho / pq;                               // alpha_k = rho_k / p.q
   const int lane = threadIdx.x & 31;
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(kGThreads) g_final_kernel(GArgs a) {
 
 int g_grid_size(int device) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)g_S_kernel, kGThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)g_S_kernel<false>, kGThreads, 0);
   if (per_sm < 1) per_sm = 1;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -246,17 +250,19 @@ cudaError_t g_build(GArgs a, int grid, cudaGraphExec_t* exec) {
   if (e == cudaSuccess) {
     a.cond = h;
     a.n_part = grid;
-    cudaGraphNode_t n_init, n_loop, n_final, n_S, n_U;
+    cudaGraphNode_t n_init, n_S0, n_U0, n_loop, n_final, n_S, n_U;
     e = add_kernel(&n_init, g, nullptr, 0, (const void*)g_init_kernel, 1, &a);
+    if (e == cudaSuccess) e = add_kernel(&n_S0, g, &n_init, 1, (const void*)g_S_kernel<true>, grid, &a);
+    if (e == cudaSuccess) e = add_kernel(&n_U0, g, &n_S0, 1, (const void*)g_U_kernel, grid, &a);
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = h;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
-    if (e == cudaSuccess) e = cudaGraphAddNode(&n_loop, g, &n_init, 1, &cp);
+    if (e == cudaSuccess) e = cudaGraphAddNode(&n_loop, g, &n_U0, 1, &cp);
     if (e == cudaSuccess) {
       cudaGraph_t body = cp.conditional.phGraph_out[0];
-      e = add_kernel(&n_S, body, nullptr, 0, (const void*)g_S_kernel, grid, &a);
+      e = add_kernel(&n_S, body, nullptr, 0, (const void*)g_S_kernel<false>, grid, &a);
       if (e == cudaSuccess) e = add_kernel(&n_U, body, &n_S, 1, (const void*)g_U_kernel, grid, &a);
     }
     if (e == cudaSuccess) e = add_kernel(&n_final, g, &n_loop, 1, (const void*)g_final_kernel, grid, &a);
