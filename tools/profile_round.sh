@@ -12,6 +12,8 @@ done
 python bench.py --workload nversion_dx0.1_tt --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/${R}_bench_nversion01.json 2>&1
 python bench.py --workload nversion_dx0.5_tt --steps 200 --warmup 5 --no-cpu-baseline > gpurun_out/${R}_bench_nversion05.json 2>&1
 python bench.py --workload cohort100_nversion05_tt --steps 50 --warmup 5 > gpurun_out/${R}_bench_cohort.json 2>&1
+python bench.py --workload sphere655k_ms --steps 50 --warmup 5 > gpurun_out/${R}_bench_sphere655k_ms.json 2>&1
+python bench.py --workload sphere2.6M_ms --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/${R}_bench_sphere2.6M_ms.json 2>&1
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${R}_bench_reference.json 2>&1
 # launch list of the default bench: step kernels only (setup kernels excluded by name);
 # timed region = after the preroll (500 x 3 + 200 stimulus + 1 epilogue) and warmup (5 x 3 + 1)
@@ -40,6 +42,8 @@ ncu --set full --clock-control none --import-source on -k regex:"pcg_kernel|rhs_
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
     --master-port 29517 bench.py --gpus 1 --steps 20 --warmup 5 --dist > gpurun_out/${R}_bench_dist_world1.json \
     2> gpurun_out/${R}_bench_dist_world1.err
+# FP64 instruction counts of the ionic kernels (bench.py's ionic_roofline)
+bash tools/ncu_fp64.sh ${R}
 # cluster engine: one launch of 20 steps of configs[0]
 python tools/run_small.py > gpurun_out/${R}_plain_small.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:cohort -s 1 -c 1 \
