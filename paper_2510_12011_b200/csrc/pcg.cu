@@ -80,8 +80,10 @@ __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : VAR == 4 
                  const double* __restrict__ Kv = a.K;
                  const ColIdx ci = col_of<COMP>(a, i, base);
                  if (VAR == 4 && TCB_RHS_BATCH_NB > 0) {
-                   sum = row_rhs_batch<(TCB_RHS_BATCH_NB > 0 ? TCB_RHS_BATCH_NB : 1)>(base, w, lane, a.col, Av, Kv,
-                                                                                      a.up, a.vp);
+                   sum = (TCB_BATCH_SMALL && w <= 8)
+                             ? row_rhs_batch<8>(base, w, lane, a.col, Av, Kv, a.up, a.vp)
+                             : row_rhs_batch<(TCB_RHS_BATCH_NB > 0 ? TCB_RHS_BATCH_NB : 1)>(base, w, lane, a.col, Av,
+                                                                                             Kv, a.up, a.vp);
                  } else if (KEEP) {
 #pragma unroll 4
                    for (int k = 0; k < w; ++k) {
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
                    [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
                      const double pi = a.z[i];
                      const double sum = staged ? row_Ap_staged<true>(w, lane, As, Cs, a.z, nullptr, 0.0)
-                                      : BATCH ? row_Ap_batch<true, TCB_BATCH_NB>(base, w, lane, col, Av, a.z, nullptr, 0.0)
+                                      : BATCH ? row_Ap_batch_w<true>(base, w, lane, col, Av, a.z, nullptr, 0.0)
                                                : row_Ap_direct<true, KEEP>(base, w, lane, col_of<COMP>(a, i, base), Av, a.z, nullptr, 0.0);
                      pnew[i] = pi;
                      a.q[i] = sum;
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
                      const double pi = a.z[i] + beta * po;
                      a.x[i] = xi + alpha * po;
                      const double sum = staged ? row_Ap_staged<false>(w, lane, As, Cs, a.z, pold, beta)
-                                      : BATCH ? row_Ap_batch<false, TCB_BATCH_NB>(base, w, lane, col, Av, a.z, pold, beta)
+                                      : BATCH ? row_Ap_batch_w<false>(base, w, lane, col, Av, a.z, pold, beta)
                                                : row_Ap_direct<false, KEEP>(base, w, lane, col_of<COMP>(a, i, base), Av, a.z, pold, beta);
                      pnew[i] = pi;
                      a.q[i] = sum;

@@ -361,6 +361,19 @@ __device__ __forceinline__ double row_Ap_batch(int64_t base, int w, int lane, co
   return sum;
 }
 
+// Narrow slices (w <= 8: triangle surface meshes, ~7 slots per row) take a batch
+// of 8 instead of NB (fewer clamped reloads); TCB_BATCH_SMALL = 0 disables.
+#ifndef TCB_BATCH_SMALL
+#define TCB_BATCH_SMALL 1
+#endif
+template <bool FIRST>
+__device__ __forceinline__ double row_Ap_batch_w(int64_t base, int w, int lane, const int* col,
+                                                 const double* A, const double* z, const double* pold,
+                                                 double beta) {
+  if (TCB_BATCH_SMALL && w <= 8) return row_Ap_batch<FIRST, 8>(base, w, lane, col, A, z, pold, beta);
+  return row_Ap_batch<FIRST, TCB_BATCH_NB>(base, w, lane, col, A, z, pold, beta);
+}
+
 // r_0 row (A u' - K v') of the latency variant: NB slots in flight at once.
 template <int NB>
 __device__ __forceinline__ double row_rhs_batch(int64_t base, int w, int lane, const int* col,

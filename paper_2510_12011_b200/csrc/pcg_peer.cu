@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
           const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
           const int64_t i = (int64_t)s * kSellC + lane;
           const double pi = X.z[i];
-          const double sum = BATCH ? row_Ap_batch<true, TCB_BATCH_NB>(base, w, lane, X.col, X.A, X.z, nullptr, 0.0)
+          const double sum = BATCH ? row_Ap_batch_w<true>(base, w, lane, X.col, X.A, X.z, nullptr, 0.0)
                                    : row_Ap_direct<true>(base, w, lane, ci, X.A, X.z, nullptr, 0.0);
           pnew[i] = pi;
           X.q[i] = sum;
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
           const double xi = x[i];
           const double pi = X.z[i] + beta * po;
           x[i] = xi + alpha * po;
-          const double sum = BATCH ? row_Ap_batch<false, TCB_BATCH_NB>(base, w, lane, X.col, X.A, X.z, pold, beta)
+          const double sum = BATCH ? row_Ap_batch_w<false>(base, w, lane, X.col, X.A, X.z, pold, beta)
                                    : row_Ap_direct<false>(base, w, lane, ci, X.A, X.z, pold, beta);
           pnew[i] = pi;
           X.q[i] = sum;

@@ -325,10 +325,11 @@ def test_mms_on_gpu_matches_oracle_and_converges(T):
     assert 1.7 < order < 2.3
 
 
-@pytest.mark.parametrize("model,parts,rot,engine", [("ms", 1, False, "grid"), ("tt2006", 1, True, "cluster"),
-                                                    ("tt2006", 3, False, "auto"), ("ms", 2, True, "auto"),
-                                                    ("ms", 1, True, "cluster")])
-def test_surface_sphere_trajectory_parity(T, model, parts, rot, engine):
+@pytest.mark.parametrize("model,parts,rot,engine,variant", [("ms", 1, False, "grid", -1), ("tt2006", 1, True, "cluster", -1),
+                                                            ("tt2006", 3, False, "auto", -1), ("ms", 2, True, "auto", -1),
+                                                            ("ms", 1, True, "cluster", -1), ("ms", 2, False, "auto", 4),
+                                                            ("tt2006", 1, False, "grid", 0)])
+def test_surface_sphere_trajectory_parity(T, model, parts, rot, engine, variant):
     """Surface (triangle) meshes: an icosphere with tangent
     fibres, two regions, stimulus at one pole; V per step within rel-L2 1e-8,
     LAT within one dt, also under a rigid rotation and on row-block partitions."""
@@ -347,7 +348,8 @@ def test_surface_sphere_trajectory_parity(T, model, parts, rot, engine):
     dt = 0.05
     ref = O.Monodomain(xyz, tris, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0),
                        stims)
-    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, partitions=parts, engine=engine)
+    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-8, rel_tol=0.0, partitions=parts, engine=engine,
+                              pcg_variant=variant)
     sim = T.Monodomain(xyz, tris, region, fib, cond, cfg, stims)
     try:
         for k in range(150):
