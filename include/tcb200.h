@@ -310,9 +310,15 @@ tc_status tc_engine_info(tc_ctx* ctx, int64_t out[4]);
 typedef struct tc_cohort tc_cohort;
 /* members: host array of `count` context pointers (copied).  cluster_size: CTAs
  * per member cluster (1, 2, 4, 8, 16) or 0 = chosen from the largest member.
- * resident: 1 = keep each CTA's matrix block and own-row vectors in shared
- * memory for the whole launch when the largest member's block fits, 0 = stream
- * from global memory.
+ * resident: 0 = stream from global memory; 2 = "full": keep each CTA's matrix
+ * block (values, column indices) and own-row vectors in shared memory for the
+ * whole launch when the largest member's block fits; 3 = "compact": keep only
+ * the column indices and the vectors there (the matrix values are read through
+ * L2), a smaller footprint; 1 = automatic: compact when it keeps more clusters
+ * resident than full and the members outnumber the full-mode clusters, else
+ * full.  A mode whose footprint does not fit falls back to streaming
+ * (tc_cohort_info reports what was chosen).
+ * TC_EINVAL if resident is outside 0..3.
  * TC_ESTATE if a member is not assembled or is partitioned / multi-GPU;
  * TC_EINVAL on mixed devices or models, MMS members, or a bad cluster size. */
 tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluster_size,
@@ -325,8 +331,11 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
  * TC_ENAN naming the first such member, after all members were advanced. */
 tc_status tc_cohort_step(tc_cohort* cohort, int64_t n_steps, tc_step_stat* stats);
 /* out[0] members, out[1] CTAs per cluster, out[2] clusters resident at once,
- * out[3] dynamic shared memory per CTA (0 = streaming). */
-tc_status tc_cohort_info(const tc_cohort* cohort, int32_t out[4]);
+ * out[3] dynamic shared memory per CTA (0 = streaming), out[4] 1 when the
+ * resident launch keeps only the column indices (and vectors) in shared
+ * memory and reads the matrix values through L2 (chosen when that keeps more
+ * clusters resident and the members outnumber the full-resident clusters). */
+tc_status tc_cohort_info(const tc_cohort* cohort, int32_t out[5]);
 const char* tc_cohort_last_error(const tc_cohort* cohort);
 tc_status tc_cohort_destroy(tc_cohort* cohort);
 

@@ -337,7 +337,7 @@ def tc_engine_info(ctx) -> dict:
 
 
 # ---------------------------------------------------------------- cohorts
-def tc_cohort_create(members, cluster_size: int = 0, resident: bool = True):
+def tc_cohort_create(members, cluster_size: int = 0, resident: int = 1):
     """members: contexts (assembled, single partition, same device and model)."""
     arr = (C.c_void_p * len(members))(*[m.value if isinstance(m, C.c_void_p) else m for m in members])
     out = C.c_void_p()
@@ -362,12 +362,12 @@ def tc_cohort_step(co, n_steps: int, count: int | None = None, want_stats: bool 
 
 
 def tc_cohort_info(co) -> dict:
-    out = np.zeros(4, np.int32)
+    out = np.zeros(5, np.int32)
     st = _L.tc_cohort_info(co, _ptr(out))
     if st != TC_OK:
         raise TcError(st, "tc_cohort_info")
     return dict(members=int(out[0]), cluster_size=int(out[1]), resident_clusters=int(out[2]),
-                smem_per_cta=int(out[3]))
+                smem_per_cta=int(out[3]), compact=bool(out[4]))
 
 
 def tc_cohort_last_error(co) -> str:
@@ -511,7 +511,7 @@ class Cohort:
     """Owning wrapper over tc_cohort_*: ``Cohort([Monodomain, ...])``; the members
     stay usable (``m.V``, ``m.activation()``) and must outlive the cohort."""
 
-    def __init__(self, members, cluster_size: int = 0, resident: bool = True):
+    def __init__(self, members, cluster_size: int = 0, resident: int = 1):
         self.members = list(members)
         self.co = tc_cohort_create([m.ctx for m in self.members], cluster_size, resident)
 

@@ -1953,6 +1953,7 @@ struct tc_cohort {
   std::vector<tc_ctx*> m;
   int device = 0, model = 0, csize = 1;
   size_t smem = 0;                 // dynamic shared memory per CTA (0 = streaming)
+  bool compact = false;            // resident launch with only the column indices in shared memory
   cudaStream_t stream = nullptr;
   cudaEvent_t ev = nullptr;
   std::string err;
@@ -2036,14 +2037,33 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
     delete co;
     return fail(m0, TC_EINVAL, "cohort: the device cannot run clusters of the requested size");
   }
+  if (resident < 0 || resident > 3) {
+    delete co;
+    return fail(m0, TC_EINVAL, "cohort: resident must be 0..3");
+  }
   if (resident) {  // cluster-resident when the largest member block fits
-    size_t need = 0;
+    // full: matrix values, indices and vectors in shared memory; compact: indices
+    // and vectors only (A, K read through L2) -- a smaller footprint that keeps more
+    // clusters resident when the members outnumber those that fit in full mode
+    size_t need = 0, need_c = 0;
     for (int i : co->small) {
       const tc_ctx* c = co->m[i];
       need = std::max(need, cohort_smem_bytes(c->parts[0].h_sp.data(), c->parts[0].nslices, co->csize));
+      need_c = std::max(need_c, cohort_smem_bytes(c->parts[0].h_sp.data(), c->parts[0].nslices, co->csize, true));
     }
-    if (need <= cohort_smem_limit(co->model) && cohort_active_clusters(co->model, co->csize, need) > 0)
+    const size_t lim = cohort_smem_limit(co->model);
+    const int ncl = need <= lim ? cohort_active_clusters(co->model, co->csize, need) : 0;
+    const int ncl_c = need_c <= lim ? cohort_active_clusters(co->model, co->csize, need_c) : 0;
+    // resident 1: automatic; 2: full only; 3: compact only (each falls back to streaming)
+    const bool use_c = resident == 3 ? ncl_c > 0
+                     : resident == 2 ? false
+                     : (ncl_c > ncl && (int64_t)co->small.size() > ncl);
+    if (use_c) {
+      co->smem = need_c;
+      co->compact = true;
+    } else if (ncl > 0) {
       co->smem = need;
+    }
   }
   if (cudaEventCreateWithFlags(&co->ev, cudaEventDisableTiming) != cudaSuccess ||
       co_alloc(co, &co->d_reps, count) != cudaSuccess || co_alloc(co, &co->d_status, count) != cudaSuccess) {
@@ -2077,6 +2097,7 @@ tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
     if (make_corep(c, co->h[j], co->d_stats + (int64_t)i * nsteps) != TC_OK)
       return cfail(co, TC_ECUDA, "cohort member " + std::to_string(i) + ": " + c->err);
     co->h[j].status = co->d_status + i;
+    co->h[j].compact = co->compact ? 1 : 0;
   }
   if (ns_small > 0) {
     // order after every member's pending work
@@ -2124,12 +2145,13 @@ tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
   return TC_OK;
 }
 
-tc_status tc_cohort_info(const tc_cohort* co, int32_t out[4]) {
+tc_status tc_cohort_info(const tc_cohort* co, int32_t out[5]) {
   if (!co || !out) return TC_EINVAL;
   out[0] = (int32_t)co->m.size();
   out[1] = co->csize;
   out[2] = cohort_active_clusters(co->model, co->csize, co->smem);
   out[3] = (int32_t)co->smem;
+  out[4] = co->compact ? 1 : 0;
   return TC_OK;
 }
 

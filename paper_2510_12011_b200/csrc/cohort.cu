@@ -182,19 +182,23 @@ __global__ void __launch_bounds__(kCoThreads, 1)
   uint32_t vbase = 0;  // RES: this CTA's vector block in its own shared window
   if (RES) {
     // layout (cohort_smem_bytes): kNVec vectors x rpc | slice offsets | pad | A K col [tn]
+    // (compact: col [tn] only; A and K stay in global memory and are read through L2)
     double* sv = reinterpret_cast<double*>(dsm);
     int64_t* ssp = reinterpret_cast<int64_t*>(sv + (size_t)kNVec * rpc);
     const size_t moff = ((size_t)kNVec * rpc * 8 + (size_t)(spc + 1) * 8 + 127) & ~(size_t)127;
+    const bool cmp = R.compact != 0;
     double* sA = reinterpret_cast<double*>(dsm + moff);
     double* sK = sA + tn;
-    int* sC = reinterpret_cast<int*>(sK + tn);
+    int* sC = cmp ? reinterpret_cast<int*>(dsm + moff) : reinterpret_cast<int*>(sK + tn);
     if (threadIdx.x == 0 && tn > 0) {
       mbar_init(&mbar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       const uint64_t pol = policy_evict_first();
-      mbar_expect_tx(&mbar, (uint32_t)(tn * 20));
-      tma_load(sA, R.A + t0, (uint32_t)(tn * 8), &mbar, pol);
-      tma_load(sK, R.K + t0, (uint32_t)(tn * 8), &mbar, pol);
+      mbar_expect_tx(&mbar, (uint32_t)(tn * (cmp ? 4 : 20)));
+      if (!cmp) {
+        tma_load(sA, R.A + t0, (uint32_t)(tn * 8), &mbar, pol);
+        tma_load(sK, R.K + t0, (uint32_t)(tn * 8), &mbar, pol);
+      }
       tma_load(sC, R.col + t0, (uint32_t)(tn * 4), &mbar, pol);
     }
     if ((int)threadIdx.x < C) cbase[threadIdx.x] = map_rank(sv, (int)threadIdx.x);
@@ -215,8 +219,10 @@ __global__ void __launch_bounds__(kCoThreads, 1)
       sC[j] = (o << kOwnerShift) | (c - o * rpc);
     }
     // pointers offset so that global slot / row indices address the shared copies
-    Av = sA - t0;
-    Kv = sK - t0;
+    if (!cmp) {
+      Av = sA - t0;
+      Kv = sK - t0;
+    }
     col = sC - t0;
     sp = ssp - s0;
     for (int b = 0; b < 3; ++b) Vb[b] = sv + (size_t)b * rpc - row0;
@@ -568,7 +574,7 @@ void cohort_pack_params(int model, const TTParams& tp, const MSParams& mp, const
 
 // Shared memory a cluster-resident launch needs for a replica with slice
 // pointers sp[0..ns] cut into C blocks (the largest block decides).
-size_t cohort_smem_bytes(const int64_t* sp, int32_t ns, int C) {
+size_t cohort_smem_bytes(const int64_t* sp, int32_t ns, int C, bool compact) {
   const int spc = (ns + C - 1) / C;
   if ((int64_t)spc * kSellC >= (1 << kOwnerShift)) return (size_t)1 << 40;  // packed columns overflow
   const size_t moff = ((size_t)kNVec * spc * kSellC * 8 + (size_t)(spc + 1) * 8 + 127) & ~(size_t)127;
@@ -577,7 +583,7 @@ size_t cohort_smem_bytes(const int64_t* sp, int32_t ns, int C) {
     const int s0 = std::min(ns, r * spc), s1 = std::min(ns, s0 + spc);
     tmax = std::max(tmax, (size_t)(sp[s1] - sp[s0]));
   }
-  return moff + tmax * 20;
+  return moff + tmax * (compact ? 4 : 20);
 }
 
 // Largest dynamic shared memory a cluster-resident launch may use.

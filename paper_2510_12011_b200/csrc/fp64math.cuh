@@ -2,8 +2,8 @@
 // kernels.  The CUDA math library versions carry
 // special-case branches and materialise their 64-bit constants through uniform
 // registers (~20 % of the TT2006 kernel's instructions were UMOV); these
-// versions keep the FP64 pipe busy instead.  Accuracy ~1 ulp over the range
-// the cell models use (|x| < 700); NaN propagates (blow-up detection).
+// versions keep the FP64 pipe busy instead.  Accuracy ~1 ulp for |x| < 708;
+// below, 0 (exp_range).
 #pragma once
 
 #include <cstdint>
@@ -26,6 +26,21 @@ struct Exp2Table {
 __device__ __forceinline__ void exp2_table_init(Exp2Table* T) {
   for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) T->t[j] = exp2((double)j / kExpTab);
   __syncthreads();
+}
+
+// Range.  The scale 2^m is added to the exponent field of v = 2^(j/N) P(r),
+// which wraps for x < -708 (into the sign bit: the TT2006 m gate near -99 mV at
+// dt 0.05 gave -1e300, Rush-Larsen e^{-dt/tau} with tiny tau) and, for
+// |x| > 2.3e7 (V ~ -150 mV at dt 0.1), the integer m itself overflows.  So
+// anything but x >= -708 returns 0 (one FP64 compare and two selects, the cost
+// the former NaN test had) and m is clamped to <= 1023 (integer min; above
+// x ~ 709.8 a finite value below 2^1024 instead of inf).  Accepted: e^x for
+// -745 < x < -708 is 0 instead of a denormal (< 3.3e-308); NaN x gives 0 (a NaN
+// state still reaches the currents directly -- y in yinf - (yinf - y) e^x, V in
+// g (V - E) -- and the PCG NaN test); x > 2.3e7 is not handled.
+__device__ __forceinline__ double exp_range(double x, double v, int m) {
+  const double s = __hiloint2double(__double2hiint(v) + (min(m, 1023) << 20), __double2loint(v));
+  return x >= -708.0 ? s : 0.0;
 }
 
 // e^x = 2^m 2^(j/N) P(r),  x = (N m + j) ln2/N + r,  |r| <= ln2/(2N) (Cody-Waite);
@@ -58,8 +73,7 @@ __device__ __forceinline__ double tc_exp(double x, const Exp2Table* __restrict__
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const double v = T->t[k & 63] * p;
-  const double s = __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
-  return (x != x) ? x : s;
+  return exp_range(x, v, k >> 6);
 #else
   const double kInvLn2_32 = 46.16624130844683;          // 32 / ln 2
   const double kLn2_32_hi = 0.02166084938653512;        // (ln 2)_hi / 32, 32 significant bits
@@ -77,8 +91,7 @@ __device__ __forceinline__ double tc_exp(double x, const Exp2Table* __restrict__
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const double v = T->t[k & 31] * p;
-  const double s = __hiloint2double(__double2hiint(v) + ((k >> 5) << 20), __double2loint(v));
-  return (x != x) ? x : s;
+  return exp_range(x, v, k >> 5);
 #endif
 }
 

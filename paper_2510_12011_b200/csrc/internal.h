@@ -271,7 +271,8 @@ struct CoRep {
   const int32_t* stim_idx;
   const double* stim_s;
   int32_t n_ep;
-  int32_t iVk, iVkm1, iX, has_prev, max_iters, rel_mode, pad;
+  int32_t iVk, iVkm1, iX, has_prev, max_iters, rel_mode;
+  int32_t compact;               // resident launch: 1 = only column indices in shared memory (A, K from L2)
   int64_t k0;
   double dt, theta, eps_a, eps_r, lat_thr, lrt_thr;
   const double* params;          // cohort_pack_params block (device)
@@ -281,7 +282,7 @@ void cohort_pack_params(int model, const TTParams& tp, const MSParams& mp, const
                         double* out);
 int cohort_cluster_size(int model, int want);
 int cohort_active_clusters(int model, int csize, size_t smem);  // smem 0 = streaming launch
-size_t cohort_smem_bytes(const int64_t* sp, int32_t ns, int C);
+size_t cohort_smem_bytes(const int64_t* sp, int32_t ns, int C, bool compact = false);
 size_t cohort_smem_limit(int model);
 // smem > 0: cluster-resident launch with that much dynamic shared memory per CTA
 cudaError_t launch_cohort(int model, const CoRep* d_reps, int nrep, int csize, size_t smem,

@@ -150,7 +150,7 @@ COHORT = [
 ]
 
 
-@pytest.mark.parametrize("cluster_size,resident", [(0, True), (1, False), (4, True), (4, False), (16, True)])
+@pytest.mark.parametrize("cluster_size,resident", [(0, 1), (1, 0), (4, 1), (4, 0), (16, 1), (4, 2), (4, 3), (8, 3)])
 def test_cohort_parity(T, cluster_size, resident):
     """A heterogeneous cohort (meshes of 8 .. ~5k nodes, structured and BiV, other
     dt / tolerances / conductivities / ionic parameters / stimuli) advanced in
@@ -168,6 +168,10 @@ def test_cohort_parity(T, cluster_size, resident):
             assert info["members"] == len(COHORT)
             if not resident:
                 assert info["smem_per_cta"] == 0
+            if resident == 2:
+                assert not info["compact"]
+            if resident == 3:   # indices-only residency fits every member of this cohort
+                assert info["compact"] and info["smem_per_cta"] > 0
             if cluster_size:
                 assert info["cluster_size"] == cluster_size
             assert info["resident_clusters"] >= 1
@@ -272,6 +276,9 @@ def test_cohort_errors(T):
             T.Cohort([a, a])                       # repeated member
         with pytest.raises(T.TcError):
             T.Cohort([a], cluster_size=3)          # not a power of two
+        with pytest.raises(T.TcError) as ei:
+            T.Cohort([a], resident=4)              # no such residency mode
+        assert ei.value.status == T.TC_EINVAL
     finally:
         for s in (a, b, p):
             s.close()

@@ -240,6 +240,69 @@ def test_state_injection_one_step(T, engine):
         sim.close()
 
 
+@pytest.mark.parametrize("model,engine,dt", [("tt2006", "grid", 0.05), ("tt2006", "cluster", 0.1),
+                                             ("crn", "grid", 0.05), ("crn", "cluster", 0.1),
+                                             ("ms", "grid", 0.05)])
+def test_ionic_voltage_range_one_step(T, model, engine, dt):
+    """One step from an injected state whose V^k spans -130 .. +70 mV node by node
+    (plus exact points around the TT2006 m-gate underflow, V ~ -99 mV at dt 0.05,
+    where the Rush-Larsen factor e^{-dt/tau_m} drops below e^{-708}): every gate
+    and concentration equals the oracle's libm-exp update, V^{k+1} the oracle's.
+    A cohort member reached V = -98.9 mV after 394 steps and the fast exp wrapped
+    there (regression)."""
+    xyz, tets, region, fib, cond, stims = _slab_case(model, 21, 8, 5, 0.5, permute=True, seed=3)
+    n = xyz.shape[0]
+    rng = np.random.default_rng(11)
+    V = rng.uniform(-130.0, 70.0, n)
+    V[:8] = [-99.0, -98.93, -100.0, -105.0, -110.0, -120.0, -130.0, -150.0]
+    init = {"tt2006": O.tt_initial_state, "crn": O.crn_initial_state,
+            "ms": lambda m: O.ms_initial_state(m)}[model]
+    _, U = init(n)
+    U = np.ascontiguousarray(U, dtype=np.float64).reshape(-1, n)
+    ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, model=model, abs_tol=1e-9, rel_tol=0.0),
+                       stims)
+    ref.set_state(V, V, U, 60)
+    buf = np.concatenate([V, V, U.reshape(-1), [60, 1.0]])
+    cfg = T.tc_config_default(dt=dt, model=model, abs_tol=1e-9, rel_tol=0.0, engine=engine)
+    sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+    try:
+        sim.set_state(buf)
+        sim.step(1)
+        ref.step()
+        ns = U.shape[0]
+        s = sim.get_state()
+        U1 = s[2 * n:(2 + ns) * n].reshape(ns, n)
+        assert np.all(np.isfinite(s))
+        assert np.allclose(U1, ref.U.reshape(ns, n), rtol=1e-10, atol=1e-14)
+        v = sim.V
+        assert np.linalg.norm(v - ref.Vk) / np.linalg.norm(ref.Vk) <= 1e-8
+    finally:
+        sim.close()
+
+
+@pytest.mark.parametrize("engine,where", [("grid", "V"), ("cluster", "V"), ("grid", "gate"), ("cluster", "gate")])
+def test_blow_up_is_reported(T, engine, where):
+    """A non-finite value in V^k or in one gate of one node makes tc_step fail
+    with TC_ENAN ("NaN detected in any inner product"), and the context then
+    refuses further steps."""
+    xyz, tets, region, fib, cond, stims = _slab_case("tt2006", 13, 6, 4, 0.5)
+    n = xyz.shape[0]
+    cfg = T.tc_config_default(dt=0.05, engine=engine)
+    sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+    try:
+        sim.step(2)
+        buf = sim.get_state()
+        buf[n // 2 if where == "V" else 2 * n + 6 * n + n // 3] = np.nan   # V or the m gate
+        sim.set_state(buf)
+        with pytest.raises(T.TcError) as ei:
+            sim.step(3)
+        assert ei.value.status == T.TC_ENAN
+        with pytest.raises(T.TcError):
+            sim.step(1)
+    finally:
+        sim.close()
+
+
 @pytest.mark.parametrize("engine,nparts", [("grid", 1), ("cluster", 1), ("auto", 2)])
 def test_step_io_equals_serial_calls(T, engine, nparts):
     """tc_step_io (pipelined H2D / step / D2H over copy streams) returns, for every
