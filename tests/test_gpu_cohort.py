@@ -307,3 +307,44 @@ def test_cohort_mixes_small_and_large_members(T):
     finally:
         for s in members:
             s.close()
+
+
+def test_cohort_long_horizon_bench_members(T):
+    """The bench's cohort members 8 and 1 (meshgen.cohort_members, seeded; the
+    ones whose trajectories undershoot to V ~ -99 mV, where the fast exp once
+    wrapped: DESIGN.md "Exp range") advanced 450 steps (22.5 ms, past the
+    first repolarisation undershoot) in one cohort, each against its own oracle
+    run every 50 steps with the north_star tolerances."""
+    ms = G.cohort_members(100, seed=G.SEED)
+    members, refs = [], []
+    try:
+        for i in (8, 1):
+            m = ms[i]
+            E = m["tets"].shape[0]
+            cond = {0: (SIG[0] * m["sigma_scale"], SIG[1] * m["sigma_scale"])}
+            stims = [O.Stimulus(m["stim_nodes"], 0.0, 2.0, 50.0)]
+            names, params = O.tt_param_names(), O.tt_default_params().copy()
+            for k, f in m["param_factors"].items():
+                params[names.index(k)] *= f
+            spec = dict(params={k: params[names.index(k)] for k in m["param_factors"]})
+            region = np.zeros(E, np.int32)
+            refs.append(O.Monodomain(m["xyz"], m["tets"], region, m["fibre"], cond,
+                                     O.Config(dt=0.05, abs_tol=1e-8, rel_tol=0.0, params=params), stims))
+            members.append(_gpu(T, spec, m["xyz"], m["tets"], region, m["fibre"], cond, stims))
+        co = T.Cohort(members)
+        vmin = np.inf
+        try:
+            for c in range(9):
+                stats = co.step(50)
+                for j, (sim, ref) in enumerate(zip(members, refs)):
+                    reps = []
+                    for _ in range(50):
+                        reps.append(ref.step())
+                        vmin = min(vmin, float(ref.Vk.min()))
+                    _check(sim, ref, stats[j], reps, 0.05, f"member {j} chunk {c}")
+            assert vmin < -98.0   # member 8 reaches -98.93 mV at step 394
+        finally:
+            co.close()
+    finally:
+        for s in members:
+            s.close()

@@ -28,10 +28,10 @@ def bench_members(T, sid):
     return sims
 
 
-def run(T, torch, stream, label, make_members):
+def run(T, torch, stream, label, make_members, grid=((2, 4, 8, 16), (0, 2, 3))):
     """Fresh members for every (cluster size, mode): the same simulated interval."""
-    for cs in (2, 4, 8, 16):
-        for res in (0, 2, 3):
+    for cs in grid[0]:
+        for res in grid[1]:
             mem = make_members()
             nodes = sum(T.tc_num_nodes(m.ctx) for m in mem)
             try:
@@ -56,10 +56,11 @@ def main():
     import paper_2510_12011_b200 as T
     stream = torch.cuda.current_stream()
     sid = stream.cuda_stream
-    for cnt in (74, 148):
+    grid = ((1, 2, 4, 8, 16), (1,)) if "--small" in sys.argv else ((2, 4, 8, 16), (0, 2, 3))
+    for cnt in ((16, 74, 148) if "--small" in sys.argv else (74, 148)):
         run(T, torch, stream, f"configs0 x{cnt}",
-            lambda: [E.make(T, (41, 15, 7), 0.5, "tt2006", 0.05, "cluster", sid)[0] for _ in range(cnt)])
-    run(T, torch, stream, "cohort100", lambda: bench_members(T, sid))
+            lambda: [E.make(T, (41, 15, 7), 0.5, "tt2006", 0.05, "cluster", sid)[0] for _ in range(cnt)], grid)
+    run(T, torch, stream, "cohort100", lambda: bench_members(T, sid), grid)
 
 
 if __name__ == "__main__":
