@@ -309,7 +309,9 @@ tc_status tc_engine_info(tc_ctx* ctx, int64_t out[4]);
  * members must not be stepped concurrently with tc_cohort_step. */
 typedef struct tc_cohort tc_cohort;
 /* members: host array of `count` context pointers (copied).  cluster_size: CTAs
- * per member cluster (1, 2, 4, 8, 16) or 0 = chosen from the largest member.
+ * per member cluster (1, 2, 4, 8, 16) or 0 = automatic: one SELL slice per warp
+ * for the largest member, reduced to the largest size whose resident clusters
+ * hold every member at once (one wave), else 2.
  * resident: 0 = stream from global memory; 2 = "full": keep each CTA's matrix
  * block (values, column indices) and own-row vectors in shared memory for the
  * whole launch when the largest member's block fits; 3 = "compact": keep only

@@ -2027,44 +2027,66 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
   co->device = m0->device;
   co->model = m0->cfg.model;
   co->stream = m0->stream;
-  // auto: one slice per warp where possible; when the members outnumber the clusters of
-  // that size that fit at once, halve the size (more members in flight; measured on the
-  // configs[0] cohort: 16 CTAs 0.39, 8 CTAs 0.69 G node-steps/s at 74 members)
-  int want = cluster_size ? cluster_size : cluster_want(max_slices);
-  if (!cluster_size && want > 8 && (int64_t)co->small.size() > cohort_active_clusters(co->model, want, 0)) want = 8;
+  if (resident < 0 || resident > 3) {
+    delete co;
+    return fail(m0, TC_EINVAL, "cohort: resident must be 0..3");
+  }
+  // Residency for cluster size C (the largest small member decides); returns the
+  // clusters resident at once.  full: matrix values, indices and vectors in shared
+  // memory; compact: indices and vectors only (A, K read through L2) -- a smaller
+  // footprint that keeps more clusters resident when the members outnumber those
+  // that fit in full mode.  resident 1: automatic; 2: full only; 3: compact only
+  // (each falls back to streaming).
+  auto plan = [&](int C, size_t* smem, bool* compact) -> int {
+    *smem = 0;
+    *compact = false;
+    if (resident) {
+      size_t need = 0, need_c = 0;
+      for (int i : co->small) {
+        const tc_ctx* c = co->m[i];
+        need = std::max(need, cohort_smem_bytes(c->parts[0].h_sp.data(), c->parts[0].nslices, C));
+        need_c = std::max(need_c, cohort_smem_bytes(c->parts[0].h_sp.data(), c->parts[0].nslices, C, true));
+      }
+      const size_t lim = cohort_smem_limit(co->model);
+      const int ncl = need <= lim ? cohort_active_clusters(co->model, C, need) : 0;
+      const int ncl_c = need_c <= lim ? cohort_active_clusters(co->model, C, need_c) : 0;
+      const bool use_c = resident == 3 ? ncl_c > 0
+                       : resident == 2 ? false
+                       : (ncl_c > ncl && (int64_t)co->small.size() > ncl);
+      if (use_c) {
+        *smem = need_c;
+        *compact = true;
+      } else if (ncl > 0) {
+        *smem = need;
+      }
+    }
+    return cohort_active_clusters(co->model, C, *smem);
+  };
+  // auto size: one slice per warp where possible (want), then the largest C <= want
+  // whose resident clusters hold every small member at once (one wave), else 2.
+  // Measured (profiles/r01g_exp_cohort_cluster_size.txt, configs[0]-sized TT2006
+  // members, ms/step for C = 1/2/4/8/16): 16 members 0.51/0.29/0.15/0.18/0.23,
+  // 74 members 0.60/0.35/0.44/0.46/0.83, 148 members 0.88/0.65/0.74/0.92/1.65;
+  // cohort100 0.94/0.64/0.63/0.70/1.04.  C = 1 (no cluster) is never faster.
+  const int want = cluster_size ? cluster_size : cluster_want(max_slices);
   co->csize = cohort_cluster_size(co->model, want);
   if (co->csize == 0 || (cluster_size && co->csize != cluster_size)) {
     delete co;
     return fail(m0, TC_EINVAL, "cohort: the device cannot run clusters of the requested size");
   }
-  if (resident < 0 || resident > 3) {
-    delete co;
-    return fail(m0, TC_EINVAL, "cohort: resident must be 0..3");
-  }
-  if (resident) {  // cluster-resident when the largest member block fits
-    // full: matrix values, indices and vectors in shared memory; compact: indices
-    // and vectors only (A, K read through L2) -- a smaller footprint that keeps more
-    // clusters resident when the members outnumber those that fit in full mode
-    size_t need = 0, need_c = 0;
-    for (int i : co->small) {
-      const tc_ctx* c = co->m[i];
-      need = std::max(need, cohort_smem_bytes(c->parts[0].h_sp.data(), c->parts[0].nslices, co->csize));
-      need_c = std::max(need_c, cohort_smem_bytes(c->parts[0].h_sp.data(), c->parts[0].nslices, co->csize, true));
+  if (!cluster_size && co->csize > 2) {
+    int pick = 2;
+    for (int C = co->csize; C > 2; C >>= 1) {
+      size_t sm;
+      bool cp;
+      if (cohort_cluster_size(co->model, C) == C && plan(C, &sm, &cp) >= (int64_t)co->small.size()) {
+        pick = C;
+        break;
+      }
     }
-    const size_t lim = cohort_smem_limit(co->model);
-    const int ncl = need <= lim ? cohort_active_clusters(co->model, co->csize, need) : 0;
-    const int ncl_c = need_c <= lim ? cohort_active_clusters(co->model, co->csize, need_c) : 0;
-    // resident 1: automatic; 2: full only; 3: compact only (each falls back to streaming)
-    const bool use_c = resident == 3 ? ncl_c > 0
-                     : resident == 2 ? false
-                     : (ncl_c > ncl && (int64_t)co->small.size() > ncl);
-    if (use_c) {
-      co->smem = need_c;
-      co->compact = true;
-    } else if (ncl > 0) {
-      co->smem = need;
-    }
+    co->csize = cohort_cluster_size(co->model, pick);
   }
+  plan(co->csize, &co->smem, &co->compact);
   if (cudaEventCreateWithFlags(&co->ev, cudaEventDisableTiming) != cudaSuccess ||
       co_alloc(co, &co->d_reps, count) != cudaSuccess || co_alloc(co, &co->d_status, count) != cudaSuccess) {
     tc_cohort_destroy(co);

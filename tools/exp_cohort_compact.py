@@ -56,7 +56,7 @@ def main():
     import paper_2510_12011_b200 as T
     stream = torch.cuda.current_stream()
     sid = stream.cuda_stream
-    grid = ((1, 2, 4, 8, 16), (1,)) if "--small" in sys.argv else ((2, 4, 8, 16), (0, 2, 3))
+    grid = ((0, 1, 2, 4, 8, 16), (1,)) if "--small" in sys.argv else ((2, 4, 8, 16), (0, 2, 3))
     for cnt in ((16, 74, 148) if "--small" in sys.argv else (74, 148)):
         run(T, torch, stream, f"configs0 x{cnt}",
             lambda: [E.make(T, (41, 15, 7), 0.5, "tt2006", 0.05, "cluster", sid)[0] for _ in range(cnt)], grid)
