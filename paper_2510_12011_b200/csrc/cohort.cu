@@ -122,8 +122,13 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define PH(k) do { } while (0)
 #endif
 
+// Streaming launches (no dynamic shared memory) may keep TCB_CO_STREAM_MINB CTAs
+// per SM (register cap 65536 / (threads x MINB)); resident launches keep one.
+#ifndef TCB_CO_STREAM_MINB
+#define TCB_CO_STREAM_MINB 1
+#endif
 template <int MODEL, bool RES>
-__global__ void __launch_bounds__(kCoThreads, 1)
+__global__ void __launch_bounds__(kCoThreads, RES ? 1 : TCB_CO_STREAM_MINB)
     cohort_kernel(const CoRep* __restrict__ reps, int64_t nsteps) {
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks();
