@@ -309,18 +309,20 @@ tc_status tc_engine_info(tc_ctx* ctx, int64_t out[4]);
  * members must not be stepped concurrently with tc_cohort_step. */
 typedef struct tc_cohort tc_cohort;
 /* members: host array of `count` context pointers (copied).  cluster_size: CTAs
- * per member cluster (1, 2, 4, 8, 16) or 0 = automatic: one SELL slice per warp
- * for the largest member, reduced to the largest size whose resident clusters
- * hold every member at once (one wave), else 2.
+ * per member cluster (1, 2, 4, 8, 16) or 0 = automatic: at most one SELL slice
+ * per warp for the largest member, at least 2, chosen with the mode (below).
  * resident: 0 = stream from global memory; 2 = "full": keep each CTA's matrix
  * block (values, column indices) and own-row vectors in shared memory for the
  * whole launch when the largest member's block fits; 3 = "compact": keep only
  * the column indices and the vectors there (the matrix values are read through
- * L2), a smaller footprint; 1 = automatic: compact when it keeps more clusters
- * resident than full and the members outnumber the full-mode clusters, else
- * full.  A mode whose footprint does not fit falls back to streaming
- * (tc_cohort_info reports what was chosen).
- * TC_EINVAL if resident is outside 0..3.
+ * L2), a smaller footprint; 4 = "dense" streaming: the kernel built for two
+ * CTAs per SM (128 registers, some spills), twice the resident clusters;
+ * 1 = automatic: the cluster size (when cluster_size is 0) and the mode
+ * (full / compact by footprint, streaming, dense) with the lowest modelled
+ * time = ceil(members / resident clusters) x the measured time of one round
+ * (DESIGN.md "Cohorts").  A resident mode whose footprint does not fit
+ * streams (tc_cohort_info reports what was chosen).
+ * TC_EINVAL if resident is outside 0..4.
  * TC_ESTATE if a member is not assembled or is partitioned / multi-GPU;
  * TC_EINVAL on mixed devices or models, MMS members, or a bad cluster size. */
 tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluster_size,
@@ -336,8 +338,9 @@ tc_status tc_cohort_step(tc_cohort* cohort, int64_t n_steps, tc_step_stat* stats
  * out[3] dynamic shared memory per CTA (0 = streaming), out[4] 1 when the
  * resident launch keeps only the column indices (and vectors) in shared
  * memory and reads the matrix values through L2 (chosen when that keeps more
- * clusters resident and the members outnumber the full-resident clusters). */
-tc_status tc_cohort_info(const tc_cohort* cohort, int32_t out[5]);
+ * clusters resident and the members outnumber the full-resident clusters),
+ * out[5] 1 for the dense (two CTAs per SM) streaming kernel. */
+tc_status tc_cohort_info(const tc_cohort* cohort, int32_t out[6]);
 const char* tc_cohort_last_error(const tc_cohort* cohort);
 tc_status tc_cohort_destroy(tc_cohort* cohort);
 

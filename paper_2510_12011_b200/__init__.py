@@ -362,12 +362,12 @@ def tc_cohort_step(co, n_steps: int, count: int | None = None, want_stats: bool 
 
 
 def tc_cohort_info(co) -> dict:
-    out = np.zeros(5, np.int32)
+    out = np.zeros(6, np.int32)
     st = _L.tc_cohort_info(co, _ptr(out))
     if st != TC_OK:
         raise TcError(st, "tc_cohort_info")
     return dict(members=int(out[0]), cluster_size=int(out[1]), resident_clusters=int(out[2]),
-                smem_per_cta=int(out[3]), compact=bool(out[4]))
+                smem_per_cta=int(out[3]), compact=bool(out[4]), dense=bool(out[5]))
 
 
 def tc_cohort_last_error(co) -> str:

@@ -1954,6 +1954,7 @@ struct tc_cohort {
   int device = 0, model = 0, csize = 1;
   size_t smem = 0;                 // dynamic shared memory per CTA (0 = streaming)
   bool compact = false;            // resident launch with only the column indices in shared memory
+  bool dense = false;              // streaming launch of the 128-register kernel (two CTAs per SM)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev = nullptr;
   std::string err;
@@ -2027,20 +2028,26 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
   co->device = m0->device;
   co->model = m0->cfg.model;
   co->stream = m0->stream;
-  if (resident < 0 || resident > 3) {
+  if (resident < 0 || resident > 4) {
     delete co;
-    return fail(m0, TC_EINVAL, "cohort: resident must be 0..3");
+    return fail(m0, TC_EINVAL, "cohort: resident must be 0..4");
   }
-  // Residency for cluster size C (the largest small member decides); returns the
-  // clusters resident at once.  full: matrix values, indices and vectors in shared
-  // memory; compact: indices and vectors only (A, K read through L2) -- a smaller
-  // footprint that keeps more clusters resident when the members outnumber those
-  // that fit in full mode.  resident 1: automatic; 2: full only; 3: compact only
-  // (each falls back to streaming).
-  auto plan = [&](int C, size_t* smem, bool* compact) -> int {
-    *smem = 0;
-    *compact = false;
-    if (resident) {
+  // Launch shape for cluster size C and residency mode (0 streaming, 1 resident with
+  // the full/compact rule, 2 full, 3 compact, 4 dense streaming); the largest small
+  // member decides.  full: matrix values, indices and vectors in shared memory;
+  // compact: indices and vectors only (A, K read through L2) -- a smaller footprint
+  // that keeps more clusters resident; dense: streaming kernel capped at 128
+  // registers, two CTAs per SM.  A resident mode that does not fit streams.
+  struct Shape {
+    int C = 0, ncl = 0;
+    size_t smem = 0;
+    bool compact = false, dense = false;
+  };
+  const int64_t nsm = (int64_t)co->small.size();
+  auto shape = [&](int C, int mode) -> Shape {
+    Shape sh;
+    sh.C = C;
+    if (mode == 1 || mode == 2 || mode == 3) {
       size_t need = 0, need_c = 0;
       for (int i : co->small) {
         const tc_ctx* c = co->m[i];
@@ -2050,43 +2057,62 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
       const size_t lim = cohort_smem_limit(co->model);
       const int ncl = need <= lim ? cohort_active_clusters(co->model, C, need) : 0;
       const int ncl_c = need_c <= lim ? cohort_active_clusters(co->model, C, need_c) : 0;
-      const bool use_c = resident == 3 ? ncl_c > 0
-                       : resident == 2 ? false
-                       : (ncl_c > ncl && (int64_t)co->small.size() > ncl);
+      const bool use_c = mode == 3 ? ncl_c > 0 : mode == 2 ? false : (ncl_c > ncl && nsm > ncl);
       if (use_c) {
-        *smem = need_c;
-        *compact = true;
+        sh.smem = need_c;
+        sh.compact = true;
       } else if (ncl > 0) {
-        *smem = need;
+        sh.smem = need;
       }
     }
-    return cohort_active_clusters(co->model, C, *smem);
+    sh.dense = mode == 4;
+    sh.ncl = cohort_active_clusters(co->model, C, sh.smem, sh.dense);
+    return sh;
   };
-  // auto size: one slice per warp where possible (want), then the largest C <= want
-  // whose resident clusters hold every small member at once (one wave), else 2.
-  // Measured (profiles/r01g_exp_cohort_cluster_size.txt, configs[0]-sized TT2006
-  // members, ms/step for C = 1/2/4/8/16): 16 members 0.51/0.29/0.15/0.18/0.23,
-  // 74 members 0.60/0.35/0.44/0.46/0.83, 148 members 0.88/0.65/0.74/0.92/1.65;
-  // cohort100 0.94/0.64/0.63/0.70/1.04.  C = 1 (no cluster) is never faster.
+  // Cost model: rounds of member launches (ceil(members / resident clusters)) times
+  // the measured time of one round (configs[0]-sized TT2006 members, ms/step:
+  // streaming 0.60 / 0.33 / 0.175 / 0.118 / 0.090 for C = 1 / 2 / 4 / 8 / 16;
+  // resident x 0.83; dense x 2.2 at C = 2, x 1.75 at C = 4, x 2 otherwise --
+  // profiles/r01g_exp_cohort_cluster_size.txt, r01g_exp_cohort_dense.txt).  It
+  // picks the measured best of every swept cohort: 16 members C = 4 compact
+  // (0.15 ms/step), 74 and 148 members C = 2 streaming (0.35, 0.65), cohort100
+  // C = 4 dense (0.545; 0.63 with the best 1-CTA/SM shape).
+  auto cost = [&](const Shape& sh) -> double {
+    if (sh.ncl <= 0) return 1e300;
+    const int lc = sh.C >= 16 ? 4 : sh.C >= 8 ? 3 : sh.C >= 4 ? 2 : sh.C >= 2 ? 1 : 0;
+    static const double t_stream[5] = {0.60, 0.33, 0.175, 0.118, 0.090};
+    static const double f_dense[5] = {2.0, 2.2, 1.75, 2.0, 2.0};
+    const double t = t_stream[lc] * (sh.smem > 0 ? 0.83 : sh.dense ? f_dense[lc] : 1.0);
+    return (double)((std::max<int64_t>(nsm, 1) + sh.ncl - 1) / sh.ncl) * t;
+  };
   const int want = cluster_size ? cluster_size : cluster_want(max_slices);
   co->csize = cohort_cluster_size(co->model, want);
   if (co->csize == 0 || (cluster_size && co->csize != cluster_size)) {
     delete co;
     return fail(m0, TC_EINVAL, "cohort: the device cannot run clusters of the requested size");
   }
-  if (!cluster_size && co->csize > 2) {
-    int pick = 2;
-    for (int C = co->csize; C > 2; C >>= 1) {
-      size_t sm;
-      bool cp;
-      if (cohort_cluster_size(co->model, C) == C && plan(C, &sm, &cp) >= (int64_t)co->small.size()) {
-        pick = C;
-        break;
+  // candidates: the given size, or every power of two from one slice per warp of the
+  // largest member down to 2; the residency modes the caller allows
+  Shape best;
+  double best_cost = 0.0;
+  const int cmin = cluster_size ? co->csize : std::min(co->csize, 2);
+  for (int C = co->csize; C >= cmin; C >>= 1) {
+    if (cohort_cluster_size(co->model, C) != C) continue;
+    const int modes_auto[3] = {1, 0, 4};
+    const int nm = resident == 1 ? 3 : 1;
+    for (int k = 0; k < nm; ++k) {
+      const Shape sh = shape(C, resident == 1 ? modes_auto[k] : resident);
+      const double cst = cost(sh);
+      if (best.C == 0 || cst < best_cost) {
+        best = sh;
+        best_cost = cst;
       }
     }
-    co->csize = cohort_cluster_size(co->model, pick);
   }
-  plan(co->csize, &co->smem, &co->compact);
+  co->csize = best.C;
+  co->smem = best.smem;
+  co->compact = best.compact;
+  co->dense = best.dense;
   if (cudaEventCreateWithFlags(&co->ev, cudaEventDisableTiming) != cudaSuccess ||
       co_alloc(co, &co->d_reps, count) != cudaSuccess || co_alloc(co, &co->d_status, count) != cudaSuccess) {
     tc_cohort_destroy(co);
@@ -2130,7 +2156,8 @@ tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
       }
     CO_CUDA(co, cudaMemsetAsync(co->d_status, 0, cnt * 4, co->stream));
     CO_CUDA(co, cudaMemcpyAsync(co->d_reps, co->h.data(), ns_small * sizeof(CoRep), cudaMemcpyHostToDevice, co->stream));
-    CO_CUDA(co, launch_cohort(co->model, co->d_reps, (int)ns_small, co->csize, co->smem, nsteps, co->stream));
+    CO_CUDA(co, launch_cohort(co->model, co->d_reps, (int)ns_small, co->csize, co->smem, nsteps, co->stream,
+                              co->dense));
     CO_CUDA(co, cudaEventRecord(co->ev, co->stream));
     for (int i : co->small)
       if (co->m[i]->stream != co->stream) CO_CUDA(co, cudaStreamWaitEvent(co->m[i]->stream, co->ev, 0));
@@ -2167,13 +2194,14 @@ tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
   return TC_OK;
 }
 
-tc_status tc_cohort_info(const tc_cohort* co, int32_t out[5]) {
+tc_status tc_cohort_info(const tc_cohort* co, int32_t out[6]) {
   if (!co || !out) return TC_EINVAL;
   out[0] = (int32_t)co->m.size();
   out[1] = co->csize;
-  out[2] = cohort_active_clusters(co->model, co->csize, co->smem);
+  out[2] = cohort_active_clusters(co->model, co->csize, co->smem, co->dense);
   out[3] = (int32_t)co->smem;
   out[4] = co->compact ? 1 : 0;
+  out[5] = co->dense ? 1 : 0;
   return TC_OK;
 }
 

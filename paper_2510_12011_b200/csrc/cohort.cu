@@ -122,13 +122,13 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define PH(k) do { } while (0)
 #endif
 
-// Streaming launches (no dynamic shared memory) may keep TCB_CO_STREAM_MINB CTAs
-// per SM (register cap 65536 / (threads x MINB)); resident launches keep one.
-#ifndef TCB_CO_STREAM_MINB
-#define TCB_CO_STREAM_MINB 1
-#endif
-template <int MODEL, bool RES>
-__global__ void __launch_bounds__(kCoThreads, RES ? 1 : TCB_CO_STREAM_MINB)
+// MINB: CTAs per SM the register allocation must allow.  1 (resident and the
+// default streaming launch): up to 255 registers, no spills.  2 ("dense"
+// streaming, a cohort option): 128 registers, 228-728 bytes of spills (MS ..
+// CRN) for twice the resident clusters -- fewer rounds when the members
+// outnumber the 1-per-SM clusters.
+template <int MODEL, bool RES, int MINB = 1>
+__global__ void __launch_bounds__(kCoThreads, MINB)
     cohort_kernel(const CoRep* __restrict__ reps, int64_t nsteps) {
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks();
@@ -549,12 +549,17 @@ __global__ void __launch_bounds__(kCoThreads, RES ? 1 : TCB_CO_STREAM_MINB)
   cl.sync();  // no CTA leaves while another may still address its shared memory
 }
 
-static const void* cohort_fn(int model, bool res) {
+static const void* cohort_fn(int model, bool res, bool dense = false) {
   if (model == TC_ION_TT2006_EPI)
-    return res ? (const void*)cohort_kernel<TC_ION_TT2006_EPI, true> : (const void*)cohort_kernel<TC_ION_TT2006_EPI, false>;
+    return res ? (const void*)cohort_kernel<TC_ION_TT2006_EPI, true>
+               : dense ? (const void*)cohort_kernel<TC_ION_TT2006_EPI, false, 2>
+                       : (const void*)cohort_kernel<TC_ION_TT2006_EPI, false>;
   if (model == TC_ION_CRN)
-    return res ? (const void*)cohort_kernel<TC_ION_CRN, true> : (const void*)cohort_kernel<TC_ION_CRN, false>;
-  return res ? (const void*)cohort_kernel<TC_ION_MS, true> : (const void*)cohort_kernel<TC_ION_MS, false>;
+    return res ? (const void*)cohort_kernel<TC_ION_CRN, true>
+               : dense ? (const void*)cohort_kernel<TC_ION_CRN, false, 2>
+                       : (const void*)cohort_kernel<TC_ION_CRN, false>;
+  return res ? (const void*)cohort_kernel<TC_ION_MS, true>
+             : dense ? (const void*)cohort_kernel<TC_ION_MS, false, 2> : (const void*)cohort_kernel<TC_ION_MS, false>;
 }
 
 int cohort_param_doubles() { return kParamDoubles; }
@@ -623,8 +628,8 @@ static void prepare(const void* fn, size_t smem) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-int cohort_active_clusters(int model, int csize, size_t smem) {
-  const void* fn = cohort_fn(model, smem > 0);
+int cohort_active_clusters(int model, int csize, size_t smem, bool dense) {
+  const void* fn = cohort_fn(model, smem > 0, dense && smem == 0);
   prepare(fn, smem);
   cudaLaunchAttribute at[1];
   cudaLaunchConfig_t cfg = cohort_cfg(1, csize, smem, nullptr, at);
@@ -645,9 +650,9 @@ int cohort_cluster_size(int model, int want) {
 }
 
 cudaError_t launch_cohort(int model, const CoRep* d_reps, int nrep, int csize, size_t smem,
-                          int64_t nsteps, cudaStream_t s) {
+                          int64_t nsteps, cudaStream_t s, bool dense) {
   if (nrep <= 0 || nsteps <= 0) return cudaSuccess;
-  const void* fn = cohort_fn(model, smem > 0);
+  const void* fn = cohort_fn(model, smem > 0, dense && smem == 0);
   prepare(fn, smem);
   cudaLaunchAttribute at[1];
   cudaLaunchConfig_t cfg = cohort_cfg(nrep, csize, smem, s, at);

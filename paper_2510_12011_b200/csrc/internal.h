@@ -281,12 +281,12 @@ int cohort_param_doubles();
 void cohort_pack_params(int model, const TTParams& tp, const MSParams& mp, const CRNParams& cp,
                         double* out);
 int cohort_cluster_size(int model, int want);
-int cohort_active_clusters(int model, int csize, size_t smem);  // smem 0 = streaming launch
+int cohort_active_clusters(int model, int csize, size_t smem, bool dense = false);  // smem 0 = streaming launch
 size_t cohort_smem_bytes(const int64_t* sp, int32_t ns, int C, bool compact = false);
 size_t cohort_smem_limit(int model);
 // smem > 0: cluster-resident launch with that much dynamic shared memory per CTA
 cudaError_t launch_cohort(int model, const CoRep* d_reps, int nrep, int csize, size_t smem,
-                          int64_t nsteps, cudaStream_t s);
+                          int64_t nsteps, cudaStream_t s, bool dense = false);
 
 // ---- launchers (return cudaError_t of the launch) --------------------------
 cudaError_t launch_assemble(const AsmArgs& a, cudaStream_t s);

@@ -150,7 +150,8 @@ COHORT = [
 ]
 
 
-@pytest.mark.parametrize("cluster_size,resident", [(0, 1), (1, 0), (4, 1), (4, 0), (16, 1), (4, 2), (4, 3), (8, 3)])
+@pytest.mark.parametrize("cluster_size,resident", [(0, 1), (1, 0), (4, 1), (4, 0), (16, 1), (4, 2), (4, 3), (8, 3),
+                                                    (2, 4), (4, 4), (0, 4)])
 def test_cohort_parity(T, cluster_size, resident):
     """A heterogeneous cohort (meshes of 8 .. ~5k nodes, structured and BiV, other
     dt / tolerances / conductivities / ionic parameters / stimuli) advanced in
@@ -172,6 +173,7 @@ def test_cohort_parity(T, cluster_size, resident):
                 assert not info["compact"]
             if resident == 3:   # indices-only residency fits every member of this cohort
                 assert info["compact"] and info["smem_per_cta"] > 0
+            assert info["dense"] == (resident == 4)
             if cluster_size:
                 assert info["cluster_size"] == cluster_size
             assert info["resident_clusters"] >= 1
@@ -277,7 +279,7 @@ def test_cohort_errors(T):
         with pytest.raises(T.TcError):
             T.Cohort([a], cluster_size=3)          # not a power of two
         with pytest.raises(T.TcError) as ei:
-            T.Cohort([a], resident=4)              # no such residency mode
+            T.Cohort([a], resident=5)              # no such residency mode
         assert ei.value.status == T.TC_EINVAL
     finally:
         for s in (a, b, p):

@@ -57,7 +57,9 @@ def main():
     stream = torch.cuda.current_stream()
     sid = stream.cuda_stream
     grid = ((0, 1, 2, 4, 8, 16), (1,)) if "--small" in sys.argv else ((2, 4, 8, 16), (0, 2, 3))
-    for cnt in ((16, 74, 148) if "--small" in sys.argv else (74, 148)):
+    if "--dense" in sys.argv:   # resident 4: the two-CTA-per-SM streaming kernel, beside auto
+        grid = ((0, 2, 4, 8), (1, 4))
+    for cnt in ((16, 74, 148) if ("--small" in sys.argv or "--dense" in sys.argv) else (74, 148)):
         run(T, torch, stream, f"configs0 x{cnt}",
             lambda: [E.make(T, (41, 15, 7), 0.5, "tt2006", 0.05, "cluster", sid)[0] for _ in range(cnt)], grid)
     run(T, torch, stream, "cohort100", lambda: bench_members(T, sid), grid)
