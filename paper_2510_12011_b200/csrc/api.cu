@@ -2025,6 +2025,13 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
       max_slices = std::max<int64_t>(max_slices, members[i]->parts[0].nslices);
     }
   }
+  // largest members first: clusters are dispatched in launch order, so the long
+  // runs start in the first round and the short ones fill the gaps (LPT order)
+  std::stable_sort(co->small.begin(), co->small.end(), [&](int a, int b) {
+    const tc_ctx* ca = members[a];
+    const tc_ctx* cb = members[b];
+    return ca->parts[0].h_sp[ca->parts[0].nslices] > cb->parts[0].h_sp[cb->parts[0].nslices];
+  });
   co->device = m0->device;
   co->model = m0->cfg.model;
   co->stream = m0->stream;
