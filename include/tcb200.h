@@ -221,7 +221,10 @@ tc_status tc_get_activation(tc_ctx* ctx, double* lat, double* lrt);
 /* Full cell state for checkpoint / state injection:
  * [V^k (n) | V^{k-1} (n) | u_0 (n) ... u_{S-1} (n) | k | has_prev], original order,
  * S = 18 (TT2006, state order Ki Nai Cai CaSS CaSR Rbar m h j xr1 xr2 xs r s d f
- * f2 fCass), 1 (MS: h), 0 (MMS).  has_prev = 0 means V^{k-1} := V^k. */
+ * f2 fCass), 1 (MS: h), 0 (MMS).  has_prev = 0 means V^{k-1} := V^k.
+ * Both calls return once buf has been read / written (the caller owns buf;
+ * tc_set_state is one host->device copy and one synchronisation in a
+ * single-process context, staging in the tc_step_io buffers). */
 int64_t tc_state_len(const tc_ctx* ctx);
 tc_status tc_get_state(tc_ctx* ctx, double* buf, int64_t len);
 tc_status tc_set_state(tc_ctx* ctx, const double* buf, int64_t len);

@@ -1684,6 +1684,8 @@ tc_status tc_get_state(tc_ctx* c, double* buf, int64_t len) {
   return TC_OK;
 }
 
+static tc_status io_setup(tc_ctx* c);  // below (tc_step_io staging)
+
 tc_status tc_set_state(tc_ctx* c, const double* buf, int64_t len) {
   if (!c || !buf) return TC_EINVAL;
   if (!c->assembled) return fail(c, TC_ESTATE, "tc_set_state before tc_assemble");
@@ -1692,6 +1694,21 @@ tc_status tc_set_state(tc_ctx* c, const double* buf, int64_t len) {
   const double kk = buf[(2 + c->nstates) * n], hp = buf[(2 + c->nstates) * n + 1];
   if (!(kk >= 0) || kk != std::floor(kk)) return fail(c, TC_EINVAL, "tc_set_state: bad step index");
   const int iv = c->iVk, ip = c->iVkm1;
+  if (!c->use_comm) {
+    // one H2D copy of every field into the staging buffer of tc_step_io, the
+    // permutation gathers on the device, one synchronisation (was: one per field)
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    TC_TRY(io_setup(c));
+    double* in = c->d_sin[0];
+    CUDA_TRY(c, cudaMemcpyAsync(in, buf, (2 + c->nstates) * n * 8, cudaMemcpyHostToDevice, c->stream));
+    for (Part& P : c->parts)
+      CUDA_TRY(c, launch_gather_state(P.n, c->d_perm_g + P.plan.g0, in, n, P.d_V[iv], P.d_V[ip], P.d_U, P.n_pad,
+                                      c->nstates, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->k = (int64_t)kk;
+    c->has_prev = hp != 0.0;
+    return TC_OK;
+  }
   TC_TRY(scatter_field(c, buf, per_part(c, [iv](Part& P) { return P.d_V[iv]; }).data()));
   TC_TRY(scatter_field(c, buf + n, per_part(c, [ip](Part& P) { return P.d_V[ip]; }).data()));
   for (int q = 0; q < c->nstates; ++q)
@@ -1758,12 +1775,9 @@ tc_status tc_step_io(tc_ctx* c, int64_t n_steps, const double* states, int64_t s
     CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->e_loaded[b], 0));
     const double* in = c->d_sin[b];
     const int iv = c->iVk, ip = c->iVkm1;
-    for (Part& P : c->parts) {
-      CUDA_TRY(c, launch_gather(P.n, c->d_perm_g + P.plan.g0, in, P.d_V[iv], c->stream));
-      CUDA_TRY(c, launch_gather(P.n, c->d_perm_g + P.plan.g0, in + n, P.d_V[ip], c->stream));
-      for (int q = 0; q < c->nstates; ++q)
-        CUDA_TRY(c, launch_gather(P.n, c->d_perm_g + P.plan.g0, in + (2 + q) * n, P.d_U + q * P.n_pad, c->stream));
-    }
+    for (Part& P : c->parts)
+      CUDA_TRY(c, launch_gather_state(P.n, c->d_perm_g + P.plan.g0, in, n, P.d_V[iv], P.d_V[ip], P.d_U, P.n_pad,
+                                      c->nstates, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->e_used[b], c->stream));
     c->k = (int64_t)states[j * stride + (2 + c->nstates) * n];
     c->has_prev = states[j * stride + (2 + c->nstates) * n + 1] != 0.0;

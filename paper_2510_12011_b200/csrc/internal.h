@@ -299,6 +299,8 @@ cudaError_t launch_stimulus(int32_t m, const int32_t* idx, const double* s, doub
 cudaError_t launch_lat_epilogue(const IonArgs& a, cudaStream_t s);
 cudaError_t launch_gather(int64_t n, const int32_t* idx, const double* in, double* out, cudaStream_t s);
 cudaError_t launch_scatter(int64_t n, const int32_t* idx, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_gather_state(int64_t n, const int32_t* idx, const double* in, int64_t in_stride, double* v0,
+                                double* v1, double* U, int64_t upad, int32_t nstates, cudaStream_t s);
 cudaError_t launch_spmv(const int64_t* slice_ptr, const int32_t* col, const double* A, int32_t nslices,
                         const double* x, double* y, cudaStream_t s);
 // PCG: mode 0 = plain (r0 = b - A x0), 1 = monodomain RHS (r0 = A u' - K v')

@@ -142,6 +142,18 @@ __global__ void gather_kernel(int64_t n, const int32_t* __restrict__ idx,
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = in[idx[i]];
 }
+// every field of a host-layout state (tc_set_state: V^k | V^{k-1} | u_0 .. u_{S-1},
+// field stride in_stride, original order) into the internal order: one launch,
+// blockIdx.y = field.
+__global__ void gather_state_kernel(int64_t n, const int32_t* __restrict__ idx, const double* __restrict__ in,
+                                    int64_t in_stride, double* __restrict__ v0, double* __restrict__ v1,
+                                    double* __restrict__ U, int64_t upad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int f = blockIdx.y;
+  double* out = f == 0 ? v0 : f == 1 ? v1 : U + (int64_t)(f - 2) * upad;
+  out[i] = in[(int64_t)f * in_stride + idx[i]];
+}
 __global__ void scatter_kernel(int64_t n, const int32_t* __restrict__ idx,
                                const double* __restrict__ in, double* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -225,6 +237,13 @@ cudaError_t launch_gather(int64_t n, const int32_t* idx, const double* in, doubl
                           cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   gather_kernel<<<nblk(n, 256), 256, 0, s>>>(n, idx, in, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_gather_state(int64_t n, const int32_t* idx, const double* in, int64_t in_stride, double* v0,
+                                double* v1, double* U, int64_t upad, int32_t nstates, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  gather_state_kernel<<<dim3((unsigned)nblk(n, 256), (unsigned)(2 + nstates)), 256, 0, s>>>(n, idx, in, in_stride,
+                                                                                         v0, v1, U, upad);
   return cudaGetLastError();
 }
 cudaError_t launch_scatter(int64_t n, const int32_t* idx, const double* in, double* out,
