@@ -480,26 +480,23 @@ def run_cohort(args, w):
         hin.append(h)
     hout = [torch.empty(n_, dtype=torch.float64, pin_memory=True).numpy() for n_ in n_nodes]
     ke = max(1, args.e2e_steps)
-    for s_, h in zip(sims, hin):   # untimed: the first call allocates each member's staging (tc_step_io buffers)
-        T.tc_set_state(s_.ctx, h)
+    co.set_states(hin)   # untimed: the first call allocates each member's staging (tc_step_io buffers)
     torch.cuda.synchronize()
     split = [0.0, 0.0, 0.0]
     t0 = time.perf_counter()
     for _ in range(ke):
         ta = time.perf_counter()
-        for s_, h in zip(sims, hin):
-            T.tc_set_state(s_.ctx, h)
+        co.set_states(hin)
         tb = time.perf_counter()
         co.step(1, want_stats=False)
         tc_ = time.perf_counter()
-        for s_, h in zip(sims, hout):
-            T.tc_get_v(s_.ctx, h)
+        co.get_v(hout)
         td = time.perf_counter()
         split[0] += tb - ta; split[1] += tc_ - tb; split[2] += td - tc_
     e2e_s = time.perf_counter() - t0
     e2e = {"value": N * world * ke / e2e_s, "unit": "node-steps/s",
            "h2d_bytes_per_step": int(sum(h.nbytes for h in hin)), "d2h_bytes_per_step": int(sum(h.nbytes for h in hout)),
-           "what": "per step: tc_set_state of every member (pinned host) + tc_cohort_step(1) + tc_get_v of every member",
+           "what": "per step: tc_cohort_set_states (every member's state, pinned host) + tc_cohort_step(1) + tc_cohort_get_v (every member's V)",
            "split_ms_per_step": {"set_state": 1e3 * split[0] / ke, "cohort_step": 1e3 * split[1] / ke,
                                  "get_v": 1e3 * split[2] / ke}}
     iters = float(stats["iters"].mean())

@@ -23,7 +23,7 @@ __all__ = [
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
     "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "tc_nccl_unique_id", "tc_comm_init",
     "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "Monodomain", "LIB_PATH",
-    "tc_engine_info", "tc_node_order", "tc_apply", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
+    "tc_engine_info", "tc_node_order", "tc_apply", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_set_states", "tc_cohort_get_v", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
     "TC_ENGINE_AUTO", "TC_ENGINE_GRID", "TC_ENGINE_CLUSTER",
     "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS", "TC_ION_CRN",
 ]
@@ -109,6 +109,8 @@ def _load():
         "tc_cohort_create": ([P, I32, I32, I32, P], I32),
         "tc_cohort_step": ([P, I64, P], I32),
         "tc_cohort_info": ([P, P], I32),
+        "tc_cohort_set_states": ([P, P], I32),
+        "tc_cohort_get_v": ([P, P], I32),
         "tc_cohort_last_error": ([P], C.c_char_p),
         "tc_cohort_destroy": ([P], I32),
         "tc_mesh_pattern": ([I64, I64, P, P, P], I32),
@@ -361,6 +363,29 @@ def tc_cohort_step(co, n_steps: int, count: int | None = None, want_stats: bool 
     return stats
 
 
+def _ptr_array(arrs):
+    for a in arrs:
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+            raise ValueError("cohort I/O: contiguous float64 arrays")
+    return (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+
+
+def _co_check(co, st):
+    if st != TC_OK:
+        m = _L.tc_cohort_last_error(co)
+        raise TcError(st, m.decode() if m else "")
+
+
+def tc_cohort_set_states(co, bufs) -> None:
+    """bufs: one tc_set_state-layout float64 host array per member (member order)."""
+    _co_check(co, _L.tc_cohort_set_states(co, _ptr_array(bufs)))
+
+
+def tc_cohort_get_v(co, outs) -> None:
+    """outs: one float64 host array of n_nodes per member, filled with V^k."""
+    _co_check(co, _L.tc_cohort_get_v(co, _ptr_array(outs)))
+
+
 def tc_cohort_info(co) -> dict:
     out = np.zeros(6, np.int32)
     st = _L.tc_cohort_info(co, _ptr(out))
@@ -517,6 +542,12 @@ class Cohort:
 
     def step(self, n: int = 1, want_stats: bool = True):
         return tc_cohort_step(self.co, n, len(self.members), want_stats)
+
+    def set_states(self, bufs) -> None:
+        tc_cohort_set_states(self.co, bufs)
+
+    def get_v(self, outs) -> None:
+        tc_cohort_get_v(self.co, outs)
 
     def info(self) -> dict:
         return tc_cohort_info(self.co)

@@ -2215,6 +2215,55 @@ tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
   return TC_OK;
 }
 
+// Batched member I/O: every member's copies and permutation kernels enqueued on
+// its own stream, then one synchronisation per member stream (tc_set_state /
+// tc_get_v per member synchronise once per call).
+tc_status tc_cohort_set_states(tc_cohort* co, const double* const* bufs) {
+  if (!co || !bufs) return TC_EINVAL;
+  const size_t cnt = co->m.size();
+  for (size_t i = 0; i < cnt; ++i) {  // validate every input before touching any member
+    tc_ctx* c = co->m[i];
+    if (!bufs[i]) return cfail(co, TC_EINVAL, "tc_cohort_set_states: null state of member " + std::to_string(i));
+    const double kk = bufs[i][(2 + c->nstates) * c->n];
+    if (!(kk >= 0) || kk != std::floor(kk))
+      return cfail(co, TC_EINVAL, "tc_cohort_set_states: bad step index in member " + std::to_string(i));
+  }
+  CO_CUDA(co, cudaSetDevice(co->device));
+  for (size_t i = 0; i < cnt; ++i) {
+    tc_ctx* c = co->m[i];
+    if (io_setup(c) != TC_OK) return cfail(co, TC_ECUDA, "cohort member " + std::to_string(i) + ": " + c->err);
+    const int64_t n = c->n;
+    double* in = c->d_sin[0];
+    CO_CUDA(co, cudaMemcpyAsync(in, bufs[i], (2 + c->nstates) * n * 8, cudaMemcpyHostToDevice, c->stream));
+    for (Part& P : c->parts)
+      CO_CUDA(co, launch_gather_state(P.n, c->d_perm_g + P.plan.g0, in, n, P.d_V[c->iVk], P.d_V[c->iVkm1], P.d_U,
+                                      P.n_pad, c->nstates, c->stream));
+  }
+  for (size_t i = 0; i < cnt; ++i) {
+    tc_ctx* c = co->m[i];
+    CO_CUDA(co, cudaStreamSynchronize(c->stream));
+    c->k = (int64_t)bufs[i][(2 + c->nstates) * c->n];
+    c->has_prev = bufs[i][(2 + c->nstates) * c->n + 1] != 0.0;
+  }
+  return TC_OK;
+}
+
+tc_status tc_cohort_get_v(tc_cohort* co, double* const* v_out) {
+  if (!co || !v_out) return TC_EINVAL;
+  const size_t cnt = co->m.size();
+  for (size_t i = 0; i < cnt; ++i)
+    if (!v_out[i]) return cfail(co, TC_EINVAL, "tc_cohort_get_v: null output of member " + std::to_string(i));
+  CO_CUDA(co, cudaSetDevice(co->device));
+  for (size_t i = 0; i < cnt; ++i) {
+    tc_ctx* c = co->m[i];
+    for (Part& P : c->parts)
+      CO_CUDA(co, launch_scatter(P.n, c->d_perm_g + P.plan.g0, P.d_V[c->iVk], c->d_io, c->stream));
+    CO_CUDA(co, cudaMemcpyAsync(v_out[i], c->d_io, c->n * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  for (size_t i = 0; i < cnt; ++i) CO_CUDA(co, cudaStreamSynchronize(co->m[i]->stream));
+  return TC_OK;
+}
+
 tc_status tc_cohort_info(const tc_cohort* co, int32_t out[6]) {
   if (!co || !out) return TC_EINVAL;
   out[0] = (int32_t)co->m.size();

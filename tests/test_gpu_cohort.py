@@ -350,3 +350,39 @@ def test_cohort_long_horizon_bench_members(T):
     finally:
         for s in members:
             s.close()
+
+
+def test_cohort_batched_io_equals_serial_calls(T):
+    """tc_cohort_set_states / tc_cohort_get_v give bitwise what the per-member
+    tc_set_state / tc_get_v give (include/tcb200.h); a bad state is rejected
+    before any member changes."""
+    specs = [dict(dims=(21, 8, 5)), dict(dims=(17, 9, 6), permute=5), dict(dims=(25, 7, 5), permute=9)]
+    members = [_gpu(T, sp, *_member(sp)) for sp in specs]
+    try:
+        co = T.Cohort(members)
+        co.step(20, want_stats=False)
+        states = [s.get_state() for s in members]
+        for s, st in zip(members, states):
+            T.tc_set_state(s.ctx, st)
+        co.step(3, want_stats=False)
+        v_serial = [T.tc_get_v(s.ctx) for s in members]
+        full_serial = [s.get_state() for s in members]
+        co.set_states(states)
+        co.step(3, want_stats=False)
+        outs = [np.full(T.tc_num_nodes(s.ctx), np.nan) for s in members]
+        co.get_v(outs)
+        for i, s in enumerate(members):
+            assert np.array_equal(outs[i], v_serial[i]), i
+            assert np.array_equal(s.get_state(), full_serial[i]), i
+        bad = [st.copy() for st in states]
+        bad[2][-2] = -1.0                      # step index of member 2
+        before = [s.get_state() for s in members]
+        with pytest.raises(T.TcError) as ei:
+            co.set_states(bad)
+        assert ei.value.status == T.TC_EINVAL and "member 2" in str(ei.value)
+        for s, b in zip(members, before):
+            assert np.array_equal(s.get_state(), b)
+        co.close()
+    finally:
+        for s in members:
+            s.close()
