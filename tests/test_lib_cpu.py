@@ -47,6 +47,19 @@ def test_config_defaults_match_paper(lib):
     assert c.pcg_variant == -1       # automatic PCG kernel choice (include/tcb200.h)
 
 
+def test_cohort_io_argument_errors(lib):
+    """tc_cohort_set_states / tc_cohort_get_v reject null arguments with TC_EINVAL
+    before any device work (include/tcb200.h); the binding rejects non-float64 arrays."""
+    import numpy as np
+    import paper_2510_12011_b200 as T
+    assert T._L.tc_cohort_set_states(None, None) == T.TC_EINVAL
+    assert T._L.tc_cohort_get_v(None, None) == T.TC_EINVAL
+    with pytest.raises(ValueError):
+        T._ptr_array([np.zeros(4, np.float32)])
+    with pytest.raises(ValueError):
+        T._ptr_array([np.zeros((4, 2))[:, 0]])
+
+
 def test_no_cpu_fallback():
     import torch
     if torch.cuda.is_available():
