@@ -8,7 +8,9 @@ times (same inputs, config, engine and preroll):
 * a property that holds at any size: the V^{k+1} the GPU returns solves
   Eq. 3 to Algorithm 1's tolerance, with b built on the host from
   the literal Eq. 3 formula and the oracle's ionic currents;
-* configs[2] (442 k nodes) is small enough for the whole oracle step.
+* configs[2] (442 k nodes), a 1.28 M-node TT2006 slab and a 416 k-node BiV
+  against the whole oracle step from injected GPU states, on the multi-slice
+  PCG kernels (variants 0, 1 and the automatic choice).
 """
 import math
 
@@ -148,29 +150,75 @@ def test_fullsize_step_solves_eq3_to_tolerance(T):
         sim.close()
 
 
-def test_configs2_full_oracle_step(T):
-    """configs[2] (N-version dx 0.1 mm, 442 401 nodes, TT2006, dt 0.01) at full
-    size: one step from the GPU state after the bench preroll, GPU vs the whole
-    oracle step (rel-L2 of V <= 1e-8, states to 1e-9)."""
-    name = "nversion_dx0.1_tt"
-    w, sim, xyz, tets, region, fibre = _bench_sim(T, name)
+def _warps_per_cta():
+    return 16            # kCgWarps (csrc/internal.h: 512-thread PCG CTAs)
+
+
+# Whole-oracle-step parity on the grid engine's multi-slice paths (VERDICT r01
+# item 1): the automatic variant and the forced direct (0) and TMA-staged (1)
+# kernels at sizes where every warp walks several SELL slices (variant 0's
+# grid-stride slice loop, variant 1's TMA ring wrapping), on
+#   * configs[2] (N-version dx 0.1 mm, 442 401 nodes, the bench's preroll),
+#   * a 1.28 M-node TT2006 slab (160 x 100 x 80, planar front; the automatic
+#     choice is variant 0 at > 4 slices per resident warp -- the kernel the
+#     north-star / configs[4] bench lines time),
+#   * the BiV recipe at h = 0.65 mm (416 k nodes, permuted numbering, rotating
+#     fibres, two regions).
+# One step from the GPU's own state, injected into the oracle (SURVEY 8c "one-
+# step parity from injected states at all sizes"): rel-L2(V) <= 1e-8
+# (north_star), every cell state to 1e-9, PCG iterations within 1.
+_MULTI = {
+    "configs2": dict(w="nversion_dx0.1_tt", dims=None, preroll=500),
+    "slab1.28M_tt": dict(w="slab10M_tt", dims=(160, 100, 80), preroll=300),
+    "biv416k_tt": dict(w="biv3M_tt", dims=0.65, preroll=300),
+}
+
+
+@pytest.mark.parametrize("case,variant", [("configs2", -1), ("configs2", 0), ("configs2", 1),
+                                          ("slab1.28M_tt", -1), ("slab1.28M_tt", 1),
+                                          ("biv416k_tt", -1), ("biv416k_tt", 0)])
+def test_multislice_full_oracle_step(T, case, variant):
+    c = _MULTI[case]
+    w = bench.WORKLOADS[c["w"]]
+    xyz, tets, stims, region, fibre = bench.make_inputs(w, c["dims"])
+    E = tets.shape[0]
+    cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=bench.CHI, cm=bench.CM, abs_tol=1e-5,
+                              rel_tol=1e-5, max_iters=100, use_rcm=1, pcg_variant=variant, partitions=1)
+    sim = T.Monodomain(xyz, tets, region, fibre, {0: bench.SIGMA, 1: bench.SIGMA}, cfg, stims)
     try:
+        info = T.tc_matrix_info(sim.ctx)
+        assert T.tc_engine_info(sim.ctx)["engine"] == "grid"
+        used = info["pcg_variant"]
+        if variant >= 0:
+            assert used == variant
+        spw = info["nslices"] / (info["pcg_grid"] * _warps_per_cta())
+        if used in (0, 1):
+            assert spw > 1.0, spw          # the multi-slice loop / ring wrap is exercised
+        sim.step(c["preroll"])
         n = xyz.shape[0]
+        ns = {"tt2006": 18, "crn": 20, "ms": 1}[w["model"]]
         s = sim.get_state()
-        Vk, Vkm1, U = _split_state(s, n, 18)
+        Vk, Vkm1, U = _split_state(s, n, ns)
         k = int(round(s[-2]))
-        E = tets.shape[0]
-        ref = O.Monodomain(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: bench.SIGMA},
-                           O.Config(dt=w["dt"], abs_tol=1e-5, rel_tol=1e-5, max_iters=100),
-                           [O.Stimulus(*st_) for st_ in bench.make_inputs(w)[2]])
+        assert k == c["preroll"]
+        assert (Vk > 0).any() and (Vk < -80).any()       # a front is in the domain
+        ref = O.Monodomain(xyz, tets, np.zeros(E, np.int32) if region is None else region,
+                           G.uniform_fibres(E) if fibre is None else fibre,
+                           {0: bench.SIGMA, 1: bench.SIGMA},
+                           O.Config(dt=w["dt"], model=w["model"], chi=bench.CHI, cm=bench.CM,
+                                    abs_tol=1e-5, rel_tol=1e-5, max_iters=100),
+                           [O.Stimulus(*st_) for st_ in stims])
         ref.set_state(Vk, Vkm1, U, k)
         rep = ref.step()
         stg = sim.step(1)
         v = sim.V
-        assert abs(int(stg["iters"][0]) - rep.iters) <= 1
-        assert np.linalg.norm(v - ref.Vk) / np.linalg.norm(ref.Vk) <= 1e-8
-        _, _, U1 = _split_state(sim.get_state(), n, 18)
+        assert abs(int(stg["iters"][0]) - rep.iters) <= 1, (int(stg["iters"][0]), rep.iters)
+        rel = np.linalg.norm(v - ref.Vk) / np.linalg.norm(ref.Vk)
+        assert rel <= 1e-8, rel
+        _, _, U1 = _split_state(sim.get_state(), n, ns)
         assert np.allclose(U1, ref.U, rtol=1e-9, atol=1e-14)
+        print(f"{case} variant {used}: {n} nodes, {spw:.2f} slices/warp, iters {int(stg['iters'][0])} "
+              f"vs {rep.iters}, rel-L2 {rel:.2e}")
     finally:
         sim.close()
 

@@ -188,16 +188,39 @@ def test_mms_matches_dense_direct_solve():
     assert np.abs(out["V"] - V).max() < 1e-10
 
 
-def test_mms_convergence_order():
+def test_mms_convergence_order(golden):
     """BASELINE config 2 / S:487: L2 (M-norm) error order in [1.7, 2.3] under
-    h-refinement with dt proportional to h (readings M2, T1)."""
+    h-refinement with dt proportional to h (readings M2, T1); the errors
+    themselves equal the independent direct-solve values of SURVEY 8(c) M2
+    (tests/golden/mms_reference_errors.json) to their printed precision."""
+    g = golden["mms_reference_errors"]
     errs = []
-    for N in (8, 16, 32):
+    for i, N in enumerate(g["N"]):
         xyz, tets = G.unit_cube(N)
         out = O.run_mms(xyz, tets, G.box_boundary(xyz), dt=0.01 * 8 / N, T=0.5, tol=1e-10)
         errs.append(out["err_M"])
+        assert out["err_M"] == pytest.approx(g["err_M"][i], rel=g["rel_tol"]), (N, out["err_M"])
+        assert out["err_inf"] == pytest.approx(g["err_inf"][i], rel=g["rel_tol"]), (N, out["err_inf"])
     orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert np.all((orders > 1.7) & (orders < 2.3)), orders
+
+
+def test_mms_source_golden_and_pde_residual(golden):
+    """The source r of Eq. 8: (i) the worked value at the origin
+    (S:451, tests/golden/worked_examples.json 'mms_r_origin'); (ii) r is the
+    residual of the PDE it manufactures, r = dw/dt - (w_xx + w_yy) (monodomain
+    with chi = C_m = 1, sigma = I, I_ion = 0, P:217-228), checked with central
+    differences of Eq. 5's w at random points -- independent of r's formula."""
+    g = golden["worked_examples"]["mms_r_origin"]
+    r0 = O.mms_r(0.0, 0.0, 0.0, k=g["k"], w1=g["w1"], w2=g["w2"], lam=g["lam"])
+    assert r0 == pytest.approx(g["r"], rel=1e-14)
+    rng = np.random.default_rng(3)
+    x, y, t = rng.uniform(0, 1, 50), rng.uniform(0, 1, 50), rng.uniform(0, 0.5, 50)
+    h = 1e-4
+    w = O.mms_w
+    wt = (w(x, y, t + h) - w(x, y, t - h)) / (2 * h)
+    lap = (w(x + h, y, t) + w(x - h, y, t) + w(x, y + h, t) + w(x, y - h, t) - 4 * w(x, y, t)) / (h * h)
+    assert np.allclose(O.mms_r(x, y, t), wt - lap, rtol=0, atol=2e-5)
 
 
 def test_mms_wrong_sign_breaks_order():
