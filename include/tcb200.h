@@ -338,16 +338,20 @@ tc_status tc_cohort_create(tc_ctx* const* members, int32_t count, int32_t cluste
  * TC_ENAN naming the first such member, after all members were advanced. */
 tc_status tc_cohort_step(tc_cohort* cohort, int64_t n_steps, tc_step_stat* stats);
 /* Batched member I/O (the per-member tc_set_state / tc_get_v, one
- * synchronisation per call instead of one per member).  bufs[i]: host state of
- * member i in the tc_set_state layout (tc_state_len(member i) doubles); v_out[i]:
- * host array of the member's n_nodes doubles, filled with its V^k in the
- * original order.  Arrays of `count` pointers, member order of tc_cohort_create;
- * the caller owns every buffer (pinned memory lets the copies run at full
- * rate).  Both return after every copy completed.  TC_EINVAL: a null pointer
- * or a bad step index (tc_cohort_set_states validates every state before it
- * changes any member). */
-tc_status tc_cohort_set_states(tc_cohort* cohort, const double* const* bufs);
-tc_status tc_cohort_get_v(tc_cohort* cohort, double* const* v_out);
+ * synchronisation per call instead of one per member).  count: the number of
+ * members (must equal the cohort's); bufs[i]: host state of member i in the
+ * tc_set_state layout, lens[i] its length in doubles (must equal
+ * tc_state_len(member i)); v_out[i]: host array of lens[i] == n_nodes(member i)
+ * doubles, filled with the member's V^k in the original order.  Arrays of
+ * `count` pointers / lengths, member order of tc_cohort_create; the caller owns
+ * every buffer (pinned memory lets the copies run at full rate).  Both return
+ * after every copy completed.  TC_EINVAL: a null pointer, a count or length
+ * mismatch, or a bad step index -- every input is validated, and every
+ * member's staging allocated (TC_ENOMEM / TC_ECUDA), before any member
+ * changes.  A TC_ECUDA from a copy or kernel launch after that point leaves
+ * the members' states undefined (the device context is then unusable). */
+tc_status tc_cohort_set_states(tc_cohort* cohort, int64_t count, const double* const* bufs, const int64_t* lens);
+tc_status tc_cohort_get_v(tc_cohort* cohort, int64_t count, double* const* v_out, const int64_t* lens);
 /* out[0] members, out[1] CTAs per cluster, out[2] clusters resident at once,
  * out[3] dynamic shared memory per CTA (0 = streaming), out[4] 1 when the
  * resident launch keeps only the column indices (and vectors) in shared

@@ -109,8 +109,8 @@ def _load():
         "tc_cohort_create": ([P, I32, I32, I32, P], I32),
         "tc_cohort_step": ([P, I64, P], I32),
         "tc_cohort_info": ([P, P], I32),
-        "tc_cohort_set_states": ([P, P], I32),
-        "tc_cohort_get_v": ([P, P], I32),
+        "tc_cohort_set_states": ([P, I64, P, P], I32),
+        "tc_cohort_get_v": ([P, I64, P, P], I32),
         "tc_cohort_last_error": ([P], C.c_char_p),
         "tc_cohort_destroy": ([P], I32),
         "tc_mesh_pattern": ([I64, I64, P, P, P], I32),
@@ -367,7 +367,9 @@ def _ptr_array(arrs):
     for a in arrs:
         if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
             raise ValueError("cohort I/O: contiguous float64 arrays")
-    return (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    lens = np.array([a.size for a in arrs], np.int64)
+    return len(arrs), ptrs, lens
 
 
 def _co_check(co, st):
@@ -377,13 +379,16 @@ def _co_check(co, st):
 
 
 def tc_cohort_set_states(co, bufs) -> None:
-    """bufs: one tc_set_state-layout float64 host array per member (member order)."""
-    _co_check(co, _L.tc_cohort_set_states(co, _ptr_array(bufs)))
+    """bufs: one tc_set_state-layout float64 host array per member (member order);
+    the library checks the count and every length."""
+    cnt, ptrs, lens = _ptr_array(bufs)
+    _co_check(co, _L.tc_cohort_set_states(co, cnt, ptrs, _ptr(lens)))
 
 
 def tc_cohort_get_v(co, outs) -> None:
     """outs: one float64 host array of n_nodes per member, filled with V^k."""
-    _co_check(co, _L.tc_cohort_get_v(co, _ptr_array(outs)))
+    cnt, ptrs, lens = _ptr_array(outs)
+    _co_check(co, _L.tc_cohort_get_v(co, cnt, ptrs, _ptr(lens)))
 
 
 def tc_cohort_info(co) -> dict:

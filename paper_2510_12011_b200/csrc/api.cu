@@ -1694,11 +1694,11 @@ tc_status tc_set_state(tc_ctx* c, const double* buf, int64_t len) {
   const double kk = buf[(2 + c->nstates) * n], hp = buf[(2 + c->nstates) * n + 1];
   if (!(kk >= 0) || kk != std::floor(kk)) return fail(c, TC_EINVAL, "tc_set_state: bad step index");
   const int iv = c->iVk, ip = c->iVkm1;
-  if (!c->use_comm) {
-    // one H2D copy of every field into the staging buffer of tc_step_io, the
-    // permutation gathers on the device, one synchronisation (was: one per field)
-    CUDA_TRY(c, cudaSetDevice(c->device));
-    TC_TRY(io_setup(c));
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  // one H2D copy of every field into the staging buffer of tc_step_io, the
+  // permutation gathers on the device, one synchronisation (was: one per field);
+  // without room for the staging buffers, the per-field path below (n doubles)
+  if (!c->use_comm && (c->s_in || io_setup(c) == TC_OK)) {
     double* in = c->d_sin[0];
     CUDA_TRY(c, cudaMemcpyAsync(in, buf, (2 + c->nstates) * n * 8, cudaMemcpyHostToDevice, c->stream));
     for (Part& P : c->parts)
@@ -1726,17 +1726,46 @@ tc_status tc_set_state(tc_ctx* c, const double* buf, int64_t len) {
 // staging is double-buffered; events order every reuse.  Same arithmetic as
 // tc_set_state + tc_step(1) + tc_get_v per input.
 static tc_status io_setup(tc_ctx* c) {
-  if (c->s_in) return TC_OK;
-  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
-  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
-  for (int b = 0; b < 2; ++b) {
-    CUDA_TRY(c, cudaEventCreateWithFlags(&c->e_loaded[b], cudaEventDisableTiming));
-    CUDA_TRY(c, cudaEventCreateWithFlags(&c->e_used[b], cudaEventDisableTiming));
-    CUDA_TRY(c, cudaEventCreateWithFlags(&c->e_done[b], cudaEventDisableTiming));
-    CUDA_TRY(c, cudaEventCreateWithFlags(&c->e_read[b], cudaEventDisableTiming));
-    CUDA_TRY(c, dalloc(c, &c->d_sin[b], tc_state_len(c)));
-    CUDA_TRY(c, dalloc(c, &c->d_sout[b], c->n));
+  if (c->s_in) return TC_OK;  // set only once every stream, event and buffer exists
+  // Everything goes into locals first; a failure part-way frees what was made
+  // and leaves the context as before (no half-initialised staging).
+  cudaStream_t si = nullptr, so = nullptr;
+  cudaEvent_t ev[4][2] = {};
+  double* bin[2] = {nullptr, nullptr};
+  double* bout[2] = {nullptr, nullptr};
+  const int64_t len = tc_state_len(c);
+  cudaError_t e = cudaStreamCreateWithFlags(&si, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&so, cudaStreamNonBlocking);
+  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    for (int q = 0; q < 4 && e == cudaSuccess; ++q) e = cudaEventCreateWithFlags(&ev[q][b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMalloc(&bin[b], (size_t)std::max<int64_t>(len, 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&bout[b], (size_t)std::max<int64_t>(c->n, 1) * 8);
   }
+  if (e != cudaSuccess) {
+    for (int b = 0; b < 2; ++b) {
+      for (int q = 0; q < 4; ++q)
+        if (ev[q][b]) cudaEventDestroy(ev[q][b]);
+      if (bin[b]) cudaFree(bin[b]);
+      if (bout[b]) cudaFree(bout[b]);
+    }
+    if (si) cudaStreamDestroy(si);
+    if (so) cudaStreamDestroy(so);
+    cudaGetLastError();  // a failed cudaMalloc is not sticky; clear it
+    return fail(c, e == cudaErrorMemoryAllocation ? TC_ENOMEM : TC_ECUDA,
+                std::string("host I/O staging: ") + cudaGetErrorString(e));
+  }
+  for (int b = 0; b < 2; ++b) {
+    c->e_loaded[b] = ev[0][b];
+    c->e_used[b] = ev[1][b];
+    c->e_done[b] = ev[2][b];
+    c->e_read[b] = ev[3][b];
+    c->d_sin[b] = bin[b];
+    c->d_sout[b] = bout[b];
+    c->allocs.push_back(bin[b]);   // freed with the context
+    c->allocs.push_back(bout[b]);
+  }
+  c->s_out = so;
+  c->s_in = si;
   return TC_OK;
 }
 
@@ -2218,41 +2247,62 @@ tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
 // Batched member I/O: every member's copies and permutation kernels enqueued on
 // its own stream, then one synchronisation per member stream (tc_set_state /
 // tc_get_v per member synchronise once per call).
-tc_status tc_cohort_set_states(tc_cohort* co, const double* const* bufs) {
-  if (!co || !bufs) return TC_EINVAL;
+tc_status tc_cohort_set_states(tc_cohort* co, int64_t count, const double* const* bufs, const int64_t* lens) {
+  if (!co) return TC_EINVAL;
   const size_t cnt = co->m.size();
+  if (!bufs || !lens) return cfail(co, TC_EINVAL, "tc_cohort_set_states: null argument");
+  if (count != (int64_t)cnt)
+    return cfail(co, TC_EINVAL, "tc_cohort_set_states: " + std::to_string(count) + " states for " +
+                                    std::to_string(cnt) + " members");
   for (size_t i = 0; i < cnt; ++i) {  // validate every input before touching any member
     tc_ctx* c = co->m[i];
     if (!bufs[i]) return cfail(co, TC_EINVAL, "tc_cohort_set_states: null state of member " + std::to_string(i));
+    if (lens[i] != tc_state_len(c))
+      return cfail(co, TC_EINVAL, "tc_cohort_set_states: member " + std::to_string(i) + " state has " +
+                                      std::to_string(lens[i]) + " doubles, tc_state_len is " +
+                                      std::to_string(tc_state_len(c)));
     const double kk = bufs[i][(2 + c->nstates) * c->n];
     if (!(kk >= 0) || kk != std::floor(kk))
       return cfail(co, TC_EINVAL, "tc_cohort_set_states: bad step index in member " + std::to_string(i));
   }
   CO_CUDA(co, cudaSetDevice(co->device));
+  // staging for every member before any copy is enqueued: an allocation
+  // failure leaves every member unchanged
   for (size_t i = 0; i < cnt; ++i) {
     tc_ctx* c = co->m[i];
-    if (io_setup(c) != TC_OK) return cfail(co, TC_ECUDA, "cohort member " + std::to_string(i) + ": " + c->err);
+    const tc_status st = io_setup(c);
+    if (st != TC_OK) return cfail(co, st, "cohort member " + std::to_string(i) + ": " + c->err);
+  }
+  for (size_t i = 0; i < cnt; ++i) {
+    tc_ctx* c = co->m[i];
     const int64_t n = c->n;
     double* in = c->d_sin[0];
     CO_CUDA(co, cudaMemcpyAsync(in, bufs[i], (2 + c->nstates) * n * 8, cudaMemcpyHostToDevice, c->stream));
     for (Part& P : c->parts)
       CO_CUDA(co, launch_gather_state(P.n, c->d_perm_g + P.plan.g0, in, n, P.d_V[c->iVk], P.d_V[c->iVkm1], P.d_U,
                                       P.n_pad, c->nstates, c->stream));
+    // the step counter moves with the member's enqueued state
+    c->k = (int64_t)bufs[i][(2 + c->nstates) * n];
+    c->has_prev = bufs[i][(2 + c->nstates) * n + 1] != 0.0;
   }
-  for (size_t i = 0; i < cnt; ++i) {
-    tc_ctx* c = co->m[i];
-    CO_CUDA(co, cudaStreamSynchronize(c->stream));
-    c->k = (int64_t)bufs[i][(2 + c->nstates) * c->n];
-    c->has_prev = bufs[i][(2 + c->nstates) * c->n + 1] != 0.0;
-  }
+  for (size_t i = 0; i < cnt; ++i) CO_CUDA(co, cudaStreamSynchronize(co->m[i]->stream));
   return TC_OK;
 }
 
-tc_status tc_cohort_get_v(tc_cohort* co, double* const* v_out) {
-  if (!co || !v_out) return TC_EINVAL;
+tc_status tc_cohort_get_v(tc_cohort* co, int64_t count, double* const* v_out, const int64_t* lens) {
+  if (!co) return TC_EINVAL;
   const size_t cnt = co->m.size();
-  for (size_t i = 0; i < cnt; ++i)
+  if (!v_out || !lens) return cfail(co, TC_EINVAL, "tc_cohort_get_v: null argument");
+  if (count != (int64_t)cnt)
+    return cfail(co, TC_EINVAL, "tc_cohort_get_v: " + std::to_string(count) + " outputs for " +
+                                    std::to_string(cnt) + " members");
+  for (size_t i = 0; i < cnt; ++i) {
     if (!v_out[i]) return cfail(co, TC_EINVAL, "tc_cohort_get_v: null output of member " + std::to_string(i));
+    if (lens[i] != co->m[i]->n)
+      return cfail(co, TC_EINVAL, "tc_cohort_get_v: member " + std::to_string(i) + " output holds " +
+                                      std::to_string(lens[i]) + " doubles, the member has " +
+                                      std::to_string(co->m[i]->n) + " nodes");
+  }
   CO_CUDA(co, cudaSetDevice(co->device));
   for (size_t i = 0; i < cnt; ++i) {
     tc_ctx* c = co->m[i];

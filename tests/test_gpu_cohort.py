@@ -382,6 +382,17 @@ def test_cohort_batched_io_equals_serial_calls(T):
         assert ei.value.status == T.TC_EINVAL and "member 2" in str(ei.value)
         for s, b in zip(members, before):
             assert np.array_equal(s.get_state(), b)
+        # count and length mismatches are rejected in C before any member changes
+        for args, what in (([st.copy() for st in states[:2]], "2 states for 3 members"),
+                           ([states[0], states[1][:-3].copy(), states[2]], "member 1 state has")):
+            with pytest.raises(T.TcError) as ei:
+                co.set_states(args)
+            assert ei.value.status == T.TC_EINVAL and what in str(ei.value), str(ei.value)
+        with pytest.raises(T.TcError) as ei:
+            co.get_v([np.zeros(T.tc_num_nodes(s.ctx) + (1 if i == 1 else 0)) for i, s in enumerate(members)])
+        assert ei.value.status == T.TC_EINVAL and "member 1 output" in str(ei.value)
+        for s, b in zip(members, before):
+            assert np.array_equal(s.get_state(), b)
         co.close()
     finally:
         for s in members:

@@ -52,8 +52,8 @@ def test_cohort_io_argument_errors(lib):
     before any device work (include/tcb200.h); the binding rejects non-float64 arrays."""
     import numpy as np
     import paper_2510_12011_b200 as T
-    assert T._L.tc_cohort_set_states(None, None) == T.TC_EINVAL
-    assert T._L.tc_cohort_get_v(None, None) == T.TC_EINVAL
+    assert T._L.tc_cohort_set_states(None, 0, None, None) == T.TC_EINVAL
+    assert T._L.tc_cohort_get_v(None, 0, None, None) == T.TC_EINVAL
     with pytest.raises(ValueError):
         T._ptr_array([np.zeros(4, np.float32)])
     with pytest.raises(ValueError):
