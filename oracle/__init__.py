@@ -33,11 +33,12 @@ OR_OK, OR_EINVAL, OR_EDEGEN, OR_ENAN, OR_ENOMEM, OR_EREGION, OR_EFIBRE = range(7
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c with gcc (plain -O2, no FMA contraction, no fast-math)."""
+    """Compile oracle.c with gcc (plain -O2, no FMA contraction, no fast-math;
+    -fopenmp for the independent per-row / per-node loops)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         tmp = _SO + ".tmp%d" % os.getpid()
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", _SRC, "-o", tmp, "-lm"])
+                               "-fopenmp", "-fPIC", "-shared", _SRC, "-o", tmp, "-lm"])
         os.replace(tmp, _SO)
     return _SO
 
@@ -60,6 +61,9 @@ def _lib():
         L.or_tri_local.argtypes = [P, P, P, P, P]
         L.or_assemble.argtypes = [I64, P, I64, P, P, P, I32, P, P, P, P, P, P, P]
         L.or_rcm.argtypes = [I32, P, P, P]
+        L.or_set_threads.argtypes = [I32]
+        L.or_set_threads.restype = None
+        L.or_max_threads.restype = I32
         L.or_spmv.argtypes = [I32, P, P, P, P, P]
         L.or_spmv.restype = None
         L.or_pcg.argtypes = [I32, P, P, P, P, P, I32, D, D, I32, I32, P, P, P, P, P]
@@ -101,6 +105,25 @@ def _lib():
         L.or_crn_state_name.restype = C.c_char_p
         _L = L
     return _L
+
+
+def set_threads(k: int) -> None:
+    """Threads for the oracle's per-row / per-node loops (results are bitwise
+    independent of k; 1 = sequential)."""
+    max_threads()
+    _lib().or_set_threads(int(k))
+
+
+_DEFAULT_THREADS = None
+
+
+def max_threads() -> int:
+    """The OpenMP default (all host cores unless OMP_NUM_THREADS says otherwise),
+    captured before any set_threads call."""
+    global _DEFAULT_THREADS
+    if _DEFAULT_THREADS is None:
+        _DEFAULT_THREADS = int(_lib().or_max_threads())
+    return _DEFAULT_THREADS
 
 
 def _p(a: np.ndarray):

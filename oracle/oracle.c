@@ -7,8 +7,13 @@
  * constant generator with the CUDA path in paper_2510_12011_b200/ and neither
  * side includes or links the other.
  *
- * Everything is IEEE double, sequential loops, no blocking or fusion; built with
- * -O2 -ffp-contract=off (no FMA contraction, no fast-math).
+ * Everything is IEEE double, no blocking or fusion; built with -O2
+ * -ffp-contract=off (no FMA contraction, no fast-math) and -fopenmp.  OpenMP
+ * pragmas sit ONLY on loops whose iterations are independent (one output row /
+ * node per iteration: SpMV rows, PCG elementwise updates, per-node ionic
+ * steps), so every result is bitwise the same at any thread count
+ * (tests/test_oracle_solver.py::test_oracle_threads_bitwise); reductions (dot
+ * products), assembly and RCM stay sequential.  Thread count: or_set_threads.
  *
  * Citation convention: "P:n" = line n of the paper text,
  * "S:n" = line n of SPEC.md (used only for interfaces / tie rules), "SURVEY"
@@ -19,6 +24,9 @@
  */
 #include <math.h>
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -309,8 +317,25 @@ int or_rcm(int32_t n, const int32_t* rowptr, const int32_t* col, int32_t* perm) 
 /* ======================================================================== */
 /* 4. CSR SpMV ("exact CSR row-wise product in float64")              */
 /* ======================================================================== */
+/* threads for the per-row / per-node loops (1 = the sequential oracle) */
+void or_set_threads(int32_t k) {
+#ifdef _OPENMP
+  omp_set_num_threads(k > 0 ? k : 1);
+#else
+  (void)k;
+#endif
+}
+int32_t or_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
 void or_spmv(int32_t n, const int32_t* rowptr, const int32_t* col, const double* val,
              const double* x, double* y) {
+#pragma omp parallel for schedule(static)
   for (int32_t i = 0; i < n; ++i) {
     double s = 0.0;
     for (int32_t t = rowptr[i]; t < rowptr[i + 1]; ++t) s += val[t] * x[col[t]];
@@ -356,6 +381,7 @@ int or_pcg(int32_t n, const int32_t* rowptr, const int32_t* col, const double* v
   }
   /* r_0 = b - A x_0 ; M z_0 = r_0 ; p_0 = z_0 ; x = x_0 ; rho_0 = r_0^T z_0 */
   or_spmv(n, rowptr, col, val, x0, q);
+#pragma omp parallel for schedule(static)
   for (int32_t i = 0; i < n; ++i) {
     r[i] = b[i] - q[i];
     z[i] = r[i] / d[i];
@@ -374,8 +400,11 @@ int or_pcg(int32_t n, const int32_t* rowptr, const int32_t* col, const double* v
     double pq = dot(n, p, q);
     if (isnan(pq)) { status = OR_ENAN; goto done; }
     double alpha = rho / pq;                      /* alpha_k = rho_k / p_k^T q_k */
+#pragma omp parallel for schedule(static)
     for (int32_t i = 0; i < n; ++i) x[i] += alpha * p[i];    /* x = x + alpha p */
+#pragma omp parallel for schedule(static)
     for (int32_t i = 0; i < n; ++i) r[i] -= alpha * q[i];    /* r_{k+1} */
+#pragma omp parallel for schedule(static)
     for (int32_t i = 0; i < n; ++i) z[i] = r[i] / d[i];      /* M z_{k+1} = r_{k+1} (C2) */
     double zeta_new = sqrt(dot(n, z, z));
     if (trace) trace[k + 1] = zeta_new;
@@ -385,6 +414,7 @@ int or_pcg(int32_t n, const int32_t* rowptr, const int32_t* col, const double* v
     double rho_new = dot(n, r, z);                /* rho_{k+1} = r^T z */
     if (isnan(rho_new)) { status = OR_ENAN; goto done; }
     double beta = rho_new / rho;                  /* beta_k */
+#pragma omp parallel for schedule(static)
     for (int32_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
     rho = rho_new;
     if (rel_mode == 0) zref = zeta_new;           /* literal consecutive ratio (C1) */
@@ -413,6 +443,7 @@ void or_ms_step(int64_t n, const double* V, double* h, double dt, const double* 
                 double* In) {
   double tin = p[0], tout = p[1], topen = p[2], tclose = p[3], vg = p[4];
   double vmin = p[5], vrange = p[6] - p[5];
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) {
     double v = (V[i] - vmin) / vrange;
     double dh = (v < vg) ? (1.0 - h[i]) / topen : -h[i] / tclose;  /* g(V^k,u^k) */
@@ -651,8 +682,9 @@ static double tt_cell_step(double V, double* u, double dt, const double* p) {
 /* Field version: U is state-major SoA (U[s*n + i]). */
 void or_tt_step(int64_t n, const double* V, double* U, double dt, const double* p,
                 double* In) {
-  double u[TT_NS];
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) {
+    double u[TT_NS];
     for (int s = 0; s < TT_NS; ++s) u[s] = U[(int64_t)s * n + i];
     In[i] = tt_cell_step(V[i], u, dt, p);
     for (int s = 0; s < TT_NS; ++s) U[(int64_t)s * n + i] = u[s];
@@ -871,8 +903,9 @@ static double crn_cell_step(double V, double* u, double dt, const double* p) {
 }
 
 void or_crn_step(int64_t n, const double* V, double* U, double dt, const double* p, double* In) {
-  double u[CR_NS];
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) {
+    double u[CR_NS];
     for (int s = 0; s < CR_NS; ++s) u[s] = U[(int64_t)s * n + i];
     In[i] = crn_cell_step(V[i], u, dt, p);
     for (int s = 0; s < CR_NS; ++s) U[(int64_t)s * n + i] = u[s];

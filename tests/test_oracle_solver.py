@@ -204,3 +204,27 @@ def test_rcm_reduces_bandwidth_on_permuted_mesh():
     # same bandwidth class as scipy's RCM (a library routine, different ties)
     sperm = csg.reverse_cuthill_mckee(sp.csr_matrix((np.ones(len(col)), col, rp)), symmetric_mode=True)
     assert _bandwidth(rp, col, perm) <= 1.5 * _bandwidth(rp, col, np.asarray(sperm))
+
+
+@pytest.mark.parametrize("model", ["tt2006", "ms", "crn"])
+def test_oracle_threads_bitwise(model):
+    """The OpenMP pragmas sit only on independent per-row / per-node loops
+    (oracle.c header): a trajectory at 1 thread and at 4 threads is bitwise
+    identical (V, every cell state, LAT, iteration counts)."""
+    import meshgen as G
+    xyz, tets = G.kuhn_box(23, 9, 6, 0.5)
+    E = tets.shape[0]
+    stim = O.Stimulus(G.nodes_in_box(xyz, (0, 0, 0), (1.5, 1.5, 1.5)), 0.0, 2.0, 50.0)
+    runs = []
+    try:
+        for k in (1, 4):
+            O.set_threads(k)
+            sim = O.Monodomain(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E),
+                               {0: (0.1334177, 0.0173515)}, O.Config(dt=0.05, model=model), [stim]).run(60)
+            runs.append(sim)
+    finally:
+        O.set_threads(O.max_threads())
+    a, b = runs
+    assert np.array_equal(a.Vk, b.Vk) and np.array_equal(a.U, b.U) and np.array_equal(a.lat, b.lat)
+    assert [r.iters for r in a.reports] == [r.iters for r in b.reports]
+    assert (a.lat >= 0).any()
