@@ -18,14 +18,52 @@ namespace tcb {
 #endif
 constexpr int kExpTab = TCB_EXP_T64 ? 64 : 32;
 
-// 2^(j/N), j = 0..N-1, filled once per CTA into shared memory.
+constexpr int kLogTab = 64;
+
+// Per-CTA shared-memory tables of the branch-free exp and log:
+//   t[j]  = 2^(j/N), j = 0..N-1 (tc_exp);
+//   lg[j] = {c_j, -log c_j}, c_j = 1/(1 + (j + 1/2)/64) (tc_log; one 16-byte load).
 struct Exp2Table {
   double t[kExpTab];
+  double2 lg[kLogTab];
 };
 
 __device__ __forceinline__ void exp2_table_init(Exp2Table* T) {
   for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) T->t[j] = exp2((double)j / kExpTab);
+  for (int j = threadIdx.x; j < kLogTab; j += blockDim.x) {
+    const double c = 1.0 / (1.0 + (j + 0.5) / kLogTab);
+    T->lg[j] = make_double2(c, -log(c));
+  }
   __syncthreads();
+}
+
+// log(x) for positive normal x, branch-free (replaces libm log: ~80 SASS
+// instructions with special-case branches and 29 FP64 ops -> ~20 and 12).
+//   x = 2^e m, m in [1, 2);  j = top 6 mantissa bits;  r = m c_j - 1, |r| < 2^-7
+//   log x = e ln2 + (-log c_j) + log(1 + r),  log(1 + r) by its degree-7 Taylor
+//   polynomial (truncation |r|^8/8 < 1.7e-18 absolute, < 2.2e-16 of log(1 + r)).
+//   Accuracy ~2 ulp.  NaN / inf in,
+//   NaN out (the x * 0 term); zero, negative and denormal inputs are not
+//   handled (concentrations of the ionic models; a blown-up state still trips
+//   the NaN checks through V).
+__device__ __forceinline__ double tc_log(double x, const Exp2Table* __restrict__ T) {
+  const int hi = __double2hiint(x);
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(x));
+  const double2 cl = T->lg[(hi >> 14) & 63];
+  // e + 2^52 + 1023 as a double (biased exponent in the low word), x*0 carries NaN
+  const double eb = fma(x, 0.0, __hiloint2double(0x43300000, (unsigned)hi >> 20));
+  const double e = eb - 4503599627371519.0;             // - (2^52 + 1023)
+  const double r = fma(m, cl.x, -1.0);
+  double q = 1.0 / 7.0;
+  q = fma(q, r, -1.0 / 6.0);
+  q = fma(q, r, 0.2);
+  q = fma(q, r, -0.25);
+  q = fma(q, r, 1.0 / 3.0);
+  q = fma(q, r, -0.5);
+  const double l1p = fma(q, r * r, r);
+  const double kLn2Hi = 6.93147180369123816490e-01;     // 0x3FE62E42FEE00000: e * hi exact
+  const double kLn2Lo = 1.90821492927058770002e-10;
+  return fma(e, kLn2Hi, cl.y) + fma(e, kLn2Lo, l1p);
 }
 
 // Range.  The scale 2^m is added to the exponent field of v = 2^(j/N) P(r),
@@ -38,9 +76,20 @@ __device__ __forceinline__ void exp2_table_init(Exp2Table* T) {
 // -745 < x < -708 is 0 instead of a denormal (< 3.3e-308); NaN x gives 0 (a NaN
 // state still reaches the currents directly -- y in yinf - (yinf - y) e^x, V in
 // g (V - E) -- and the PCG NaN test); x > 2.3e7 is not handled.
+// TCB_EXP_SCALE (experiment): scale by a DMUL with 2^m built from the clamped m,
+// m in [-1022, 1023] (no compare / selects; e^x below -708 is a value below
+// 2.3e-308 instead of 0, NaN x stays NaN).
+#ifndef TCB_EXP_SCALE
+#define TCB_EXP_SCALE 0
+#endif
 __device__ __forceinline__ double exp_range(double x, double v, int m) {
+#if TCB_EXP_SCALE
+  const int mc = max(min(m, 1023), -1022);
+  return v * __hiloint2double((mc + 1023) << 20, 0);
+#else
   const double s = __hiloint2double(__double2hiint(v) + (min(m, 1023) << 20), __double2loint(v));
   return x >= -708.0 ? s : 0.0;
+#endif
 }
 
 // e^x = 2^m 2^(j/N) P(r),  x = (N m + j) ln2/N + r,  |r| <= ln2/(2N) (Cody-Waite);

@@ -20,8 +20,13 @@ namespace tcb {
 #define TCB_ION_THREADS 128   // measured: 128 / 256
 #endif
 constexpr int kIonThreads = TCB_ION_THREADS;
+// minimum resident CTAs per SM for the FP64-bound TT2006 / CRN kernels (register
+// cap 65536 / (threads x this)): 4 = 128 registers (no cap), 5 = 96, 6 = 80
+#ifndef TCB_ION_MINB
+#define TCB_ION_MINB 4
+#endif
 
-__global__ void __launch_bounds__(kIonThreads) ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D) {
+__global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB) ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D) {
   __shared__ Exp2Table T;
   exp2_table_init(&T);
   if (a.flags[0]) return;
@@ -57,6 +62,10 @@ TTDerived tt_derived(const TTParams& P) {
   D.cap_2vcf = P.CAP / (2.0 * P.Vc * P.F);
   D.cap_vcf = P.CAP / (P.Vc * P.F);
   D.kup2 = P.Kup * P.Kup;
+  D.log_ko = std::log(P.Ko);
+  D.log_nao = std::log(P.Nao);
+  D.log_eks_num = std::log(D.eks_num);
+  D.log_cao = std::log(P.Cao);
   D.x_m12 = std::exp(-12.0);        // (-60 - V)/5   = -12 - V/5
   D.x_7 = std::exp(7.0);            // (V + 35)/5    =   7 + V/5
   D.x_m3_2 = std::exp(-3.2);        // -0.1 (V + 32) = -3.2 - V/10
@@ -195,10 +204,13 @@ CRNDerived crn_derived(const CRNParams& P) {
   D.vrel_vup = P.Vrel / P.Vup;
   D.inv_kq10 = 1.0 / P.KQ10;
   D.fn_c = 1e-15 / (2.0 * P.F) * P.Cm;  // currents per capacitance -> pA
+  D.log_nao = std::log(P.Nao);
+  D.log_ko = std::log(P.Ko);
+  D.log_cao = std::log(P.Cao);
   return D;
 }
 
-__global__ void __launch_bounds__(kIonThreads) ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D) {
+__global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB) ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D) {
   __shared__ Exp2Table T;
   exp2_table_init(&T);
   if (a.flags[0]) return;

@@ -54,6 +54,7 @@ struct TTDerived {      // parameter-only factors (host-computed per launch)
   double vc_vss, vsr_vss, vsr_vc;
   double cap_2vssf, cap_2vcf, cap_vcf;
   double kup2;          // Kup^2
+  double log_ko, log_nao, log_eks_num, log_cao;   // logs of the Nernst numerators
   // e^c of the constant offsets of the shared-slope voltage exponentials
   double x_m12, x_7, x_m3_2, x_m26_7, x_m4_5, x_m3, x_5_6, x_20_6, x_4, x_m4, x_1, x_2_5, x_3,
       x_20_7, x_1_3, x_5, x_m1;
@@ -103,10 +104,12 @@ __device__ __forceinline__ TTVolt tt_volt(double V, const TTParams& P, const TTD
 
 TCB_CUR_ATTR TTCur tt_cur(double V, const double* u, const TTParams& P,
                                         const TTDerived& D, const TTVolt& f, const Exp2Table* T) {
-  const double ek = D.rtf * log(P.Ko * tc_rcp(u[sKi]));
-  const double ena = D.rtf * log(P.Nao * tc_rcp(u[sNai]));
-  const double eks = D.rtf * log(D.eks_num * tc_rcp(u[sKi] + P.pKNa * u[sNai]));
-  const double eca = 0.5 * D.rtf * log(P.Cao * tc_rcp(u[sCai]));
+  // Nernst potentials RT/F log(c_o / c_i) = RT/F (log c_o - log c_i): the
+  // numerators' logs come from the host, the branch-free tc_log does the rest
+  const double ek = D.rtf * (D.log_ko - tc_log(u[sKi], T));
+  const double ena = D.rtf * (D.log_nao - tc_log(u[sNai], T));
+  const double eks = D.rtf * (D.log_eks_num - tc_log(u[sKi] + P.pKNa * u[sNai], T));
+  const double eca = 0.5 * D.rtf * (D.log_cao - tc_log(u[sCai], T));
   TTCur c;
   c.ina = P.GNa * u[sm] * u[sm] * u[sm] * u[sh] * u[sj] * (V - ena);
   {
@@ -311,6 +314,7 @@ struct CRNDerived {   // parameter-only factors (host-computed)
   double inak_k;              // INaK_max Ko / (Ko + KmKo)
   double inaca_k;             // INaCa_max / ((KmNa^3 + Nao^3)(KmCa + Cao))
   double nao3, inv_tautr, iupleak_k, vup_vi, vrel_vi, vrel_vup, inv_kq10, fn_c;
+  double log_nao, log_ko, log_cao;   // logs of the Nernst numerators
 };
 
 struct CRNCur {
@@ -321,8 +325,8 @@ TCB_CUR_ATTR CRNCur crn_cur(double V, const double* u, const CRNParams& P,
                                           const CRNDerived& D, const Exp2Table* T) {
   CRNCur c;
   const double nai = u[cNai], ki = u[cKi], cai = u[cCai];
-  const double ena = D.rtf * log(P.Nao / nai), ek = D.rtf * log(P.Ko / ki);
-  const double eca = 0.5 * D.rtf * log(P.Cao / cai);
+  const double ena = D.rtf * (D.log_nao - tc_log(nai, T)), ek = D.rtf * (D.log_ko - tc_log(ki, T));
+  const double eca = 0.5 * D.rtf * (D.log_cao - tc_log(cai, T));
   const double m = u[cm], oa = u[coa], ua = u[cua], xs = u[cxs];
   c.ina = P.gNa * m * m * m * u[chh] * u[cj] * (V - ena);
   c.ik1 = P.gK1 * (V - ek) * tc_rcp(1.0 + EXP(0.07 * (V + 80.0)));
@@ -334,7 +338,7 @@ TCB_CUR_ATTR CRNCur crn_cur(double V, const double* u, const CRNParams& P,
   c.ical = P.gCaL * u[cd] * u[cf] * u[cfCa] * (V - 65.0);
   const double e = EXP(-V * D.frt);                         // exp(-F V / RT)
   const double fnak = tc_rcp(1.0 + 0.1245 * EXP(-0.1 * V * D.frt) + D.sigma_k * e);
-  const double q = P.KmNai / nai;
+  const double q = P.KmNai * tc_rcp(nai);
   c.inak = D.inak_k * fnak * tc_rcp(1.0 + q * sqrt(q));
   const double eg = EXP(P.gamma * V * D.frt), eg1 = eg * e;  // exp((gamma-1) F V / RT)
   c.inaca = D.inaca_k * (eg * nai * nai * nai * P.Cao - eg1 * D.nao3 * cai) *
