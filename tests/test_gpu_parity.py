@@ -363,29 +363,41 @@ def test_ionic_params_match_oracle_transcription(T):
             T.tc_destroy(ctx)
 
 
-def test_mms_on_gpu_matches_oracle_and_converges(T):
+def test_mms_on_gpu_matches_oracle_and_converges(T, golden):
+    """configs[1] (readings M2/M3/T1): h-refinement N = 8, 16, 32, 64
+    on the GPU.  N <= 32: V at T equals the oracle's to 1e-8 and the M-norm
+    errors equal the independent direct-solve values of SURVEY 8(c)
+    (tests/golden/mms_reference_errors.json); every ratio N -> 2N has observed
+    L2 order in [1.7, 2.3], including 32 -> 64."""
+    g = golden["mms_reference_errors"]
     errs = []
-    for N in (8, 16):
+    for N in (8, 16, 32, 64):
         xyz, tets = G.unit_cube(N)
         B = G.box_boundary(xyz)
         dt = 0.01 * 8 / N
-        out = O.run_mms(xyz, tets, B, dt=dt, T=0.5, tol=1e-10)
         E = tets.shape[0]
         cfg = T.tc_config_default(dt=dt, model="mms", chi=1.0, cm=1.0, abs_tol=1e-10, rel_tol=1e-10,
                                   max_iters=1000)
         sim = T.Monodomain(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: (1.0, 1.0)}, cfg,
                            mms=(1.0, np.pi, np.pi, np.pi, B))
         try:
-            sim.step(int(round(0.5 / dt)))
+            st = sim.step(int(round(0.5 / dt)))
             v = sim.V
         finally:
             sim.close()
-        assert np.abs(v - out["V"]).max() <= 1e-8
+        assert st["converged"].all()
         e = v - O.mms_w(xyz[:, 0], xyz[:, 1], 0.5)
         rp, col, M, _ = O.assemble(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: (1.0, 1.0)})
         errs.append(np.sqrt(e @ O.spmv(rp, col, M, e)))
-    order = np.log2(errs[0] / errs[1])
-    assert 1.7 < order < 2.3
+        if N <= 32:
+            out = O.run_mms(xyz, tets, B, dt=dt, T=0.5, tol=1e-10)
+            assert np.abs(v - out["V"]).max() <= 1e-8, N
+            i = g["N"].index(N)
+            assert errs[-1] == pytest.approx(g["err_M"][i], rel=g["rel_tol"]), (N, errs[-1])
+        print(f"MMS N={N}: ||e||_M = {errs[-1]:.4e}, mean PCG iterations {np.mean(st['iters']):.1f}")
+    orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    print("observed orders", orders)
+    assert np.all((orders > 1.7) & (orders < 2.3)), orders
 
 
 @pytest.mark.parametrize("model,parts,rot,engine,variant", [("ms", 1, False, "grid", -1), ("tt2006", 1, True, "cluster", -1),
