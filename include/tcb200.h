@@ -118,7 +118,12 @@ typedef struct {
   int32_t device_setup;  /* 1 (default): single-partition systems build their pattern, RCM,
                             SELL layout and element incidence on the GPU (
                             identical result to the host path); 0: host setup */
-  int32_t reserved;
+  int32_t peer_timeout_s; /* multi-GPU peer kernels: wall-clock bound (seconds, %globaltimer)
+                            of every wait for another rank (halo flags, reduction slots,
+                            group barriers); a rank that does not answer within it turns
+                            the step into TC_ENCCL instead of a hang.  0 = default 300 s
+                            (a collective-style timeout: rank skew from host-side work such
+                            as checkpoint writes stays far below it) */
 } tc_config;
 
 /* Per-step PCG report. */
@@ -131,7 +136,7 @@ typedef struct {
 /* Fills the defaults: theta 0.5, dt 0.01, chi 140, cm 0.01, tolerances 1e-5,
  * max_iters 100, consecutive rel-mode, TT2006 epi, fail_budget 3,
  * thresholds 0 / -70 mV, use_rcm 1, pcg_variant -1, partitions 1, check_every 4, peer 1,
- * engine auto, device_setup 1. */
+ * engine auto, device_setup 1, peer_timeout_s 0 (= 300 s). */
 void tc_config_default(tc_config* cfg);
 
 /* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
@@ -224,7 +229,10 @@ tc_status tc_get_activation(tc_ctx* ctx, double* lat, double* lrt);
  * f2 fCass), 1 (MS: h), 0 (MMS).  has_prev = 0 means V^{k-1} := V^k.
  * Both calls return once buf has been read / written (the caller owns buf;
  * tc_set_state is one host->device copy and one synchronisation in a
- * single-process context, staging in the tc_step_io buffers). */
+ * single-process context, staging in the tc_step_io buffers, or one copy per
+ * field when those buffers cannot be allocated).  tc_set_state also clears a
+ * sticky abort of the context (NaN, fail budget, peer timeout): the new state
+ * is a fresh start. */
 int64_t tc_state_len(const tc_ctx* ctx);
 tc_status tc_get_state(tc_ctx* ctx, double* buf, int64_t len);
 tc_status tc_set_state(tc_ctx* ctx, const double* buf, int64_t len);

@@ -47,7 +47,7 @@ class tc_config(C.Structure):
                 ("use_rcm", C.c_int32), ("pcg_variant", C.c_int32),
                 ("partitions", C.c_int32), ("check_every", C.c_int32),
                 ("peer", C.c_int32), ("engine", C.c_int32), ("device_setup", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("peer_timeout_s", C.c_int32)]
 
 
 class tc_step_stat(C.Structure):

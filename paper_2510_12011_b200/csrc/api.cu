@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -35,6 +36,7 @@ struct Part {
   PartPlan plan;
   int64_t n = 0, n_pad = 0, n_ghost = 0, n_vec = 0, nnz = 0, nnz_pad = 0;
   int32_t nslices = 0;
+  int32_t nslices_int = 0;  // leading slices without ghost columns (interior-first order, P > 1)
   int64_t n_wide = 0;
   int grid = 1;  // persistent kernel grid (1 part) or split-kernel grid
   int pcg_var = 0;  // PCG kernel variant launched for this part (cg_pick_variant)
@@ -127,6 +129,8 @@ struct tc_ctx {
   double* d_io = nullptr;          // original-order staging for host I/O
   // tc_step_io: copy streams, double-buffered device staging, events
   cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaStream_t s_halo = nullptr;           // split path: halo exchange stream (overlapped)
+  cudaEvent_t e_packed = nullptr, e_halo = nullptr;
   double* d_sin[2] = {nullptr, nullptr};   // staged input states (original order)
   double* d_sout[2] = {nullptr, nullptr};  // staged outputs V^{k+1} (original order)
   cudaEvent_t e_loaded[2] = {}, e_used[2] = {}, e_done[2] = {}, e_read[2] = {};
@@ -135,6 +139,7 @@ struct tc_ctx {
   int64_t nnz = 0;
   int nstates = 0;
   int32_t* d_flags = nullptr;
+  double* d_sync = nullptr;         // multi-GPU peer path: the entry all-reduce's element
   tc_step_stat* d_stats = nullptr;
   int64_t stats_cap = 0;
   int iVk = 0, iVkm1 = 1, iX = 2;
@@ -217,7 +222,7 @@ static unsigned long long* inbox_flags(char* inbox, int world) {
 
 extern "C" {
 
-int32_t tc_abi_version(void) { return 3; }
+int32_t tc_abi_version(void) { return 4; }
 
 void tc_config_default(tc_config* c) {
   c->theta = 0.5;
@@ -239,7 +244,7 @@ void tc_config_default(tc_config* c) {
   c->peer = 1;
   c->engine = TC_ENGINE_AUTO;
   c->device_setup = 1;
-  c->reserved = 0;
+  c->peer_timeout_s = 0;
 }
 
 tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx** out) {
@@ -292,6 +297,12 @@ tc_status tc_destroy(tc_ctx* c) {
       cudaEventDestroy(c->e_done[b]);
       cudaEventDestroy(c->e_read[b]);
     }
+  }
+  if (c->s_halo) {
+    cudaStreamSynchronize(c->s_halo);
+    cudaStreamDestroy(c->s_halo);
+    cudaEventDestroy(c->e_packed);
+    cudaEventDestroy(c->e_halo);
   }
   free_all(c);
   c->comm.destroy();
@@ -592,6 +603,7 @@ static tc_status setup_peer(tc_ctx* c, const std::vector<PartPlan>& plans) {
   if (bpg_rhs < 1) ok = false;
   if (bpg < 1) ok = false;
   if (!c->use_comm && !ok) return TC_OK;
+  if (c->use_comm && !c->d_sync) CUDA_TRY(c, dalloc(c, &c->d_sync, 1));
   for (Part& P : c->parts) {
     CUDA_TRY(c, dalloc(c, &P.d_inbox, (int64_t)inbox_bytes(world)));
     CUDA_TRY(c, dalloc(c, &P.d_bar, 2));
@@ -678,6 +690,7 @@ static tc_status setup_peer(tc_ctx* c, const std::vector<PartPlan>& plans) {
     X = XPart{};
     X.slice_ptr = P.d_sp; X.col = P.d_col; X.A = P.d_A; X.K = P.d_K; X.dinv = P.d_dinv;
     X.nslices = P.nslices;
+    X.nslices_int = P.nslices_int;
     X.nbr_count = (int32_t)P.plan.nbr.size();
     for (int b = 0; b < 3; ++b) X.V[b] = P.d_V[b];
     X.r = P.d_r; X.z = P.d_z; X.q = P.d_q; X.p0 = P.d_p0; X.p1 = P.d_p1; X.up = P.d_up; X.vp = P.d_vp;
@@ -736,6 +749,34 @@ static tc_status assemble_host(tc_ctx* c, const std::vector<int32_t>& ereg, std:
   std::vector<int64_t> rp2;
   std::vector<int32_t> col2;
   permute_csr(n, rp, col, c->perm, c->inv, rp2, col2);
+  // Interior-first order inside every row block: the
+  // rows of block [g0, g1) with no column outside it come first, the boundary
+  // rows (those that read ghosts) last, each group in RCM order.  The blocks
+  // and their ghost sets are unchanged; the S / RHS passes then run the
+  // interior slices while the halo is in flight.  TCB_NO_INTERIOR_FIRST=1
+  // (environment, A/B measurements) keeps the plain RCM order.
+  std::vector<int64_t> n_int(c->nparts, 0);
+  const char* nif = std::getenv("TCB_NO_INTERIOR_FIRST");
+  if (c->nparts > 1 && !(nif && nif[0] == '1')) {
+    std::vector<int32_t> pnew(n);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int p = 0; p < c->nparts; ++p) {
+      const int64_t g0 = (n * p) / c->nparts, g1 = (n * (p + 1)) / c->nparts;  // plan_partitions' bounds
+      std::vector<uint8_t> inner(g1 - g0, 1);
+      for (int64_t i = g0; i < g1; ++i)
+        for (int64_t t = rp2[i]; t < rp2[i + 1]; ++t)
+          if (col2[t] < g0 || col2[t] >= g1) { inner[i - g0] = 0; break; }
+      int64_t w = g0;
+      for (int64_t i = g0; i < g1; ++i)
+        if (inner[i - g0]) pnew[w++] = c->perm[i];
+      n_int[p] = w - g0;
+      for (int64_t i = g0; i < g1; ++i)
+        if (!inner[i - g0]) pnew[w++] = c->perm[i];
+    }
+    c->perm.swap(pnew);
+    for (int64_t i = 0; i < n; ++i) c->inv[c->perm[i]] = (int32_t)i;
+    permute_csr(n, rp, col, c->perm, c->inv, rp2, col2);
+  }
   rp.clear(); rp.shrink_to_fit(); col.clear(); col.shrink_to_fit();
   c->nnz = rp2[n];
   std::vector<int32_t> tets2((int64_t)k * E);
@@ -746,6 +787,7 @@ static tc_status assemble_host(tc_ctx* c, const std::vector<int32_t>& ereg, std:
   build_incidence(n, E, k, tets2.data(), iptr, inc);
   // partitions
   plan_partitions(n, rp2.data(), col2.data(), c->nparts, plans);
+  for (int p = 0; p < c->nparts; ++p) plans[p].n_interior = n_int[p];
   c->bounds.resize(c->nparts + 1);
   for (int p = 0; p < c->nparts; ++p) c->bounds[p] = plans[p].g0;
   c->bounds[c->nparts] = n;
@@ -790,6 +832,7 @@ static tc_status assemble_host(tc_ctx* c, const std::vector<int32_t>& ereg, std:
     std::vector<int32_t> colg;
     local_sell(P.plan, rp2.data(), col2.data(), hs, colg);
     P.nslices = hs.nslices;
+    P.nslices_int = (int32_t)(P.plan.n_interior / kSellC);
     P.n_pad = hs.n_pad;
     P.n_ghost = (int64_t)P.plan.ghosts.size();
     P.n_vec = P.n_pad + P.n_ghost;
@@ -1185,6 +1228,9 @@ static SplitArgs split_args(tc_ctx* c, Part& P) {
   a.K = P.d_K;
   a.dinv = P.d_dinv;
   a.nslices = P.nslices;
+  a.s0 = 0;
+  a.s1 = P.nslices;
+  a.phase = 2;
   a.x = P.d_V[c->iX];
   a.r = P.d_r;
   a.z = P.d_z;
@@ -1228,7 +1274,7 @@ static int local_index(const tc_ctx* c, int gid) {
 // halo: values packed in each part's send buffer (at offset `half` x n_send)
 // land in the receivers' ghost regions of dst(part)
 template <class DstF>
-static tc_status halo_exchange(tc_ctx* c, int half, DstF dst) {
+static tc_status halo_exchange(tc_ctx* c, int half, DstF dst, cudaStream_t hs) {
   if (c->use_comm) {
     Part& P = c->parts[0];
     std::vector<HaloMsg> sends, recvs;
@@ -1239,7 +1285,7 @@ static tc_status halo_exchange(tc_ctx* c, int half, DstF dst) {
       recvs.push_back({P.plan.nbr[j], dst(P) + P.n_pad + P.plan.recv_off[j],
                        (size_t)(P.plan.recv_off[j + 1] - P.plan.recv_off[j])});
     }
-    NCCL_TRY(c, c->comm.exchange(sends, recvs, c->stream));
+    NCCL_TRY(c, c->comm.exchange(sends, recvs, hs));
     return TC_OK;
   }
   for (Part& R : c->parts) {  // receiver
@@ -1252,7 +1298,7 @@ static tc_status halo_exchange(tc_ctx* c, int half, DstF dst) {
       if (cnt)
         CUDA_TRY(c, cudaMemcpyAsync(dst(R) + R.n_pad + R.plan.recv_off[j],
                                     S.d_send_buf + half * ns + S.plan.send_off[js], cnt * 8,
-                                    cudaMemcpyDeviceToDevice, c->stream));
+                                    cudaMemcpyDeviceToDevice, hs));
     }
   }
   return TC_OK;
@@ -1268,18 +1314,74 @@ static tc_status allreduce(tc_ctx* c, int slot) {
   return TC_OK;
 }
 
+// The halo runs on its own stream (NCCL send/recv, or the loopback copies),
+// overlapped with the interior slices of the following S / RHS pass; the
+// boundary slices wait for it (interior-first row order).
+static tc_status halo_stream(tc_ctx* c) {
+  if (c->s_halo) return TC_OK;
+  cudaStream_t h = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&e0, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&e1, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    if (h) cudaStreamDestroy(h);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    return fail(c, TC_ECUDA, std::string("halo stream: ") + cudaGetErrorString(e));
+  }
+  c->e_packed = e0;
+  c->e_halo = e1;
+  c->s_halo = h;
+  return TC_OK;
+}
+
+// pass(P, args) launches one S or RHS pass of part P with the given SplitArgs;
+// halo(): enqueue the exchange on stream hs.
+template <class Pass, class Halo>
+static tc_status overlapped_pass(tc_ctx* c, Pass pass, Halo halo) {
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c, cudaEventRecord(c->e_packed, s));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s_halo, c->e_packed, 0));
+  TC_TRY(halo(c->s_halo));
+  CUDA_TRY(c, cudaEventRecord(c->e_halo, c->s_halo));
+  for (Part& P : c->parts) {
+    if (P.nslices_int > 0) {
+      SplitArgs a = split_args(c, P);
+      a.s0 = 0;
+      a.s1 = P.nslices_int;
+      a.phase = 0;
+      CUDA_TRY(c, pass(P, a));
+    }
+  }
+  CUDA_TRY(c, cudaStreamWaitEvent(s, c->e_halo, 0));
+  for (Part& P : c->parts) {
+    SplitArgs a = split_args(c, P);
+    a.s0 = P.nslices_int;
+    a.s1 = P.nslices;
+    a.phase = P.nslices_int > 0 ? 1 : 2;
+    CUDA_TRY(c, pass(P, a));
+    c->launches += P.nslices_int > 0 ? 1 : 0;
+  }
+  return TC_OK;
+}
+
 // RHS + Algorithm 1 on the partitioned system
 static tc_status pcg_split(tc_ctx* c) {
   cudaStream_t s = c->stream;
-  // halo of u' and v' (once per step)
+  TC_TRY(halo_stream(c));
+  // halo of u' and v' (once per step), overlapped with the interior rows of the RHS
   for (Part& P : c->parts) {
     const int64_t ns = (int64_t)P.plan.send_g.size();
     CUDA_TRY(c, launch_pack_gather(ns, P.d_send_idx, P.d_up, P.d_send_buf, s));
     CUDA_TRY(c, launch_pack_gather(ns, P.d_send_idx, P.d_vp, P.d_send_buf + ns, s));
   }
-  TC_TRY(halo_exchange(c, 0, [](Part& P) { return P.d_up; }));
-  TC_TRY(halo_exchange(c, 1, [](Part& P) { return P.d_vp; }));
-  for (Part& P : c->parts) CUDA_TRY(c, launch_split_rhs(split_args(c, P), P.grid, s));
+  TC_TRY(overlapped_pass(
+      c, [&](Part& P, const SplitArgs& a) { return launch_split_rhs(a, P.grid, s); },
+      [&](cudaStream_t hs) -> tc_status {
+        TC_TRY(halo_exchange(c, 0, [](Part& P) { return P.d_up; }, hs));
+        return halo_exchange(c, 1, [](Part& P) { return P.d_vp; }, hs);
+      }));
   TC_TRY(allreduce(c, 0));
   for (Part& P : c->parts) CUDA_TRY(c, launch_split_init(split_args(c, P), s));
   for (Part& P : c->parts) c->launches += 2 + (P.plan.send_g.empty() ? 0 : 2);
@@ -1288,8 +1390,9 @@ static tc_status pcg_split(tc_ctx* c) {
   while (true) {
     for (int q = 0; q < c->cfg.check_every; ++q) {
       for (Part& P : c->parts) CUDA_TRY(c, launch_split_pack_p(split_args(c, P), s));
-      TC_TRY(halo_exchange(c, 0, [](Part& P) { return P.d_z; }));
-      for (Part& P : c->parts) CUDA_TRY(c, launch_split_S(split_args(c, P), P.grid, s));
+      TC_TRY(overlapped_pass(
+          c, [&](Part& P, const SplitArgs& a) { return launch_split_S(a, P.grid, s); },
+          [&](cudaStream_t hs) { return halo_exchange(c, 0, [](Part& P) { return P.d_z; }, hs); }));
       TC_TRY(allreduce(c, 1));
       for (Part& P : c->parts) CUDA_TRY(c, launch_split_U(split_args(c, P), P.grid, s));
       TC_TRY(allreduce(c, 0));
@@ -1449,8 +1552,17 @@ static tc_status enqueue_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* dstats, 
     if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
     // (3) RHS + Algorithm 1
     if (c->peer) {
+      // ranks enter the peer kernels of a tc_step call together: a one-element
+      // NCCL all-reduce on the stream before the first of them (device-side;
+      // host-side skew between calls never reaches the kernels' bounded waits)
+      if (st == 0 && c->use_comm) {
+        NCCL_TRY(c, c->comm.allreduce_sum(c->d_sync, 1, c->stream));
+        c->launches += 1;
+      }
+      const unsigned long long tmo =
+          1000000000ull * (unsigned long long)(c->cfg.peer_timeout_s > 0 ? c->cfg.peer_timeout_s : 300);
       CUDA_TRY(c, launch_pcg_peer(c->xparts.data(), (int)c->parts.size(), c->peer_bpg, c->peer_bpg_rhs, c->peer_batch, c->iX, c->iVk,
-                                  c->cfg.abs_tol, c->cfg.rel_tol, c->cfg.max_iters, c->cfg.rel_mode,
+                                  tmo, c->cfg.abs_tol, c->cfg.rel_tol, c->cfg.max_iters, c->cfg.rel_mode,
                                   dstats + st, c->d_flags, (int32_t)c->k, c->stream));
       c->launches += 2;  // RHS + loop kernels
     } else if (split_mode(c)) {
@@ -1691,6 +1803,11 @@ tc_status tc_set_state(tc_ctx* c, const double* buf, int64_t len) {
   if (!c->assembled) return fail(c, TC_ESTATE, "tc_set_state before tc_assemble");
   if (len != tc_state_len(c)) return fail(c, TC_EINVAL, "tc_set_state: wrong length");
   const int64_t n = c->n;
+  {  // a new state is a fresh start: clear a sticky abort (NaN, fail budget, peer timeout)
+    int32_t flags[8] = {0, 0, 0, c->cfg.fail_budget, -1, 0, 0, 0};
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_flags, flags, sizeof(flags), cudaMemcpyHostToDevice, c->stream));
+  }
   const double kk = buf[(2 + c->nstates) * n], hp = buf[(2 + c->nstates) * n + 1];
   if (!(kk >= 0) || kk != std::floor(kk)) return fail(c, TC_EINVAL, "tc_set_state: bad step index");
   const int iv = c->iVk, ip = c->iVkm1;

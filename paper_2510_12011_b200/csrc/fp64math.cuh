@@ -10,13 +10,14 @@
 
 namespace tcb {
 
-// TCB_EXP_T64 (default): 64-entry table and a degree-5 polynomial (|r| <= ln2/128,
-// truncation r^6/720 < 3.5e-17 relative); 0: 32 entries and degree 6.  Measured:
-// TT2006 ionic 1.374 -> 1.328 ms, CRN 1.400 -> 1.377 ms at 10 M nodes.
-#ifndef TCB_EXP_T64
-#define TCB_EXP_T64 1
+// Exp table size: TCB_EXP_TAB = 256 (default): 256-entry table and a degree-4
+// polynomial (|r| <= ln2/512, truncation r^5/120 < 3.8e-17 relative); 64: degree 5
+// (r01 default, truncation < 3.5e-17); 32: degree 6.
+#ifndef TCB_EXP_TAB
+#define TCB_EXP_TAB 256
 #endif
-constexpr int kExpTab = TCB_EXP_T64 ? 64 : 32;
+constexpr int kExpTab = TCB_EXP_TAB;
+constexpr int kExpShift = TCB_EXP_TAB == 256 ? 8 : (TCB_EXP_TAB == 64 ? 6 : 5);
 
 constexpr int kLogTab = 64;
 
@@ -106,52 +107,54 @@ static __device__ __noinline__ double tc_exp(double x, const Exp2Table* __restri
 __device__ __forceinline__ double tc_exp(double x, const Exp2Table* __restrict__ T) {
 #endif
   const double kShift = 6755399441055744.0;             // 1.5 * 2^52
-#if TCB_EXP_T64
-  const double kInvLn2_64 = 92.33248261689366;          // 64 / ln 2
-  const double kLn2_64_hi = 0.01083042469326756;        // (ln 2)_hi / 64
-  const double kLn2_64_lo = 2.9815858269852933e-12;     // (ln 2)_lo / 64
-  const double kd = fma(x, kInvLn2_64, kShift);
-  const int k = __double2loint(kd);
+  // x = (N m + j) ln2/N + r (Cody-Waite: ln2/N in a hi part exact for |k| < 2^20 and a lo part)
+  const double kInvLn2N = kExpTab / 0.69314718055994530942;
+  const double kLn2N_hi = 0.69314718036912381649 / kExpTab;   // ln2_hi (0x3FE62E42FEE00000) / N
+  const double kLn2N_lo = 1.9082149292705877000e-10 / kExpTab;
+  const double kd = fma(x, kInvLn2N, kShift);
+  const int k = __double2loint(kd);                     // round-to-nearest integer
   const double kf = kd - kShift;
-  double r = fma(-kf, kLn2_64_hi, x);
-  r = fma(-kf, kLn2_64_lo, r);
+  double r = fma(-kf, kLn2N_hi, x);
+  r = fma(-kf, kLn2N_lo, r);
+#if TCB_EXP_TAB == 256
+  double p = 1.0 / 24.0;
+  p = fma(p, r, 1.0 / 6.0);
+#elif TCB_EXP_TAB == 64
   double p = 1.0 / 120.0;
   p = fma(p, r, 1.0 / 24.0);
   p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  const double v = T->t[k & 63] * p;
-  return exp_range(x, v, k >> 6);
 #else
-  const double kInvLn2_32 = 46.16624130844683;          // 32 / ln 2
-  const double kLn2_32_hi = 0.02166084938653512;        // (ln 2)_hi / 32, 32 significant bits
-  const double kLn2_32_lo = 5.9631716539705866e-12;     // (ln 2)_lo / 32
-  const double kd = fma(x, kInvLn2_32, kShift);
-  const int k = __double2loint(kd);                     // round-to-nearest integer
-  const double kf = kd - kShift;
-  double r = fma(-kf, kLn2_32_hi, x);
-  r = fma(-kf, kLn2_32_lo, r);
   double p = 1.0 / 720.0;
   p = fma(p, r, 1.0 / 120.0);
   p = fma(p, r, 1.0 / 24.0);
   p = fma(p, r, 1.0 / 6.0);
+#endif
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const double v = T->t[k & 31] * p;
-  return exp_range(x, v, k >> 5);
-#endif
+  const double v = T->t[k & (kExpTab - 1)] * p;
+  return exp_range(x, v, k >> kExpShift);
 }
 
-// 1/b: hardware approximation + two Newton steps (relative error ~1e-16).
+// 1/b: hardware approximation r0 (MUFU.RCP64H, ~2^-22 relative) refined by
+// r = r0 (1 + e + e^2), e = 1 - b r0 (error e^3 ~ 2^-66 plus rounding: as
+// accurate as two Newton steps, 3 dependent DFMA instead of 4).
+// TCB_RCP_NEWTON2 = 1: the two Newton steps of r01.
+#ifndef TCB_RCP_NEWTON2
+#define TCB_RCP_NEWTON2 0
+#endif
 __device__ __forceinline__ double tc_rcp(double b) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+#if TCB_RCP_NEWTON2
   double e = fma(-b, r, 1.0);
   r = fma(r, e, r);
   e = fma(-b, r, 1.0);
   return fma(r, e, r);
+#else
+  const double e = fma(-b, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+#endif
 }
 
 // a/b with one residual correction.

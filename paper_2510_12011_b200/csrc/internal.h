@@ -134,6 +134,8 @@ struct SplitArgs {
   const double* K;
   const double* dinv;
   int32_t nslices;
+  int32_t s0, s1;        // slice range of this S / RHS launch ([0, nslices_int) interior, then the rest)
+  int32_t phase;         // S / RHS: 0 interior launch (partials kept per CTA), 1 boundary launch (+ reduce), 2 both
   double* x;
   double* r;
   double* z;             // ghost region receives the neighbours' p
@@ -171,6 +173,7 @@ struct XPart {
   const double* K;
   const double* dinv;
   int32_t nslices, nbr_count;
+  int32_t nslices_int;           // leading slices whose rows have no ghost column (no halo wait)
   double* V[3];
   double *r, *z, *q, *p0, *p1, *up, *vp;
   double2* part;                 // 2 x CTAs-per-group partials
@@ -190,6 +193,8 @@ struct XPart {
   unsigned long long* epoch;      // [0] epoch counter, [1] cross-rank reductions done
   double2* red0;                  // rho_0, ||z_0||^2 handed from the RHS kernel to the loop
   int32_t rank, world;
+  int32_t* flags;                 // the context's flags ([5] peer timeout), set per launch
+  unsigned long long timeout_ns;  // bound of every wait (%globaltimer), set per launch
 };
 
 struct IonArgs {
@@ -360,7 +365,8 @@ cudaError_t launch_sum_partials(double2* const* reds, int nparts, int slot, cuda
 int peer_blocks_per_sm(int which);  // 0 loop kernel, 1 RHS kernel, 2 loop kernel (batch variant)
 int peer_max_groups();
 // parts: HOST array of `groups` XParts (passed by value in kernel-parameter space)
-cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, bool batch, int iX, int iVk, double eps_a,
+cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, bool batch, int iX, int iVk,
+                            unsigned long long timeout_ns, double eps_a,
                             double eps_r, int32_t max_iters, int32_t rel_mode, tc_step_stat* stat,
                             int32_t* flags, int32_t step_tag, cudaStream_t s);
 
@@ -403,6 +409,7 @@ cudaError_t dev_gather3(int64_t n, const int32_t* perm, const double* in, double
 // contiguous rows [g0, g1); ghosts = columns of owned rows outside the block.
 struct PartPlan {
   int64_t g0 = 0, g1 = 0;
+  int64_t n_interior = 0;          // leading owned rows with no ghost column (interior-first order)
   std::vector<int32_t> ghosts;     // sorted internal indices
   std::vector<int32_t> nbr;        // neighbour parts, ascending
   std::vector<int64_t> recv_off;   // nbr.size()+1 offsets into ghosts (ghosts of one owner are contiguous)

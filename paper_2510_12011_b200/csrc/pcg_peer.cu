@@ -6,7 +6,10 @@
 //   halo  : p_it = z + beta p_{it-1} of the send-list nodes is stored straight
 //           into the neighbours' ghost regions of z (remote stores), then a
 //           per-neighbour flag carries the epoch; readers wait on their flags
-//   S     : q = A p, x += alpha p_{it-1}, p.q partial -> rank sum (group barrier)
+//   S     : q = A p, x += alpha p_{it-1}, p.q partial -> rank sum (group barrier);
+//           rows are numbered interior-first, so every CTA runs its share of
+//           the interior slices (no ghost column) before it waits for the
+//           halo, and only the boundary slices after it
 //   reduce: the rank sum is stored into slot [epoch&1][rank] of EVERY rank's
 //           inbox, then every CTA waits for all ranks' slots of this epoch and
 //           sums them in rank order -> bitwise-identical scalars on all ranks
@@ -15,18 +18,22 @@
 // store; readers poll with volatile loads, then __threadfence() (which also
 // drops stale L1 lines) before touching the data.  Slots are double-buffered
 // by epoch parity (a rank can be at most one reduction ahead of another).
-// Every wait is bounded (~2 s): on timeout the kernel records an error flag,
-// skips all further waits and finishes its iterations; tc_step reports
-// TC_ENCCL.  With several groups in one cooperative launch on one GPU the same
+// Every wait is bounded in wall-clock time (%globaltimer; tc_config.peer_timeout_s,
+// default 300 s, like a collective timeout): on timeout the kernel records an
+// error flag in the context's flags, skips all further waits and finishes its
+// iterations; tc_step reports TC_ENCCL.  The launch state (PeerRun) is built
+// per call and every flag pointer belongs to the launching context, so
+// independent contexts never share launch state.  With several groups in one cooperative launch on one GPU the same
 // code runs the partitions of a single device ("peer emulation"), which is how
 // the protocol is tested without 8 GPUs.
+#include <memory>
+
 #include "pcg_common.cuh"
 
 namespace tcb {
 
 constexpr int kPeerThreads = kPeerThreadsHost;
 constexpr int kPeerWarps = kPeerThreads / 32;
-constexpr long long kWaitCycles = 4000000000LL;  // ~2 s at 1.9 GHz
 
 constexpr int kMaxGroups = 8;  // partitions of one GPU in a peer launch (kernel-parameter space)
 
@@ -58,25 +65,29 @@ __device__ __forceinline__ void vstore2(double2* p, double2 v) {
   q[1] = v.y;
 }
 
-__device__ int32_t* g_peer_flags;  // flags of the running launch (timeouts)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Barrier of the CTAs of one group (sense-reversing generation counter),
 // bounded like every other wait.
-__device__ __forceinline__ void group_barrier(unsigned int* count, unsigned int* gen, int nblocks) {
+__device__ __forceinline__ void group_barrier(const XPart& X, int nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned int* vg = gen;
+    volatile unsigned int* vg = X.bar_gen;
     const unsigned int g = *vg;
     __threadfence();
-    if (atomicAdd(count, 1u) == (unsigned int)nblocks - 1) {
-      *count = 0u;
+    if (atomicAdd(X.bar_count, 1u) == (unsigned int)nblocks - 1) {
+      *X.bar_count = 0u;
       __threadfence();
-      atomicAdd(gen, 1u);
+      atomicAdd(X.bar_gen, 1u);
     } else {
-      const long long t0 = clock64();
+      const unsigned long long t0 = gtimer();
       while (*vg == g) {
-        if (clock64() - t0 > kWaitCycles) {
-          atomicExch(g_peer_flags + 5, 1);
+        if (gtimer() - t0 > X.timeout_ns) {
+          atomicExch(X.flags + 5, 1);
           break;
         }
       }
@@ -89,11 +100,11 @@ __device__ __forceinline__ void group_barrier(unsigned int* count, unsigned int*
 // Deterministic sum over the group's CTAs (valid in every thread of every CTA).
 // part: 2 x nb slots, alternated by the caller's reduction counter (a CTA can be
 // one reduction ahead of another, never two: the next barrier separates them).
-__device__ __forceinline__ double2 group_sum2(double2 v, double2* part, int lb, int nb, double2* sh,
-                                              unsigned int* bc, unsigned int* bg) {
+__device__ __forceinline__ double2 group_sum2(const XPart& X, double2 v, double2* part, int lb, int nb,
+                                              double2* sh) {
   const double2 b = block_sum2(v, sh);
   if (threadIdx.x == 0) part[lb] = b;
-  group_barrier(bc, bg, nb);
+  group_barrier(X, nb);
   double2 acc = make_double2(0.0, 0.0);
   for (int t = threadIdx.x; t < nb; t += blockDim.x) {
     const double2 u = __ldcg(part + t);
@@ -106,12 +117,12 @@ __device__ __forceinline__ double2 group_sum2(double2 v, double2* part, int lb, 
 // Bounded spin until *p == want (GE: *p >= want), thread 0 of a CTA; false on timeout.
 template <bool GE>
 __device__ __forceinline__ bool wait_for(const unsigned long long* p, unsigned long long want,
-                                         int32_t* flags) {
-  const long long t0 = clock64();
+                                         const XPart& X) {
+  const unsigned long long t0 = gtimer();
   while (GE ? vload(p) < want : vload(p) != want) {
-    if (*reinterpret_cast<volatile int32_t*>(flags + 5)) return false;
-    if (clock64() - t0 > kWaitCycles) {
-      atomicExch(flags + 5, 1);
+    if (*reinterpret_cast<volatile int32_t*>(X.flags + 5)) return false;
+    if (gtimer() - t0 > X.timeout_ns) {
+      atomicExch(X.flags + 5, 1);
       return false;
     }
   }
@@ -122,8 +133,7 @@ __device__ __forceinline__ bool wait_for(const unsigned long long* p, unsigned l
 // Slot parity follows the reduction count `nr` (not the epoch, which halos also
 // advance): a rank cannot start reduction nr+2 before every rank has read nr.
 __device__ __forceinline__ double2 cross_sum2(const XPart& X, double2 v, unsigned long long epoch,
-                                              unsigned long long nr, int lb, int32_t* flags,
-                                              double2* sh1) {
+                                              unsigned long long nr, int lb, double2* sh1) {
   const int slot = (int)(nr & 1ull);
   if (lb == 0 && threadIdx.x == 0) {
     for (int r = 0; r < X.world; ++r) {
@@ -134,7 +144,7 @@ __device__ __forceinline__ double2 cross_sum2(const XPart& X, double2 v, unsigne
     }
   }
   if (threadIdx.x == 0) {
-    for (int r = 0; r < X.world; ++r) wait_for<false>(&X.myred[slot * X.world + r].e, epoch, flags);
+    for (int r = 0; r < X.world; ++r) wait_for<false>(&X.myred[slot * X.world + r].e, epoch, X);
     __threadfence();
     double2 s = make_double2(0.0, 0.0);
     for (int r = 0; r < X.world; ++r) {
@@ -163,13 +173,13 @@ __device__ __forceinline__ void halo_push(const XPart& X, int which, unsigned lo
     wrote = true;
   }
   if (wrote) __threadfence_system();   // this thread's remote stores before the flag
-  group_barrier(X.bar_count, X.bar_gen, nb);
+  group_barrier(X, nb);
   if (lb == 0 && threadIdx.x < X.nbr_count) vstore(X.rflag[threadIdx.x], epoch);
 }
 
-__device__ __forceinline__ void halo_wait(const XPart& X, unsigned long long epoch, int32_t* flags) {
+__device__ __forceinline__ void halo_wait(const XPart& X, unsigned long long epoch) {
   if (threadIdx.x == 0) {
-    for (int q = 0; q < X.nbr_count; ++q) wait_for<true>(X.myflag[q], epoch, flags);
+    for (int q = 0; q < X.nbr_count; ++q) wait_for<true>(X.myflag[q], epoch, X);
     __threadfence();
   }
   __syncthreads();
@@ -195,9 +205,8 @@ __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_
   halo_push(X, 1, ep, lb, nb, [&](int32_t i) { return X.up[i]; });
   ++ep;
   halo_push(X, 2, ep, lb, nb, [&](int32_t i) { return X.vp[i]; });
-  halo_wait(X, ep, R.flags);  // flags are monotone: >= ep covers both halos
   double2 acc = make_double2(0.0, 0.0);
-  for (int s = gw; s < X.nslices; s += nw) {
+  auto row = [&](int s) {
     const int64_t base = __ldg(X.slice_ptr + s);
     const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
     const int64_t i = (int64_t)s * kSellC + lane;
@@ -207,11 +216,15 @@ __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_
     X.z[i] = zi;
     acc.x += sum * zi;
     acc.y += zi * zi;
-  }
-  double2 tot = group_sum2(acc, X.part, lb, nb, sh, X.bar_count, X.bar_gen);
+  };
+  // interior slices (no ghost column) while the halo is in flight, then the rest
+  for (int s = gw; s < X.nslices_int; s += nw) row(s);
+  halo_wait(X, ep);  // flags are monotone: >= ep covers both halos
+  for (int s = X.nslices_int + gw; s < X.nslices; s += nw) row(s);
+  double2 tot = group_sum2(X, acc, X.part, lb, nb, sh);
   ++ep;
-  tot = cross_sum2(X, tot, ep, nrx++, lb, R.flags, &sh1);
-  group_barrier(X.bar_count, X.bar_gen, nb);  // every CTA is done with the counters
+  tot = cross_sum2(X, tot, ep, nrx++, lb, &sh1);
+  group_barrier(X, nb);  // every CTA is done with the counters
   if (lb == 0 && threadIdx.x == 0) {
     *X.red0 = tot;
     X.epoch[0] = ep;
@@ -253,12 +266,13 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
       // halo of p_it into the neighbours' z ghosts
       ++ep;
       halo_push(X, 0, ep, lb, nb, [&](int32_t i) { return first ? X.z[i] : X.z[i] + beta * pold[i]; });
-      halo_wait(X, ep, R.flags);
-      // S (separate first / later loops, as in the single-GPU kernel)
+      // S (separate first / later loops, as in the single-GPU kernel): the
+      // interior slices overlap the halo, the boundary slices wait for it
       acc = make_double2(0.0, 0.0);
       const ColIdx ci{X.col, nullptr, nullptr};
+      const int ni = X.nslices_int;
       if (first) {
-        for (int s = gw; s < ns; s += nw) {
+        auto row = [&](int s) {
           const int64_t base = __ldg(X.slice_ptr + s);
           const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
           const int64_t i = (int64_t)s * kSellC + lane;
@@ -268,9 +282,12 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
           pnew[i] = pi;
           X.q[i] = sum;
           acc.x += pi * sum;
-        }
+        };
+        for (int s = gw; s < ni; s += nw) row(s);
+        halo_wait(X, ep);
+        for (int s = ni + gw; s < ns; s += nw) row(s);
       } else {
-        for (int s = gw; s < ns; s += nw) {
+        auto row = [&](int s) {
           const int64_t base = __ldg(X.slice_ptr + s);
           const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
           const int64_t i = (int64_t)s * kSellC + lane;
@@ -283,12 +300,15 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
           pnew[i] = pi;
           X.q[i] = sum;
           acc.x += pi * sum;
-        }
+        };
+        for (int s = gw; s < ni; s += nw) row(s);
+        halo_wait(X, ep);
+        for (int s = ni + gw; s < ns; s += nw) row(s);
       }
       plast = it & 1;
-      tot = group_sum2(acc, X.part + (nred++ & 1) * nb, lb, nb, sh, X.bar_count, X.bar_gen);
+      tot = group_sum2(X, acc, X.part + (nred++ & 1) * nb, lb, nb, sh);
       ++ep;
-      tot = cross_sum2(X, tot, ep, nrx++, lb, R.flags, &sh1);
+      tot = cross_sum2(X, tot, ep, nrx++, lb, &sh1);
       const double pq = tot.x;
       if (isnan(pq)) { nan = 1; break; }
       alpha = rho / pq;
@@ -303,9 +323,9 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
         acc.x += ri * zi;
         acc.y += zi * zi;
       }
-      tot = group_sum2(acc, X.part + (nred++ & 1) * nb, lb, nb, sh, X.bar_count, X.bar_gen);
+      tot = group_sum2(X, acc, X.part + (nred++ & 1) * nb, lb, nb, sh);
       ++ep;
-      tot = cross_sum2(X, tot, ep, nrx++, lb, R.flags, &sh1);
+      tot = cross_sum2(X, tot, ep, nrx++, lb, &sh1);
       ++it;
       zeta = sqrt(tot.y);
       if (isnan(zeta) || isnan(tot.x)) { nan = 1; break; }
@@ -323,7 +343,7 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
     }
   }
   // all CTAs of the group are past their last use of the epoch counter
-  group_barrier(X.bar_count, X.bar_gen, nb);
+  group_barrier(X, nb);
   if (lb == 0 && threadIdx.x == 0) {
     X.epoch[0] = ep;
     X.epoch[1] = nrx;
@@ -360,20 +380,25 @@ int peer_blocks_per_sm(int which) {
 
 int peer_max_groups() { return kMaxGroups; }
 
-cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, bool batch, int iX, int iVk, double eps_a,
-                            double eps_r, int32_t max_iters, int32_t rel_mode, tc_step_stat* stat,
-                            int32_t* flags, int32_t step_tag, cudaStream_t s) {
+cudaError_t launch_pcg_peer(const XPart* parts, int groups, int bpg, int bpg_rhs, bool batch, int iX, int iVk,
+                            unsigned long long timeout_ns, double eps_a, double eps_r, int32_t max_iters,
+                            int32_t rel_mode, tc_step_stat* stat, int32_t* flags, int32_t step_tag, cudaStream_t s) {
   if (groups < 1 || groups > kMaxGroups) return cudaErrorInvalidValue;
-  static PeerRun R;  // large: keep it off the stack (host, one launch at a time per process)
-  for (int g = 0; g < groups; ++g) R.parts[g] = parts[g];
+  // per call (kernel parameters are copied at launch): no state shared between
+  // contexts or host threads (large: heap, not stack)
+  std::unique_ptr<PeerRun> Rp(new PeerRun());
+  PeerRun& R = *Rp;
+  for (int g = 0; g < groups; ++g) {
+    R.parts[g] = parts[g];
+    R.parts[g].flags = flags;
+    R.parts[g].timeout_ns = timeout_ns;
+  }
   R.groups = groups; R.iX = iX; R.iVk = iVk; R.eps_a = eps_a; R.eps_r = eps_r;
   R.max_iters = max_iters; R.rel_mode = rel_mode; R.stat = stat; R.flags = flags; R.step_tag = step_tag;
-  cudaError_t e = cudaMemcpyToSymbolAsync(g_peer_flags, &flags, sizeof(flags), 0, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return e;
   void* args[] = {(void*)&R};
   R.bpg = bpg_rhs;
-  e = cudaLaunchCooperativeKernel((const void*)rhs_peer_kernel, dim3(groups * bpg_rhs), dim3(kPeerThreads),
-                                  args, 0, s);
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)rhs_peer_kernel, dim3(groups * bpg_rhs),
+                                              dim3(kPeerThreads), args, 0, s);
   if (e != cudaSuccess) return e;
   R.bpg = bpg;
   return cudaLaunchCooperativeKernel(peer_fn(batch ? 2 : 0), dim3(groups * bpg), dim3(kPeerThreads),

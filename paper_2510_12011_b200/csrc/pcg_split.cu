@@ -49,6 +49,27 @@ __device__ __forceinline__ void reduce_to_rank(double2 acc, double2* part, unsig
   }
 }
 
+// Halo overlap: the rows of a partition are numbered
+// interior-first, so an S / RHS pass runs as two launches on the same grid --
+// phase 0 over the interior slices [0, nslices_int) while the halo is in
+// flight, phase 1 over the rest once it has landed.  Phase 0 leaves each CTA's
+// partial in part[grid + blockIdx]; phase 1 adds it to its own before the
+// deterministic reduction (the same per-CTA order at any timing).  Phase 2 =
+// one launch over every slice (no halo).
+__device__ __forceinline__ void reduce_phase(const SplitArgs& a, double2 acc, double2* out, double2* sh) {
+  if (a.phase == 0) {
+    const double2 b = block_sum2(acc, sh);
+    if (threadIdx.x == 0) a.part[gridDim.x + blockIdx.x] = b;
+    return;
+  }
+  if (a.phase == 1 && threadIdx.x == 0) {
+    const double2 b0 = a.part[gridDim.x + blockIdx.x];
+    acc.x += b0.x;   // thread 0 carries the interior partial into the block sum
+    acc.y += b0.y;
+  }
+  reduce_to_rank(acc, a.part, a.ticket, out, sh);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kSplitThreads, 4) split_rhs_kernel(SplitArgs a) {
   __shared__ double2 sh[kSplitWarps];
@@ -56,7 +77,7 @@ __global__ void __launch_bounds__(kSplitThreads, 4) split_rhs_kernel(SplitArgs a
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * kSplitWarps + (threadIdx.x >> 5), nw = gridDim.x * kSplitWarps;
   double2 acc = make_double2(0.0, 0.0);
-  for (int s = gw; s < a.nslices; s += nw) {
+  for (int s = a.s0 + gw; s < a.s1; s += nw) {
     const int64_t base = __ldg(a.slice_ptr + s);
     const int w = (int)((__ldg(a.slice_ptr + s + 1) - base) >> 5);
     const int64_t i = (int64_t)s * kSellC + lane;
@@ -67,7 +88,7 @@ __global__ void __launch_bounds__(kSplitThreads, 4) split_rhs_kernel(SplitArgs a
     acc.x += sum * zi;
     acc.y += zi * zi;
   }
-  reduce_to_rank(acc, a.part, a.ticket, a.red, sh);
+  reduce_phase(a, acc, a.red, sh);
 }
 
 // rho_0 = r.z, ||z_0|| from the all-reduced sums (reading C4: ||z_0|| < eps_a -> done)
@@ -112,7 +133,7 @@ __global__ void __launch_bounds__(kSplitThreads, 8) split_S_kernel(SplitArgs a) 
   const double* __restrict__ pold = (s.it & 1) ? a.p0 : a.p1;
   const bool first = s.it == 0;
   double2 acc = make_double2(0.0, 0.0);
-  for (int sl = gw; sl < a.nslices; sl += nw) {
+  for (int sl = a.s0 + gw; sl < a.s1; sl += nw) {
     const int64_t base = __ldg(a.slice_ptr + sl);
     const int w = (int)((__ldg(a.slice_ptr + sl + 1) - base) >> 5);
     const int64_t i = (int64_t)sl * kSellC + lane;
@@ -132,7 +153,7 @@ __global__ void __launch_bounds__(kSplitThreads, 8) split_S_kernel(SplitArgs a) 
     a.q[i] = sum;
     acc.x += pi * sum;
   }
-  reduce_to_rank(acc, a.part, a.ticket, a.red + 1, sh);
+  reduce_phase(a, acc, a.red + 1, sh);
 }
 
 __global__ void __launch_bounds__(kSplitThreads, 8) split_U_kernel(SplitArgs a) {

@@ -4,7 +4,7 @@
 #   bash tools/exp_ionic_r02.sh   -> ionic ms/step at 10 M nodes (TT2006, CRN)
 cd "$(dirname "$0")/.."
 # r01 = the library before the table log (built from the parent commit by hand)
-VARS="base: minb5:-DTCB_ION_MINB=5 minb6:-DTCB_ION_MINB=6 scale:-DTCB_EXP_SCALE=1 minb5s:-DTCB_ION_MINB=5+-DTCB_EXP_SCALE=1"
+VARS="new: new5:-DTCB_ION_MINB=5 t64:-DTCB_EXP_TAB=64 nwt2:-DTCB_RCP_NEWTON2=1 logonly:-DTCB_EXP_TAB=64+-DTCB_RCP_NEWTON2=1 new6:-DTCB_ION_MINB=6"
 if [ "$1" == "build" ]; then
   for v in $VARS; do n=${v%%:*}; f=$(echo ${v#*:} | tr + ' ')
     bash tools/build_variant.sh tools/ion_$n.so $f; done; exit 0
