@@ -38,6 +38,15 @@ extern "C" {
 
 typedef struct tc_ctx tc_ctx;
 
+/* Device allocator callbacks (the torch caching allocator).
+ * alloc(bytes, cuda_stream, user) returns device memory of at least `bytes`
+ * on the context's device, usable on cuda_stream, or NULL; release(ptr,
+ * cuda_stream, user) gives it back.  Called from the thread that calls the
+ * library, during setup (tc_assemble, first tc_step_io / tc_set_state) and
+ * tc_destroy; never inside tc_step. */
+typedef void* (*tc_alloc_fn)(size_t bytes, void* cuda_stream, void* user);
+typedef void (*tc_free_fn)(void* ptr, void* cuda_stream, void* user);
+
 typedef enum {
   TC_OK = 0,
   TC_EINVAL = 1,   /* bad argument (index out of range, bad size, zero fibre ...) */
@@ -149,6 +158,14 @@ tc_status tc_destroy(tc_ctx* ctx);
 
 /* Message describing the last error on ctx ("" if none). */
 const char* tc_last_error(const tc_ctx* ctx);
+/* Route the context's persistent device memory (matrix, vectors, cell state,
+ * I/O staging) through the caller's allocator (both callbacks, or both NULL
+ * for cudaMalloc).  Call right after tc_create, before anything allocates
+ * (TC_ESTATE otherwise).  Ignored for multi-process contexts (tc_comm_init),
+ * whose buffers are shared over CUDA IPC and need whole cudaMalloc blocks.
+ * Setup scratch memory is always cudaMalloc'ed and freed within the call.
+ * The callbacks and `user` must stay valid until tc_destroy returns. */
+tc_status tc_set_allocator(tc_ctx* ctx, tc_alloc_fn alloc, tc_free_fn release, void* user);
 
 /* Mesh.  xyz: n_nodes*3 doubles (mm).  tets: n_tets*4
  * zero-based node indices (any orientation; negatively oriented tets get two
@@ -378,6 +395,13 @@ tc_status tc_mesh_pattern(int64_t n, int64_t n_tets, const int32_t* tets, int64_
 /* Reverse Cuthill-McKee of a symmetric pattern (SPEC S:146 tie rules);
  * perm[new] = old. */
 tc_status tc_rcm(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t* perm);
+/* Interior-first order of the nparts row blocks of a pattern in internal order
+ * (what tc_assemble applies to partitioned systems):
+ * order[new] = old, n_interior[p] (nparts entries) = leading rows of block p
+ * with no column outside the block; the multi-GPU PCG computes those while
+ * the halo is in flight.  Blocks and ghost sets are unchanged. */
+tc_status tc_interior_first(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t nparts,
+                            int32_t* order, int64_t* n_interior);
 /* The row-block partition plan of part `part` (of nparts) for a pattern in
  * internal order: sizes = {ghosts, neighbours, send entries, owned rows};
  * bounds (nparts+1), ghosts (sorted), nbr, recv_off (nbr+1), send_off (nbr+1),

@@ -22,7 +22,7 @@ __all__ = [
     "tc_num_nodes", "tc_current_step", "tc_get_v", "tc_get_activation", "tc_state_len",
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
     "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "tc_nccl_unique_id", "tc_comm_init",
-    "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "Monodomain", "LIB_PATH",
+    "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "tc_interior_first", "tc_set_allocator", "TorchAllocator", "Monodomain", "LIB_PATH",
     "tc_engine_info", "tc_node_order", "tc_apply", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_set_states", "tc_cohort_get_v", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
     "TC_ENGINE_AUTO", "TC_ENGINE_GRID", "TC_ENGINE_CLUSTER",
     "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS", "TC_ION_CRN",
@@ -116,6 +116,8 @@ def _load():
         "tc_mesh_pattern": ([I64, I64, P, P, P], I32),
         "tc_rcm": ([I64, P, P, P], I32),
         "tc_partition_plan": ([I64, P, P, I32, I32, P, P, P, P, P, P, P], I32),
+        "tc_interior_first": ([I64, P, P, I32, P, P], I32),
+        "tc_set_allocator": ([P, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -432,6 +434,57 @@ def tc_rcm(rowptr, col):
     return perm
 
 
+def tc_interior_first(rowptr, col, nparts: int):
+    """-> (order[new] = old, n_interior per block) of the interior-first block order."""
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    col = _i32(col)
+    n = rowptr.shape[0] - 1
+    order = np.zeros(n, np.int32)
+    nint = np.zeros(nparts, np.int64)
+    st = _L.tc_interior_first(n, _ptr(rowptr), _ptr(col), nparts, _ptr(order), _ptr(nint))
+    if st != TC_OK:
+        raise TcError(st, "tc_interior_first")
+    return order, nint
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class TorchAllocator:
+    """tc_set_allocator callbacks backed by torch's CUDA caching allocator
+    (SURVEY 8(b)); keeps the ctypes trampolines alive and counts live blocks."""
+
+    def __init__(self, device: int = 0):
+        import torch
+        self.torch, self.device, self.live = torch, device, {}
+
+        def _alloc(nbytes, stream, user):
+            try:
+                p = self.torch.cuda.caching_allocator_alloc(int(nbytes), self.device, int(stream or 0))
+            except Exception:
+                return None
+            self.live[p] = int(nbytes)
+            return p
+
+        def _free(ptr, stream, user):
+            if ptr:
+                self.live.pop(int(ptr), None)
+                self.torch.cuda.caching_allocator_delete(int(ptr))
+
+        self.alloc_fn = ALLOC_FN(_alloc)
+        self.free_fn = FREE_FN(_free)
+
+
+def tc_set_allocator(ctx, allocator) -> None:
+    """allocator: an object with alloc_fn / free_fn ctypes callbacks (TorchAllocator), or None."""
+    if allocator is None:
+        _check(ctx, _L.tc_set_allocator(ctx, None, None, None))
+    else:
+        _check(ctx, _L.tc_set_allocator(ctx, C.cast(allocator.alloc_fn, C.c_void_p),
+                                        C.cast(allocator.free_fn, C.c_void_p), None))
+
+
 def tc_partition_plan(rowptr, col, nparts: int, part: int) -> dict:
     rowptr = np.ascontiguousarray(rowptr, np.int64)
     col = _i32(col)
@@ -484,9 +537,12 @@ class Monodomain:
 
     def __init__(self, xyz, tets, region, fibre, conductivities: dict, cfg: tc_config,
                  stimuli=(), device: int = 0, stream: int = 0, mms=None, params: dict | None = None,
-                 comm=None):
+                 comm=None, allocator=None):
         self.ctx = tc_create(cfg, device, stream)
+        self.allocator = allocator        # kept alive until close()
         try:
+            if allocator is not None:
+                tc_set_allocator(self.ctx, allocator)
             if comm is not None:          # (rank, world, nccl_unique_id)
                 tc_comm_init(self.ctx, *comm)
             tc_set_mesh(self.ctx, xyz, tets, region, fibre)

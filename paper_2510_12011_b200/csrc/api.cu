@@ -139,6 +139,9 @@ struct tc_ctx {
   int64_t nnz = 0;
   int nstates = 0;
   int32_t* d_flags = nullptr;
+  tc_alloc_fn alloc_fn = nullptr;   // tc_set_allocator (nullable)
+  tc_free_fn free_fn = nullptr;
+  void* alloc_user = nullptr;
   double* d_sync = nullptr;         // multi-GPU peer path: the entry all-reduce's element
   tc_step_stat* d_stats = nullptr;
   int64_t stats_cap = 0;
@@ -180,11 +183,28 @@ static tc_status fail(tc_ctx* c, tc_status st, const std::string& msg) {
     if (s_ != TC_OK) return s_;     \
   } while (0)
 
+// Device memory owned by the context: through the caller's allocator
+// (tc_set_allocator, e.g. torch's caching allocator) when one is set and the
+// context is single-process, cudaMalloc otherwise (multi-process buffers are
+// shared over CUDA IPC, which needs whole cudaMalloc allocations).
+static cudaError_t raw_alloc(tc_ctx* c, void** v, size_t bytes) {
+  if (c->alloc_fn && !c->use_comm) {
+    *v = c->alloc_fn(bytes, (void*)c->stream, c->alloc_user);
+    return *v ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  return cudaMalloc(v, bytes);
+}
+static void raw_free(tc_ctx* c, void* v) {
+  if (!v) return;
+  if (c->alloc_fn && !c->use_comm) c->free_fn(v, (void*)c->stream, c->alloc_user);
+  else cudaFree(v);
+}
+
 template <class T>
 static cudaError_t dalloc(tc_ctx* c, T** p, int64_t count) {
   size_t bytes = (size_t)std::max<int64_t>(count, 1) * sizeof(T);
   void* v = nullptr;
-  cudaError_t e = cudaMalloc(&v, bytes);
+  cudaError_t e = raw_alloc(c, &v, bytes);
   if (e != cudaSuccess) return e;
   c->allocs.push_back(v);
   *p = (T*)v;
@@ -206,7 +226,7 @@ static void free_all(tc_ctx* c) {
     }
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   c->ipc_opened.clear();
-  for (void* p : c->allocs) cudaFree(p);
+  for (void* p : c->allocs) raw_free(c, p);
   c->allocs.clear();
   for (auto e : c->evs) cudaEventDestroy(e);
   c->evs.clear();
@@ -312,6 +332,25 @@ tc_status tc_destroy(tc_ctx* c) {
 }
 
 const char* tc_last_error(const tc_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+tc_status tc_set_allocator(tc_ctx* c, tc_alloc_fn alloc, tc_free_fn release, void* user) {
+  if (!c) return TC_EINVAL;
+  if ((alloc == nullptr) != (release == nullptr)) return fail(c, TC_EINVAL, "tc_set_allocator: both or neither");
+  // tc_create's flag word is the only allocation allowed so far: move it
+  const bool only_flags = c->allocs.size() == 1 && c->allocs[0] == (void*)c->d_flags;
+  if (c->assembled || !(c->allocs.empty() || only_flags))
+    return fail(c, TC_ESTATE, "tc_set_allocator after device memory was allocated");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (void* p : c->allocs) raw_free(c, p);
+  c->allocs.clear();
+  c->d_flags = nullptr;
+  c->alloc_fn = alloc;
+  c->free_fn = release;
+  c->alloc_user = user;
+  CUDA_TRY(c, dalloc(c, &c->d_flags, 8));
+  return TC_OK;
+}
 
 int64_t tc_num_nodes(const tc_ctx* c) { return c ? c->n : 0; }
 int64_t tc_current_step(const tc_ctx* c) { return c ? c->k : 0; }
@@ -758,21 +797,9 @@ static tc_status assemble_host(tc_ctx* c, const std::vector<int32_t>& ereg, std:
   std::vector<int64_t> n_int(c->nparts, 0);
   const char* nif = std::getenv("TCB_NO_INTERIOR_FIRST");
   if (c->nparts > 1 && !(nif && nif[0] == '1')) {
-    std::vector<int32_t> pnew(n);
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int p = 0; p < c->nparts; ++p) {
-      const int64_t g0 = (n * p) / c->nparts, g1 = (n * (p + 1)) / c->nparts;  // plan_partitions' bounds
-      std::vector<uint8_t> inner(g1 - g0, 1);
-      for (int64_t i = g0; i < g1; ++i)
-        for (int64_t t = rp2[i]; t < rp2[i + 1]; ++t)
-          if (col2[t] < g0 || col2[t] >= g1) { inner[i - g0] = 0; break; }
-      int64_t w = g0;
-      for (int64_t i = g0; i < g1; ++i)
-        if (inner[i - g0]) pnew[w++] = c->perm[i];
-      n_int[p] = w - g0;
-      for (int64_t i = g0; i < g1; ++i)
-        if (!inner[i - g0]) pnew[w++] = c->perm[i];
-    }
+    std::vector<int32_t> order, pnew(n);
+    interior_first(n, rp2.data(), col2.data(), c->nparts, order, n_int);
+    for (int64_t i = 0; i < n; ++i) pnew[i] = c->perm[order[i]];
     c->perm.swap(pnew);
     for (int64_t i = 0; i < n; ++i) c->inv[c->perm[i]] = (int32_t)i;
     permute_csr(n, rp, col, c->perm, c->inv, rp2, col2);
@@ -1855,15 +1882,15 @@ static tc_status io_setup(tc_ctx* c) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&so, cudaStreamNonBlocking);
   for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
     for (int q = 0; q < 4 && e == cudaSuccess; ++q) e = cudaEventCreateWithFlags(&ev[q][b], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaMalloc(&bin[b], (size_t)std::max<int64_t>(len, 1) * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&bout[b], (size_t)std::max<int64_t>(c->n, 1) * 8);
+    if (e == cudaSuccess) e = raw_alloc(c, (void**)&bin[b], (size_t)std::max<int64_t>(len, 1) * 8);
+    if (e == cudaSuccess) e = raw_alloc(c, (void**)&bout[b], (size_t)std::max<int64_t>(c->n, 1) * 8);
   }
   if (e != cudaSuccess) {
     for (int b = 0; b < 2; ++b) {
       for (int q = 0; q < 4; ++q)
         if (ev[q][b]) cudaEventDestroy(ev[q][b]);
-      if (bin[b]) cudaFree(bin[b]);
-      if (bout[b]) cudaFree(bout[b]);
+      raw_free(c, bin[b]);
+      raw_free(c, bout[b]);
     }
     if (si) cudaStreamDestroy(si);
     if (so) cudaStreamDestroy(so);
@@ -2061,6 +2088,17 @@ tc_status tc_rcm(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t* 
   std::vector<int32_t> p;
   rcm_order(n, rp, cl, p);
   std::copy(p.begin(), p.end(), perm);
+  return TC_OK;
+}
+
+tc_status tc_interior_first(int64_t n, const int64_t* rowptr, const int32_t* col, int32_t nparts,
+                            int32_t* order, int64_t* n_interior) {
+  if (n <= 0 || !rowptr || !col || nparts < 1 || !order || !n_interior) return TC_EINVAL;
+  std::vector<int32_t> o;
+  std::vector<int64_t> ni;
+  interior_first(n, rowptr, col, nparts, o, ni);
+  std::copy(o.begin(), o.end(), order);
+  std::copy(ni.begin(), ni.end(), n_interior);
   return TC_OK;
 }
 

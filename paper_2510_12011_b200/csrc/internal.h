@@ -418,5 +418,7 @@ struct PartPlan {
 };
 void plan_partitions(int64_t n, const int64_t* rowptr, const int32_t* col, int nparts,
                      std::vector<PartPlan>& plans);
+void interior_first(int64_t n, const int64_t* rowptr, const int32_t* col, int nparts,
+                    std::vector<int32_t>& order, std::vector<int64_t>& n_int);
 
 }  // namespace tcb

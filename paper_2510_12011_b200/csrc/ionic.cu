@@ -21,9 +21,15 @@ namespace tcb {
 #endif
 constexpr int kIonThreads = TCB_ION_THREADS;
 // minimum resident CTAs per SM for the FP64-bound TT2006 / CRN kernels (register
-// cap 65536 / (threads x this)): 4 = 128 registers (no cap), 5 = 96, 6 = 80
+// cap 65536 / (threads x this)): 4 = 128 registers (no cap), 5 = 96, 6 = 80.
+// Measured at 10 M nodes (profiles/r02b_exp_ionic.txt, ionic ms/step):
+// TT2006 4 / 5 / 6 = 1.19 / 1.13 / 1.17 (5: 96 registers, no spills);
+// CRN 4 / 5 / 6 = 1.20 / 1.20 / 1.20 (5 spills 32 bytes) -> 5 and 4.
 #ifndef TCB_ION_MINB
-#define TCB_ION_MINB 4
+#define TCB_ION_MINB 5
+#endif
+#ifndef TCB_ION_MINB_CRN
+#define TCB_ION_MINB_CRN 4
 #endif
 
 __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB) ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D) {
@@ -210,7 +216,7 @@ CRNDerived crn_derived(const CRNParams& P) {
   return D;
 }
 
-__global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB) ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D) {
+__global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN) ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D) {
   __shared__ Exp2Table T;
   exp2_table_init(&T);
   if (a.flags[0]) return;

@@ -291,4 +291,32 @@ void plan_partitions(int64_t n, const int64_t* rowptr, const int32_t* col, int n
   }
 }
 
+// Interior-first order of the row blocks of plan_partitions (DESIGN.md
+// "Multi-GPU"): inside block [g0, g1) the rows with no column outside the block
+// come first, then the boundary rows (the ones that read ghosts), each group in
+// the incoming order.  order[new] = old (internal indices); n_int[p] = interior
+// rows of block p.  The blocks and their ghost sets are unchanged.
+void interior_first(int64_t n, const int64_t* rowptr, const int32_t* col, int nparts,
+                    std::vector<int32_t>& order, std::vector<int64_t>& n_int) {
+  order.resize(n);
+  n_int.assign(nparts, 0);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int p = 0; p < nparts; ++p) {
+    const int64_t g0 = (n * p) / nparts, g1 = (n * (p + 1)) / nparts;  // plan_partitions' bounds
+    std::vector<uint8_t> inner(g1 - g0, 1);
+    for (int64_t i = g0; i < g1; ++i)
+      for (int64_t t = rowptr[i]; t < rowptr[i + 1]; ++t)
+        if (col[t] < g0 || col[t] >= g1) {
+          inner[i - g0] = 0;
+          break;
+        }
+    int64_t w = g0;
+    for (int64_t i = g0; i < g1; ++i)
+      if (inner[i - g0]) order[w++] = (int32_t)i;
+    n_int[p] = w - g0;
+    for (int64_t i = g0; i < g1; ++i)
+      if (!inner[i - g0]) order[w++] = (int32_t)i;
+  }
+}
+
 }  // namespace tcb

@@ -500,3 +500,38 @@ def test_errors_are_reported(T):
         assert ei.value.status == T.TC_ESTATE
     finally:
         T.tc_destroy(ctx)
+
+
+def test_torch_allocator_hook(T):
+    """tc_set_allocator: with torch's caching allocator the
+    context's device memory comes from torch (memory_allocated grows, every block
+    is returned by tc_destroy) and the trajectory is bitwise the default one."""
+    import torch
+    xyz, tets, region, fib, cond, stims = _slab_case("tt2006")
+    cfg = T.tc_config_default(dt=0.05, engine="grid")
+    ref = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+    before = torch.cuda.memory_allocated()
+    al = T.TorchAllocator(0)
+    sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims, allocator=al)
+    try:
+        assert len(al.live) > 10 and torch.cuda.memory_allocated() > before
+        a = ref.step(40)
+        b = sim.step(40)
+        assert np.array_equal(ref.V, sim.V) and np.array_equal(a["iters"], b["iters"])
+        st = sim.get_state()
+        sim.set_state(st)                       # staging buffers through the hook too
+        assert np.array_equal(sim.get_state(), st)
+    finally:
+        sim.close()
+        ref.close()
+    assert not al.live and torch.cuda.memory_allocated() == before
+    ctx = T.tc_create(T.tc_config_default())
+    try:                                        # too late once the context has allocated
+        T.tc_set_mesh(ctx, xyz, tets)
+        T.tc_set_conductivity(ctx, [0], [0.13], [0.02])
+        T.tc_assemble(ctx)
+        with pytest.raises(T.TcError) as ei:
+            T.tc_set_allocator(ctx, T.TorchAllocator(0))
+        assert ei.value.status == T.TC_ESTATE
+    finally:
+        T.tc_destroy(ctx)

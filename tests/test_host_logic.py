@@ -39,17 +39,63 @@ def test_rcm_matches_oracle(T, dims, seed):
     assert np.array_equal(T.tc_rcm(rp.astype(np.int64), col), O.rcm(rp, col))
 
 
-def _internal_pattern(dims, seed=7):
+def _internal_pattern(dims, seed=7, nparts=None):
+    """RCM internal order (oracle RCM == library RCM); with nparts, followed by
+    the library's interior-first order of the nparts row blocks."""
     xyz, tets = G.kuhn_box(*dims, 1.0)
     xyz, tets, _ = G.permute_nodes(xyz, tets, seed=seed)
     n = xyz.shape[0]
     rp, col = O.pattern(n, tets)
     perm = O.rcm(rp, col)
+    if nparts:
+        import paper_2510_12011_b200 as T
+        inv = np.empty(n, np.int64)
+        inv[perm] = np.arange(n)
+        rpi, coli = O.pattern(n, inv[tets].astype(np.int32))
+        order, _ = T.tc_interior_first(rpi.astype(np.int64), coli, nparts)
+        perm = perm[order]
     inv = np.empty(n, np.int64)
     inv[perm] = np.arange(n)
     tets_i = inv[tets].astype(np.int32)
     rpi, coli = O.pattern(n, tets_i)
     return xyz[perm], tets_i, rpi, coli
+
+
+@pytest.mark.parametrize("dims,nparts", [((11, 6, 5), 2), ((9, 7, 4), 3), ((14, 5, 5), 5)])
+def test_interior_first_order(T, dims, nparts):
+    """tc_interior_first: a permutation inside each row block of the plan;
+    the first n_interior rows of a block read no column outside it, every
+    later row reads at least one; ghost sets and block bounds are unchanged."""
+    xyz, tets, rp, col = _internal_pattern(dims)
+    n = rp.shape[0] - 1
+    order, nint = T.tc_interior_first(rp.astype(np.int64), col, nparts)
+    assert np.array_equal(np.sort(order), np.arange(n))
+    b = T.tc_partition_plan(rp, col, nparts, 0)["bounds"]
+    inv = np.empty(n, np.int64)
+    inv[order] = np.arange(n)
+    for p in range(nparts):
+        g0, g1 = b[p], b[p + 1]
+        assert np.all((order[g0:g1] >= g0) & (order[g0:g1] < g1))          # block preserved
+        outside = [np.any((col[rp[i]:rp[i + 1]] < g0) | (col[rp[i]:rp[i + 1]] >= g1)) for i in order[g0:g1]]
+        k = int(nint[p])
+        assert 0 < k < g1 - g0 and not any(outside[:k]) and all(outside[k:])
+        assert np.all(np.diff(order[g0:g0 + k]) > 0) and np.all(np.diff(order[g0 + k:g1]) > 0)   # stable
+    # the plan of the reordered pattern has the same ghost sets (as sets of old indices)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    m = np.zeros(n + 1, np.int64)
+    np.add.at(m, inv[rows] + 1, 1)
+    rp2 = np.cumsum(m)
+    col2 = np.empty_like(col)
+    fill = rp2[:-1].copy()
+    for r, c in zip(inv[rows], inv[col]):
+        col2[fill[r]] = c
+        fill[r] += 1
+    for r in range(n):
+        col2[rp2[r]:rp2[r + 1]] = np.sort(col2[rp2[r]:rp2[r + 1]])
+    for p in range(nparts):
+        g_old = T.tc_partition_plan(rp, col, nparts, p)["ghosts"]
+        g_new = T.tc_partition_plan(rp2, col2, nparts, p)["ghosts"]
+        assert np.array_equal(np.sort(order[g_new]), g_old)
 
 
 @pytest.mark.parametrize("nparts", [2, 3, 5])
@@ -93,7 +139,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2510_12011_b200 as T
-        xyz, tets, rp, col = _internal_pattern((10, 6, 5))
+        xyz, tets, rp, col = _internal_pattern((10, 6, 5), nparts=world)
         n = rp.shape[0] - 1
         E = tets.shape[0]
         rpA, colA, M, K = O.assemble(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: (0.13, 0.02)})
@@ -115,19 +161,40 @@ def _worker(rank, world, port, q):
             dist.all_reduce(t)
             return t.numpy()
 
-        def halo(values, dst):  # values: owned vector; dst: ghost region of a length nl+ng vector
-            reqs = []
+        # the pattern is already interior-first; the library finds the same split
+        order, nints = T.tc_interior_first(rp.astype(np.int64), col, world)
+        assert np.array_equal(order, np.arange(n))
+        nint = int(nints[rank])
+
+        def halo_start(values):  # values: owned vector -> nonblocking sends and receives
+            reqs, recvs = [], []
             for j, qn in enumerate(pl["nbr"]):
                 buf = torch.tensor(values[send_loc[pl["send_off"][j]:pl["send_off"][j + 1]]])
                 reqs.append(dist.isend(buf, int(qn)))
             for j, qn in enumerate(pl["nbr"]):
                 r = torch.zeros(int(pl["recv_off"][j + 1] - pl["recv_off"][j]), dtype=torch.float64)
-                dist.recv(r, int(qn))
+                recvs.append((j, r, dist.irecv(r, int(qn))))
+            return reqs, recvs
+
+        def halo_finish(h, dst):  # dst: ghost region of a length nl+ng vector
+            reqs, recvs = h
+            for j, r, rq in recvs:
+                rq.wait()
                 dst[nl + pl["recv_off"][j]: nl + pl["recv_off"][j + 1]] = r.numpy()
             for rq in reqs:
                 rq.wait()
 
-        spmv = lambda v: np.array([a @ v[c] for c, a in rows])
+        def halo(values, dst):
+            halo_finish(halo_start(values), dst)
+
+        spmv = lambda v, lo=0, hi=None: np.array([a @ v[c] for c, a in rows[lo:hi]])
+
+        # the block is interior-first: rows [0, nint) read no ghost (the plan of the
+        # reordered pattern), so they are computed while the halo is in flight --
+        # with the ghost region still holding the previous iteration's values
+        assert 0 < nint < nl
+        for c, _ in rows[:nint]:
+            assert np.all(c < nl)
         # r0 = b - A x0 (x0 halo), z0, rho0, ||z0||
         xv = np.zeros(nl + ng); xv[:nl] = x0[g0:g1]; halo(xv[:nl], xv)
         r = b[g0:g1] - spmv(xv)
@@ -141,11 +208,15 @@ def _worker(rank, world, port, q):
             pold, pnew = p[(it + 1) % 2], p[it % 2]
             # pack + halo of p into the ghost region of z
             pb = z[:nl] + (beta * pold[:nl] if it else 0.0)
-            halo(pb, z)
+            h = halo_start(pb)                      # halo in flight ...
             if it:
                 x += alpha * pold[:nl]
             pnew[:nl] = pb
-            q_ = spmv(z + (beta * pold if it else 0.0))
+            zp = z.copy()
+            zp[:nl] = pb                            # ghost region: still the last halo
+            q_int = spmv(zp, 0, nint)               # ... interior rows meanwhile
+            halo_finish(h, z)
+            q_ = np.concatenate([q_int, spmv(z + (beta * pold if it else 0.0), nint, None)])
             pq = allreduce([pnew[:nl] @ q_, 0.0])[0]
             alpha = rho / pq
             r -= alpha * q_
@@ -165,8 +236,9 @@ def _worker(rank, world, port, q):
 
 
 def test_distributed_pcg_gloo_world2():
-    """world_size 2 over gloo: the partitioned schedule (library plan, ghost-p
-    trick, two all-reduces per iteration) reproduces the oracle's PCG."""
+    """world_size 2 over gloo: the partitioned schedule (library plan and
+    interior-first order, ghost-p trick, interior rows computed while the halo is
+    in flight, two all-reduces per iteration) reproduces the oracle's PCG."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -177,7 +249,7 @@ def test_distributed_pcg_gloo_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    xyz, tets, rp, col = _internal_pattern((10, 6, 5))
+    xyz, tets, rp, col = _internal_pattern((10, 6, 5), nparts=2)
     n = rp.shape[0] - 1
     E = tets.shape[0]
     rpA, colA, M, K = O.assemble(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: (0.13, 0.02)})
