@@ -576,14 +576,11 @@ static tc_status init_state(tc_ctx* c) {
 // Local SELL of one part from the internal-order CSR rows [g0, g1): columns
 // stay sorted by internal index (same summation order as one part); local
 // index = g - g0 for owned, n_pad + (ghost rank) for ghosts.
-static void local_sell(const PartPlan& pl, const int64_t* rp, const int32_t* col, HostSell& hs,
-                       std::vector<int32_t>& colg) {
+// lrp / lcol: the rows [g0, g1) alone (row pointers rebased to 0).
+static void local_sell_rows(const PartPlan& pl, const int64_t* lrp, const int32_t* lcol, HostSell& hs,
+                            std::vector<int32_t>& colg) {
   const int64_t n = pl.g1 - pl.g0;
-  std::vector<int64_t> lrp(n + 1, 0);
-  for (int64_t i = 0; i < n; ++i) lrp[i + 1] = lrp[i] + (rp[pl.g0 + i + 1] - rp[pl.g0 + i]);
-  std::vector<int32_t> lcol(lrp[n]);
-  std::copy(col + rp[pl.g0], col + rp[pl.g1], lcol.begin());
-  csr_to_sell((int32_t)n, lrp.data(), lcol.data(), hs);  // hs.col = internal (global) indices
+  csr_to_sell((int32_t)n, lrp, lcol, hs);  // hs.col = internal (global) indices
   colg = hs.col;
   const int64_t np = hs.n_pad;
   for (int64_t sl = 0; sl < hs.nslices; ++sl) {
@@ -607,6 +604,14 @@ static void local_sell(const PartPlan& pl, const int64_t* rp, const int32_t* col
       }
     }
   }
+}
+
+static void local_sell(const PartPlan& pl, const int64_t* rp, const int32_t* col, HostSell& hs,
+                       std::vector<int32_t>& colg) {
+  const int64_t n = pl.g1 - pl.g0;
+  std::vector<int64_t> lrp(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) lrp[i + 1] = lrp[i] + (rp[pl.g0 + i + 1] - rp[pl.g0 + i]);
+  local_sell_rows(pl, lrp.data(), col + rp[pl.g0], hs, colg);
 }
 
 
@@ -973,7 +978,7 @@ static tc_status assemble_device(tc_ctx* c, const std::vector<int32_t>& ereg) {
   cudaMemcpyAsync(d_sl, c->sig_l.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_st, c->sig_t.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemsetAsync(d_err, 0, 4, c->stream);
-  cudaError_t e = dev_setup(n, E, k, d_tets, c->cfg.use_rcm, dp, c->stream);
+  cudaError_t e = dev_setup(n, E, k, d_tets, c->cfg.use_rcm, 1, dp, c->stream);
   if (e == cudaSuccess) e = dev_gather3(n, dp.perm, d_xyz, d_xyz2, c->stream);
   if (e != cudaSuccess) {
     cleanup();
@@ -1049,6 +1054,167 @@ static tc_status assemble_device(tc_ctx* c, const std::vector<int32_t>& ereg) {
   return TC_OK;
 }
 
+// Device setup of a PARTITIONED system (SURVEY 8f f3 "RCM/partition on device";
+// every rank of a multi-GPU run, or the parts emulated on one GPU): dev_setup
+// builds the global pattern, RCM and the interior-first block order on this
+// GPU (identical on every rank: deterministic sorts); each part's plan comes
+// from its own rows (plan_from_rows, symmetric pattern), its SELL layout from
+// the same rows, and its rows are assembled from the device incidence.  Only
+// the rows of the local parts and of their neighbours cross to the host --
+// never the global pattern (host path: assemble_host).
+static tc_status assemble_device_parts(tc_ctx* c, const std::vector<int32_t>& ereg, std::vector<PartPlan>& plans) {
+  const int64_t n = c->n, E = c->E;
+  const int k = c->kel;
+  const size_t nr = c->reg_ids.size();
+  double *d_xyz = nullptr, *d_xyz2 = nullptr, *d_fib = nullptr, *d_sl = nullptr, *d_st = nullptr;
+  int32_t *d_tets = nullptr, *d_ereg = nullptr, *d_err = nullptr;
+  DevPattern dp;
+  auto cleanup = [&]() {
+    cudaFree(d_xyz); cudaFree(d_xyz2); cudaFree(d_fib); cudaFree(d_sl); cudaFree(d_st);
+    cudaFree(d_tets); cudaFree(d_ereg); cudaFree(d_err);
+    dev_setup_free(dp);
+  };
+  bool ok = cudaMalloc(&d_xyz, 3 * n * 8) == cudaSuccess && cudaMalloc(&d_xyz2, 3 * n * 8) == cudaSuccess &&
+            cudaMalloc(&d_fib, std::max<int64_t>(3 * E, 1) * 8) == cudaSuccess &&
+            cudaMalloc(&d_sl, nr * 8) == cudaSuccess && cudaMalloc(&d_st, nr * 8) == cudaSuccess &&
+            cudaMalloc(&d_tets, std::max<int64_t>((int64_t)k * E, 1) * 4) == cudaSuccess &&
+            cudaMalloc(&d_ereg, std::max<int64_t>(E, 1) * 4) == cudaSuccess && cudaMalloc(&d_err, 4) == cudaSuccess;
+  if (!ok) {
+    cleanup();
+    return fail(c, TC_ENOMEM, "tc_assemble: device allocation failed");
+  }
+  cudaMemcpyAsync(d_xyz, c->xyz.data(), 3 * n * 8, cudaMemcpyHostToDevice, c->stream);
+  if (E > 0) {
+    cudaMemcpyAsync(d_fib, c->fibre.data(), 3 * E * 8, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_tets, c->tets.data(), (size_t)k * E * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_ereg, ereg.data(), E * 4, cudaMemcpyHostToDevice, c->stream);
+  }
+  cudaMemcpyAsync(d_sl, c->sig_l.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
+  cudaMemcpyAsync(d_st, c->sig_t.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
+  cudaMemsetAsync(d_err, 0, 4, c->stream);
+  const char* nif = std::getenv("TCB_NO_INTERIOR_FIRST");
+  const bool reorder = !(nif && nif[0] == '1');
+  cudaError_t e = dev_setup(n, E, k, d_tets, c->cfg.use_rcm, reorder ? c->nparts : -c->nparts, dp, c->stream);
+  if (e == cudaSuccess) e = dev_gather3(n, dp.perm, d_xyz, d_xyz2, c->stream);
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(c, e == cudaErrorMemoryAllocation ? TC_ENOMEM : TC_ECUDA,
+                std::string("device setup: ") + cudaGetErrorString(e));
+  }
+  c->perm.resize(n);
+  c->inv.resize(n);
+  CUDA_TRY(c, cudaMemcpyAsync(c->perm.data(), dp.perm, n * 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int64_t i = 0; i < n; ++i) c->inv[c->perm[i]] = (int32_t)i;
+  c->nnz = dp.nnz;
+  const int P_ = c->nparts;
+  c->bounds.resize(P_ + 1);
+  for (int p = 0; p <= P_; ++p) c->bounds[p] = block_start(n, P_, p);
+  c->part_ids.clear();
+  if (c->use_comm) c->part_ids.push_back(c->comm.rank);
+  else for (int p = 0; p < P_; ++p) c->part_ids.push_back(p);
+  c->parts.resize(c->part_ids.size());
+  // rows of a block from the device (rebased row pointers) and its plan
+  plans.assign(P_, PartPlan());
+  std::vector<char> have(P_, 0);
+  std::vector<std::vector<int64_t>> lrp(P_);
+  std::vector<std::vector<int32_t>> lcol(P_);
+  auto fetch = [&](int p) -> tc_status {
+    if (have[p]) return TC_OK;
+    const int64_t g0 = c->bounds[p], g1 = c->bounds[p + 1];
+    std::vector<int64_t>& r = lrp[p];
+    r.resize(g1 - g0 + 1);
+    CUDA_TRY(c, cudaMemcpyAsync(r.data(), dp.rowptr + g0, (g1 - g0 + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    const int64_t b = r[0];
+    for (int64_t& v : r) v -= b;
+    lcol[p].resize(r.back());
+    CUDA_TRY(c, cudaMemcpyAsync(lcol[p].data(), dp.colidx + b, r.back() * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    plans[p] = plan_from_rows(n, P_, p, r.data(), lcol[p].data());
+    plans[p].n_interior = reorder ? dp.n_int[p] : 0;
+    have[p] = 1;
+    return TC_OK;
+  };
+  for (int gid : c->part_ids) {
+    TC_TRY(fetch(gid));
+    for (int q : std::vector<int32_t>(plans[gid].nbr)) TC_TRY(fetch(q));   // setup_peer's remote offsets
+  }
+  for (size_t pi = 0; pi < c->parts.size(); ++pi) {
+    Part& P = c->parts[pi];
+    const int gid = c->part_ids[pi];
+    P.plan = plans[gid];
+    const int64_t g0 = P.plan.g0, g1 = P.plan.g1;
+    P.n = g1 - g0;
+    HostSell hs;
+    std::vector<int32_t> colg;
+    local_sell_rows(P.plan, lrp[gid].data(), lcol[gid].data(), hs, colg);
+    P.nslices = hs.nslices;
+    P.nslices_int = (int32_t)(P.plan.n_interior / kSellC);
+    P.n_pad = hs.n_pad;
+    P.n_ghost = (int64_t)P.plan.ghosts.size();
+    P.n_vec = P.n_pad + P.n_ghost;
+    P.nnz = lrp[gid].back();
+    P.nnz_pad = hs.slice_ptr[hs.nslices];
+    P.h_sp = hs.slice_ptr;
+    CUDA_TRY(c, upload(c, &P.d_sp, hs.slice_ptr));
+    CUDA_TRY(c, upload(c, &P.d_col, hs.col));
+    CUDA_TRY(c, dalloc(c, &P.d_A, P.nnz_pad));
+    CUDA_TRY(c, dalloc(c, &P.d_K, P.nnz_pad));
+    TC_TRY(alloc_part_vectors(c, P));
+    CUDA_TRY(c, dalloc(c, &P.d_U, (int64_t)std::max(c->nstates, 1) * P.n_pad));
+    CUDA_TRY(c, dalloc(c, &P.d_act, P.n_pad));
+    CUDA_TRY(c, dalloc(c, &P.d_lat, P.n_pad));
+    CUDA_TRY(c, dalloc(c, &P.d_lrt, P.n_pad));
+    std::vector<int32_t> sidx(P.plan.send_g.size());
+    for (size_t t = 0; t < sidx.size(); ++t) sidx[t] = (int32_t)(P.plan.send_g[t] - g0);
+    CUDA_TRY(c, upload(c, &P.d_send_idx, sidx));
+    CUDA_TRY(c, dalloc(c, &P.d_send_buf, 2 * (int64_t)sidx.size()));
+    if (c->cfg.model == TC_ION_MMS) {
+      std::vector<uint8_t> dir(P.n_pad, 0);
+      for (int32_t o : c->dirichlet_nodes) {
+        const int64_t g = c->inv[o];
+        if (g >= g0 && g < g1) dir[g - g0] = 1;
+      }
+      CUDA_TRY(c, upload(c, &P.d_dir, dir));
+      CUDA_TRY(c, dalloc(c, &P.d_xyz, 3 * P.n_pad));
+      CUDA_TRY(c, cudaMemcpyAsync(P.d_xyz, d_xyz2 + 3 * g0, 3 * P.n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    // assembly of the owned rows: the device incidence of rows [g0, g1) (absolute offsets)
+    int32_t *d_rowlen = nullptr, *d_colg = nullptr;
+    if (cudaMalloc(&d_rowlen, std::max<int64_t>(P.n, 1) * 4) != cudaSuccess ||
+        cudaMalloc(&d_colg, std::max<size_t>(colg.size(), 1) * 4) != cudaSuccess) {
+      cudaFree(d_rowlen); cudaFree(d_colg);
+      cleanup();
+      return fail(c, TC_ENOMEM, "tc_assemble: device allocation failed");
+    }
+    cudaMemcpyAsync(d_rowlen, hs.rowlen.data(), P.n * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_colg, colg.data(), colg.size() * 4, cudaMemcpyHostToDevice, c->stream);
+    AsmArgs a{};
+    a.n = (int32_t)P.n; a.row0 = (int32_t)g0; a.k = k; a.xyz = d_xyz2; a.tets = dp.tets2; a.ereg = d_ereg;
+    a.fibre = d_fib; a.sig_l = d_sl; a.sig_t = d_st; a.inc_ptr = dp.iptr + g0; a.inc = dp.inc;
+    a.slice_ptr = P.d_sp; a.col = d_colg; a.rowlen = d_rowlen;
+    a.A = P.d_A; a.K = P.d_K; a.dinv = P.d_dinv; a.dirichlet = P.d_dir;
+    a.c_mass = c->cfg.chi * c->cfg.cm; a.c_stiff = c->cfg.theta * c->cfg.dt; a.err = d_err;
+    cudaError_t le = launch_assemble(a, c->stream);
+    cudaError_t ss = cudaStreamSynchronize(c->stream);
+    cudaFree(d_rowlen); cudaFree(d_colg);
+    if (le != cudaSuccess || ss != cudaSuccess) {
+      cleanup();
+      return fail(c, TC_ECUDA, std::string("assembly kernel: ") + cudaGetErrorString(le != cudaSuccess ? le : ss));
+    }
+    P.grid = split_grid(P.nslices);
+    CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
+  }
+  int32_t herr = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cleanup();
+  if (herr == 1) return fail(c, TC_EDEGEN, "assembly: zero-volume element");
+  if (herr == 2) return fail(c, TC_EINVAL, "assembly: pattern slot missing (internal)");
+  return TC_OK;
+}
+
 // Graph engine (variant 5): scalar block, partials and the instantiated solve graph.
 static tc_status setup_graph(tc_ctx* c, Part& P) {
   CUDA_TRY(c, dalloc(c, &P.d_gpart, 2 * (int64_t)P.grid));
@@ -1116,8 +1282,11 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
                : c->cfg.model == TC_ION_MS    ? 1
                                               : 0;
   const bool on_dev = c->cfg.device_setup && c->nparts == 1 && !c->use_comm && c->cfg.pcg_variant != 2;
+  const bool on_dev_parts = c->cfg.device_setup && split_mode(c) && c->cfg.pcg_variant != 2;
   if (on_dev) {
     TC_TRY(assemble_device(c, ereg));
+  } else if (on_dev_parts) {
+    TC_TRY(assemble_device_parts(c, ereg, plans));
   } else {
     TC_TRY(assemble_host(c, ereg, plans));
   }
@@ -1184,6 +1353,8 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
   c->fibre.clear(); c->fibre.shrink_to_fit();
   c->region.clear(); c->region.shrink_to_fit();
   TC_TRY(init_state(c));
+  if (c->cfg.model == TC_ION_TT2006_EPI || c->cfg.model == TC_ION_CRN)
+    if (!device_tables()) return fail(c, TC_ENOMEM, "exp / log tables: device allocation failed");
   c->assembled = true;
   return TC_OK;
 }
@@ -1471,6 +1642,8 @@ static bool use_cluster(tc_ctx* c) {
 // Descriptor of this context for a cluster-engine launch starting at step c->k;
 // uploads the packed ionic parameters when they changed.
 static tc_status make_corep(tc_ctx* c, CoRep& R, tc_step_stat* stats) {
+  R.tab = device_tables();
+  if (!R.tab) return fail(c, TC_ENOMEM, "exp / log tables: device allocation failed");
   Part& P = c->parts[0];
   if (!c->d_params) CUDA_TRY(c, dalloc(c, &c->d_params, cohort_param_doubles()));
   if (c->params_uploaded != c->param_version) {

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kCoThreads, MINB)
   __syncthreads();
   const CoRep& R = S.R;
   for (int j = threadIdx.x; j < kParamDoubles; j += blockDim.x) S.prm[j] = R.params[j];
-  if (MODEL != TC_ION_MS) exp2_table_init(&T);  // includes __syncthreads
+  if (MODEL != TC_ION_MS) exp2_table_init(&T, R.tab);  // includes __syncthreads
   __syncthreads();
   const TTParams& TP = *reinterpret_cast<const TTParams*>(S.prm);
   const TTDerived& TD = *reinterpret_cast<const TTDerived*>(S.prm + sizeof(TTParams) / 8);

@@ -29,12 +29,20 @@ struct Exp2Table {
   double2 lg[kLogTab];
 };
 
-__device__ __forceinline__ void exp2_table_init(Exp2Table* T) {
+// Fill the tables (libm exp2 / log, once per device: ionic.cu device_tables).
+__device__ __forceinline__ void exp2_table_fill(Exp2Table* T) {
   for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) T->t[j] = exp2((double)j / kExpTab);
   for (int j = threadIdx.x; j < kLogTab; j += blockDim.x) {
     const double c = 1.0 / (1.0 + (j + 0.5) / kLogTab);
     T->lg[j] = make_double2(c, -log(c));
   }
+}
+
+// Per-CTA shared-memory copy of the device tables G (long-running kernels).
+__device__ __forceinline__ void exp2_table_init(Exp2Table* T, const Exp2Table* __restrict__ G) {
+  const double* g = reinterpret_cast<const double*>(G);
+  double* t = reinterpret_cast<double*>(T);
+  for (int j = threadIdx.x; j < (int)(sizeof(Exp2Table) / 8); j += blockDim.x) t[j] = __ldg(g + j);
   __syncthreads();
 }
 

@@ -257,6 +257,7 @@ struct StimEpoch {
 };
 // Device descriptor of one replica: a single-partition context's buffers and
 // settings at the start of a cluster-engine launch.
+struct Exp2Table;
 struct CoRep {
   const int64_t* slice_ptr;
   const int32_t* col;
@@ -281,6 +282,7 @@ struct CoRep {
   int64_t k0;
   double dt, theta, eps_a, eps_r, lat_thr, lrt_thr;
   const double* params;          // cohort_pack_params block (device)
+  const Exp2Table* tab;          // device_tables() (exp / log tables, copied to shared memory)
 };
 int cohort_param_doubles();
 void cohort_pack_params(int model, const TTParams& tp, const MSParams& mp, const CRNParams& cp,
@@ -295,6 +297,9 @@ cudaError_t launch_cohort(int model, const CoRep* d_reps, int nrep, int csize, s
 
 // ---- launchers (return cudaError_t of the launch) --------------------------
 cudaError_t launch_assemble(const AsmArgs& a, cudaStream_t s);
+struct Exp2Table;
+// exp / log tables of the ionic kernels, filled once per device (ionic.cu); null on failure
+const Exp2Table* device_tables();
 cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s);
 cudaError_t launch_ionic_ms(const IonArgs& a, const MSParams& p, cudaStream_t s);
 cudaError_t launch_ionic_mms(const IonArgs& a, const MMSParams& p, cudaStream_t s);
@@ -399,9 +404,13 @@ struct DevPattern {         // device arrays, cudaMalloc'ed by dev_setup (dev_se
   int64_t* iptr = nullptr;      // [n + 1] incidence of the permuted elements
   int32_t* inc = nullptr;       // [k E] 4 e + a, ascending e per node
   int32_t* tets2 = nullptr;     // [k E] element nodes in internal numbering
+  // partitioned systems (nparts > 1): the permuted CSR instead of SELL
+  int64_t* rowptr = nullptr;    // [n + 1]
+  int32_t* colidx = nullptr;    // [nnz]
+  std::vector<int64_t> n_int;   // interior rows of each block (interior-first order)
 };
-cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int use_rcm, DevPattern& out,
-                      cudaStream_t s);
+cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int use_rcm, int nparts,
+                      DevPattern& out, cudaStream_t s);
 void dev_setup_free(DevPattern& p);
 cudaError_t dev_gather3(int64_t n, const int32_t* perm, const double* in, double* out, cudaStream_t s);
 
@@ -418,6 +427,8 @@ struct PartPlan {
 };
 void plan_partitions(int64_t n, const int64_t* rowptr, const int32_t* col, int nparts,
                      std::vector<PartPlan>& plans);
+int64_t block_start(int64_t n, int nparts, int p);
+PartPlan plan_from_rows(int64_t n, int nparts, int p, const int64_t* lrp, const int32_t* lcol);
 void interior_first(int64_t n, const int64_t* rowptr, const int32_t* col, int nparts,
                     std::vector<int32_t>& order, std::vector<int64_t>& n_int);
 

@@ -10,6 +10,8 @@
 // Stimuli add dt s and theta dt^2 s (s = Isv / (chi C_m)) in stimulus_kernel.
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "ionic_node.cuh"
 
@@ -32,9 +34,44 @@ constexpr int kIonThreads = TCB_ION_THREADS;
 #define TCB_ION_MINB_CRN 4
 #endif
 
-__global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB) ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D) {
-  __shared__ Exp2Table T;
-  exp2_table_init(&T);
+// The exp / log tables (fp64math.cuh): filled once per device and process into
+// global memory (read-only, 3 KB, L1-resident).  TCB_ION_TAB_SMEM = 1: every CTA
+// copies them into shared memory first (r01 computed them per CTA: 2 exp2 and
+// half a log per thread plus a barrier, ~5 % of the kernel, ncu r02c).
+#ifndef TCB_ION_TAB_SMEM
+#define TCB_ION_TAB_SMEM 0
+#endif
+__global__ void tables_fill_kernel(Exp2Table* T) { exp2_table_fill(T); }
+
+const Exp2Table* device_tables() {
+  static std::mutex mu;
+  static std::map<int, Exp2Table*> tabs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  Exp2Table*& t = tabs[dev];
+  if (!t) {
+    Exp2Table* d = nullptr;
+    if (cudaMalloc(&d, sizeof(Exp2Table)) != cudaSuccess) return nullptr;
+    tables_fill_kernel<<<1, 256>>>(d);
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      cudaFree(d);
+      return nullptr;
+    }
+    t = d;
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB)
+    ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D, const Exp2Table* __restrict__ G) {
+#if TCB_ION_TAB_SMEM
+  __shared__ Exp2Table Ts;
+  exp2_table_init(&Ts, G);
+  const Exp2Table* T = &Ts;
+#else
+  const Exp2Table* __restrict__ T = G;
+#endif
   if (a.flags[0]) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
@@ -44,7 +81,7 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB) ionic_tt_kernel(Ion
   double u[kTTStates];
 #pragma unroll
   for (int s = 0; s < kTTStates; ++s) u[s] = a.U[s * a.stride + i];
-  const double In = tt_advance(V, u, a.dt, P, D, &T);
+  const double In = tt_advance(V, u, a.dt, P, D, T);
 #pragma unroll
   for (int s = 0; s < kTTStates; ++s) a.U[s * a.stride + i] = u[s];
   write_rhs(a, i, V, Vp, In);
@@ -179,7 +216,9 @@ static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  ionic_tt_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, tt_derived(p));
+  const Exp2Table* G = device_tables();
+  if (!G) return cudaErrorMemoryAllocation;
+  ionic_tt_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, tt_derived(p), G);
   return cudaGetLastError();
 }
 cudaError_t launch_ionic_ms(const IonArgs& a, const MSParams& p, cudaStream_t s) {
@@ -216,9 +255,15 @@ CRNDerived crn_derived(const CRNParams& P) {
   return D;
 }
 
-__global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN) ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D) {
-  __shared__ Exp2Table T;
-  exp2_table_init(&T);
+__global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN)
+    ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D, const Exp2Table* __restrict__ G) {
+#if TCB_ION_TAB_SMEM
+  __shared__ Exp2Table Ts;
+  exp2_table_init(&Ts, G);
+  const Exp2Table* T = &Ts;
+#else
+  const Exp2Table* __restrict__ T = G;
+#endif
   if (a.flags[0]) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
@@ -228,7 +273,7 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN) ionic_crn_kerne
   double u[kCRNStates];
 #pragma unroll
   for (int s = 0; s < kCRNStates; ++s) u[s] = a.U[s * a.stride + i];
-  const double In = crn_advance(V, u, a.dt, P, D, &T);
+  const double In = crn_advance(V, u, a.dt, P, D, T);
 #pragma unroll
   for (int s = 0; s < kCRNStates; ++s) a.U[s * a.stride + i] = u[s];
   write_rhs(a, i, V, Vp, In);
@@ -236,7 +281,9 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN) ionic_crn_kerne
 
 cudaError_t launch_ionic_crn(const IonArgs& a, const CRNParams& p, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  ionic_crn_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, crn_derived(p));
+  const Exp2Table* G = device_tables();
+  if (!G) return cudaErrorMemoryAllocation;
+  ionic_crn_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, crn_derived(p), G);
   return cudaGetLastError();
 }
 

@@ -158,11 +158,29 @@ __device__ __forceinline__ double rl_rate(double y, double yinf, double inv_tau,
   return yinf - (yinf - y) * EXP(-dt * inv_tau);
 }
 
+// TCB_CUR_LOOP = 1: the two current evaluations of a step (at u^k for the
+// concentration updates, at u^{k+1} for I_n, reading I2) are one copy of the
+// code run twice (a two-pass loop) -- half the current code in the instruction
+// cache (ncu r02c: 9 % of warp stalls were instruction fetch); 0 (default): two
+// inlined copies -- the loop keeps the currents, states and V-factors live across
+// the back edge and spills 630-720 bytes (ptxas, r02), and its code is larger.
+#ifndef TCB_CUR_LOOP
+#define TCB_CUR_LOOP 0
+#endif
+
 // Advances u in place; returns I_n(V, u^{k+1}).
 __device__ __forceinline__ double tt_advance(double V, double* u, double dt, const TTParams& P,
                                              const TTDerived& D, const Exp2Table* T) {
   const TTVolt f = tt_volt(V, P, D, T);
+#if TCB_CUR_LOOP
+  TTCur c;
+#pragma unroll 1
+  for (int pass = 0;; ++pass) {
+  c = tt_cur(V, u, P, D, f, T);
+  if (pass) break;
+#else
   const TTCur c = tt_cur(V, u, P, D, f, T);
+#endif
   // -- calcium dynamics (currents and fluxes at (V^k, u^k)) --
   const double casr = u[sCaSR], cass = u[sCaSS], cai = u[sCai];
   const double ec = P.EC * tc_rcp(casr);
@@ -278,7 +296,12 @@ __device__ __forceinline__ double tt_advance(double V, double* u, double dt, con
     const double den = tc_rcp(1.0 + q * q);
     u[sfc] = rl_rate(u[sfc], 0.6 * den + 0.4, tc_rcp(80.0 * den + 2.0), dt, T);
   }
+#if TCB_CUR_LOOP
+  }
+  return tt_total(c);  // I_ion(V^k, u^{k+1}) (reading I2): the second pass
+#else
   return tt_total(tt_cur(V, u, P, D, f, T));  // I_ion(V^k, u^{k+1}) (reading I2)
+#endif
 }
 
 // ------------------------------------------------------------------ Mitchell-Schaeffer
@@ -371,7 +394,15 @@ __device__ __forceinline__ double rl_tau(double y, double yinf, double tau, doub
 // Advances u in place; returns I_n(V, u^{k+1}).
 __device__ __forceinline__ double crn_advance(double V, double* u, double dt, const CRNParams& P,
                                               const CRNDerived& D, const Exp2Table* T) {
+#if TCB_CUR_LOOP
+  CRNCur c;
+#pragma unroll 1
+  for (int pass = 0;; ++pass) {
+  c = crn_cur(V, u, P, D, T);
+  if (pass) break;
+#else
   const CRNCur c = crn_cur(V, u, P, D, T);
+#endif
   const double cai = u[cCai], caup = u[cCaup], carel = u[cCarel];
   const double irel = P.Krel * u[cu] * u[cu] * u[cv] * u[cw] * (carel - cai);
   const double itr = (caup - carel) * D.inv_tautr;
@@ -459,7 +490,12 @@ __device__ __forceinline__ double crn_advance(double V, double* u, double dt, co
   u[cCai] += dt * (b1 * tc_rcp(b2));
   u[cCaup] += dt * dcaup;
   u[cCarel] += dt * dcarel;
+#if TCB_CUR_LOOP
+  }
+  return crn_total(c);  // I_ion(V^k, u^{k+1}) (reading I2): the second pass
+#else
   return crn_total(crn_cur(V, u, P, D, T));  // I_ion(V^k, u^{k+1}) (reading I2)
+#endif
 }
 
 TTDerived tt_derived(const TTParams& P);

@@ -15,7 +15,12 @@
 //    neighbour, degree, index); one 64-bit key sort per level reproduces the
 //    sequential order exactly;
 //  * incidence: a stable sort of (node, element slot) pairs keeps each node's
-//    elements in ascending element order (the assembly's summation order).
+//    elements in ascending element order (the assembly's summation order);
+//  * partitioned systems (nparts > 1, SURVEY 8f f3 "RCM/partition on device"):
+//    the interior-first order of the row blocks (setup_host.cpp interior_first)
+//    as one 64-bit key sort (block, reads-a-ghost, row), and the global permuted
+//    CSR as output instead of a SELL layout; each part's plan and SELL are then
+//    built from its own rows (api.cu assemble_device_parts).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -176,6 +181,44 @@ __global__ void k_inc_code(int64_t m, int k, const int32_t* __restrict__ slot, i
   inc[t] = 4 * e + a;
 }
 
+// block of plan_partitions' bounds g0(p) = floor(n p / P) holding row i
+__device__ __forceinline__ int block_of(int64_t i, int64_t n, int P) {
+  int p = (int)((i * P) / n);
+  while (p + 1 < P && (n * (p + 1)) / P <= i) ++p;
+  while (p > 0 && (n * p) / P > i) --p;
+  return p;
+}
+
+// interior-first keys: (block, reads-a-ghost flag, row);
+// sorting them gives, per block, the interior rows then the boundary rows, each
+// in the incoming order.  Interior rows are counted per block.
+__global__ void k_interior_keys(int64_t n, int P, const int64_t* __restrict__ rowptr,
+                                const int32_t* __restrict__ col, uint64_t* __restrict__ keys,
+                                unsigned long long* __restrict__ n_int) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int p = block_of(i, n, P);
+  const int64_t g0 = (n * p) / P, g1 = (n * (p + 1)) / P;
+  uint64_t out = 0;
+  for (int64_t t = rowptr[i]; t < rowptr[i + 1]; ++t)
+    if (col[t] < g0 || col[t] >= g1) {
+      out = 1;
+      break;
+    }
+  keys[i] = ((uint64_t)p << 33) | (out << 32) | (uint64_t)i;
+  if (!out) atomicAdd(n_int + p, 1ull);
+}
+
+// perm2[new] = perm[order[new]] (order = low 32 bits of the sorted keys), inv2
+__global__ void k_compose(int64_t n, const uint64_t* __restrict__ keys, const int32_t* __restrict__ perm,
+                          int32_t* __restrict__ perm2, int32_t* __restrict__ inv2) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int32_t o = perm[(int64_t)(keys[j] & 0xffffffffull)];
+  perm2[j] = o;
+  inv2[o] = (int32_t)j;
+}
+
 inline unsigned nb(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
 struct Scratch {  // cudaMalloc'ed temporaries freed on scope exit
@@ -242,8 +285,8 @@ cudaError_t sort_unique(Scratch& S, uint64_t* a, uint64_t* b, int64_t m, int bit
 
 }  // namespace
 
-cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int use_rcm, DevPattern& out,
-                      cudaStream_t s) {
+cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int use_rcm, int nparts,
+                      DevPattern& out, cudaStream_t s) {
   Scratch S;
   int sh = 1;
   while ((1ll << sh) < n) ++sh;
@@ -325,20 +368,67 @@ cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int us
     k_identity<<<nb(n), 256, 0, s>>>(n, out.perm, out.inv);
   }
   DS_TRY(cudaGetLastError());
-  // ---- permuted pattern (P A P^T), SELL-32 ----------------------------------------
-  k_permuted_keys<<<nb(n), 256, 0, s>>>(n, sh, rp, cl, out.inv, kb);
-  DS_TRY(cudaGetLastError());
-  {
+  // ---- permuted pattern (P A P^T) -------------------------------------------------
+  // (rp, cl) = original pattern; the permuted one goes to (rp2, cl2), which is
+  // (rp, cl) itself for a single partition (the original is no longer needed)
+  const bool reorder = nparts > 1;   // nparts < -1: partitioned output, plain RCM order (A/B)
+  if (nparts < 0) nparts = -nparts;
+  int64_t* rp2 = rp;
+  int32_t* cl2 = cl;
+  if (nparts > 1) {
+    DS_TRY(cudaMalloc(&out.rowptr, (n + 1) * 8));
+    DS_TRY(cudaMalloc(&out.colidx, nnz * 4));
+    rp2 = out.rowptr;
+    cl2 = out.colidx;
+  }
+  auto permute = [&]() -> cudaError_t {
+    k_permuted_keys<<<nb(n), 256, 0, s>>>(n, sh, rp, cl, out.inv, kb);
+    DS_TRY(cudaGetLastError());
     cub::DoubleBuffer<uint64_t> db(kb, ka);
     DS_TRY(cub_call(S, [&](void* t, size_t& by) {
       return cub::DeviceRadixSort::SortKeys(t, by, db, nnz, 0, 2 * sh, s);
     }));
-    k_keys_to_csr<<<nb(nnz), 256, 0, s>>>(nnz, sh, db.Current(), rp, cl);
+    k_keys_to_csr<<<nb(nnz), 256, 0, s>>>(nnz, sh, db.Current(), rp2, cl2);
+    return cudaGetLastError();
+  };
+  DS_TRY(permute());
+  if (reorder) {
+    // interior-first order inside each row block (setup_host.cpp interior_first),
+    // then the pattern again in the final order
+    unsigned long long* cnt_int = nullptr;
+    int32_t *perm2 = nullptr, *inv2 = nullptr;
+    DS_TRY(S.get(&cnt_int, nparts));
+    DS_TRY(S.get(&perm2, n));
+    DS_TRY(S.get(&inv2, n));
+    DS_TRY(cudaMemsetAsync(cnt_int, 0, nparts * 8, s));
+    k_interior_keys<<<nb(n), 256, 0, s>>>(n, nparts, rp2, cl2, kb, cnt_int);
+    DS_TRY(cudaGetLastError());
+    int pbits = 1;
+    while ((1 << pbits) < nparts) ++pbits;
+    cub::DoubleBuffer<uint64_t> db(kb, ka);
+    DS_TRY(cub_call(S, [&](void* t, size_t& by) {
+      return cub::DeviceRadixSort::SortKeys(t, by, db, n, 0, 33 + pbits, s);
+    }));
+    k_compose<<<nb(n), 256, 0, s>>>(n, db.Current(), out.perm, perm2, inv2);
+    DS_TRY(cudaGetLastError());
+    DS_TRY(cudaMemcpyAsync(out.perm, perm2, n * 4, cudaMemcpyDeviceToDevice, s));
+    DS_TRY(cudaMemcpyAsync(out.inv, inv2, n * 4, cudaMemcpyDeviceToDevice, s));
+    std::vector<unsigned long long> h(nparts);
+    DS_TRY(cudaMemcpyAsync(h.data(), cnt_int, nparts * 8, cudaMemcpyDeviceToHost, s));
+    DS_TRY(cudaStreamSynchronize(s));
+    out.n_int.assign(h.begin(), h.end());
+    DS_TRY(permute());
   }
   S.drop(ka);
   S.drop(kb);
   out.n = n;
   out.nnz = nnz;
+  if (nparts > 1) {  // partitioned: the global CSR is the output; SELL is per part (host)
+    S.drop(rp);
+    S.drop(cl);
+    out.nslices = 0;
+    out.nnz_pad = 0;
+  } else {
   out.nslices = (int32_t)((n + kSellC - 1) / kSellC);
   DS_TRY(cudaMalloc(&out.rowlen, n * 4));
   DS_TRY(cudaMalloc(&out.slice_ptr, (out.nslices + 1) * 8));
@@ -356,6 +446,7 @@ cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int us
   DS_TRY(cudaGetLastError());
   S.drop(rp);
   S.drop(cl);
+  }
   // ---- permuted elements and their incidence (ascending element order per node) ----
   const int64_t ke = E * k;
   DS_TRY(cudaMalloc(&out.tets2, std::max<int64_t>(ke, 1) * 4));
@@ -396,6 +487,8 @@ cudaError_t dev_gather3(int64_t n, const int32_t* perm, const double* in, double
 }
 
 void dev_setup_free(DevPattern& p) {
+  cudaFree(p.rowptr);
+  cudaFree(p.colidx);
   cudaFree(p.perm);
   cudaFree(p.inv);
   cudaFree(p.slice_ptr);

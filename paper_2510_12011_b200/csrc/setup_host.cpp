@@ -245,49 +245,68 @@ void compress_sell(HostSell& s) {
   s.n_wide = wide;
 }
 
-// Balanced contiguous row blocks of the internal (RCM) order.  With RCM's
-// level structure the ghosts of a block come from its neighbouring blocks.
+// Balanced contiguous row blocks of the internal (RCM) order: block p owns
+// [g0, g1) = [floor(n p / P), floor(n (p+1) / P)).  With RCM's level structure
+// the ghosts of a block come from its neighbouring blocks.
+int64_t block_start(int64_t n, int nparts, int p) { return (n * p) / nparts; }
+
+// The plan of block p from ITS OWN ROWS alone (lrp: rowptr of rows [g0, g1)
+// rebased to 0, lcol: their columns, internal indices).  The pattern is
+// structurally symmetric (P1 FEM), so what neighbour q needs from p -- q's
+// ghosts inside p's block -- is the set of p's rows with a column in q's block;
+// both sides list it in ascending internal index.  Each rank can plan itself
+// (and its neighbours) without the others' rows.
+PartPlan plan_from_rows(int64_t n, int nparts, int p, const int64_t* lrp, const int32_t* lcol) {
+  PartPlan P;
+  P.g0 = block_start(n, nparts, p);
+  P.g1 = block_start(n, nparts, p + 1);
+  const int64_t m = P.g1 - P.g0;
+  auto owner = [&](int64_t g) {
+    int q = (int)((g * nparts) / n);
+    while (q + 1 < nparts && block_start(n, nparts, q + 1) <= g) ++q;
+    while (q > 0 && block_start(n, nparts, q) > g) --q;
+    return q;
+  };
+  std::vector<int32_t> gh;
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t t = lrp[i]; t < lrp[i + 1]; ++t)
+      if (lcol[t] < P.g0 || lcol[t] >= P.g1) gh.push_back(lcol[t]);
+  std::sort(gh.begin(), gh.end());
+  gh.erase(std::unique(gh.begin(), gh.end()), gh.end());
+  P.ghosts = std::move(gh);
+  P.recv_off.push_back(0);
+  for (size_t t = 0; t < P.ghosts.size(); ++t) {
+    const int q = owner(P.ghosts[t]);
+    if (P.nbr.empty() || P.nbr.back() != q) {
+      if (!P.nbr.empty()) P.recv_off.push_back((int64_t)t);
+      P.nbr.push_back(q);
+    }
+  }
+  if (!P.nbr.empty()) P.recv_off.push_back((int64_t)P.ghosts.size());
+  // send lists, neighbour by neighbour (ascending), rows ascending
+  P.send_off.assign(1, 0);
+  for (int q : P.nbr) {
+    const int64_t b0 = block_start(n, nparts, q), b1 = block_start(n, nparts, q + 1);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t t = lrp[i]; t < lrp[i + 1]; ++t)
+        if (lcol[t] >= b0 && lcol[t] < b1) {
+          P.send_g.push_back((int32_t)(P.g0 + i));
+          break;
+        }
+    P.send_off.push_back((int64_t)P.send_g.size());
+  }
+  return P;
+}
+
 void plan_partitions(int64_t n, const int64_t* rowptr, const int32_t* col, int nparts,
                      std::vector<PartPlan>& plans) {
   plans.assign(nparts, PartPlan());
-  std::vector<int64_t> bounds(nparts + 1);
-  for (int p = 0; p <= nparts; ++p) bounds[p] = (n * p) / nparts;
-  auto owner = [&](int64_t g) {
-    return (int)(std::upper_bound(bounds.begin(), bounds.end(), g) - bounds.begin()) - 1;
-  };
 #pragma omp parallel for schedule(dynamic, 1)
   for (int p = 0; p < nparts; ++p) {
-    PartPlan& P = plans[p];
-    P.g0 = bounds[p];
-    P.g1 = bounds[p + 1];
-    std::vector<int32_t> gh;
-    for (int64_t i = P.g0; i < P.g1; ++i)
-      for (int64_t t = rowptr[i]; t < rowptr[i + 1]; ++t)
-        if (col[t] < P.g0 || col[t] >= P.g1) gh.push_back(col[t]);
-    std::sort(gh.begin(), gh.end());
-    gh.erase(std::unique(gh.begin(), gh.end()), gh.end());
-    P.ghosts = std::move(gh);
-    P.recv_off.push_back(0);
-    for (size_t t = 0; t < P.ghosts.size(); ++t) {
-      const int q = owner(P.ghosts[t]);
-      if (P.nbr.empty() || P.nbr.back() != q) {
-        if (!P.nbr.empty()) P.recv_off.push_back((int64_t)t);
-        P.nbr.push_back(q);
-      }
-    }
-    if (!P.nbr.empty()) P.recv_off.push_back((int64_t)P.ghosts.size());
-  }
-  // send lists: what neighbour q receives from p = q's ghosts inside p's block
-  for (int p = 0; p < nparts; ++p) {
-    PartPlan& P = plans[p];
-    P.send_off.assign(1, 0);
-    for (int q : P.nbr) {
-      const PartPlan& Q = plans[q];
-      auto lo = std::lower_bound(Q.ghosts.begin(), Q.ghosts.end(), (int32_t)P.g0);
-      auto hi = std::lower_bound(Q.ghosts.begin(), Q.ghosts.end(), (int32_t)P.g1);
-      P.send_g.insert(P.send_g.end(), lo, hi);
-      P.send_off.push_back((int64_t)P.send_g.size());
-    }
+    const int64_t g0 = block_start(n, nparts, p), g1 = block_start(n, nparts, p + 1);
+    std::vector<int64_t> lrp(g1 - g0 + 1);
+    for (int64_t i = g0; i <= g1; ++i) lrp[i - g0] = rowptr[i] - rowptr[g0];
+    plans[p] = plan_from_rows(n, nparts, p, lrp.data(), col + rowptr[g0]);
   }
 }
 

@@ -94,3 +94,33 @@ def test_device_setup_trajectory_matches_oracle(T):
             assert np.linalg.norm(sim.V - ref.Vk) / np.linalg.norm(ref.Vk) <= 1e-8, k
     finally:
         sim.close()
+
+
+@pytest.mark.parametrize("kind,parts,peer", [("slab_perm", 2, 1), ("slab_perm", 3, 0), ("two_components", 3, 1),
+                                             ("biv", 4, 1), ("slab58k", 5, 0)])
+def test_partitioned_device_setup_equals_host_setup(T, kind, parts, peer):
+    """SURVEY 8f f3 "RCM/partition on device": a partitioned context set up on the
+    GPU (global pattern + RCM + interior-first order there, each part planned
+    from its own rows) equals the host path -- same node order, same blocks,
+    ghosts and layout, bitwise-identical trajectories."""
+    xyz, el, region, fib = _mesh(kind)
+    cond = {0: SIG, 1: SIG}
+    stim = [(G.nodes_in_box(xyz, xyz.min(0), xyz.min(0) + 1.5), 0.0, 2.0, 50.0)]
+    sims = []
+    try:
+        for dev in (1, 0):
+            cfg = T.tc_config_default(dt=0.05, abs_tol=1e-8, rel_tol=0.0, device_setup=dev, partitions=parts,
+                                      peer=peer)
+            sims.append(T.Monodomain(xyz, el, region, fib, cond, cfg, stim))
+        d, h = sims
+        assert np.array_equal(T.tc_node_order(d.ctx), T.tc_node_order(h.ctx))
+        mi, mh = T.tc_matrix_info(d.ctx), T.tc_matrix_info(h.ctx)
+        for key in ("n", "nnz", "nnz_pad", "nslices", "partitions", "ghosts", "path"):
+            assert mi[key] == mh[key], key
+        for _ in range(5 if kind == "slab58k" else 15):
+            sd, sh = d.step(1), h.step(1)
+            assert np.array_equal(d.V, h.V)
+            assert sd["iters"][0] == sh["iters"][0]
+    finally:
+        for s in sims:
+            s.close()

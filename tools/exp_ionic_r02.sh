@@ -4,13 +4,13 @@
 #   bash tools/exp_ionic_r02.sh   -> ionic ms/step at 10 M nodes (TT2006, CRN)
 cd "$(dirname "$0")/.."
 # r01 = the library before the table log (built from the parent commit by hand)
-VARS="new: new5:-DTCB_ION_MINB=5 t64:-DTCB_EXP_TAB=64 nwt2:-DTCB_RCP_NEWTON2=1 logonly:-DTCB_EXP_TAB=64+-DTCB_RCP_NEWTON2=1 new6:-DTCB_ION_MINB=6"
+VARS="g5: g4:-DTCB_ION_MINB=4 g6:-DTCB_ION_MINB=6 smem5:-DTCB_ION_TAB_SMEM=1 t64g5:-DTCB_EXP_TAB=64 crn5:-DTCB_ION_MINB_CRN=5"
 if [ "$1" == "build" ]; then
   for v in $VARS; do n=${v%%:*}; f=$(echo ${v#*:} | tr + ' ')
     bash tools/build_variant.sh tools/ion_$n.so $f; done; exit 0
 fi
 for W in slab10M_tt slab10M_crn; do
-for v in r01: $VARS; do
+for v in $VARS; do
   n=${v%%:*}
   TCB200_LIB=tools/ion_$n.so python bench.py --workload $W --steps 20 --warmup 5 --windows 1 --no-cpu-baseline --e2e-steps 0 | \
     python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); r=d['roofline']; print('$W $n', round(d['value']/1e9,4), round(d['ms_per_step'],4), 'ionic_ms', round(r['ionic_ms_per_step'],4), 'clk', d['clocks']['sm_mhz'])"
