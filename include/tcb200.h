@@ -387,6 +387,15 @@ tc_status tc_cohort_info(const tc_cohort* cohort, int32_t out[6]);
 const char* tc_cohort_last_error(const tc_cohort* cohort);
 tc_status tc_cohort_destroy(tc_cohort* cohort);
 
+/* Index audit of an assembled context: downloads
+ * every device index array the step kernels address memory through and checks
+ * it against its allocation -- node permutation, SELL slice pointers and column
+ * indices (owned rows and ghost region, padding, diagonal slot, interior slices
+ * free of ghosts), halo send / receive lists, stimulus lists -- plus finite
+ * matrix values and diag(A)^-1.  checked (nullable): number of indices checked.
+ * TC_EINVAL with the first violation in tc_last_error.  Debug / test use. */
+tc_status tc_validate(tc_ctx* ctx, int64_t* checked);
+
 /* ---- Host-only helpers (no GPU needed; used by the CPU tests) ------------- */
 /* CSR pattern of a tet mesh: (i,j) iff an element holds both.  Call
  * with col = NULL to get rowptr (n+1) first, then again with col (rowptr[n]). */

@@ -22,7 +22,7 @@ __all__ = [
     "tc_num_nodes", "tc_current_step", "tc_get_v", "tc_get_activation", "tc_state_len",
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
     "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "tc_nccl_unique_id", "tc_comm_init",
-    "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "tc_interior_first", "tc_set_allocator", "TorchAllocator", "Monodomain", "LIB_PATH",
+    "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "tc_interior_first", "tc_set_allocator", "TorchAllocator", "tc_validate", "Monodomain", "LIB_PATH",
     "tc_engine_info", "tc_node_order", "tc_apply", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_set_states", "tc_cohort_get_v", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
     "TC_ENGINE_AUTO", "TC_ENGINE_GRID", "TC_ENGINE_CLUSTER",
     "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS", "TC_ION_CRN",
@@ -118,6 +118,7 @@ def _load():
         "tc_partition_plan": ([I64, P, P, I32, I32, P, P, P, P, P, P, P], I32),
         "tc_interior_first": ([I64, P, P, I32, P, P], I32),
         "tc_set_allocator": ([P, P, P, P], I32),
+        "tc_validate": ([P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -474,6 +475,13 @@ class TorchAllocator:
 
         self.alloc_fn = ALLOC_FN(_alloc)
         self.free_fn = FREE_FN(_free)
+
+
+def tc_validate(ctx) -> int:
+    """Index audit of an assembled context (include/tcb200.h); returns the number of checked indices."""
+    out = np.zeros(1, np.int64)
+    _check(ctx, _L.tc_validate(ctx, _ptr(out)))
+    return int(out[0])
 
 
 def tc_set_allocator(ctx, allocator) -> None:

@@ -35,11 +35,14 @@ constexpr int kIonThreads = TCB_ION_THREADS;
 #endif
 
 // The exp / log tables (fp64math.cuh): filled once per device and process into
-// global memory (read-only, 3 KB, L1-resident).  TCB_ION_TAB_SMEM = 1: every CTA
-// copies them into shared memory first (r01 computed them per CTA: 2 exp2 and
-// half a log per thread plus a barrier, ~5 % of the kernel, ncu r02c).
+// global memory (read-only, 3 KB).  TCB_ION_TAB_SMEM = 1 (default): every CTA
+// copies them into shared memory (384 coalesced 8-byte loads, one barrier);
+// 0: the kernels read them from global memory (L1).  r01 computed them per CTA
+// (2 exp2 and half a log per thread plus a barrier: ~5 % of the kernel, ncu
+// r02c).  Measured at 10 M nodes (profiles/r02d_exp_ionic.txt, ionic ms/step):
+// TT2006 1.015 (shared) vs 1.060 (global), CRN 1.148 vs 1.211.
 #ifndef TCB_ION_TAB_SMEM
-#define TCB_ION_TAB_SMEM 0
+#define TCB_ION_TAB_SMEM 1
 #endif
 __global__ void tables_fill_kernel(Exp2Table* T) { exp2_table_fill(T); }
 

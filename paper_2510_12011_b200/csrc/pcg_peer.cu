@@ -7,9 +7,10 @@
 //           into the neighbours' ghost regions of z (remote stores), then a
 //           per-neighbour flag carries the epoch; readers wait on their flags
 //   S     : q = A p, x += alpha p_{it-1}, p.q partial -> rank sum (group barrier);
-//           rows are numbered interior-first, so every CTA runs its share of
-//           the interior slices (no ghost column) before it waits for the
-//           halo, and only the boundary slices after it
+//           rows are numbered interior-first, so in the one grid-stride pass a
+//           warp meets the boundary slices (the ones that read ghosts) only in
+//           its last round(s): it waits for the halo flags there (per warp, no
+//           CTA barrier), its interior slices overlap the transfer
 //   reduce: the rank sum is stored into slot [epoch&1][rank] of EVERY rank's
 //           inbox, then every CTA waits for all ranks' slots of this epoch and
 //           sums them in rank order -> bitwise-identical scalars on all ranks
@@ -177,6 +178,17 @@ __device__ __forceinline__ void halo_push(const XPart& X, int which, unsigned lo
   if (lb == 0 && threadIdx.x < X.nbr_count) vstore(X.rflag[threadIdx.x], epoch);
 }
 
+// Per-warp halo wait (no CTA barrier): lane 0 polls the flags, then the fence
+// orders the flag reads before the data reads and __syncwarp hands that order to
+// the other lanes.  A warp calls it once, before its first boundary slice.
+__device__ __forceinline__ void halo_wait_warp(const XPart& X, unsigned long long epoch) {
+  if ((threadIdx.x & 31) == 0) {
+    for (int q = 0; q < X.nbr_count; ++q) wait_for<true>(X.myflag[q], epoch, X);
+    __threadfence();
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void halo_wait(const XPart& X, unsigned long long epoch) {
   if (threadIdx.x == 0) {
     for (int q = 0; q < X.nbr_count; ++q) wait_for<true>(X.myflag[q], epoch, X);
@@ -217,10 +229,18 @@ __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_
     acc.x += sum * zi;
     acc.y += zi * zi;
   };
-  // interior slices (no ghost column) while the halo is in flight, then the rest
-  for (int s = gw; s < X.nslices_int; s += nw) row(s);
-  halo_wait(X, ep);  // flags are monotone: >= ep covers both halos
-  for (int s = X.nslices_int + gw; s < X.nslices; s += nw) row(s);
+  // one grid-stride pass; rows are interior-first, so a warp reaches the
+  // boundary slices (the ones that read ghosts) only in its last round(s): it
+  // waits for the halo there, the interior slices before it overlap the transfer
+  // (flags are monotone: >= ep covers both halos)
+  bool waited = false;
+  for (int s = gw; s < X.nslices; s += nw) {
+    if (!waited && s >= X.nslices_int) {
+      halo_wait_warp(X, ep);
+      waited = true;
+    }
+    row(s);
+  }
   double2 tot = group_sum2(X, acc, X.part, lb, nb, sh);
   ++ep;
   tot = cross_sum2(X, tot, ep, nrx++, lb, &sh1);
@@ -283,9 +303,14 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
           X.q[i] = sum;
           acc.x += pi * sum;
         };
-        for (int s = gw; s < ni; s += nw) row(s);
-        halo_wait(X, ep);
-        for (int s = ni + gw; s < ns; s += nw) row(s);
+        bool waited = false;
+        for (int s = gw; s < ns; s += nw) {
+          if (!waited && s >= ni) {
+            halo_wait_warp(X, ep);
+            waited = true;
+          }
+          row(s);
+        }
       } else {
         auto row = [&](int s) {
           const int64_t base = __ldg(X.slice_ptr + s);
@@ -301,9 +326,14 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
           X.q[i] = sum;
           acc.x += pi * sum;
         };
-        for (int s = gw; s < ni; s += nw) row(s);
-        halo_wait(X, ep);
-        for (int s = ni + gw; s < ns; s += nw) row(s);
+        bool waited = false;
+        for (int s = gw; s < ns; s += nw) {
+          if (!waited && s >= ni) {
+            halo_wait_warp(X, ep);
+            waited = true;
+          }
+          row(s);
+        }
       }
       plast = it & 1;
       tot = group_sum2(X, acc, X.part + (nred++ & 1) * nb, lb, nb, sh);

@@ -535,3 +535,54 @@ def test_torch_allocator_hook(T):
         assert ei.value.status == T.TC_ESTATE
     finally:
         T.tc_destroy(ctx)
+
+
+@pytest.mark.parametrize("case", ["grid_v0", "grid_v1", "grid_v2", "grid_v4", "grid_v5", "parts2_peer",
+                                  "parts3_split", "parts5_peer_host", "sphere_parts3", "biv_parts4", "mms_parts2",
+                                  "cluster"])
+def test_index_audit(T, case):
+    """Memory safety without compute-sanitizer (closed on the GPU pool): every
+    device index array the step kernels address memory through is inside its
+    allocation (tc_validate, include/tcb200.h), for every layout and path;
+    then 10 steps run and the audit still holds."""
+    kw = dict(dt=0.05, abs_tol=1e-8, rel_tol=0.0)
+    mms = None
+    if case.startswith("sphere"):
+        xyz, el = G.sphere(4)
+        region, fib = np.zeros(el.shape[0], np.int32), G.sphere_fibres(xyz, el)
+        cond = {0: (0.1334177, 0.0173515)}
+        stims = [(np.nonzero(xyz[:, 2] > 0.9 * xyz[:, 2].max())[0].astype(np.int32), 0.0, 2.0, 50.0)]
+        kw.update(model="ms", partitions=3)
+    elif case.startswith("biv"):
+        m = G.biv(2.5)
+        xyz, el, region, fib = m["xyz"], m["tets"], m["region"], m["fibre"]
+        cond = {0: (0.1334177, 0.0173515), 1: (0.1334177, 0.0173515)}
+        stims = [(nodes, 0.0, 2.0, 50.0) for nodes in G.biv_stimuli(m, radius=3.0)]
+        kw.update(partitions=4)
+    elif case.startswith("mms"):
+        xyz, el = G.unit_cube(12)
+        region, fib = np.zeros(el.shape[0], np.int32), G.uniform_fibres(el.shape[0])
+        cond = {0: (1.0, 1.0)}
+        stims = []
+        mms = (1.0, np.pi, np.pi, np.pi, G.box_boundary(xyz))
+        kw.update(model="mms", chi=1.0, cm=1.0, dt=0.01, partitions=2)
+    else:
+        xyz, el, region, fib, cond, stims = _slab_case("tt2006", permute=True, seed=3)
+        if case.startswith("grid_v"):
+            kw.update(engine="grid", pcg_variant=int(case[6:]))
+        elif case == "parts2_peer":
+            kw.update(partitions=2, peer=1)
+        elif case == "parts3_split":
+            kw.update(partitions=3, peer=0)
+        elif case == "parts5_peer_host":
+            kw.update(partitions=5, peer=1, device_setup=0)
+        elif case == "cluster":
+            kw.update(engine="cluster")
+    sim = T.Monodomain(xyz, el, region, fib, cond, T.tc_config_default(**kw), stims, mms=mms)
+    try:
+        n0 = T.tc_validate(sim.ctx)
+        assert n0 >= xyz.shape[0]
+        sim.step(10)
+        assert T.tc_validate(sim.ctx) == n0
+    finally:
+        sim.close()
