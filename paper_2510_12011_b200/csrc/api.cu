@@ -978,7 +978,7 @@ static tc_status assemble_device(tc_ctx* c, const std::vector<int32_t>& ereg) {
   cudaMemcpyAsync(d_sl, c->sig_l.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(d_st, c->sig_t.data(), nr * 8, cudaMemcpyHostToDevice, c->stream);
   cudaMemsetAsync(d_err, 0, 4, c->stream);
-  cudaError_t e = dev_setup(n, E, k, d_tets, c->cfg.use_rcm, 1, dp, c->stream);
+  cudaError_t e = dev_setup(n, E, k, d_tets, c->cfg.use_rcm, 1, false, false, dp, c->stream);
   if (e == cudaSuccess) e = dev_gather3(n, dp.perm, d_xyz, d_xyz2, c->stream);
   if (e != cudaSuccess) {
     cleanup();
@@ -1094,7 +1094,7 @@ static tc_status assemble_device_parts(tc_ctx* c, const std::vector<int32_t>& er
   cudaMemsetAsync(d_err, 0, 4, c->stream);
   const char* nif = std::getenv("TCB_NO_INTERIOR_FIRST");
   const bool reorder = !(nif && nif[0] == '1');
-  cudaError_t e = dev_setup(n, E, k, d_tets, c->cfg.use_rcm, reorder ? c->nparts : -c->nparts, dp, c->stream);
+  cudaError_t e = dev_setup(n, E, k, d_tets, c->cfg.use_rcm, c->nparts, reorder, true, dp, c->stream);
   if (e == cudaSuccess) e = dev_gather3(n, dp.perm, d_xyz, d_xyz2, c->stream);
   if (e != cudaSuccess) {
     cleanup();
@@ -1132,7 +1132,7 @@ static tc_status assemble_device_parts(tc_ctx* c, const std::vector<int32_t>& er
     CUDA_TRY(c, cudaMemcpyAsync(lcol[p].data(), dp.colidx + b, r.back() * 4, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     plans[p] = plan_from_rows(n, P_, p, r.data(), lcol[p].data());
-    plans[p].n_interior = reorder ? dp.n_int[p] : 0;
+    plans[p].n_interior = (reorder && P_ > 1) ? dp.n_int[p] : 0;
     have[p] = 1;
     return TC_OK;
   };

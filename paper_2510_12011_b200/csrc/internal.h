@@ -410,7 +410,7 @@ struct DevPattern {         // device arrays, cudaMalloc'ed by dev_setup (dev_se
   std::vector<int64_t> n_int;   // interior rows of each block (interior-first order)
 };
 cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int use_rcm, int nparts,
-                      DevPattern& out, cudaStream_t s);
+                      bool reorder_parts, bool csr_out, DevPattern& out, cudaStream_t s);
 void dev_setup_free(DevPattern& p);
 cudaError_t dev_gather3(int64_t n, const int32_t* perm, const double* in, double* out, cudaStream_t s);
 

@@ -286,7 +286,7 @@ cudaError_t sort_unique(Scratch& S, uint64_t* a, uint64_t* b, int64_t m, int bit
 }  // namespace
 
 cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int use_rcm, int nparts,
-                      DevPattern& out, cudaStream_t s) {
+                      bool reorder_parts, bool csr_out, DevPattern& out, cudaStream_t s) {
   Scratch S;
   int sh = 1;
   while ((1ll << sh) < n) ++sh;
@@ -371,11 +371,12 @@ cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int us
   // ---- permuted pattern (P A P^T) -------------------------------------------------
   // (rp, cl) = original pattern; the permuted one goes to (rp2, cl2), which is
   // (rp, cl) itself for a single partition (the original is no longer needed)
-  const bool reorder = nparts > 1;   // nparts < -1: partitioned output, plain RCM order (A/B)
-  if (nparts < 0) nparts = -nparts;
+  // partitioned output (csr_out): the global permuted CSR; reorder_parts: the
+  // interior-first order of the nparts blocks first (off: plain RCM order, A/B)
+  const bool reorder = csr_out && reorder_parts && nparts > 1;
   int64_t* rp2 = rp;
   int32_t* cl2 = cl;
-  if (nparts > 1) {
+  if (csr_out) {
     DS_TRY(cudaMalloc(&out.rowptr, (n + 1) * 8));
     DS_TRY(cudaMalloc(&out.colidx, nnz * 4));
     rp2 = out.rowptr;
@@ -423,7 +424,7 @@ cudaError_t dev_setup(int64_t n, int64_t E, int k, const int32_t* d_tets, int us
   S.drop(kb);
   out.n = n;
   out.nnz = nnz;
-  if (nparts > 1) {  // partitioned: the global CSR is the output; SELL is per part (host)
+  if (csr_out) {  // partitioned: the global CSR is the output; SELL is per part (host)
     S.drop(rp);
     S.drop(cl);
     out.nslices = 0;
