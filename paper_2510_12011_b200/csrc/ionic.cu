@@ -10,6 +10,7 @@
 // Stimuli add dt s and theta dt^2 s (s = Isv / (chi C_m)) in stimulus_kernel.
 #include <cmath>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <mutex>
 
@@ -88,6 +89,98 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB)
 #pragma unroll
   for (int s = 0; s < kTTStates; ++s) a.U[s * a.stride + i] = u[s];
   write_rhs(a, i, V, Vp, In);
+}
+
+// ---- persistent variant with asynchronous state prefetch (TCB_ION_PERSIST) ----
+// One wave of CTAs walks the node tiles (128 nodes each) in a grid-stride loop;
+// while a tile computes, the next tile's V^k, V^{k-1} and cell states travel
+// from HBM into this thread's own shared-memory slots by cp.async (no register
+// cost, no barrier: every thread reads and refills only its own slots), so the
+// start-of-CTA load stall of the one-node-per-thread kernel (12 % of the warp
+// samples, ncu r02c) and the per-CTA table copy are paid once per CTA.
+#ifndef TCB_ION_PERSIST
+#define TCB_ION_PERSIST 0
+#endif
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// fields of a node in the stage: [0] V^k, [1] V^{k-1}, [2 ..) states
+template <int NS>
+__device__ __forceinline__ void prefetch_node(const IonArgs& a, int64_t i, double* st) {
+  if (i >= a.n) return;
+  cp_async8(st, a.Vk + i);
+  cp_async8(st + kIonThreads, (a.has_prev ? a.Vkm1 : a.Vk) + i);
+#pragma unroll
+  for (int s = 0; s < NS; ++s) cp_async8(st + (2 + s) * kIonThreads, a.U + s * a.stride + i);
+}
+
+template <int MODEL>
+__global__ void __launch_bounds__(kIonThreads, MODEL == TC_ION_CRN ? TCB_ION_MINB_CRN : TCB_ION_MINB)
+    ionic_persist_kernel(IonArgs a, TTParams P, TTDerived D, CRNParams CP, CRNDerived CD,
+                         const Exp2Table* __restrict__ G) {
+  constexpr int NS = MODEL == TC_ION_CRN ? kCRNStates : kTTStates;
+  extern __shared__ __align__(16) double stage[];   // (2 + NS) x kIonThreads
+  __shared__ Exp2Table Ts;
+  exp2_table_init(&Ts, G);
+  if (a.flags[0]) return;
+  double* my = stage + threadIdx.x;
+  const int64_t ntiles = ((int64_t)a.n + kIonThreads - 1) / kIonThreads;
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) prefetch_node<NS>(a, tile * kIonThreads + threadIdx.x, my);
+  cp_async_commit();
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * kIonThreads + threadIdx.x;
+    cp_async_wait0();
+    double u[NS];
+    const double V = my[0], Vp = my[kIonThreads];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) u[s] = my[(2 + s) * kIonThreads];
+    // the slots are free again: start the next tile's loads, then compute this one
+    const int64_t inext = (tile + gridDim.x) * kIonThreads + threadIdx.x;
+    if (tile + gridDim.x < ntiles) prefetch_node<NS>(a, inext, my);
+    cp_async_commit();
+    if (i < a.n) {
+      if (a.do_lat) activation_update(a, i, V, Vp);
+      double In;
+      if constexpr (MODEL == TC_ION_CRN) In = crn_advance(V, u, a.dt, CP, CD, &Ts);
+      else In = tt_advance(V, u, a.dt, P, D, &Ts);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) a.U[s * a.stride + i] = u[s];
+      write_rhs(a, i, V, Vp, In);
+    }
+  }
+  cp_async_wait0();
+}
+
+template <int MODEL>
+static cudaError_t launch_persist(const IonArgs& a, const TTParams& tp, const CRNParams& cp, cudaStream_t s) {
+  const Exp2Table* G = device_tables();
+  if (!G) return cudaErrorMemoryAllocation;
+  constexpr int NS = MODEL == TC_ION_CRN ? kCRNStates : kTTStates;
+  const size_t smem = (size_t)(2 + NS) * kIonThreads * 8;
+  static int grid_cache[2] = {0, 0};
+  int& per = grid_cache[MODEL == TC_ION_CRN ? 1 : 0];
+  if (!per) {
+    cudaFuncSetAttribute(ionic_persist_kernel<MODEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ionic_persist_kernel<MODEL>, kIonThreads, smem);
+    if (per < 1) per = 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ntiles = ((int64_t)a.n + kIonThreads - 1) / kIonThreads;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)per * sms);
+  TTDerived td{};
+  CRNDerived cd{};
+  if (MODEL == TC_ION_CRN) cd = crn_derived(cp);
+  else td = tt_derived(tp);
+  ionic_persist_kernel<MODEL><<<grid, kIonThreads, smem, s>>>(a, tp, td, cp, cd, G);
+  return cudaGetLastError();
 }
 
 TTDerived tt_derived(const TTParams& P) {
@@ -219,6 +312,7 @@ static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
+  if (TCB_ION_PERSIST) return launch_persist<TC_ION_TT2006_EPI>(a, p, CRNParams{}, s);
   const Exp2Table* G = device_tables();
   if (!G) return cudaErrorMemoryAllocation;
   ionic_tt_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, tt_derived(p), G);
@@ -284,6 +378,7 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN)
 
 cudaError_t launch_ionic_crn(const IonArgs& a, const CRNParams& p, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
+  if (TCB_ION_PERSIST) return launch_persist<TC_ION_CRN>(a, TTParams{}, p, s);
   const Exp2Table* G = device_tables();
   if (!G) return cudaErrorMemoryAllocation;
   ionic_crn_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, crn_derived(p), G);

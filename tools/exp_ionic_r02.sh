@@ -4,7 +4,7 @@
 #   bash tools/exp_ionic_r02.sh   -> ionic ms/step at 10 M nodes (TT2006, CRN)
 cd "$(dirname "$0")/.."
 # r01 = the library before the table log (built from the parent commit by hand)
-VARS="g5: g4:-DTCB_ION_MINB=4 g6:-DTCB_ION_MINB=6 smem5:-DTCB_ION_TAB_SMEM=1 t64g5:-DTCB_EXP_TAB=64 crn5:-DTCB_ION_MINB_CRN=5"
+VARS="base: persist:-DTCB_ION_PERSIST=1 persist4:-DTCB_ION_PERSIST=1+-DTCB_ION_MINB=4"
 if [ "$1" == "build" ]; then
   for v in $VARS; do n=${v%%:*}; f=$(echo ${v#*:} | tr + ' ')
     bash tools/build_variant.sh tools/ion_$n.so $f; done; exit 0
