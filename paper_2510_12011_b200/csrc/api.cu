@@ -1119,6 +1119,9 @@ static tc_status assemble_device_parts(tc_ctx* c, const std::vector<int32_t>& er
   std::vector<char> have(P_, 0);
   std::vector<std::vector<int64_t>> lrp(P_);
   std::vector<std::vector<int32_t>> lcol(P_);
+  // copies of the rows first (stream-ordered), then the host work of all the
+  // parts in parallel (OpenMP): the local parts' plans, their neighbours'
+  // plans (setup_peer's remote ghost offsets), the local SELL layouts
   auto fetch = [&](int p) -> tc_status {
     if (have[p]) return TC_OK;
     const int64_t g0 = c->bounds[p], g1 = c->bounds[p + 1];
@@ -1131,14 +1134,33 @@ static tc_status assemble_device_parts(tc_ctx* c, const std::vector<int32_t>& er
     lcol[p].resize(r.back());
     CUDA_TRY(c, cudaMemcpyAsync(lcol[p].data(), dp.colidx + b, r.back() * 4, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    plans[p] = plan_from_rows(n, P_, p, r.data(), lcol[p].data());
-    plans[p].n_interior = (reorder && P_ > 1) ? dp.n_int[p] : 0;
     have[p] = 1;
     return TC_OK;
   };
-  for (int gid : c->part_ids) {
-    TC_TRY(fetch(gid));
-    for (int q : std::vector<int32_t>(plans[gid].nbr)) TC_TRY(fetch(q));   // setup_peer's remote offsets
+  auto plan_all = [&](const std::vector<int>& ps) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int t = 0; t < (int)ps.size(); ++t) {
+      const int p = ps[t];
+      plans[p] = plan_from_rows(n, P_, p, lrp[p].data(), lcol[p].data());
+      plans[p].n_interior = (reorder && P_ > 1) ? dp.n_int[p] : 0;
+    }
+  };
+  for (int gid : c->part_ids) TC_TRY(fetch(gid));
+  plan_all(c->part_ids);
+  std::vector<int> nbrs;
+  for (int gid : c->part_ids)
+    for (int q : plans[gid].nbr)
+      if (!have[q]) {
+        TC_TRY(fetch(q));
+        nbrs.push_back(q);
+      }
+  plan_all(nbrs);
+  std::vector<HostSell> hss(c->parts.size());
+  std::vector<std::vector<int32_t>> colgs(c->parts.size());
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int pi = 0; pi < (int)c->parts.size(); ++pi) {
+    const int gid = c->part_ids[pi];
+    local_sell_rows(plans[gid], lrp[gid].data(), lcol[gid].data(), hss[pi], colgs[pi]);
   }
   for (size_t pi = 0; pi < c->parts.size(); ++pi) {
     Part& P = c->parts[pi];
@@ -1146,9 +1168,8 @@ static tc_status assemble_device_parts(tc_ctx* c, const std::vector<int32_t>& er
     P.plan = plans[gid];
     const int64_t g0 = P.plan.g0, g1 = P.plan.g1;
     P.n = g1 - g0;
-    HostSell hs;
-    std::vector<int32_t> colg;
-    local_sell_rows(P.plan, lrp[gid].data(), lcol[gid].data(), hs, colg);
+    HostSell& hs = hss[pi];
+    std::vector<int32_t>& colg = colgs[pi];
     P.nslices = hs.nslices;
     P.nslices_int = (int32_t)(P.plan.n_interior / kSellC);
     P.n_pad = hs.n_pad;
