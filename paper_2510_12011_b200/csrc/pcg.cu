@@ -6,7 +6,8 @@
 //   S: p_it = z + beta p_{it-1} is formed on the fly for every gathered column,
 //      q = A p_it (SELL-32, warp per slice, thread per row), the deferred
 //      x += alpha_{it-1} p_{it-1}, and the partial sums of p.q.
-//   U: alpha = rho / p.q;  r -= alpha q;  z = r / diag(A);  partials r.z, z.z;
+//   U: alpha = rho / p.q;  z -= alpha q / diag(A) (z-form: r = diag(A) z is
+//      not stored);  partials r.z = sum z^2 diag(A), z.z;
 //      then every CTA evaluates the stopping test of Alg. 1 identically.
 // Two memory pipelines (measured side by side):
 //  * DIRECT (default, variant 0): 32 registers/thread, 64 warps/SM; every warp
@@ -30,12 +31,15 @@ namespace tcb {
 // 3: direct loads with the matrix kept in L2 (evict-last; systems whose A + col fit in L2),
 // 4: latency variant for systems with few slices per resident warp: every slot
 //    of a row in flight at once (row_Ap_batch), one 16-warp CTA per SM
-// TCB_ZFORM (experiment): the U phase keeps z only -- z_{k+1} = z_k - alpha
-// D^-1 q_k and r.z = sum z^2 / d^-1 -- instead of r and z (Alg. 1 literal):
+// TCB_ZFORM = 1 (default): the U phase keeps z only -- z_{k+1} = z_k - alpha
+// D^-1 q_k and r.z = sum z^2 / d^-1 -- instead of r and z (Alg. 1 literal, 0):
 // 32 instead of 40 bytes per row, the iteration 80n + 12 nnz instead of 88n.
-// Same iterates in exact arithmetic; rounding differs from the oracle's.
+// Same iterates in exact arithmetic; rounding differs from the oracle's at the
+// 1e-16 level (parity unchanged, profiles/r02g_zform_tests.log).  Measured
+// (profiles/r02g_exp_zform.txt, ms per PCG iteration): 20 M MS 1.100 -> 1.070,
+// 10 M TT2006 0.508 -> 0.501; PCG-path frac 0.844 -> 0.869 / 0.863 -> 0.876.
 #ifndef TCB_ZFORM
-#define TCB_ZFORM 0
+#define TCB_ZFORM 1
 #endif
 #ifndef TCB_VEC_U
 #define TCB_VEC_U 0   // 1: U phase and final x update over 16-byte row pairs (measured slower)
