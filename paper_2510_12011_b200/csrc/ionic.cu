@@ -67,8 +67,65 @@ const Exp2Table* device_tables() {
   return t;
 }
 
+// Load-latency hiding (ncu r02f: 16 % of the warp samples wait on the state
+// loads at the top of the kernel).  TCB_ION_EARLY_LOADS = 1: the node's V and
+// states are loaded BEFORE the per-CTA table copy and its barrier, so the DRAM
+// latency overlaps them.  TCB_ION_L2PF = 1: every thread also prefetches (into
+// L2, no registers) the V and states of the node one resident wave ahead
+// (pf_dist nodes), which a CTA of the next wave then finds in L2.
+#ifndef TCB_ION_EARLY_LOADS
+#define TCB_ION_EARLY_LOADS 1
+#endif
+#ifndef TCB_ION_L2PF
+#define TCB_ION_L2PF 0
+#endif
+__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// nodes of one resident wave of a one-node-per-thread ionic kernel (the L2
+// prefetch distance)
+template <class K>
+static int64_t ion_wave(K kernel) {
+  static int64_t wave = 0;  // per kernel (B200 only: one SM count)
+  if (!wave) {
+    int per = 0, dev = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kIonThreads, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    wave = (int64_t)std::max(per, 1) * sms * kIonThreads;
+  }
+  return wave;
+}
+
+template <int NS>
+__device__ __forceinline__ void ion_prefetch(const IonArgs& a, int64_t j) {
+#if TCB_ION_L2PF
+  if (j < a.n && ((threadIdx.x & 3) == 0)) {   // one 32-byte sector per 4 nodes
+    pf_l2(a.Vk + j);
+    if (a.has_prev) pf_l2(a.Vkm1 + j);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) pf_l2(a.U + s * a.stride + j);
+  }
+#else
+  (void)a;
+  (void)j;
+#endif
+}
+
 __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB)
-    ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D, const Exp2Table* __restrict__ G) {
+    ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D, const Exp2Table* __restrict__ G, int64_t pf_dist) {
+  if (a.flags[0]) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double V = 0.0, Vp = 0.0;
+  double u[kTTStates];
+#if TCB_ION_EARLY_LOADS
+  if (i < a.n) {
+    V = a.Vk[i];
+    Vp = a.has_prev ? a.Vkm1[i] : V;
+#pragma unroll
+    for (int s = 0; s < kTTStates; ++s) u[s] = a.U[s * a.stride + i];
+  }
+#endif
+  ion_prefetch<kTTStates>(a, i + pf_dist);
 #if TCB_ION_TAB_SMEM
   __shared__ Exp2Table Ts;
   exp2_table_init(&Ts, G);
@@ -76,15 +133,14 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB)
 #else
   const Exp2Table* __restrict__ T = G;
 #endif
-  if (a.flags[0]) return;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
-  const double V = a.Vk[i];
-  const double Vp = a.has_prev ? a.Vkm1[i] : V;
-  if (a.do_lat) activation_update(a, i, V, Vp);
-  double u[kTTStates];
+#if !TCB_ION_EARLY_LOADS
+  V = a.Vk[i];
+  Vp = a.has_prev ? a.Vkm1[i] : V;
 #pragma unroll
   for (int s = 0; s < kTTStates; ++s) u[s] = a.U[s * a.stride + i];
+#endif
+  if (a.do_lat) activation_update(a, i, V, Vp);
   const double In = tt_advance(V, u, a.dt, P, D, T);
 #pragma unroll
   for (int s = 0; s < kTTStates; ++s) a.U[s * a.stride + i] = u[s];
@@ -315,7 +371,7 @@ cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s)
   if (TCB_ION_PERSIST) return launch_persist<TC_ION_TT2006_EPI>(a, p, CRNParams{}, s);
   const Exp2Table* G = device_tables();
   if (!G) return cudaErrorMemoryAllocation;
-  ionic_tt_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, tt_derived(p), G);
+  ionic_tt_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, tt_derived(p), G, ion_wave(ionic_tt_kernel));
   return cudaGetLastError();
 }
 cudaError_t launch_ionic_ms(const IonArgs& a, const MSParams& p, cudaStream_t s) {
@@ -353,7 +409,20 @@ CRNDerived crn_derived(const CRNParams& P) {
 }
 
 __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN)
-    ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D, const Exp2Table* __restrict__ G) {
+    ionic_crn_kernel(IonArgs a, CRNParams P, CRNDerived D, const Exp2Table* __restrict__ G, int64_t pf_dist) {
+  if (a.flags[0]) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double V = 0.0, Vp = 0.0;
+  double u[kCRNStates];
+#if TCB_ION_EARLY_LOADS
+  if (i < a.n) {
+    V = a.Vk[i];
+    Vp = a.has_prev ? a.Vkm1[i] : V;
+#pragma unroll
+    for (int s = 0; s < kCRNStates; ++s) u[s] = a.U[s * a.stride + i];
+  }
+#endif
+  ion_prefetch<kCRNStates>(a, i + pf_dist);
 #if TCB_ION_TAB_SMEM
   __shared__ Exp2Table Ts;
   exp2_table_init(&Ts, G);
@@ -361,15 +430,14 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN)
 #else
   const Exp2Table* __restrict__ T = G;
 #endif
-  if (a.flags[0]) return;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
-  const double V = a.Vk[i];
-  const double Vp = a.has_prev ? a.Vkm1[i] : V;
-  if (a.do_lat) activation_update(a, i, V, Vp);
-  double u[kCRNStates];
+#if !TCB_ION_EARLY_LOADS
+  V = a.Vk[i];
+  Vp = a.has_prev ? a.Vkm1[i] : V;
 #pragma unroll
   for (int s = 0; s < kCRNStates; ++s) u[s] = a.U[s * a.stride + i];
+#endif
+  if (a.do_lat) activation_update(a, i, V, Vp);
   const double In = crn_advance(V, u, a.dt, P, D, T);
 #pragma unroll
   for (int s = 0; s < kCRNStates; ++s) a.U[s * a.stride + i] = u[s];
@@ -381,7 +449,7 @@ cudaError_t launch_ionic_crn(const IonArgs& a, const CRNParams& p, cudaStream_t 
   if (TCB_ION_PERSIST) return launch_persist<TC_ION_CRN>(a, TTParams{}, p, s);
   const Exp2Table* G = device_tables();
   if (!G) return cudaErrorMemoryAllocation;
-  ionic_crn_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, crn_derived(p), G);
+  ionic_crn_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, crn_derived(p), G, ion_wave(ionic_crn_kernel));
   return cudaGetLastError();
 }
 

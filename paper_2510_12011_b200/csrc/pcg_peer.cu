@@ -14,7 +14,8 @@
 //   reduce: the rank sum is stored into slot [epoch&1][rank] of EVERY rank's
 //           inbox, then every CTA waits for all ranks' slots of this epoch and
 //           sums them in rank order -> bitwise-identical scalars on all ranks
-//   U     : r, z, (r.z, z.z) partials -> rank sum -> cross-rank reduce, test, beta
+//   U     : z (z-form: z -= alpha D^-1 q), (r.z, z.z) partials -> rank sum ->
+//           cross-rank reduce, test, beta
 // Memory ordering: data stores, __threadfence_system(), then the flag/epoch
 // store; readers poll with volatile loads, then __threadfence() (which also
 // drops stale L1 lines) before touching the data.  Slots are double-buffered
@@ -346,11 +347,11 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
       acc = make_double2(0.0, 0.0);
       for (int s = gw; s < ns; s += nw) {
         const int64_t i = (int64_t)s * kSellC + lane;
-        const double ri = X.r[i] - alpha * X.q[i];
-        const double zi = __ldg(X.dinv + i) * ri;
-        X.r[i] = ri;
+        // z-form (pcg.cu TCB_ZFORM): z -= alpha D^-1 q, r.z = sum z^2 / d^-1
+        const double di = __ldg(X.dinv + i);
+        const double zi = X.z[i] - alpha * (di * X.q[i]);
         X.z[i] = zi;
-        acc.x += ri * zi;
+        acc.x += di != 0.0 ? zi * (zi / di) : 0.0;
         acc.y += zi * zi;
       }
       tot = group_sum2(X, acc, X.part + (nred++ & 1) * nb, lb, nb, sh);

@@ -9,7 +9,7 @@
 //            so z_c + beta p_c == p_c for every ghost column c)
 //   S      : q = A p_it, x += alpha_{it-1} p_{it-1}, rank partial of p.q
 //   (allreduce p.q)
-//   U      : alpha = rho / p.q, r -= alpha q, z = r / diag, rank partials r.z, z.z
+//   U      : alpha = rho / p.q, z -= alpha q / diag (z-form), rank partials r.z, z.z
 //   (allreduce)
 //   scalar : one thread: stopping test, beta, rho (identical on every partition,
 //            because the all-reduced sums are bitwise identical)
@@ -165,11 +165,11 @@ __global__ void __launch_bounds__(kSplitThreads, 8) split_U_kernel(SplitArgs a) 
   const int64_t n = (int64_t)a.nslices * kSellC;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double ri = a.r[i] - alpha * a.q[i];
-    const double zi = __ldg(a.dinv + i) * ri;
-    a.r[i] = ri;
+    // z-form (pcg.cu TCB_ZFORM): z -= alpha D^-1 q, r.z = sum z^2 / d^-1
+    const double di = __ldg(a.dinv + i);
+    const double zi = a.z[i] - alpha * (di * a.q[i]);
     a.z[i] = zi;
-    acc.x += ri * zi;
+    acc.x += di != 0.0 ? zi * (zi / di) : 0.0;
     acc.y += zi * zi;
   }
   reduce_to_rank(acc, a.part, a.ticket, a.red, sh);
