@@ -1436,6 +1436,7 @@ static CgArgs cg_args(tc_ctx* c, Part& P, double* x) {
   a.rel_mode = c->cfg.rel_mode;
   a.flags = c->d_flags;
   a.step_tag = (int32_t)c->k;
+  a.store_r = 1;
   return a;
 }
 
@@ -1808,6 +1809,7 @@ static tc_status enqueue_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* dstats, 
       Part& P = c->parts[0];
       CgArgs ca = cg_args(c, P, P.d_V[c->iX]);
       ca.stat = dstats + st;
+      ca.store_r = (P.pcg_var == 5 || !TCB_ZFORM) ? 1 : 0;  // only the graph engine's U reads r
       if (P.pcg_var == 5) {  // RHS kernel, then the solve graph (init, WHILE{S, U}, final)
         CUDA_TRY(c, launch_rhs(1, 0, ca, P.grid, c->stream));
         CUDA_TRY(c, g_launch(P.gexec, P.d_gstep, P.d_V[c->iX], dstats + st, (int32_t)c->k, c->stream));

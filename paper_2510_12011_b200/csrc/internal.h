@@ -94,6 +94,16 @@ double* ms_param_slot(MSParams* p, const char* name);
 // ---------------------------------------------------------------------------
 // Kernel argument blocks
 // ---------------------------------------------------------------------------
+// TCB_ZFORM = 1 (default): the U phase keeps z only -- z_{k+1} = z_k - alpha
+// D^-1 q_k and r.z = sum z^2 / d^-1 -- instead of r and z (Alg. 1 literal, 0):
+// 32 instead of 40 bytes per row, the iteration 80n + 12 nnz instead of 88n.
+// Same iterates in exact arithmetic; rounding differs from the oracle's at the
+// 1e-16 level (parity unchanged, profiles/r02g_zform_tests.log).  Measured
+// (profiles/r02g_exp_zform.txt, ms per PCG iteration): 20 M MS 1.100 -> 1.070,
+// 10 M TT2006 0.508 -> 0.501; PCG-path frac 0.844 -> 0.869 / 0.863 -> 0.876.
+#ifndef TCB_ZFORM
+#define TCB_ZFORM 1
+#endif
 struct CgArgs {
   const int64_t* slice_ptr;
   const int32_t* col;
@@ -119,6 +129,7 @@ struct CgArgs {
   tc_step_stat* stat;  // where this solve's report goes
   int32_t* flags;      // [0] abort [1] nan [2] consecutive fails [3] fail budget [4] step of abort
   int32_t step_tag;    // step index recorded on abort
+  int32_t store_r;     // RHS kernel: also store r_0 (the r-form U phases: variant 5); z-form reads z only
 };
 
 // ---- split-phase (partitioned) PCG: device scalar state of Algorithm 1 -----

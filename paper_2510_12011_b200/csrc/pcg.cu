@@ -31,18 +31,11 @@ namespace tcb {
 // 3: direct loads with the matrix kept in L2 (evict-last; systems whose A + col fit in L2),
 // 4: latency variant for systems with few slices per resident warp: every slot
 //    of a row in flight at once (row_Ap_batch), one 16-warp CTA per SM
-// TCB_ZFORM = 1 (default): the U phase keeps z only -- z_{k+1} = z_k - alpha
-// D^-1 q_k and r.z = sum z^2 / d^-1 -- instead of r and z (Alg. 1 literal, 0):
-// 32 instead of 40 bytes per row, the iteration 80n + 12 nnz instead of 88n.
-// Same iterates in exact arithmetic; rounding differs from the oracle's at the
-// 1e-16 level (parity unchanged, profiles/r02g_zform_tests.log).  Measured
-// (profiles/r02g_exp_zform.txt, ms per PCG iteration): 20 M MS 1.100 -> 1.070,
-// 10 M TT2006 0.508 -> 0.501; PCG-path frac 0.844 -> 0.869 / 0.863 -> 0.876.
-#ifndef TCB_ZFORM
-#define TCB_ZFORM 1
-#endif
 #ifndef TCB_VEC_U
 #define TCB_VEC_U 0   // 1: U phase and final x update over 16-byte row pairs (measured slower)
+#endif
+#if TCB_VEC_U && TCB_ZFORM
+#error "TCB_VEC_U has only the r-form U phase: build it with -DTCB_ZFORM=0"
 #endif
 #ifndef TCB_BATCH_UU
 #define TCB_BATCH_UU 1    // slices per warp pass in variant 4's U phase (measured 1 < 2 < 4)
@@ -135,7 +128,7 @@ __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : VAR == 4 
                  sum = a.b[i] - ax;
                }
                const double zi = __ldg(a.dinv + i) * sum;
-               a.r[i] = sum;
+               if (a.store_r) a.r[i] = sum;
                a.z[i] = zi;
                acc.x += sum * zi;
                acc.y += zi * zi;
