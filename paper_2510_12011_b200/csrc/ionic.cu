@@ -73,8 +73,14 @@ const Exp2Table* device_tables() {
 // latency overlaps them.  TCB_ION_L2PF = 1: every thread also prefetches (into
 // L2, no registers) the V and states of the node one resident wave ahead
 // (pf_dist nodes), which a CTA of the next wave then finds in L2.
+// Measured (profiles/r02h_exp_ionic.txt, 10 M nodes, ionic ms/step, 1965 MHz):
+// TT2006 early 0.952-0.957 vs late 0.962; CRN early 1.087 vs late 1.062 -> early
+// loads for TT2006 only (TCB_ION_EARLY_LOADS_CRN); the L2 prefetch costs 2-4 %.
 #ifndef TCB_ION_EARLY_LOADS
 #define TCB_ION_EARLY_LOADS 1
+#endif
+#ifndef TCB_ION_EARLY_LOADS_CRN
+#define TCB_ION_EARLY_LOADS_CRN 0
 #endif
 #ifndef TCB_ION_L2PF
 #define TCB_ION_L2PF 0
@@ -414,7 +420,7 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double V = 0.0, Vp = 0.0;
   double u[kCRNStates];
-#if TCB_ION_EARLY_LOADS
+#if TCB_ION_EARLY_LOADS_CRN
   if (i < a.n) {
     V = a.Vk[i];
     Vp = a.has_prev ? a.Vkm1[i] : V;
@@ -431,7 +437,7 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB_CRN)
   const Exp2Table* __restrict__ T = G;
 #endif
   if (i >= a.n) return;
-#if !TCB_ION_EARLY_LOADS
+#if !TCB_ION_EARLY_LOADS_CRN
   V = a.Vk[i];
   Vp = a.has_prev ? a.Vkm1[i] : V;
 #pragma unroll
