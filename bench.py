@@ -220,7 +220,7 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def ncu_traffic(workload, iters_per_step):
+def ncu_traffic(workload, iters_per_step, rhs=True):
     """DRAM bytes per step of the PCG path (rhs_kernel + pcg_kernel) from the committed
     ncu --set full capture, the pcg part rescaled to the timed mean iteration count."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -229,7 +229,7 @@ def ncu_traffic(workload, iters_per_step):
             e = json.load(f).get(workload)
         if e is None:
             return None
-        return e["rhs_bytes"] + e["pcg_bytes"] * iters_per_step / e["iters"]
+        return (e["rhs_bytes"] if rhs else 0.0) + e["pcg_bytes"] * iters_per_step / e["iters"]
     except Exception:
         return None
 
@@ -432,22 +432,32 @@ def measure_grid(args, name, w, local, stream, preroll=None, e2e_steps=6, cpu=Tr
     ms, iters, prof = wins[order[len(order) // 2]]
     value = n * args.steps / (ms / 1e3)
 
-    # roofline of the dominant kernel: the cooperative PCG kernel (RHS + Alg. 1)
+    # roofline of the dominant kernel: the cooperative PCG kernel (RHS + Alg. 1);
+    # with the ionic || RHS pipeline the profile's PCG time is the PCG kernel alone
+    pipe = T.tc_pipeline_info(sim.ctx) if eng["engine"] == "grid" else {"chunks": 0, "rows_per_chunk": 0}
     peaks, which = measured_peaks()
     nnz = info["nnz"]
     b_cg, b_ion = bytes_per_step(n, nnz, iters, w["model"], args.steps)
+    if pipe["chunks"]:
+        b_cg -= (20 * nnz + 4 * (n + 1) + 44 * n) * args.steps      # RHS bytes overlap the ionic kernel
     cg_s = prof["pcg_ms"] / 1e3
     achieved = b_cg / cg_s / 1e9 if cg_s > 0 else None
-    traffic = ncu_traffic(name, iters / args.steps)
+    traffic = ncu_traffic(name, iters / args.steps, rhs=not pipe["chunks"])
     kname = ("PCG path per step: rhs_kernel + cooperative pcg_kernel (Eq. 3 RHS + Alg. 1)" if eng["engine"] == "grid"
              else "cohort_kernel (cluster engine: the whole step, ionic + RHS + Alg. 1, one launch per call)")
+    if pipe["chunks"]:
+        kname = (f"cooperative pcg_kernel (Alg. 1; the RHS runs in {pipe['chunks']} chunks overlapped with the ionic "
+                 "kernel and is not counted)")
     roof = {"kernel": kname,
             "bound": "hbm",
             "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"] if achieved else None,
             "traffic": traffic, "peak_source": which,
             "frac_of_nominal_8TBs": achieved / 8000.0 if achieved else None,
-            "bytes_model": "per step: 20nnz+4(n+1)+44n + iters*(12nnz+4(n+1)+72n) (SURVEY 8d)",
+            "bytes_model": ("per step: iters*(12nnz+4(n+1)+72n) (SURVEY 8d; RHS overlapped with the ionic kernel)"
+                            if pipe["chunks"] else
+                            "per step: 20nnz+4(n+1)+44n + iters*(12nnz+4(n+1)+72n) (SURVEY 8d)"),
+            "ionic_rhs_pipeline": pipe,
             "algorithmic_bytes_per_step": b_cg / args.steps,
             "traffic_unit": "DRAM bytes per step of the same kernels (ncu, profiles/ncu_traffic.json)",
             "share_of_step": prof["pcg_ms"] / ms,

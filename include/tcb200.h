@@ -387,6 +387,11 @@ tc_status tc_cohort_info(const tc_cohort* cohort, int32_t out[6]);
 const char* tc_cohort_last_error(const tc_cohort* cohort);
 tc_status tc_cohort_destroy(tc_cohort* cohort);
 
+/* Ionic || RHS pipeline of the grid engine:
+ * out[0] = row chunks (0: the kernels run one after the other), out[1] = rows
+ * per chunk.  With chunks, tc_profile_read's out[0] covers the overlapped ionic
+ * and RHS kernels and out[1] the PCG kernel alone. */
+tc_status tc_pipeline_info(tc_ctx* ctx, int64_t out[2]);
 /* Index audit of an assembled context: downloads
  * every device index array the step kernels address memory through and checks
  * it against its allocation -- node permutation, SELL slice pointers and column

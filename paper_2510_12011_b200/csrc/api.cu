@@ -130,6 +130,14 @@ struct tc_ctx {
   // tc_step_io: copy streams, double-buffered device staging, events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaStream_t s_halo = nullptr;           // split path: halo exchange stream (overlapped)
+  // ionic || RHS pipeline (chunked_step): row chunks, RHS stream, events
+  int ion_chunks = -1;                     // -1 undecided, 0 off, C > 0 chunks
+  int64_t ch_rows = 0;                     // rows per chunk (multiple of 128)
+  std::vector<int> ch_need;                // RHS chunk c needs the ionic output of chunks <= ch_need[c]
+  cudaStream_t s_rhs = nullptr;
+  std::vector<cudaEvent_t> e_ion;
+  cudaEvent_t e_rhs = nullptr;
+  double2* d_rpart = nullptr;              // C x grid RHS partials
   cudaEvent_t e_packed = nullptr, e_halo = nullptr;
   double* d_sin[2] = {nullptr, nullptr};   // staged input states (original order)
   double* d_sout[2] = {nullptr, nullptr};  // staged outputs V^{k+1} (original order)
@@ -317,6 +325,12 @@ tc_status tc_destroy(tc_ctx* c) {
       cudaEventDestroy(c->e_done[b]);
       cudaEventDestroy(c->e_read[b]);
     }
+  }
+  if (c->s_rhs) {
+    cudaStreamSynchronize(c->s_rhs);
+    cudaStreamDestroy(c->s_rhs);
+    for (cudaEvent_t e : c->e_ion) cudaEventDestroy(e);
+    if (c->e_rhs) cudaEventDestroy(c->e_rhs);
   }
   if (c->s_halo) {
     cudaStreamSynchronize(c->s_halo);
@@ -1436,6 +1450,10 @@ static CgArgs cg_args(tc_ctx* c, Part& P, double* x) {
   a.rel_mode = c->cfg.rel_mode;
   a.flags = c->d_flags;
   a.step_tag = (int32_t)c->k;
+  a.s0 = 0;
+  a.s1 = P.nslices;
+  a.rpart = P.d_part;
+  a.n_rpart = P.grid;
   a.store_r = 1;
   return a;
 }
@@ -1744,6 +1762,110 @@ static void advance_host(tc_ctx* c, int64_t nsteps) {
 
 static tc_status finish_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* stats, size_t evi, bool cluster);
 
+// ---- ionic || RHS pipeline -----------------
+// The ionic kernel is FP64-bound (HBM half idle), the RHS kernel HBM-bound (FP64
+// idle).  With the rows cut into C chunks (RCM order), RHS chunk c needs the
+// ionic output (u', v') of its rows' columns only, i.e. of chunks <= ch_need[c]
+// (computed once from the SELL columns): the ionic chunks run on the context
+// stream, each RHS chunk on a second stream as soon as the ionic chunks it
+// reads are done, so the two kernels' work overlaps; the PCG kernel then sums
+// the C x grid RHS partials in a fixed order.  Used for TT2006 / CRN on the
+// grid engine (one partition, PCG variant 0 or 4) when no stimulus epoch is
+// active at the step; TCB_ION_RHS_CHUNKS (environment) sets C (0 = off).
+static int ion_rhs_chunks_wanted(const tc_ctx* c) {
+  const char* e = std::getenv("TCB_ION_RHS_CHUNKS");
+  if (e) return std::max(0, std::atoi(e));
+  return 0;
+}
+
+static IonArgs ion_sub(IonArgs a, int64_t r0, int64_t r1) {
+  a.n = (int32_t)(r1 - r0);
+  a.Vk += r0;
+  a.Vkm1 += r0;
+  a.U += r0;
+  a.x0 += r0;
+  a.up += r0;
+  a.vp += r0;
+  a.act += r0;
+  a.lat += r0;
+  a.lrt += r0;
+  return a;
+}
+
+static tc_status chunk_setup(tc_ctx* c) {
+  c->ion_chunks = 0;
+  const int C = ion_rhs_chunks_wanted(c);
+  if (C < 2 || c->parts.size() != 1 || split_mode(c)) return TC_OK;
+  if (c->cfg.model != TC_ION_TT2006_EPI && c->cfg.model != TC_ION_CRN) return TC_OK;
+  Part& P = c->parts[0];
+  if (P.pcg_var != 0 && P.pcg_var != 4) return TC_OK;
+  const int64_t rows = ((P.n + C - 1) / C + 127) / 128 * 128;   // whole ionic tiles and SELL slices
+  const int nc = (int)((P.n + rows - 1) / rows);
+  if (nc < 2) return TC_OK;
+  int32_t* d_max = nullptr;
+  CUDA_TRY(c, cudaMalloc(&d_max, nc * 4));
+  CUDA_TRY(c, cudaMemsetAsync(d_max, 0, nc * 4, c->stream));
+  CUDA_TRY(c, launch_chunk_maxcol(P.d_sp, P.d_col, P.nslices, (int32_t)(rows / kSellC), d_max, c->stream));
+  std::vector<int32_t> mx(nc);
+  CUDA_TRY(c, cudaMemcpyAsync(mx.data(), d_max, nc * 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d_max);
+  c->ch_need.resize(nc);
+  for (int q = 0; q < nc; ++q) c->ch_need[q] = std::min(nc - 1, std::max(q, (int)(mx[q] / rows)));
+  const char* pr = std::getenv("TCB_RHS_PRIO");
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  CUDA_TRY(c, cudaStreamCreateWithPriority(&c->s_rhs, cudaStreamNonBlocking, (pr && pr[0] == '1') ? hi : lo));
+  c->e_ion.resize(nc);
+  for (auto& e : c->e_ion) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CUDA_TRY(c, cudaEventCreateWithFlags(&c->e_rhs, cudaEventDisableTiming));
+  CUDA_TRY(c, dalloc(c, &c->d_rpart, (int64_t)nc * P.grid));
+  c->ch_rows = rows;
+  c->ion_chunks = nc;
+  return TC_OK;
+}
+
+static bool stimulus_active(const tc_ctx* c) {
+  for (const Part& P : c->parts)
+    for (const Epoch& ep : P.epochs)
+      if (ep.k0 <= c->k && c->k < ep.k1) return true;
+  return false;
+}
+
+// ionic chunks (context stream) || RHS chunks (RHS stream), then the PCG kernel
+static tc_status chunked_step(tc_ctx* c, int do_lat, tc_step_stat* stat, bool prof, size_t& evi) {
+  Part& P = c->parts[0];
+  const int nc = c->ion_chunks;
+  const IonArgs ia = ion_args(c, P, do_lat);
+  for (int q = 0; q < nc; ++q) {
+    const int64_t r0 = (int64_t)q * c->ch_rows, r1 = std::min<int64_t>(P.n, r0 + c->ch_rows);
+    const IonArgs sub = ion_sub(ia, r0, r1);
+    CUDA_TRY(c, c->cfg.model == TC_ION_CRN ? launch_ionic_crn(sub, c->crn, c->stream)
+                                           : launch_ionic_tt(sub, c->tt, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->e_ion[q], c->stream));
+  }
+  CgArgs ca = cg_args(c, P, P.d_V[c->iX]);
+  ca.stat = stat;
+  ca.store_r = 0;
+  const int32_t spc = (int32_t)(c->ch_rows / kSellC);
+  for (int q = 0; q < nc; ++q) {
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s_rhs, c->e_ion[c->ch_need[q]], 0));
+    CgArgs cq = ca;
+    cq.s0 = q * spc;
+    cq.s1 = std::min(P.nslices, (q + 1) * spc);
+    cq.part = c->d_rpart + (int64_t)q * P.grid;
+    CUDA_TRY(c, launch_rhs(1, P.pcg_var, cq, P.grid, c->s_rhs));
+  }
+  CUDA_TRY(c, cudaEventRecord(c->e_rhs, c->s_rhs));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->e_rhs, 0));
+  if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+  ca.rpart = c->d_rpart;
+  ca.n_rpart = nc * P.grid;
+  CUDA_TRY(c, launch_pcg_only(1, P.pcg_var, ca, P.grid, c->stream));
+  c->launches += 2 * nc + 1;
+  return TC_OK;
+}
+
 // Enqueue nsteps steps on c->stream (no host synchronisation); per-step reports
 // go to dstats[0 .. nsteps).  prof: record the profiling events (tc_step only).
 static tc_status enqueue_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* dstats, bool prof, size_t& evi,
@@ -1762,8 +1884,21 @@ static tc_status enqueue_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* dstats, 
     advance_host(c, nsteps);
     return TC_OK;
   }
+  if (c->ion_chunks < 0) TC_TRY(chunk_setup(c));
   for (int64_t st = 0; st < nsteps; ++st) {
     if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+    if (c->ion_chunks > 0 && !stimulus_active(c)) {
+      // ionic || RHS, then Algorithm 1 (profiling: [ionic + RHS] [PCG kernel])
+      TC_TRY(chunked_step(c, (st > 0 && c->has_prev) ? 1 : 0, dstats + st, prof, evi));
+      if (prof) CUDA_TRY(c, cudaEventRecord(ev(c, evi++), c->stream));
+      const int old = c->iVkm1;
+      c->iVkm1 = c->iVk;
+      c->iVk = c->iX;
+      c->iX = old;
+      c->k += 1;
+      c->has_prev = true;
+      continue;
+    }
     // (1) ionic step + LAT/LRT of V^k + x0, u', v'; (2) stimulus of the epoch of step k
     for (Part& P : c->parts) {
       IonArgs ia = ion_args(c, P, (st > 0 && c->has_prev) ? 1 : 0);
@@ -2439,6 +2574,16 @@ extern "C" tc_status tc_node_order(const tc_ctx* c, int32_t* perm) {
   if (!c || !perm) return TC_EINVAL;
   if (!c->assembled || c->csr_mode) return TC_ESTATE;
   std::copy(c->perm.begin(), c->perm.end(), perm);
+  return TC_OK;
+}
+
+extern "C" tc_status tc_pipeline_info(tc_ctx* c, int64_t out[2]) {
+  if (!c || !out) return TC_EINVAL;
+  if (!c->assembled || c->csr_mode) return fail(c, TC_ESTATE, "tc_pipeline_info before tc_assemble");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->ion_chunks < 0 && !use_cluster(c)) TC_TRY(chunk_setup(c));
+  out[0] = std::max(c->ion_chunks, 0);
+  out[1] = c->ion_chunks > 0 ? c->ch_rows : 0;
   return TC_OK;
 }
 

@@ -130,6 +130,9 @@ struct CgArgs {
   int32_t* flags;      // [0] abort [1] nan [2] consecutive fails [3] fail budget [4] step of abort
   int32_t step_tag;    // step index recorded on abort
   int32_t store_r;     // RHS kernel: also store r_0 (the r-form U phases: variant 5); z-form reads z only
+  int32_t s0, s1;      // RHS kernel: slice range [s0, s1) (chunked RHS; default [0, nslices))
+  const double2* rpart;  // PCG kernel: the RHS partials it sums first (default part) ...
+  int32_t n_rpart;       // ... and how many (default gridDim.x)
 };
 
 // ---- split-phase (partitioned) PCG: device scalar state of Algorithm 1 -----
@@ -365,6 +368,10 @@ cudaError_t g_launch(cudaGraphExec_t exec, GStep* gs, double* x, tc_step_stat* s
 int cg_pick_variant(int requested, int32_t nslices, int device);
 cudaError_t launch_rhs(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_pcg_only(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
+// per-chunk maximum column of the rows of a single-partition SELL layout
+cudaError_t launch_chunk_maxcol(const int64_t* sp, const int32_t* col, int32_t nslices, int32_t slices_per_chunk,
+                                int32_t* chunk_max, cudaStream_t s);
 
 // split-phase PCG launchers (pcg_split.cu); grid = split_grid(nslices)
 int split_grid(int32_t nslices);

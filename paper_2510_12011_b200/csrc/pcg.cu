@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : VAR == 4 
   SlicePipe P;
   if (TMA) setup_pipe(P, smem, bars[TMA ? warp : 0], warp, lane);
   double2 acc = make_double2(0.0, 0.0);
-  for_slices<TMA>(P, a.slice_ptr, Av, a.col, a.nslices, gw, nw, lane,
+  for_slices<TMA>(P, a.slice_ptr, Av, a.col, a.s1, a.s0 + gw, nw, lane,
              [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
                double sum = 0.0;
                if (MODE == 1) {
@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
   double2 tot;
   {
     double2 acc0 = make_double2(0.0, 0.0);
-    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) {
-      const double2 u = partA[t];
+    for (int t = threadIdx.x; t < a.n_rpart; t += blockDim.x) {
+      const double2 u = a.rpart[t];
       acc0.x += u.x;
       acc0.y += u.y;
     }
@@ -416,6 +416,34 @@ cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStr
   if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(pcg_fn(mode, variant), dim3(grid), dim3(kCgThreads), args,
                                      pcg_smem(variant), s);
+}
+
+cudaError_t launch_pcg_only(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s) {
+  void* args[] = {(void*)&a};
+  return cudaLaunchCooperativeKernel(pcg_fn(mode, variant), dim3(grid), dim3(kCgThreads), args,
+                                     pcg_smem(variant), s);
+}
+
+__global__ void chunk_maxcol_kernel(const int64_t* __restrict__ sp, const int32_t* __restrict__ col,
+                                    int32_t nslices, int32_t spc, int32_t* chunk_max) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t s = (int32_t)(t >> 5);
+  if (s >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t base = sp[s];
+  const int w = (int)((sp[s + 1] - base) >> 5);
+  int32_t m = 0;
+  for (int k = 0; k < w; ++k) m = max(m, col[base + (int64_t)k * kSellC + lane]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) atomicMax(chunk_max + s / spc, m);
+}
+
+cudaError_t launch_chunk_maxcol(const int64_t* sp, const int32_t* col, int32_t nslices, int32_t spc,
+                                int32_t* chunk_max, cudaStream_t s) {
+  const int64_t threads = (int64_t)nslices * 32;
+  chunk_maxcol_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(sp, col, nslices, spc, chunk_max);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rhs(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s) {
