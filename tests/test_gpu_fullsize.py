@@ -174,6 +174,45 @@ _MULTI = {
 }
 
 
+@pytest.mark.parametrize("name", ["slab10M_tt", "slab20M_ms"])
+def test_fullsize_whole_oracle_step(T, name):
+    """The bench's own configurations at FULL size -- the north-star 10 M-node
+    TT2006 slab and the default 20 M-node MS slab (configs[4]) -- built and
+    prerolled exactly as bench.py times them: one step from the GPU's state
+    against the WHOLE oracle step (assembly, ionic update, Eq. 3 RHS,
+    Algorithm 1) on the same state: rel-L2(V) <= 1e-8 (north_star), every cell
+    state to 1e-9, PCG iterations within 1."""
+    w, sim, xyz, tets, region, fibre = _bench_sim(T, name)
+    try:
+        n = xyz.shape[0]
+        ns = {"tt2006": 18, "crn": 20, "ms": 1}[w["model"]]
+        s = sim.get_state()
+        Vk, Vkm1, U = _split_state(s, n, ns)
+        k = int(round(s[-2]))
+        stg = sim.step(1)
+        v = sim.V
+        _, _, U1 = _split_state(sim.get_state(), n, ns)
+        sim.close()
+        sim = None
+        del s
+        E = tets.shape[0]
+        stims = bench.make_inputs(w)[2]
+        ref = O.Monodomain(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: bench.SIGMA},
+                           O.Config(dt=w["dt"], model=w["model"], chi=bench.CHI, cm=bench.CM, abs_tol=1e-5,
+                                    rel_tol=1e-5, max_iters=100),
+                           [O.Stimulus(*st_) for st_ in stims])
+        ref.set_state(Vk, Vkm1, U, k)
+        rep = ref.step()
+        rel = np.linalg.norm(v - ref.Vk) / np.linalg.norm(ref.Vk)
+        print(f"{name}: {n} nodes, step {k}, iters {int(stg['iters'][0])} vs {rep.iters}, rel-L2 {rel:.2e}")
+        assert abs(int(stg["iters"][0]) - rep.iters) <= 1
+        assert rel <= 1e-8, rel
+        assert np.allclose(U1, ref.U, rtol=1e-9, atol=1e-14)
+    finally:
+        if sim is not None:
+            sim.close()
+
+
 @pytest.mark.parametrize("case,variant", [("configs2", -1), ("configs2", 0), ("configs2", 1),
                                           ("slab1.28M_tt", -1), ("slab1.28M_tt", 1),
                                           ("biv416k_tt", -1), ("biv416k_tt", 0)])
