@@ -362,7 +362,15 @@ tc_status tc_set_allocator(tc_ctx* c, tc_alloc_fn alloc, tc_free_fn release, voi
   c->alloc_fn = alloc;
   c->free_fn = release;
   c->alloc_user = user;
-  CUDA_TRY(c, dalloc(c, &c->d_flags, 8));
+  if (dalloc(c, &c->d_flags, 8) != cudaSuccess) {  // the hook failed: back to cudaMalloc, usable context
+    cudaGetLastError();
+    c->alloc_fn = nullptr;
+    c->free_fn = nullptr;
+    c->alloc_user = nullptr;
+    c->allocs.clear();
+    CUDA_TRY(c, dalloc(c, &c->d_flags, 8));
+    return fail(c, TC_ENOMEM, "tc_set_allocator: the allocator failed; the context keeps cudaMalloc");
+  }
   return TC_OK;
 }
 
@@ -1803,13 +1811,11 @@ static tc_status chunk_setup(tc_ctx* c) {
   const int nc = (int)((P.n + rows - 1) / rows);
   if (nc < 2) return TC_OK;
   int32_t* d_max = nullptr;
-  CUDA_TRY(c, cudaMalloc(&d_max, nc * 4));
-  CUDA_TRY(c, cudaMemsetAsync(d_max, 0, nc * 4, c->stream));
+  CUDA_TRY(c, dalloc(c, &d_max, nc));   // zeroed; freed with the context
   CUDA_TRY(c, launch_chunk_maxcol(P.d_sp, P.d_col, P.nslices, (int32_t)(rows / kSellC), d_max, c->stream));
   std::vector<int32_t> mx(nc);
   CUDA_TRY(c, cudaMemcpyAsync(mx.data(), d_max, nc * 4, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  cudaFree(d_max);
   c->ch_need.resize(nc);
   for (int q = 0; q < nc; ++q) c->ch_need[q] = std::min(nc - 1, std::max(q, (int)(mx[q] / rows)));
   const char* pr = std::getenv("TCB_RHS_PRIO");
