@@ -13,11 +13,23 @@ namespace tcb {
 // Exp table size: TCB_EXP_TAB = 256 (default): 256-entry table and a degree-4
 // polynomial (|r| <= ln2/512, truncation r^5/120 < 3.8e-17 relative); 64: degree 5
 // (r01 default, truncation < 3.5e-17); 32: degree 6.
+// 1024: degree 3 (|r| <= ln2/2048, truncation r^4/24 < 5.8e-16 relative, ~3 ulp).
 #ifndef TCB_EXP_TAB
 #define TCB_EXP_TAB 256
 #endif
 constexpr int kExpTab = TCB_EXP_TAB;
-constexpr int kExpShift = TCB_EXP_TAB == 256 ? 8 : (TCB_EXP_TAB == 64 ? 6 : 5);
+constexpr int kExpShift = TCB_EXP_TAB == 1024 ? 10 : TCB_EXP_TAB == 256 ? 8 : (TCB_EXP_TAB == 64 ? 6 : 5);
+// TCB_EXP_CW1 = 1: one-constant argument reduction r = x - k ln2/N (ln2/N rounded
+// to double): error |x| 2^-54 relative, < 6e-15 for the |x| <= 100 of the ionic
+// models' exponentials (default 0: Cody-Waite hi/lo pair, exact for |k| < 2^20).
+#ifndef TCB_EXP_CW1
+#define TCB_EXP_CW1 0
+#endif
+// TCB_EXP_IRANGE = 1: the x >= -708 range test on the integer k (INT pipe) instead
+// of a DSETP (FP64 pipe).
+#ifndef TCB_EXP_IRANGE
+#define TCB_EXP_IRANGE 0
+#endif
 
 constexpr int kLogTab = 64;
 
@@ -91,13 +103,21 @@ __device__ __forceinline__ double tc_log(double x, const Exp2Table* __restrict__
 #ifndef TCB_EXP_SCALE
 #define TCB_EXP_SCALE 0
 #endif
-__device__ __forceinline__ double exp_range(double x, double v, int m) {
+__device__ __forceinline__ double exp_range(double x, double v, int m, int k) {
 #if TCB_EXP_SCALE
   const int mc = max(min(m, 1023), -1022);
   return v * __hiloint2double((mc + 1023) << 20, 0);
 #else
   const double s = __hiloint2double(__double2hiint(v) + (min(m, 1023) << 20), __double2loint(v));
+#if TCB_EXP_IRANGE
+  // k = round(x N / ln2): x >= -708 <=> k >= ceil(-708 N / ln2) up to rounding at the edge
+  constexpr int kMin = (int)(-708.0 * kExpTab / 0.69314718055994530942);
+  (void)x;
+  return k >= kMin ? s : 0.0;
+#else
+  (void)k;
   return x >= -708.0 ? s : 0.0;
+#endif
 #endif
 }
 
@@ -122,9 +142,17 @@ __device__ __forceinline__ double tc_exp(double x, const Exp2Table* __restrict__
   const double kd = fma(x, kInvLn2N, kShift);
   const int k = __double2loint(kd);                     // round-to-nearest integer
   const double kf = kd - kShift;
+#if TCB_EXP_CW1
+  const double r = fma(-kf, 0.69314718055994530942 / kExpTab, x);
+  (void)kLn2N_hi;
+  (void)kLn2N_lo;
+#else
   double r = fma(-kf, kLn2N_hi, x);
   r = fma(-kf, kLn2N_lo, r);
-#if TCB_EXP_TAB == 256
+#endif
+#if TCB_EXP_TAB == 1024
+  double p = 1.0 / 6.0;
+#elif TCB_EXP_TAB == 256
   double p = 1.0 / 24.0;
   p = fma(p, r, 1.0 / 6.0);
 #elif TCB_EXP_TAB == 64
@@ -141,7 +169,7 @@ __device__ __forceinline__ double tc_exp(double x, const Exp2Table* __restrict__
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const double v = T->t[k & (kExpTab - 1)] * p;
-  return exp_range(x, v, k >> kExpShift);
+  return exp_range(x, v, k >> kExpShift, k);
 }
 
 // 1/b: hardware approximation r0 (MUFU.RCP64H, ~2^-22 relative) refined by

@@ -4,7 +4,7 @@
 #   bash tools/exp_ionic_r02.sh   -> ionic ms/step at 10 M nodes (TT2006, CRN)
 cd "$(dirname "$0")/.."
 # r01 = the library before the table log (built from the parent commit by hand)
-VARS="base: late:-DTCB_ION_EARLY_LOADS=0 pf:-DTCB_ION_L2PF=1"
+VARS="base: cw1:-DTCB_EXP_CW1=1 t1024:-DTCB_EXP_CW1=1+-DTCB_EXP_TAB=1024 all3:-DTCB_EXP_CW1=1+-DTCB_EXP_TAB=1024+-DTCB_EXP_IRANGE=1"
 if [ "$1" == "build" ]; then
   for v in $VARS; do n=${v%%:*}; f=$(echo ${v#*:} | tr + ' ')
     bash tools/build_variant.sh tools/ion_$n.so $f; done; exit 0
