@@ -13,20 +13,25 @@ namespace tcb {
 // Exp table size: TCB_EXP_TAB = 256 (default): 256-entry table and a degree-4
 // polynomial (|r| <= ln2/512, truncation r^5/120 < 3.8e-17 relative); 64: degree 5
 // (r01 default, truncation < 3.5e-17); 32: degree 6.
-// 1024: degree 3 (|r| <= ln2/2048, truncation r^4/24 < 5.8e-16 relative, ~3 ulp).
+// 1024 (default since r02l): degree 3 (|r| <= ln2/2048, truncation r^4/24 <
+// 5.8e-16 relative, ~3 ulp).  Measured with TCB_EXP_CW1 (profiles/r02l_exp_ionic.txt,
+// ionic cycles = ms x SM MHz at 10 M nodes): TT2006 1.91k -> 1.78k, CRN 2.14k -> 2.06k.
 #ifndef TCB_EXP_TAB
-#define TCB_EXP_TAB 256
+#define TCB_EXP_TAB 1024
 #endif
 constexpr int kExpTab = TCB_EXP_TAB;
 constexpr int kExpShift = TCB_EXP_TAB == 1024 ? 10 : TCB_EXP_TAB == 256 ? 8 : (TCB_EXP_TAB == 64 ? 6 : 5);
-// TCB_EXP_CW1 = 1: one-constant argument reduction r = x - k ln2/N (ln2/N rounded
-// to double): error |x| 2^-54 relative, < 6e-15 for the |x| <= 100 of the ionic
-// models' exponentials (default 0: Cody-Waite hi/lo pair, exact for |k| < 2^20).
+// TCB_EXP_CW1 = 1 (default): one-constant argument reduction r = x - k ln2/N
+// (ln2/N rounded to double): error |x| 2^-54 relative, < 6e-15 for the |x| <= 100
+// of the ionic models' exponentials (below -708 the result is 0 anyway); 0:
+// Cody-Waite hi/lo pair, exact for |k| < 2^20.
 #ifndef TCB_EXP_CW1
-#define TCB_EXP_CW1 0
+#define TCB_EXP_CW1 1
 #endif
-// TCB_EXP_IRANGE = 1: the x >= -708 range test on the integer k (INT pipe) instead
-// of a DSETP (FP64 pipe).
+// TCB_EXP_IRANGE = 1 (experiment, unsafe): the x >= -708 range test on the
+// integer k (INT pipe) instead of a DSETP (FP64 pipe) -- k wraps for |x| > ~2e6
+// (Rush-Larsen exponents at V = -150 mV, dt 0.05: NaN in
+// test_ionic_voltage_range_one_step), so the default keeps the FP64 compare.
 #ifndef TCB_EXP_IRANGE
 #define TCB_EXP_IRANGE 0
 #endif
