@@ -163,13 +163,40 @@ __device__ __forceinline__ void for_slices_tma(SlicePipe& P, const int64_t* sp, 
   }
 }
 
+// TCB_L2PF_MAT = D > 0 (experiment): lane 0 of a warp asks the TMA unit to
+// prefetch into L2 the values and column indices of the slice it will process
+// D rounds later (cp.async.bulk.prefetch.L2, two instructions per slice), so the
+// streamed matrix loads of the direct variant find the data in L2 and the
+// dependent index -> gather chain starts sooner.
+#ifndef TCB_L2PF_MAT
+#define TCB_L2PF_MAT 0
+#endif
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_slice(const int64_t* sp, const double* A, const int* col, int s, int ns) {
+  if (s >= ns) return;
+  const int64_t base = __ldg(sp + s), end = __ldg(sp + s + 1);
+  const uint32_t nv = (uint32_t)(end - base);
+  if (nv == 0) return;
+  l2_prefetch_bulk(A + base, nv * 8u);      // 16-byte multiples: slices hold 32 k slots
+  l2_prefetch_bulk(col + base, nv * 4u);
+}
+
 template <bool TMA, class F>
 __device__ __forceinline__ void for_slices(SlicePipe& P, const int64_t* sp, const double* A,
                                            const int* col, int ns, int gw, int nw, int lane, F&& f) {
   if (TMA) {
     for_slices_tma(P, sp, A, col, ns, gw, nw, lane, f);
   } else {
+#if TCB_L2PF_MAT > 0
+    if (lane == 0)
+      for (int d = 0; d < TCB_L2PF_MAT; ++d) prefetch_slice(sp, A, col, gw + d * nw, ns);
+#endif
     for (int s = gw; s < ns; s += nw) {
+#if TCB_L2PF_MAT > 0
+      if (lane == 0) prefetch_slice(sp, A, col, s + TCB_L2PF_MAT * nw, ns);
+#endif
       int64_t base;
       int w;
       slice_bounds(sp, s, base, w);
