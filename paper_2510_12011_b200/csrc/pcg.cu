@@ -34,6 +34,16 @@ namespace tcb {
 #ifndef TCB_VEC_U
 #define TCB_VEC_U 0   // 1: U phase and final x update over 16-byte row pairs (measured slower)
 #endif
+// TCB_XMERGE = 1: the deferred x update runs every other iteration, adding the
+// two pending terms in their original order, x = (x + a_{it-2} p_{it-2}) +
+// a_{it-1} p_{it-1} -- bitwise the sequential result -- so x is read and written
+// once per two iterations (plus one read of p_{it-2}): 4n bytes per iteration less.
+#ifndef TCB_XMERGE
+#define TCB_XMERGE 0
+#endif
+#if TCB_VEC_U && TCB_XMERGE
+#error "TCB_VEC_U has only the per-iteration x update: build it with -DTCB_XMERGE=0"
+#endif
 #if TCB_VEC_U && TCB_ZFORM
 #error "TCB_VEC_U has only the r-form U phase: build it with -DTCB_ZFORM=0"
 #endif
@@ -190,7 +200,7 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
   if (isnan(rho) || isnan(zeta)) nan = 1;
   if (!nan && zeta < a.eps_a) conv = 1;  // reading C4: return x0
 
-  double alpha = 0.0, beta = 0.0;
+  double alpha = 0.0, beta = 0.0, alpha_prev = 0.0;
   bool last_valid = false;
   if (!nan && !conv) {
     for (it = 0; it < a.max_iters;) {
@@ -213,9 +223,16 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
         for_slices<TMA>(P, sp, Av, col, ns, gw, nw, lane,
                    [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
                      const double po = pold[i];
-                     const double xi = a.x[i];
                      const double pi = a.z[i] + beta * po;
+#if TCB_XMERGE
+                     if (!(it & 1)) {   // even it >= 2: p_{it-2} (still in pnew) and p_{it-1}, in order
+                       const double xi = a.x[i], p2 = pnew[i];
+                       a.x[i] = (xi + alpha_prev * p2) + alpha * po;
+                     }
+#else
+                     const double xi = a.x[i];
                      a.x[i] = xi + alpha * po;
+#endif
                      const double sum = staged ? row_Ap_staged<false>(w, lane, As, Cs, a.z, pold, beta)
                                       : BATCH ? row_Ap_batch_w<false>(base, w, lane, col, Av, a.z, pold, beta)
                                                : row_Ap_direct<false, KEEP>(base, w, lane, col_of<COMP>(a, i, base), Av, a.z, pold, beta);
@@ -228,6 +245,7 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
       tot = grid_sum2(acc, partB, sh, grid);
       const double pq = tot.x;
       if (isnan(pq)) { nan = 1; break; }
+      alpha_prev = alpha;
       alpha = rho / pq;                                   // alpha_k = rho_k / p.q
       // ---- U: r -= alpha q, z = r / d, partials of r.z and z.z (UU slices / warp pass)
       acc = make_double2(0.0, 0.0);
@@ -305,19 +323,25 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
         const double2 xx = x2[j], pp = pl2[j];
         x2[j] = make_double2(xx.x + alpha * pp.x, xx.y + alpha * pp.y);
       }
-    } else
+    } else {
+      // TCB_XMERGE: S(it-1) skipped its x update when it-1 was odd -> p_{it-2} pending too
+      const bool two = TCB_XMERGE && !(it & 1) && it >= 2;
+      const double* __restrict__ pl2 = (it & 1) ? a.p1 : a.p0;   // p_{it-2}
     for (int s = gw; s < ns; s += UU * nw) {
-      double xx[UU], pp[UU];
+      double xx[UU], pp[UU], p2[UU];
 #pragma unroll
       for (int u = 0; u < UU; ++u)
         if (s + u * nw < ns) {
           const int64_t i = (int64_t)(s + u * nw) * kSellC + lane;
           xx[u] = a.x[i];
           pp[u] = plast[i];
+          p2[u] = two ? pl2[i] : 0.0;
         }
 #pragma unroll
       for (int u = 0; u < UU; ++u)
-        if (s + u * nw < ns) a.x[(int64_t)(s + u * nw) * kSellC + lane] = xx[u] + alpha * pp[u];
+        if (s + u * nw < ns)
+          a.x[(int64_t)(s + u * nw) * kSellC + lane] = (two ? xx[u] + alpha_prev * p2[u] : xx[u]) + alpha * pp[u];
+    }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
