@@ -34,12 +34,14 @@ namespace tcb {
 #ifndef TCB_VEC_U
 #define TCB_VEC_U 0   // 1: U phase and final x update over 16-byte row pairs (measured slower)
 #endif
-// TCB_XMERGE = 1: the deferred x update runs every other iteration, adding the
+// TCB_XMERGE = 1 (default): the deferred x update runs every other iteration, adding the
 // two pending terms in their original order, x = (x + a_{it-2} p_{it-2}) +
 // a_{it-1} p_{it-1} -- bitwise the sequential result -- so x is read and written
 // once per two iterations (plus one read of p_{it-2}): 4n bytes per iteration less.
+// Measured (profiles/r02o_exp_xmerge.txt, PCG-path frac): 20 M MS 0.873 -> 0.889,
+// 10 M TT2006 0.873-0.878 -> 0.880-0.887, BiV 3 M 0.798-0.802 -> 0.793-0.796.
 #ifndef TCB_XMERGE
-#define TCB_XMERGE 0
+#define TCB_XMERGE 1
 #endif
 #if TCB_VEC_U && TCB_XMERGE
 #error "TCB_VEC_U has only the per-iteration x update: build it with -DTCB_XMERGE=0"
