@@ -213,6 +213,12 @@ tc_status tc_add_stimulus(tc_ctx* ctx, int64_t n_idx, const int32_t* nodes, doub
  * on `nodes` (reading M3), initial V = w(x,y,0).  Must precede tc_assemble. */
 tc_status tc_set_mms(tc_ctx* ctx, double k, double w1, double w2, double lambda,
                      int64_t n_dirichlet, const int32_t* nodes);
+/* The two halves of tc_set_mms: the Dirichlet node set (values
+ * w(x,y,t_{k+1}), reading M3) and the source constants k, w1, w2, lambda of
+ * Eq. 5 / Eq. 8 (default 1, pi, pi, pi: reading M2).  Same preconditions and
+ * errors as tc_set_mms; each keeps the other half. */
+tc_status tc_set_dirichlet(tc_ctx* ctx, int64_t n_idx, const int32_t* nodes);
+tc_status tc_set_mms_source(tc_ctx* ctx, double k, double w1, double w2, double lambda);
 
 /* Build the system (boundary, not timed per step): pattern, RCM, GPU
  * assembly of M, K into A = chi Cm M + theta dt K and diag(A)^-1,

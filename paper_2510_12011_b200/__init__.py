@@ -22,7 +22,7 @@ __all__ = [
     "tc_num_nodes", "tc_current_step", "tc_get_v", "tc_get_activation", "tc_state_len",
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
     "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "tc_nccl_unique_id", "tc_comm_init",
-    "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "tc_interior_first", "tc_set_allocator", "TorchAllocator", "tc_validate", "tc_pipeline_info", "Monodomain", "LIB_PATH",
+    "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "tc_interior_first", "tc_set_allocator", "TorchAllocator", "tc_validate", "tc_pipeline_info", "tc_set_dirichlet", "tc_set_mms_source", "Monodomain", "LIB_PATH",
     "tc_engine_info", "tc_node_order", "tc_apply", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_set_states", "tc_cohort_get_v", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
     "TC_ENGINE_AUTO", "TC_ENGINE_GRID", "TC_ENGINE_CLUSTER",
     "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS", "TC_ION_CRN",
@@ -119,6 +119,8 @@ def _load():
         "tc_interior_first": ([I64, P, P, I32, P, P], I32),
         "tc_set_allocator": ([P, P, P, P], I32),
         "tc_validate": ([P, P], I32),
+        "tc_set_dirichlet": ([P, I64, P], I32),
+        "tc_set_mms_source": ([P, C.c_double, C.c_double, C.c_double, C.c_double], I32),
         "tc_pipeline_info": ([P, P], I32),
     }
     for name, (args, res) in sig.items():
@@ -223,6 +225,15 @@ def tc_add_stimulus(ctx, nodes, t_start, duration, amplitude) -> None:
 def tc_set_mms(ctx, k, w1, w2, lam, dirichlet_nodes) -> None:
     nodes = _i32(dirichlet_nodes)
     _check(ctx, _L.tc_set_mms(ctx, k, w1, w2, lam, nodes.shape[0], _ptr(nodes)))
+
+
+def tc_set_dirichlet(ctx, nodes) -> None:
+    nodes = _i32(nodes)
+    _check(ctx, _L.tc_set_dirichlet(ctx, nodes.shape[0], _ptr(nodes)))
+
+
+def tc_set_mms_source(ctx, k, w1, w2, lam) -> None:
+    _check(ctx, _L.tc_set_mms_source(ctx, k, w1, w2, lam))
 
 
 def tc_assemble(ctx) -> None:

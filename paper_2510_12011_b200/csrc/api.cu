@@ -509,6 +509,18 @@ tc_status tc_set_mms(tc_ctx* c, double k, double w1, double w2, double lam, int6
   return TC_OK;
 }
 
+// The two halves of tc_set_mms as SURVEY 8(b) names them.
+tc_status tc_set_dirichlet(tc_ctx* c, int64_t m, const int32_t* nodes) {
+  if (!c || (m > 0 && !nodes) || m < 0) return TC_EINVAL;
+  return tc_set_mms(c, c->mms.k, c->mms.w1, c->mms.w2, c->mms.lam, m, nodes);
+}
+
+tc_status tc_set_mms_source(tc_ctx* c, double k, double w1, double w2, double lam) {
+  if (!c) return TC_EINVAL;
+  const std::vector<int32_t> keep = c->dirichlet_nodes;
+  return tc_set_mms(c, k, w1, w2, lam, (int64_t)keep.size(), keep.data());
+}
+
 }  // extern "C"
 
 static double mms_w_host(const MMSParams& p, double x, double y, double t) {
