@@ -174,10 +174,11 @@ _MULTI = {
 }
 
 
-@pytest.mark.parametrize("name", ["slab10M_tt", "slab20M_ms"])
+@pytest.mark.parametrize("name", ["slab10M_tt", "slab20M_ms", "slab10M_crn", "biv3M_tt", "sphere2.6M_ms"])
 def test_fullsize_whole_oracle_step(T, name):
     """The bench's own configurations at FULL size -- the north-star 10 M-node
-    TT2006 slab and the default 20 M-node MS slab (configs[4]) -- built and
+    TT2006 slab, the default 20 M-node MS slab (configs[4]), the 10 M CRN slab
+    (f4), the 3 M BiV (configs[3]) and the 2.6 M-node triangle sphere (f2) -- built and
     prerolled exactly as bench.py times them: one step from the GPU's state
     against the WHOLE oracle step (assembly, ionic update, Eq. 3 RHS,
     Algorithm 1) on the same state: rel-L2(V) <= 1e-8 (north_star), every cell
@@ -197,7 +198,8 @@ def test_fullsize_whole_oracle_step(T, name):
         del s
         E = tets.shape[0]
         stims = bench.make_inputs(w)[2]
-        ref = O.Monodomain(xyz, tets, np.zeros(E, np.int32), G.uniform_fibres(E), {0: bench.SIGMA},
+        ref = O.Monodomain(xyz, tets, np.zeros(E, np.int32) if region is None else region,
+                           G.uniform_fibres(E) if fibre is None else fibre, {0: bench.SIGMA, 1: bench.SIGMA},
                            O.Config(dt=w["dt"], model=w["model"], chi=bench.CHI, cm=bench.CM, abs_tol=1e-5,
                                     rel_tol=1e-5, max_iters=100),
                            [O.Stimulus(*st_) for st_ in stims])
