@@ -215,25 +215,35 @@ def test_fullsize_whole_oracle_step(T, name):
             sim.close()
 
 
-@pytest.mark.parametrize("case,variant", [("configs2", -1), ("configs2", 0), ("configs2", 1),
-                                          ("slab1.28M_tt", -1), ("slab1.28M_tt", 1),
-                                          ("biv416k_tt", -1), ("biv416k_tt", 0)])
-def test_multislice_full_oracle_step(T, case, variant):
+@pytest.mark.parametrize("case,variant,parts,peer", [("configs2", -1, 1, 1), ("configs2", 0, 1, 1),
+                                                     ("configs2", 1, 1, 1), ("slab1.28M_tt", -1, 1, 1),
+                                                     ("slab1.28M_tt", 1, 1, 1), ("biv416k_tt", -1, 1, 1),
+                                                     ("biv416k_tt", 0, 1, 1),
+                                                     ("slab1.28M_tt", -1, 4, 1), ("slab1.28M_tt", -1, 3, 0),
+                                                     ("biv416k_tt", -1, 4, 1)])
+def test_multislice_full_oracle_step(T, case, variant, parts, peer):
+    """(parts > 1: the multi-GPU PCG emulated on one GPU -- interior-first row
+    blocks, halos overlapped with the interior slices, peer kernels or split
+    phases -- at a size where every part is still multi-slice.)"""
     c = _MULTI[case]
     w = bench.WORKLOADS[c["w"]]
     xyz, tets, stims, region, fibre = bench.make_inputs(w, c["dims"])
     E = tets.shape[0]
     cfg = T.tc_config_default(dt=w["dt"], model=w["model"], chi=bench.CHI, cm=bench.CM, abs_tol=1e-5,
-                              rel_tol=1e-5, max_iters=100, use_rcm=1, pcg_variant=variant, partitions=1)
+                              rel_tol=1e-5, max_iters=100, use_rcm=1, pcg_variant=variant, partitions=parts,
+                              peer=peer)
     sim = T.Monodomain(xyz, tets, region, fibre, {0: bench.SIGMA, 1: bench.SIGMA}, cfg, stims)
     try:
         info = T.tc_matrix_info(sim.ctx)
         assert T.tc_engine_info(sim.ctx)["engine"] == "grid"
         used = info["pcg_variant"]
+        if parts > 1:
+            assert info["partitions"] == parts and info["path"] == ("peer" if peer else "split")
+            assert T.tc_validate(sim.ctx) > 0
         if variant >= 0:
             assert used == variant
         spw = info["nslices"] / (info["pcg_grid"] * _warps_per_cta())
-        if used in (0, 1):
+        if used in (0, 1) and parts == 1:
             assert spw > 1.0, spw          # the multi-slice loop / ring wrap is exercised
         sim.step(c["preroll"])
         n = xyz.shape[0]
@@ -258,7 +268,7 @@ def test_multislice_full_oracle_step(T, case, variant):
         assert rel <= 1e-8, rel
         _, _, U1 = _split_state(sim.get_state(), n, ns)
         assert np.allclose(U1, ref.U, rtol=1e-9, atol=1e-14)
-        print(f"{case} variant {used}: {n} nodes, {spw:.2f} slices/warp, iters {int(stg['iters'][0])} "
+        print(f"{case} variant {used} parts {parts} ({info['path']}): {n} nodes, {spw:.2f} slices/warp, iters {int(stg['iters'][0])} "
               f"vs {rep.iters}, rel-L2 {rel:.2e}")
     finally:
         sim.close()
