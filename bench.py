@@ -289,6 +289,9 @@ def main():
     ap.add_argument("--preroll", type=int, default=None)
     ap.add_argument("--dist", action="store_true", help="use the NCCL path even at world size 1")
     ap.add_argument("--windows", type=int, default=3, help="timed windows of K steps (median reported)")
+    ap.add_argument("--weak", action="store_true",
+                    help="multi-GPU (torchrun / --dist): weak scaling, a (100 N) x 250 x 100 slab = 2.5 M nodes per GPU "
+                         "(SURVEY 8d C5); default strong scaling of the workload")
     ap.add_argument("--no-north-star", action="store_true",
                     help="skip the slab10M_tt sub-record of the default run")
     args = ap.parse_args()
