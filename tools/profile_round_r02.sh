@@ -5,7 +5,7 @@
 set -x
 R=${1:-r02}
 B="python bench.py --steps 20 --warmup 5"
-$B > gpurun_out/${R}_bench_default.json 2> gpurun_out/${R}_bench_default.err
+{ time $B > gpurun_out/${R}_bench_default.json 2> gpurun_out/${R}_bench_default.err ; } 2> gpurun_out/${R}_default_time.txt
 for W in slab10M_tt slab10M_crn biv3M_tt; do
   python bench.py --workload $W --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/${R}_bench_$W.json 2>&1
 done
@@ -49,3 +49,9 @@ python tools/run_small.py > gpurun_out/${R}_plain_small.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:cohort -s 1 -c 1 \
     -o gpurun_out/${R}_full_cluster_c1 python tools/run_small.py > gpurun_out/${R}_ncu_cluster.log 2>&1
 ls -la gpurun_out
+# weak-scaling leg at world size 1 (2.5 M nodes per GPU)
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
+    --master-port 29518 bench.py --gpus 1 --steps 20 --warmup 5 --dist --weak > gpurun_out/${R}_bench_dist_weak_world1.json \
+    2> gpurun_out/${R}_bench_dist_weak_world1.err
+# wall time of the default run (what the driver runs)
+/usr/bin/env bash -c "time python bench.py --no-north-star > /dev/null 2>&1" 2> gpurun_out/${R}_default_no_ns_time.txt
