@@ -251,7 +251,11 @@ def ionic_roofline(workload, model, n, ionic_ms_per_step):
             "unit": "TFLOP/s", "frac": ach / d["peak_tflops"], "flop_per_node": e["flop_per_node"],
             "fp64_pipe_active_ncu": e["fp64_pipe_active_ncu"],
             "peak_source": "measured DFMA rate (profiles/r01_probe_fp64.txt)",
-            "work_source": "ncu FP64 instruction counts per node (profiles/ncu_fp64.json)"}
+            "work_source": "ncu FP64 instruction counts per node (profiles/ncu_fp64.json)",
+            "ns_per_node_step": ionic_ms_per_step * 1e6 / n,
+            "note": "frac counts flops, and the flops per node are the current kernel's (r02 cut them from "
+                    "2418 to ~1745 for TT2006 with table exp/log and fewer Newton steps), so a leaner kernel "
+                    "lowers it at equal speed; fp64_pipe_active_ncu is the hardware utilisation"}
 
 
 def run_reference(args, w):
