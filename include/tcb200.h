@@ -16,13 +16,16 @@
  *  - Ownership: every pointer argument is a HOST pointer owned by the caller;
  *    the library copies what it needs during the call and never retains it.
  *    Output buffers are caller-allocated with the documented length.  Device
- *    memory is allocated and freed by the library (tc_destroy frees all).
+ *    memory is allocated and freed by the library (tc_destroy frees all),
+ *    through the caller's allocator when one is set (tc_set_allocator).
  *  - Node order: all per-node inputs/outputs use the caller's ORIGINAL node
  *    numbering; the RCM permutation is internal.
  *  - Errors: return codes only, no exception crosses the ABI; tc_last_error()
  *    returns a message (owned by the context, valid until the next call on it).
  *  - Threading: a context is used by one host thread at a time; independent
- *    contexts are independent (cohort mode).
+ *    contexts are independent (cohort mode) -- no launch state or
+ *    flag is shared between them (the exp / log tables of the ionic kernels
+ *    are one read-only copy per device).
  *  - All arithmetic of the step is IEEE fp64 on the GPU; there is no
  *    CPU fallback: without a CUDA device tc_create returns TC_ECUDA.
  */

@@ -4,12 +4,12 @@
 #   bash tools/exp_ionic_r02.sh   -> ionic ms/step at 10 M nodes (TT2006, CRN)
 cd "$(dirname "$0")/.."
 # r01 = the library before the table log (built from the parent commit by hand)
-VARS="base: cw1:-DTCB_EXP_CW1=1 t1024:-DTCB_EXP_CW1=1+-DTCB_EXP_TAB=1024 all3:-DTCB_EXP_CW1=1+-DTCB_EXP_TAB=1024+-DTCB_EXP_IRANGE=1"
+VARS="base: m6:-DTCB_ION_MINB=6 m7:-DTCB_ION_MINB=7 t256:-DTCB_EXP_TAB=256"
 if [ "$1" == "build" ]; then
   for v in $VARS; do n=${v%%:*}; f=$(echo ${v#*:} | tr + ' ')
     bash tools/build_variant.sh tools/ion_$n.so $f; done; exit 0
 fi
-for W in slab10M_tt slab10M_crn; do
+for W in slab10M_tt; do
 for v in $VARS $VARS; do
   n=${v%%:*}
   TCB200_LIB=tools/ion_$n.so python bench.py --workload $W --steps 20 --warmup 5 --windows 1 --no-cpu-baseline --e2e-steps 0 | \
