@@ -261,3 +261,21 @@ def test_distributed_pcg_gloo_world2():
         x[g0:g1] = xl
         assert it == rep.iters
     assert np.abs(x - xr).max() <= 1e-10 * np.abs(xr).max()
+
+
+def test_rcm_blocks_partition_the_biv_like_slabs(T):
+    """contiguous blocks of the RCM order cut the unstructured BiV
+    (permuted numbering) into bands with at most two neighbours each and a ghost
+    set of a small fraction of the part."""
+    m = G.biv(1.2)
+    xyz, tets = m["xyz"], m["tets"]
+    n = xyz.shape[0]
+    rp, col = T.tc_mesh_pattern(n, tets)
+    perm = T.tc_rcm(rp, col)
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n)
+    rp2, col2 = T.tc_mesh_pattern(n, inv[tets].astype(np.int32))
+    for P in (2, 4):
+        plans = [T.tc_partition_plan(rp2, col2, P, p) for p in range(P)]
+        assert max(len(pl["nbr"]) for pl in plans) <= 2
+        assert max(len(pl["ghosts"]) for pl in plans) < 0.2 * n / P
