@@ -289,7 +289,7 @@ def main():
                     help="-1 automatic (default), 0 direct loads, 1 TMA-staged, 2 direct + 16-bit indices, "
                          "3 L2-resident matrix, 4 all slots of a row in flight")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--preroll", type=int, default=None)
     ap.add_argument("--dist", action="store_true", help="use the NCCL path even at world size 1")
     ap.add_argument("--windows", type=int, default=3, help="timed windows of K steps (median reported)")
@@ -396,7 +396,7 @@ def cpu_baseline_injected(w, V_dims, device, stream, steps=20):
                        f"value = all threads")
 
 
-def measure_grid(args, name, w, local, stream, preroll=None, e2e_steps=6, cpu=True):
+def measure_grid(args, name, w, local, stream, preroll=None, e2e_steps=20, cpu=True):
     """One single-GPU workload: setup, preroll into the timing window, W warm-up
     steps, then `args.windows` windows of exactly K steps each (CUDA events on the
     library's stream, synchronised on both sides); value = the median window."""
@@ -479,19 +479,20 @@ def measure_grid(args, name, w, local, stream, preroll=None, e2e_steps=6, cpu=Tr
     if e2e_steps > 0:
         st = sim.get_state()
         ke = e2e_steps
-        hin = torch.empty((ke, st.shape[0]), dtype=torch.float64, pin_memory=True).numpy()
-        hin[:] = st[None, :]
-        hout = torch.empty((ke, n), dtype=torch.float64, pin_memory=True).numpy()
-        T.tc_step_io(sim.ctx, hin[:1], hout[:1])   # warm: staging buffers and copy streams
+        hin = torch.empty(st.shape[0], dtype=torch.float64, pin_memory=True).numpy()
+        hin[:] = st
+        hout = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+        T.tc_step_io_repeat(sim.ctx, hin, hout, 1)   # warm: staging buffers and copy streams
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        T.tc_step_io(sim.ctx, hin, hout)
+        T.tc_step_io_repeat(sim.ctx, hin, hout, ke)
         e2e_s = time.perf_counter() - t0
-        e2e = {"value": n * ke / e2e_s, "unit": "node-steps/s", "h2d_bytes_per_step": int(hin[0].nbytes),
-               "d2h_bytes_per_step": int(hout[0].nbytes), "steps": ke,
-               "what": "tc_step_io: per step the full state (V^k, V^{k-1}, u^k) H2D from pinned host, one step, "
-                       "V^{k+1} D2H to pinned host; copies of neighbouring steps overlap the compute (two copy "
-                       "streams), wall clock over all steps incl. pipeline fill and drain"}
+        e2e = {"value": n * ke / e2e_s, "unit": "node-steps/s", "h2d_bytes_per_step": int(hin.nbytes),
+               "d2h_bytes_per_step": int(hout.nbytes), "steps": ke,
+               "what": "tc_step_io (stride 0): per step the full state (V^k, V^{k-1}, u^k) H2D from one pinned "
+                       "host buffer, one step, V^{k+1} D2H to one pinned host buffer; copies of neighbouring steps "
+                       "overlap the compute (two copy streams), wall clock over all steps incl. pipeline fill "
+                       "and drain"}
         del hin, hout
     sim.close()
 

@@ -272,9 +272,14 @@ tc_status tc_set_state(tc_ctx* ctx, const double* buf, int64_t len);
  * on two copy streams while step j computes -- the result equals
  * tc_set_state + tc_step(1) + tc_get_v for every j.  stats: nullable,
  * n_steps entries.  After the call the context holds the state after the last
- * problem.  Errors: TC_EINVAL (null pointers, stride < tc_state_len, a bad step
- * index in an input), TC_ESTATE (before tc_assemble, or a multi-process
- * context), and tc_step's errors.  Host buffers stay owned by the caller. */
+ * problem.  stride = 0: every problem reads the same host state (one
+ * tc_state_len buffer, still copied host -> device once per problem) and
+ * writes its V^{k+1} to the same n_nodes output (copied back once per problem;
+ * the last one remains) -- a stream of n_steps identical problems in bounded
+ * host memory.  Errors: TC_EINVAL (null pointers, 0 < stride < tc_state_len,
+ * a bad step index in an input), TC_ESTATE (before tc_assemble, or a
+ * multi-process context), and tc_step's errors.  Host buffers stay owned by
+ * the caller. */
 tc_status tc_step_io(tc_ctx* ctx, int64_t n_steps, const double* states, int64_t stride, double* v_out,
                      tc_step_stat* stats);
 

@@ -22,7 +22,7 @@ __all__ = [
     "tc_num_nodes", "tc_current_step", "tc_get_v", "tc_get_activation", "tc_state_len",
     "tc_get_state", "tc_set_state", "tc_profile", "tc_profile_read", "tc_csr_upload",
     "tc_spmv", "tc_pcg", "tc_abi_version", "tc_matrix_info", "tc_nccl_unique_id", "tc_comm_init",
-    "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "tc_interior_first", "tc_set_allocator", "TorchAllocator", "tc_validate", "tc_pipeline_info", "tc_set_dirichlet", "tc_set_mms_source", "Monodomain", "LIB_PATH",
+    "tc_mesh_pattern", "tc_rcm", "tc_partition_plan", "tc_interior_first", "tc_set_allocator", "TorchAllocator", "tc_validate", "tc_pipeline_info", "tc_set_dirichlet", "tc_set_mms_source", "tc_step_io_repeat", "Monodomain", "LIB_PATH",
     "tc_engine_info", "tc_node_order", "tc_apply", "tc_cohort_create", "tc_cohort_step", "tc_cohort_info", "tc_cohort_set_states", "tc_cohort_get_v", "tc_cohort_destroy", "tc_cohort_last_error", "Cohort",
     "TC_ENGINE_AUTO", "TC_ENGINE_GRID", "TC_ENGINE_CLUSTER",
     "TC_ION_TT2006_EPI", "TC_ION_MS", "TC_ION_MMS", "TC_ION_CRN",
@@ -296,6 +296,21 @@ def tc_step_io(ctx, states, v_out, want_stats: bool = False):
     m = states.shape[0]
     stats = np.zeros(m, STAT_DTYPE) if want_stats else None
     _check(ctx, _L.tc_step_io(ctx, m, _ptr(states), states.strides[0] // 8, _ptr(v_out), _ptr(stats)))
+    return stats
+
+
+def tc_step_io_repeat(ctx, state, v_out, n_steps: int, want_stats: bool = False):
+    """n_steps identical one-step problems from ONE host state (tc_step_io with
+    stride 0): the state is copied host -> device and V^{k+1} device -> host once
+    per problem; v_out (n_nodes) holds the last result."""
+    if not (isinstance(state, np.ndarray) and state.dtype == np.float64 and state.flags.c_contiguous
+            and state.ndim == 1 and state.shape[0] >= tc_state_len(ctx)):
+        raise ValueError("state: contiguous float64 array of tc_state_len")
+    if not (isinstance(v_out, np.ndarray) and v_out.dtype == np.float64 and v_out.flags.c_contiguous
+            and v_out.shape == (tc_num_nodes(ctx),)):
+        raise ValueError("v_out: contiguous float64 array of n_nodes")
+    stats = np.zeros(n_steps, STAT_DTYPE) if want_stats else None
+    _check(ctx, _L.tc_step_io(ctx, n_steps, _ptr(state), 0, _ptr(v_out), _ptr(stats)))
     return stats
 
 

@@ -2278,7 +2278,8 @@ tc_status tc_step_io(tc_ctx* c, int64_t n_steps, const double* states, int64_t s
   if (!c->assembled || c->csr_mode) return fail(c, TC_ESTATE, "tc_step_io before tc_assemble");
   if (c->use_comm) return fail(c, TC_ESTATE, "tc_step_io: single-process contexts only");
   const int64_t len = tc_state_len(c), n = c->n;
-  if (stride < len) return fail(c, TC_EINVAL, "tc_step_io: stride shorter than the state");
+  if (stride != 0 && stride < len) return fail(c, TC_EINVAL, "tc_step_io: stride shorter than the state");
+  const int64_t ostride = stride == 0 ? 0 : n;   // stride 0: one host state and one output for every problem
   if (n_steps == 0) return TC_OK;
   for (int64_t j = 0; j < n_steps; ++j) {
     const double kk = states[j * stride + (2 + c->nstates) * n];
@@ -2322,7 +2323,7 @@ tc_status tc_step_io(tc_ctx* c, int64_t n_steps, const double* states, int64_t s
       CUDA_TRY(c, launch_scatter(P.n, c->d_perm_g + P.plan.g0, P.d_V[c->iVk], c->d_sout[b], c->stream));
     CUDA_TRY(c, cudaEventRecord(c->e_done[b], c->stream));
     CUDA_TRY(c, cudaStreamWaitEvent(c->s_out, c->e_done[b], 0));
-    CUDA_TRY(c, cudaMemcpyAsync(v_out + j * n, c->d_sout[b], n * 8, cudaMemcpyDeviceToHost, c->s_out));
+    CUDA_TRY(c, cudaMemcpyAsync(v_out + j * ostride, c->d_sout[b], n * 8, cudaMemcpyDeviceToHost, c->s_out));
     CUDA_TRY(c, cudaEventRecord(c->e_read[b], c->s_out));
   }
   CUDA_TRY(c, cudaStreamSynchronize(c->s_out));

@@ -338,6 +338,10 @@ def test_step_io_equals_serial_calls(T, engine, nparts):
         ref2.run(100)
         ref2.step()
         assert np.linalg.norm(out[0] - ref2.Vk) / np.linalg.norm(ref2.Vk) <= 1e-8
+        # stride 0: the same state for every problem, one output buffer (the last result)
+        one = np.zeros(n)
+        st0 = T.tc_step_io_repeat(sim.ctx, np.ascontiguousarray(pad[1]), one, 5, want_stats=True)
+        assert np.array_equal(one, serial[1]) and len(set(st0["iters"].tolist())) == 1
         with pytest.raises(ValueError):
             T.tc_step_io(sim.ctx, pad, np.zeros((len(states), n + 1)))
         bad = pad.copy()
