@@ -279,3 +279,14 @@ def test_rcm_blocks_partition_the_biv_like_slabs(T):
         plans = [T.tc_partition_plan(rp2, col2, P, p) for p in range(P)]
         assert max(len(pl["nbr"]) for pl in plans) <= 2
         assert max(len(pl["ghosts"]) for pl in plans) < 0.2 * n / P
+
+
+def test_interior_first_edge_cases(T):
+    """One block: every row is interior and the order is the identity; a block
+    count above the row count is rejected by the plan (bounds must grow)."""
+    xyz, tets, rp, col = _internal_pattern((5, 4, 3))
+    n = rp.shape[0] - 1
+    order, nint = T.tc_interior_first(rp.astype(np.int64), col, 1)
+    assert np.array_equal(order, np.arange(n)) and nint.tolist() == [n]
+    with pytest.raises(T.TcError):
+        T.tc_interior_first(rp.astype(np.int64), col, 0)
