@@ -63,6 +63,11 @@ WORKLOADS = {
     # numbering, fibres, conductivities, TT2006 parameter resets), one cluster each
     "cohort100_nversion05_tt": dict(cfg="f1 cohort", cohort=100, dims=None, dx=0.5, model="tt2006",
                                     dt=0.05, stim="corner", preroll=40),
+    # SURVEY 8f row f1 with members of configs[2]'s size (P:349-353's cohort members are 660 k-node
+    # meshes): 8 seeded N-version slabs at dx 0.1 mm (~440 k nodes each), the members sharing the GPU
+    "cohort8_nversion01_tt": dict(cfg="f1 cohort (configs[2]-sized members)", cohort=8, dims=None, dx=0.1,
+                                  member_base=(201, 71, 31), model="tt2006", dt=0.01, stim="corner",
+                                  preroll=500),
 }
 DEFAULT_WORKLOAD = "slab20M_ms"
 
@@ -541,7 +546,8 @@ def run_cohort(args, w):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
-    members = G.cohort_members(w["cohort"], seed=G.SEED + rank)
+    members = G.cohort_members(w["cohort"], seed=G.SEED + rank, base=w.get("member_base", (41, 15, 7)),
+                               dx=w["dx"])
     sims = []
     t0 = time.perf_counter()
     for m in members:

@@ -131,6 +131,9 @@ struct tc_ctx {
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaStream_t s_halo = nullptr;           // split path: halo exchange stream (overlapped)
   // ionic || RHS pipeline (chunked_step): row chunks, RHS stream, events
+  int co_var = -1, co_grid = 0;            // cohort of concurrent large members: the PCG shape for 1/share of the GPU
+  double2* d_co_part = nullptr;            // ... and its partials when that grid exceeds P.grid
+  int co_part_cap = 0;
   int ion_chunks = -1;                     // -1 undecided, 0 off, C > 0 chunks
   int64_t ch_rows = 0;                     // rows per chunk (multiple of 128)
   std::vector<int> ch_need;                // RHS chunk c needs the ionic output of chunks <= ch_need[c]
@@ -1967,6 +1970,12 @@ static tc_status enqueue_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* dstats, 
         CUDA_TRY(c, launch_rhs(1, 0, ca, P.grid, c->stream));
         CUDA_TRY(c, g_launch(P.gexec, P.d_gstep, P.d_V[c->iX], dstats + st, (int32_t)c->k, c->stream));
         c->launches += 2;    // setstep + RHS; the graph's init, final and S, U per iteration are added in finish_steps
+      } else if (c->co_var >= 0) {  // a concurrent cohort member: its share of the GPU
+        if (c->co_grid > P.grid) ca.part = c->d_co_part;
+        ca.rpart = ca.part;
+        ca.n_rpart = c->co_grid;
+        CUDA_TRY(c, launch_pcg(1, c->co_var, ca, c->co_grid, c->stream));
+        c->launches += 2;
       } else {
         CUDA_TRY(c, launch_pcg(1, P.pcg_var, ca, P.grid, c->stream));
         c->launches += 2;  // RHS kernel + cooperative PCG kernel
@@ -2843,11 +2852,47 @@ tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
       co->m[i]->launches += 1.0 / (double)ns_small;
     }
   }
-  // large members: the grid engine, while the cluster launch runs
+  // large members: the grid engine, while the cluster launch runs.  Two or
+  // more share the GPU: each member's
+  // steps are enqueued on its own stream with a PCG shaped for 1/G of the GPU
+  // (variant and cooperative grid), so the members' kernels run side by side;
+  // then every member is finished.  (TCB_COHORT_SERIAL=1: one after another.)
   std::vector<tc_step_stat> hbig(co->big.size() * nsteps);
   std::vector<tc_status> sbig(co->big.size(), TC_OK);
-  for (size_t b = 0; b < co->big.size(); ++b)
-    sbig[b] = tc_step(co->m[co->big[b]], nsteps, hbig.data() + b * nsteps);
+  const char* ser = std::getenv("TCB_COHORT_SERIAL");
+  const bool concurrent = co->big.size() >= 2 && !(ser && ser[0] == '1');
+  if (!concurrent) {
+    for (size_t b = 0; b < co->big.size(); ++b)
+      sbig[b] = tc_step(co->m[co->big[b]], nsteps, hbig.data() + b * nsteps);
+  } else {
+    const int share = (int)std::min<size_t>(co->big.size(), 8);
+    std::vector<size_t> evis(co->big.size(), 0);
+    std::vector<char> cl(co->big.size(), 0), started(co->big.size(), 0);
+    for (size_t b = 0; b < co->big.size(); ++b) {
+      tc_ctx* c = co->m[co->big[b]];
+      Part& P = c->parts[0];
+      const bool grid_path = !use_cluster(c) && !split_mode(c) && c->parts.size() == 1 && P.pcg_var != 5;
+      sbig[b] = ensure_stats(c, nsteps);
+      if (grid_path && sbig[b] == TC_OK) {
+        c->co_var = cg_pick_variant_share(c->cfg.pcg_variant, P.nslices, c->device, share);
+        c->co_grid = cg_grid_size_share(c->co_var, P.nslices, c->device, share);
+        if (c->co_grid > P.grid && c->co_part_cap < c->co_grid) {   // partials: 2 x grid
+          if (dalloc(c, &c->d_co_part, 2 * (int64_t)c->co_grid) != cudaSuccess) sbig[b] = TC_ENOMEM;
+          else c->co_part_cap = c->co_grid;
+        }
+      }
+      bool clb = false;
+      if (sbig[b] == TC_OK) sbig[b] = enqueue_steps(c, nsteps, c->d_stats, c->prof, evis[b], clb);
+      cl[b] = clb;
+      started[b] = sbig[b] == TC_OK;
+    }
+    for (size_t b = 0; b < co->big.size(); ++b) {
+      tc_ctx* c = co->m[co->big[b]];
+      if (started[b]) sbig[b] = finish_steps(c, nsteps, hbig.data() + b * nsteps, evis[b], cl[b]);
+      c->co_var = -1;
+      c->co_grid = 0;
+    }
+  }
   std::vector<int32_t> status(cnt, 0);
   if (ns_small > 0) {
     CO_CUDA(co, cudaMemcpyAsync(status.data(), co->d_status, cnt * 4, cudaMemcpyDeviceToHost, co->stream));

@@ -366,6 +366,8 @@ cudaError_t g_build(GArgs a, int grid, cudaGraphExec_t* exec);
 cudaError_t g_launch(cudaGraphExec_t exec, GStep* gs, double* x, tc_step_stat* stat, int32_t tag, cudaStream_t s);
 
 int cg_pick_variant(int requested, int32_t nslices, int device);
+int cg_pick_variant_share(int requested, int32_t nslices, int device, int share);
+int cg_grid_size_share(int variant, int32_t nslices, int device, int share);
 cudaError_t launch_rhs(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pcg(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_pcg_only(int mode, int variant, const CgArgs& a, int grid, cudaStream_t s);

@@ -22,6 +22,8 @@
 // Reductions are deterministic: per-CTA partials in a fixed slot, then every
 // CTA sums all partials in the same order (bitwise-identical scalars => all
 // CTAs take the same branch).
+#include <algorithm>
+
 #include "pcg_common.cuh"
 
 namespace tcb {
@@ -412,6 +414,17 @@ static int pcg_smem(int variant) { return variant == 1 ? kCgSmem : 0; }
 // per resident warp of the direct variant (mid-size systems such as configs[2],
 // where each warp owns 1-3 slices and the S phase is one latency chain per
 // slot batch), else the direct variant 0 (measured crossover: DESIGN.md "PCG").
+// The same choice for a system that gets 1/share of the GPU (cohorts of
+// concurrent large members, api.cu), and that share of the variant's grid.
+int cg_pick_variant_share(int requested, int32_t nslices, int device, int share) {
+  if (requested >= 0) return requested;
+  const int64_t warps = (int64_t)sm_count(device) * (2048 / 32) / std::max(share, 1);
+  return (int64_t)nslices <= kAutoBatch * warps ? 4 : 0;
+}
+int cg_grid_size_share(int variant, int32_t nslices, int device, int share) {
+  return std::max(1, cg_grid_size(1, variant, nslices, device) / std::max(share, 1));
+}
+
 int cg_pick_variant(int requested, int32_t nslices, int device) {
   if (requested >= 0) return requested;
   const int64_t warps = (int64_t)sm_count(device) * (2048 / 32);
