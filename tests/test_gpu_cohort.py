@@ -311,6 +311,37 @@ def test_cohort_mixes_small_and_large_members(T):
             s.close()
 
 
+def test_cohort_large_members_share_the_gpu(T):
+    """Three grid-engine-sized members (plus a small one) in one cohort: the large
+    ones run side by side, each on its own stream with the PCG variant and
+    cooperative grid chosen for a third of the GPU (DESIGN.md "Cohorts of large
+    members"); every member matches its own oracle run, and the shared-GPU shape
+    gives the same trajectory as the member stepped alone up to rounding."""
+    specs = [dict(dims=(61, 23, 9), permute=3, fib_seed=2), dict(dims=(21, 8, 5)),
+             dict(dims=(57, 25, 10), permute=5, sigma_scale=0.9),
+             dict(dims=(65, 21, 9), permute=7, fib_seed=4)]
+    members, refs = [], []
+    try:
+        for spec in specs:
+            args = _member(spec)
+            refs.append(_oracle(spec, *args))
+            members.append(_gpu(T, spec, *args, engine="auto"))
+        big = [m for m in members if T.tc_matrix_info(m.ctx)["nslices"] > 256]
+        assert len(big) == 3
+        co = T.Cohort(members)
+        try:
+            for c in range(3):
+                stats = co.step(10)
+                for m, (sim, ref) in enumerate(zip(members, refs)):
+                    reps = [ref.step() for _ in range(10)]
+                    _check(sim, ref, stats[m], reps, 0.05, f"member {m} chunk {c}")
+        finally:
+            co.close()
+    finally:
+        for s in members:
+            s.close()
+
+
 def test_cohort_long_horizon_bench_members(T):
     """The bench's cohort members 8 and 1 (meshgen.cohort_members, seeded; the
     ones whose trajectories undershoot to V ~ -99 mV, where the fast exp once
