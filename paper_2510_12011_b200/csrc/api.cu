@@ -131,6 +131,8 @@ struct tc_ctx {
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaStream_t s_halo = nullptr;           // split path: halo exchange stream (overlapped)
   // ionic || RHS pipeline (chunked_step): row chunks, RHS stream, events
+  bool split_overlap = false;              // split path without a communicator: overlapped launches anyway
+                                           // (TCB_SPLIT_OVERLAP=1, tests: the path real multi-GPU takes)
   int co_var = -1, co_grid = 0;            // cohort of concurrent large members: the PCG shape for 1/share of the GPU
   double2* d_co_part = nullptr;            // ... and its partials when that grid exceeds P.grid
   int co_part_cap = 0;
@@ -1402,6 +1404,10 @@ extern "C" tc_status tc_assemble(tc_ctx* c) {
     for (Part& P : c->parts) reds.push_back(P.d_red);
     CUDA_TRY(c, upload(c, &c->d_reds, reds));
   }
+  {
+    const char* so = std::getenv("TCB_SPLIT_OVERLAP");
+    c->split_overlap = so && so[0] == '1';
+  }
   if (split_mode(c)) TC_TRY(setup_peer(c, plans));
   else if (c->parts[0].pcg_var == 5) TC_TRY(setup_graph(c, c->parts[0]));
   int32_t flags[8] = {0, 0, 0, c->cfg.fail_budget, -1, 0, 0, 0};
@@ -1606,7 +1612,7 @@ static tc_status halo_stream(tc_ctx* c) {
 template <class Pass, class Halo>
 static tc_status overlapped_pass(tc_ctx* c, Pass pass, Halo halo) {
   cudaStream_t s = c->stream;
-  if (!c->use_comm) {
+  if (!c->use_comm && !c->split_overlap) {
     TC_TRY(halo(s));
     for (Part& P : c->parts) CUDA_TRY(c, pass(P, split_args(c, P)));
     return TC_OK;

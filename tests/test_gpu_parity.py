@@ -616,3 +616,36 @@ def test_mms_split_setters_equal_tc_set_mms(T):
         finally:
             T.tc_destroy(ctx)
     assert np.array_equal(vs[0], vs[1])
+
+
+@pytest.mark.parametrize("nparts", [2, 3])
+def test_split_path_overlapped_launches(T, nparts):
+    """The split path as a real communicator runs it -- the interior slices of
+    every S / RHS pass as one launch while the halo is in flight, the boundary
+    slices as a second launch that adds the first one's per-CTA partials before
+    the deterministic reduction (reduce_phase) -- forced on one GPU with
+    TCB_SPLIT_OVERLAP=1 (read at tc_assemble): a trajectory against the oracle."""
+    import os
+    xyz, tets, region, fib, cond, stims = _slab_case("tt2006", 61, 23, 9, permute=True, seed=4)
+    dt = 0.05
+    ref = O.Monodomain(xyz, tets, region, fib, cond, O.Config(dt=dt, abs_tol=1e-8, rel_tol=0.0), stims)
+    os.environ["TCB_SPLIT_OVERLAP"] = "1"
+    try:
+        cfg = T.tc_config_default(dt=dt, abs_tol=1e-8, rel_tol=0.0, partitions=nparts, peer=0)
+        sim = T.Monodomain(xyz, tets, region, fib, cond, cfg, stims)
+    finally:
+        os.environ.pop("TCB_SPLIT_OVERLAP", None)
+    try:
+        info = T.tc_matrix_info(sim.ctx)
+        assert info["path"] == "split" and info["ghosts"] > 0
+        T.tc_validate(sim.ctx)    # includes: interior slices read no ghost column
+        for k in range(60):
+            st = sim.step(1)
+            rep = ref.step()
+            rel = np.linalg.norm(sim.V - ref.Vk) / np.linalg.norm(ref.Vk)
+            assert rel <= 1e-8, (k, rel)
+            assert abs(int(st["iters"][0]) - rep.iters) <= 1
+        lat, _ = sim.activation()
+        assert np.abs(lat - ref.lat).max() <= dt + 1e-12
+    finally:
+        sim.close()
