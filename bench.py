@@ -68,6 +68,11 @@ WORKLOADS = {
     "cohort8_nversion01_tt": dict(cfg="f1 cohort (configs[2]-sized members)", cohort=8, dims=None, dx=0.1,
                                   member_base=(201, 71, 31), model="tt2006", dt=0.01, stim="corner",
                                   preroll=500),
+    # SURVEY 8f f1 at the paper's member kind: 8 left-atrium-surface-sized icospheres (655 k nodes,
+    # P1 triangles, MS; P:349-353 runs 100 LA surface meshes of 660,557 nodes), sharing the GPU
+    "cohort8_sphere655k_ms": dict(cfg="f1 cohort (LA-surface-sized members, P:349)", cohort=8, dims=None,
+                                  dx=0.13, model="ms", dt=0.01, stim="sphere", level=8, radius=28.0,
+                                  preroll=500),
 }
 DEFAULT_WORKLOAD = "slab20M_ms"
 
@@ -546,8 +551,11 @@ def run_cohort(args, w):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
-    members = G.cohort_members(w["cohort"], seed=G.SEED + rank, base=w.get("member_base", (41, 15, 7)),
-                               dx=w["dx"])
+    if w["stim"] == "sphere":
+        members = G.sphere_cohort_members(w["cohort"], seed=G.SEED + rank, level=w["level"], radius=w["radius"])
+    else:
+        members = G.cohort_members(w["cohort"], seed=G.SEED + rank, base=w.get("member_base", (41, 15, 7)),
+                                   dx=w["dx"])
     sims = []
     t0 = time.perf_counter()
     for m in members:
@@ -638,8 +646,12 @@ def run_cohort(args, w):
             import oracle as O
             m = members[0]
             E = m["tets"].shape[0]
-            names = O.tt_param_names()
-            prm = O.tt_default_params().copy()
+            if w["model"] == "ms":
+                names = ["tau_in", "tau_out", "tau_open", "tau_close", "v_gate", "V_min", "V_max"]
+                prm = O.ms_default_params().copy()
+            else:
+                names = O.tt_param_names()
+                prm = O.tt_default_params().copy()
             for k_, f_ in m["param_factors"].items():
                 prm[names.index(k_)] *= f_
             cfg = O.Config(dt=w["dt"], model=w["model"], chi=CHI, cm=CM, abs_tol=1e-5, rel_tol=1e-5,
@@ -647,11 +659,13 @@ def run_cohort(args, w):
             osim = O.Monodomain(m["xyz"], m["tets"], np.zeros(E, np.int32), m["fibre"],
                                 {0: (SIGMA[0] * m["sigma_scale"], SIGMA[1] * m["sigma_scale"])}, cfg,
                                 [O.Stimulus(m["stim_nodes"], 0.0, 2.0, 50.0)])
+            O.set_threads(1)
             k_, t1 = 0, time.perf_counter()
             while time.perf_counter() - t1 < 15.0 and k_ < 800:
                 osim.step()
                 k_ += 1
             el = time.perf_counter() - t1
+            O.set_threads(O.max_threads())
             cpu = dict(value=n_nodes[0] * k_ / el, unit="node-steps/s", cores=1, kind="oracle",
                        sample=f"member 0 ({n_nodes[0]} nodes), first {k_} steps from rest, {el:.1f} s single-thread")
         except Exception as ex:

@@ -345,3 +345,30 @@ def cohort_members(count: int, seed=SEED, base=(41, 15, 7), dx=0.5):
                                        "GCaL": float(rng.uniform(0.8, 1.2))},
                         stim_nodes=stim))
     return out
+
+
+def sphere_cohort_members(count: int, seed=SEED, level: int = 8, radius: float = 28.0):
+    """Seeded cohort of `count` atrium-surface-sized icospheres (SURVEY 8f f1 with
+    P:349-353's 660 k-node left-atrium surface meshes, Mitchell-Schaeffer):
+    member m: radius x U[0.9, 1.1], tangent fibres rotated about the local normal
+    by U[-30, 30] degrees, conductivity scale U[0.8, 1.2], MS tau_close x
+    U[0.8, 1.2] and tau_in x U[0.9, 1.1] (factors applied by the caller), a polar
+    cap stimulus (the 2 mm cap of the bench's sphere workloads, scaled).  Same
+    dict keys as cohort_members; "tets" holds the triangles."""
+    rng = np.random.default_rng(seed)
+    base_xyz, tris = sphere(level, 1.0)
+    out = []
+    for m in range(count):
+        r = radius * float(rng.uniform(0.9, 1.1))
+        xyz = base_xyz * r
+        f = sphere_fibres(xyz, tris)
+        ang = np.deg2rad(rng.uniform(-30.0, 30.0))
+        c = xyz[tris].mean(1)
+        nrm = c / np.linalg.norm(c, axis=1, keepdims=True)
+        f = np.cos(ang) * f + np.sin(ang) * np.cross(nrm, f)      # rotate in the tangent plane
+        stim = np.nonzero(xyz[:, 2] >= r - 2.0 * r / radius)[0].astype(np.int32)
+        out.append(dict(xyz=xyz, tets=tris, fibre=f, sigma_scale=float(rng.uniform(0.8, 1.2)),
+                        param_factors={"tau_close": float(rng.uniform(0.8, 1.2)),
+                                       "tau_in": float(rng.uniform(0.9, 1.1))},
+                        stim_nodes=stim))
+    return out
