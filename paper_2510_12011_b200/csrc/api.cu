@@ -1483,6 +1483,7 @@ static CgArgs cg_args(tc_ctx* c, Part& P, double* x) {
   a.s1 = P.nslices;
   a.rpart = P.d_part;
   a.n_rpart = P.grid;
+  a.fuse_rhs = 0;
   a.store_r = 1;
   return a;
 }
@@ -1982,6 +1983,10 @@ static tc_status enqueue_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* dstats, 
         ca.n_rpart = c->co_grid;
         CUDA_TRY(c, launch_pcg(1, c->co_var, ca, c->co_grid, c->stream));
         c->launches += 2;
+      } else if (P.pcg_var == 4 && TCB_FUSE_RHS4) {   // RHS inside the cooperative kernel
+        ca.fuse_rhs = 1;
+        CUDA_TRY(c, launch_pcg_only(1, 4, ca, P.grid, c->stream));
+        c->launches += 1;
       } else {
         CUDA_TRY(c, launch_pcg(1, P.pcg_var, ca, P.grid, c->stream));
         c->launches += 2;  // RHS kernel + cooperative PCG kernel

@@ -104,6 +104,11 @@ double* ms_param_slot(MSParams* p, const char* name);
 #ifndef TCB_ZFORM
 #define TCB_ZFORM 1
 #endif
+// TCB_FUSE_RHS4 = 1: the latency variant (4) computes the RHS inside its
+// cooperative kernel (one launch per solve instead of two).
+#ifndef TCB_FUSE_RHS4
+#define TCB_FUSE_RHS4 0
+#endif
 struct CgArgs {
   const int64_t* slice_ptr;
   const int32_t* col;
@@ -133,6 +138,7 @@ struct CgArgs {
   int32_t s0, s1;      // RHS kernel: slice range [s0, s1) (chunked RHS; default [0, nslices))
   const double2* rpart;  // PCG kernel: the RHS partials it sums first (default part) ...
   int32_t n_rpart;       // ... and how many (default gridDim.x)
+  int32_t fuse_rhs;      // PCG kernel, variant 4: compute the RHS itself first (one launch per solve)
 };
 
 // ---- split-phase (partitioned) PCG: device scalar state of Algorithm 1 -----

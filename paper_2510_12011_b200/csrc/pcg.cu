@@ -184,6 +184,31 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
                     ((((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)dinv) |
                       ((uintptr_t)a.x) | ((uintptr_t)a.p0) | ((uintptr_t)a.p1)) & 15) == 0;
 
+  // ---- variant 4 with fuse_rhs: the RHS phase here (rhs_kernel's batched row
+  // product), then a grid barrier -- one launch and one kernel boundary per
+  // solve fewer (mid-size systems are launch-latency sensitive) --------------
+  if constexpr (BATCH && MODE == 1) {
+    if (a.fuse_rhs) {
+      double2 acc0 = make_double2(0.0, 0.0);
+      for (int s = a.s0 + gw; s < a.s1; s += nw) {
+        const int64_t base = __ldg(sp + s);
+        const int w = (int)((__ldg(sp + s + 1) - base) >> 5);
+        const int64_t i = (int64_t)s * kSellC + lane;
+        const double sum = (TCB_BATCH_SMALL && w <= 8)
+                               ? row_rhs_batch<8>(base, w, lane, col, Av, a.K, a.up, a.vp)
+                               : row_rhs_batch<(TCB_RHS_BATCH_NB > 0 ? TCB_RHS_BATCH_NB : 1)>(base, w, lane, col, Av,
+                                                                                               a.K, a.up, a.vp);
+        const double zi = __ldg(dinv + i) * sum;
+        if (a.store_r) a.r[i] = sum;
+        a.z[i] = zi;
+        acc0.x += sum * zi;
+        acc0.y += zi * zi;
+      }
+      const double2 b0 = block_sum2(acc0, sh);
+      if (threadIdx.x == 0) a.part[blockIdx.x] = b0;
+      grid.sync();
+    }
+  }
   // ---- rho_0 = r.z, ||z_0|| from the RHS kernel's per-CTA partials ------------
   double2 tot;
   {
