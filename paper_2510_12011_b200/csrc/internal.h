@@ -104,10 +104,12 @@ double* ms_param_slot(MSParams* p, const char* name);
 #ifndef TCB_ZFORM
 #define TCB_ZFORM 1
 #endif
-// TCB_FUSE_RHS4 = 1: the latency variant (4) computes the RHS inside its
-// cooperative kernel (one launch per solve instead of two).
+// TCB_FUSE_RHS4 = 1 (default): the latency variant (4) computes the RHS inside
+// its cooperative kernel (one launch per solve instead of two).  Measured
+// (profiles/r02ab_exp_fuse4.txt, ms/step): configs[2] 0.3627 -> 0.3603,
+// sphere655k 0.1870 -> 0.1848.
 #ifndef TCB_FUSE_RHS4
-#define TCB_FUSE_RHS4 0
+#define TCB_FUSE_RHS4 1
 #endif
 struct CgArgs {
   const int64_t* slice_ptr;
