@@ -407,6 +407,8 @@ CRNDerived crn_derived(const CRNParams& P) {
   D.vrel_vi = P.Vrel / P.Vi;
   D.vrel_vup = P.Vrel / P.Vup;
   D.inv_kq10 = 1.0 / P.KQ10;
+  D.kq10 = P.KQ10;
+  D.inv_tauu = 1.0 / P.tauu;
   D.fn_c = 1e-15 / (2.0 * P.F) * P.Cm;  // currents per capacitance -> pA
   D.log_nao = std::log(P.Nao);
   D.log_ko = std::log(P.Ko);

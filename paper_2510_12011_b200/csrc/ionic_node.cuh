@@ -74,6 +74,15 @@ struct TTCur {
 
 #define EXP(x) tc_exp((x), T)
 
+// TCB_ION_FOLD = 1 (default): quotients of the model's rate expressions merged
+// over a common denominator where only their combination is used (e.g. 1/tau_m
+// = 1/(alpha_m beta_m) with alpha_m = 1/A, beta_m = 0.1/B1 + 0.1/B2 is
+// 10 A B1 B2 / (B1 + B2)), so one reciprocal replaces up to four; every merged
+// term is a sum of positive factors (no cancellation).  0: the literal forms.
+#ifndef TCB_ION_FOLD
+#define TCB_ION_FOLD 1
+#endif
+
 __device__ __forceinline__ double sig(double x, const Exp2Table* T) {  // 1 / (1 + e^x)
   return tc_rcp(1.0 + EXP(x));
 }
@@ -114,12 +123,20 @@ TCB_CUR_ATTR TTCur tt_cur(double V, const double* u, const TTParams& P,
   c.ina = P.GNa * u[sm] * u[sm] * u[sm] * u[sh] * u[sj] * (V - ena);
   {
     const double dvk = V - ek;
-    const double a1 = 0.1 * tc_rcp(1.0 + EXP(0.06 * (dvk - 200.0)));
     const double e1 = EXP(0.1 * dvk);                 // exp(0.1 (V - EK))
     const double e2 = e1 * e1, e5 = e2 * e2 * e1;     // exp(0.5 (V - EK))
+#if TCB_ION_FOLD
+    // a1 = 0.1/Q, b1 = N e5/(1 + e5):  a1/(a1 + b1) = 0.1 (1 + e5) / (0.1 (1 + e5) + N e5 Q)
+    const double Q = 1.0 + EXP(0.06 * (dvk - 200.0));
+    const double N = 3.0 * EXP(0.0002 * (dvk + 100.0)) + e1 * D.x_m1;
+    const double a1 = 0.1 * (1.0 + e5);
+    c.ik1 = P.GK1 * (a1 * tc_rcp(fma(N * e5, Q, a1))) * dvk;
+#else
+    const double a1 = 0.1 * tc_rcp(1.0 + EXP(0.06 * (dvk - 200.0)));
     const double b1 = (3.0 * EXP(0.0002 * (dvk + 100.0)) + e1 * D.x_m1) *
                       tc_rcp(1.0 + tc_rcp(e5));
     c.ik1 = P.GK1 * (a1 * tc_rcp(a1 + b1)) * dvk;
+#endif
   }
   c.ito = P.Gto * u[sr] * u[ss] * (V - ek);
   c.ikr = P.GKr * D.sq_ko * u[sxr1] * u[sxr2] * (V - ek);
@@ -183,6 +200,21 @@ __device__ __forceinline__ double tt_advance(double V, double* u, double dt, con
 #endif
   // -- calcium dynamics (currents and fluxes at (V^k, u^k)) --
   const double casr = u[sCaSR], cass = u[sCaSS], cai = u[sCai];
+#if TCB_ION_FOLD
+  // 1/(1 + (EC/casr)^2) = casr^2/(casr^2 + EC^2);  k1 = k1p/kcasr only enters
+  // oo = k1 cass^2 rbar/(k3 + k1 cass^2) = k1p cass^2 rbar/(k3 kcasr + k1p cass^2);
+  // iup = Vmaxup/(1 + Kup^2/cai^2) = Vmaxup cai^2/(cai^2 + Kup^2)
+  const double casr2 = casr * casr;
+  const double kcasr = P.maxsr - (P.maxsr - P.minsr) * (casr2 * tc_rcp(fma(P.EC, P.EC, casr2)));
+  const double k2 = P.k2p * kcasr;
+  const double rbar = u[sRbar] + dt * (P.k4 * (1.0 - u[sRbar]) - k2 * cass * u[sRbar]);
+  const double k1c = P.k1p * cass * cass;
+  const double oo = k1c * rbar * tc_rcp(fma(P.k3, kcasr, k1c));
+  const double irel = P.Vrel * oo * (casr - cass);
+  const double ileak = P.Vleak * (casr - cai);
+  const double cai2 = cai * cai;
+  const double iup = P.Vmaxup * cai2 * tc_rcp(cai2 + D.kup2);
+#else
   const double ec = P.EC * tc_rcp(casr);
   const double kcasr = P.maxsr - (P.maxsr - P.minsr) * tc_rcp(1.0 + ec * ec);
   const double k1 = P.k1p * tc_rcp(kcasr), k2 = P.k2p * kcasr;
@@ -191,6 +223,7 @@ __device__ __forceinline__ double tt_advance(double V, double* u, double dt, con
   const double irel = P.Vrel * oo * (casr - cass);
   const double ileak = P.Vleak * (casr - cai);
   const double iup = P.Vmaxup * tc_rcp(1.0 + D.kup2 * tc_rcp(cai * cai));
+#endif
   const double ixfer = P.Vxfer * (cass - cai);
   const double nu_sr = dt * (iup - irel - ileak);
   const double nu_ss = dt * (-ixfer * D.vc_vss + irel * D.vsr_vss - c.ical * D.cap_2vssf);
@@ -211,11 +244,20 @@ __device__ __forceinline__ double tt_advance(double V, double* u, double dt, con
   const double e20 = EXP(V * (1.0 / 20.0)), ie20 = tc_rcp(e20);
   const double e6 = EXP(V * (1.0 / 6.0)), ie6 = tc_rcp(e6);
   {
+#if TCB_ION_FOLD
+    // am = 1/A, bm = 0.1/B1 + 0.1/B2:  1/(am bm) = 10 A B1 B2/(B1 + B2)
+    const double A = 1.0 + D.x_m12 * ie5;                // (-60-V)/5: e^-12
+    const double B1 = 1.0 + D.x_7 * e5;                  // (V+35)/5: e^7
+    const double B2 = 1.0 + EXP((V - 50.0) * (1.0 / 200.0));
+    const double inv_tau = 10.0 * A * B1 * B2 * tc_rcp(B1 + B2);
+#else
     const double am = tc_rcp(1.0 + D.x_m12 * ie5);     // (-60-V)/5: e^-12
     const double bm = 0.1 * tc_rcp(1.0 + D.x_7 * e5)    // (V+35)/5: e^7
                       + 0.1 * sig((V - 50.0) * (1.0 / 200.0), T);
+    const double inv_tau = tc_rcp(am * bm);
+#endif
     const double mi = sig((-56.86 - V) * (1.0 / 9.03), T);
-    u[sm] = rl_rate(u[sm], mi * mi, tc_rcp(am * bm), dt, T);
+    u[sm] = rl_rate(u[sm], mi * mi, inv_tau, dt, T);
   }
   {
     const double hi = sig((V + 71.55) * (1.0 / 7.43), T);
@@ -238,21 +280,41 @@ __device__ __forceinline__ double tt_advance(double V, double* u, double dt, con
   }
   {
     const double xr1_inf = tc_rcp(1.0 + D.x_m26_7 * ie7);       // (-26-V)/7: e^(-26/7)
+#if TCB_ION_FOLD
+    // a = 450/A, b = 6/B:  1/(a b) = A B/2700
+    const double inv_tau = (1.0 + D.x_m4_5 * ie10) *            // (-45-V)/10: e^-4.5
+                           (1.0 + EXP((V + 30.0) * (1.0 / 11.5))) * (1.0 / 2700.0);
+#else
     const double a = 450.0 * tc_rcp(1.0 + D.x_m4_5 * ie10);    // (-45-V)/10: e^-4.5
     const double b = 6.0 * sig((V + 30.0) * (1.0 / 11.5), T);
-    u[sxr1] = rl_rate(u[sxr1], xr1_inf, tc_rcp(a * b), dt, T);
+    const double inv_tau = tc_rcp(a * b);
+#endif
+    u[sxr1] = rl_rate(u[sxr1], xr1_inf, inv_tau, dt, T);
   }
   {
     const double xr2_inf = sig((V + 88.0) * (1.0 / 24.0), T);
+#if TCB_ION_FOLD
+    // a = 3/A, b = 1.12/B:  1/(a b) = A B/3.36
+    const double inv_tau = (1.0 + D.x_m3 * ie20) * (1.0 + D.x_m3 * e20) * (1.0 / 3.36);
+#else
     const double a = 3.0 * tc_rcp(1.0 + D.x_m3 * ie20);      // (-60-V)/20: e^-3
     const double b = 1.12 * tc_rcp(1.0 + D.x_m3 * e20);      // (V-60)/20: e^-3
-    u[sxr2] = rl_rate(u[sxr2], xr2_inf, tc_rcp(a * b), dt, T);
+    const double inv_tau = tc_rcp(a * b);
+#endif
+    u[sxr2] = rl_rate(u[sxr2], xr2_inf, inv_tau, dt, T);
   }
   {
     const double xs_inf = sig((-5.0 - V) * (1.0 / 14.0), T);
+#if TCB_ION_FOLD
+    // tau = 1400/(sqrt(C) E) + 80, E = 1 + e^((V-35)/15):  1/tau = E/(1400/sqrt(C) + 80 E)
+    const double E = 1.0 + EXP((V - 35.0) * (1.0 / 15.0));
+    const double inv_tau = E * tc_rcp(fma(1400.0, rsqrt(1.0 + D.x_5_6 * ie6), 80.0 * E));  // (5-V)/6: e^(5/6)
+#else
     const double tau = 1400.0 * tc_rcp(sqrt(1.0 + D.x_5_6 * ie6))  // (5-V)/6: e^(5/6)
                        * sig((V - 35.0) * (1.0 / 15.0), T) + 80.0;
-    u[sxs] = rl_rate(u[sxs], xs_inf, tc_rcp(tau), dt, T);
+    const double inv_tau = tc_rcp(tau);
+#endif
+    u[sxs] = rl_rate(u[sxs], xs_inf, inv_tau, dt, T);
   }
   {
     const double r_inf = tc_rcp(1.0 + D.x_20_6 * ie6);              // (20-V)/6: e^(10/3)
@@ -263,33 +325,68 @@ __device__ __forceinline__ double tt_advance(double V, double* u, double dt, con
   {
     const double s_inf = tc_rcp(1.0 + D.x_4 * e5);              // (V+20)/5: e^4
     const double d45 = V + 45.0;
+#if TCB_ION_FOLD
+    // tau = G + 5/S:  1/tau = S/(G S + 5)
+    const double S = 1.0 + D.x_m4 * e5;                          // (V-20)/5: e^-4
+    const double G = 85.0 * EXP(-d45 * d45 * (1.0 / 320.0)) + 3.0;
+    const double inv_tau = S * tc_rcp(fma(G, S, 5.0));
+#else
     const double tau = 85.0 * EXP(-d45 * d45 * (1.0 / 320.0)) +
                        5.0 * tc_rcp(1.0 + D.x_m4 * e5) + 3.0;   // (V-20)/5: e^-4
-    u[ss] = rl_rate(u[ss], s_inf, tc_rcp(tau), dt, T);
+    const double inv_tau = tc_rcp(tau);
+#endif
+    u[ss] = rl_rate(u[ss], s_inf, inv_tau, dt, T);
   }
   {
     const double d_inf = sig((-8.0 - V) * (1.0 / 7.5), T);
+#if TCB_ION_FOLD
+    // tau = (1.4/S1 + 0.25)(1.4/D2) + 1/D3:
+    //   1/tau = S1 D2 D3 / (1.4 D3 (1.4 + 0.25 S1) + S1 D2)
+    const double S1 = 1.0 + EXP((-35.0 - V) * (1.0 / 13.0));
+    const double D2 = 1.0 + D.x_1 * e5;                          // (V+5)/5: e
+    const double D3 = 1.0 + D.x_2_5 * ie20;                      // (50-V)/20: e^2.5
+    const double S1D2 = S1 * D2;
+    const double inv_tau = S1D2 * D3 * tc_rcp(fma(1.4 * D3, fma(0.25, S1, 1.4), S1D2));
+#else
     const double tau = (1.4 * sig((-35.0 - V) * (1.0 / 13.0), T) + 0.25) *
                            (1.4 * tc_rcp(1.0 + D.x_1 * e5)) +     // (V+5)/5: e
                        tc_rcp(1.0 + D.x_2_5 * ie20);               // (50-V)/20: e^2.5
-    u[sd] = rl_rate(u[sd], d_inf, tc_rcp(tau), dt, T);
+    const double inv_tau = tc_rcp(tau);
+#endif
+    u[sd] = rl_rate(u[sd], d_inf, inv_tau, dt, T);
   }
   const double s30 = tc_rcp(1.0 + D.x_3 * e10);                 // (V+30)/10: e^3
   {
     const double f_inf = tc_rcp(1.0 + D.x_20_7 * e7);                // (V+20)/7: e^(20/7)
     const double d27 = V + 27.0;
+#if TCB_ION_FOLD
+    // tau = G + 200/F1:  1/tau = F1/(G F1 + 200)
+    const double F1 = 1.0 + D.x_1_3 * ie10;                      // (13-V)/10: e^1.3
+    const double G = 1102.5 * EXP(-d27 * d27 * (1.0 / 225.0)) + 180.0 * s30 + 20.0;
+    const double inv_tau = F1 * tc_rcp(fma(G, F1, 200.0));
+#else
     const double tau = 1102.5 * EXP(-d27 * d27 * (1.0 / 225.0)) +
                        200.0 * tc_rcp(1.0 + D.x_1_3 * ie10) +      // (13-V)/10: e^1.3
                        180.0 * s30 + 20.0;
-    u[sf] = rl_rate(u[sf], f_inf, tc_rcp(tau), dt, T);
+    const double inv_tau = tc_rcp(tau);
+#endif
+    u[sf] = rl_rate(u[sf], f_inf, inv_tau, dt, T);
   }
   {
     const double f2_inf = 0.67 * tc_rcp(1.0 + D.x_5 * e7) + 0.33; // (V+35)/7: e^5
     const double d25 = V + 25.0;
+#if TCB_ION_FOLD
+    // tau = G + 31/F2:  1/tau = F2/(G F2 + 31)
+    const double F2 = 1.0 + D.x_2_5 * ie10;                      // (25-V)/10: e^2.5
+    const double G = 600.0 * EXP(-d25 * d25 * (1.0 / 170.0)) + 16.0 * s30;
+    const double inv_tau = F2 * tc_rcp(fma(G, F2, 31.0));
+#else
     const double tau = 600.0 * EXP(-d25 * d25 * (1.0 / 170.0)) +
                        31.0 * tc_rcp(1.0 + D.x_2_5 * ie10) +        // (25-V)/10: e^2.5
                        16.0 * s30;
-    u[sf2] = rl_rate(u[sf2], f2_inf, tc_rcp(tau), dt, T);
+    const double inv_tau = tc_rcp(tau);
+#endif
+    u[sf2] = rl_rate(u[sf2], f2_inf, inv_tau, dt, T);
   }
   {
     const double q = u[sCaSS] * (1.0 / 0.05);
@@ -336,7 +433,7 @@ struct CRNDerived {   // parameter-only factors (host-computed)
   double cm_vif, cm_2vif;     // Cm / (Vi F), Cm / (2 Vi F)
   double inak_k;              // INaK_max Ko / (Ko + KmKo)
   double inaca_k;             // INaCa_max / ((KmNa^3 + Nao^3)(KmCa + Cao))
-  double nao3, inv_tautr, iupleak_k, vup_vi, vrel_vi, vrel_vup, inv_kq10, fn_c;
+  double nao3, inv_tautr, iupleak_k, vup_vi, vrel_vi, vrel_vup, inv_kq10, kq10, inv_tauu, fn_c;
   double log_nao, log_ko, log_cao;   // logs of the Nernst numerators
 };
 
@@ -391,6 +488,14 @@ __device__ __forceinline__ double rl_tau(double y, double yinf, double tau, doub
   return yinf - (yinf - y) * EXP(-dt * tc_rcp(tau));
 }
 
+// Gate with tau = 1/R, given as the rate R (TCB_ION_FOLD: 1/tau = R without the
+// reciprocal of a reciprocal) or, literally, as tau = 1/R.
+#if TCB_ION_FOLD
+#define CRN_RL_RATE(y, yinf, R) rl_rate((y), (yinf), (R), dt, T)
+#else
+#define CRN_RL_RATE(y, yinf, R) rl_tau((y), (yinf), tc_rcp(R), dt, T)
+#endif
+
 // Advances u in place; returns I_n(V, u^{k+1}).
 __device__ __forceinline__ double crn_advance(double V, double* u, double dt, const CRNParams& P,
                                               const CRNDerived& D, const Exp2Table* T) {
@@ -407,7 +512,11 @@ __device__ __forceinline__ double crn_advance(double V, double* u, double dt, co
   const double irel = P.Krel * u[cu] * u[cu] * u[cv] * u[cw] * (carel - cai);
   const double itr = (caup - carel) * D.inv_tautr;
   const double iupleak = D.iupleak_k * caup;
+#if TCB_ION_FOLD
+  const double iup = P.Iupmax * cai * tc_rcp(cai + P.Kup);     // Iupmax/(1 + Kup/cai)
+#else
   const double iup = P.Iupmax * tc_rcp(1.0 + P.Kup * tc_rcp(cai));
+#endif
   // gates at (V^k, u^k), each Rush-Larsen update applied as soon as its
   // steady state and time constant are known (nothing below reads a gate)
   {
@@ -415,7 +524,7 @@ __device__ __forceinline__ double crn_advance(double V, double* u, double dt, co
     a = (V == -47.13) ? 3.2 : 0.32 * (V + 47.13) * tc_rcp(1.0 - EXP(-0.1 * (V + 47.13)));
     b = 0.08 * EXP(V * (-1.0 / 11.0));
     ti = tc_rcp(a + b);
-    u[cm] = rl_tau(u[cm], a * ti, ti, dt, T);
+    u[cm] = CRN_RL_RATE(u[cm], a * ti, a + b);
     if (V < -40.0) {
       a = 0.135 * EXP((V + 80.0) * (1.0 / -6.8));
       b = 3.56 * EXP(0.079 * V) + 3.1e5 * EXP(0.35 * V);
@@ -424,7 +533,7 @@ __device__ __forceinline__ double crn_advance(double V, double* u, double dt, co
       b = tc_rcp(0.13 * (1.0 + EXP((V + 10.66) * (1.0 / -11.1))));
     }
     ti = tc_rcp(a + b);
-    u[chh] = rl_tau(u[chh], a * ti, ti, dt, T);
+    u[chh] = CRN_RL_RATE(u[chh], a * ti, a + b);
     if (V < -40.0) {
       a = (-127140.0 * EXP(0.2444 * V) - 3.474e-5 * EXP(-0.04391 * V)) * (V + 37.78) *
           tc_rcp(1.0 + EXP(0.311 * (V + 79.23)));
@@ -434,26 +543,30 @@ __device__ __forceinline__ double crn_advance(double V, double* u, double dt, co
       b = 0.3 * EXP(-2.535e-7 * V) * tc_rcp(1.0 + EXP(-0.1 * (V + 32.0)));
     }
     ti = tc_rcp(a + b);
-    u[cj] = rl_tau(u[cj], a * ti, ti, dt, T);
+    u[cj] = CRN_RL_RATE(u[cj], a * ti, a + b);
     // oa and ua share their rate functions
     a = 0.65 * tc_rcp(EXP((V + 10.0) * (1.0 / -8.5)) + EXP((V - 30.0) * (1.0 / -59.0)));
     b = 0.65 * tc_rcp(2.5 + EXP((V + 82.0) * (1.0 / 17.0)));
-    ti = tc_rcp(a + b) * D.inv_kq10;
-    u[coa] = rl_tau(u[coa], tc_rcp(1.0 + EXP((V + 20.47) * (1.0 / -17.54))), ti, dt, T);
-    u[cua] = rl_tau(u[cua], tc_rcp(1.0 + EXP((V + 30.3) * (1.0 / -9.6))), ti, dt, T);
+    const double rq = (a + b) * D.kq10;                       // 1/tau = (a + b) KQ10
+    u[coa] = CRN_RL_RATE(u[coa], tc_rcp(1.0 + EXP((V + 20.47) * (1.0 / -17.54))), rq);
+    u[cua] = CRN_RL_RATE(u[cua], tc_rcp(1.0 + EXP((V + 30.3) * (1.0 / -9.6))), rq);
     a = tc_rcp(18.53 + EXP((V + 113.7) * (1.0 / 10.95)));
     b = tc_rcp(35.56 + EXP((V + 1.26) * (1.0 / -7.44)));
-    u[coi] = rl_tau(u[coi], tc_rcp(1.0 + EXP((V + 43.1) * (1.0 / 5.3))), tc_rcp(a + b) * D.inv_kq10, dt, T);
+    u[coi] = CRN_RL_RATE(u[coi], tc_rcp(1.0 + EXP((V + 43.1) * (1.0 / 5.3))), (a + b) * D.kq10);
     a = tc_rcp(21.0 + EXP((V - 185.0) * (1.0 / -28.0)));
     b = EXP((V - 158.0) * (1.0 / 16.0));
-    u[cui] = rl_tau(u[cui], tc_rcp(1.0 + EXP((V - 99.45) * (1.0 / 27.48))), tc_rcp(a + b) * D.inv_kq10, dt, T);
+    u[cui] = CRN_RL_RATE(u[cui], tc_rcp(1.0 + EXP((V - 99.45) * (1.0 / 27.48))), (a + b) * D.kq10);
     a = (V == -14.1) ? 0.0015 : 0.0003 * (V + 14.1) * tc_rcp(1.0 - EXP((V + 14.1) * (1.0 / -5.0)));
     b = (V == 3.3328) ? 3.7836118e-4
                       : 7.3898e-5 * (V - 3.3328) * tc_rcp(EXP((V - 3.3328) * (1.0 / 5.1237)) - 1.0);
-    u[cxr] = rl_tau(u[cxr], tc_rcp(1.0 + EXP((V + 14.1) * (1.0 / -6.5))), tc_rcp(a + b), dt, T);
+    u[cxr] = CRN_RL_RATE(u[cxr], tc_rcp(1.0 + EXP((V + 14.1) * (1.0 / -6.5))), a + b);
     a = (V == 19.9) ? 0.00068 : 4e-5 * (V - 19.9) * tc_rcp(1.0 - EXP((V - 19.9) * (1.0 / -17.0)));
     b = (V == 19.9) ? 0.000315 : 3.5e-5 * (V - 19.9) * tc_rcp(EXP((V - 19.9) * (1.0 / 9.0)) - 1.0);
+#if TCB_ION_FOLD
+    u[cxs] = rl_rate(u[cxs], rsqrt(1.0 + EXP((V - 19.9) * (1.0 / -12.7))), 2.0 * (a + b), dt, T);
+#else
     u[cxs] = rl_tau(u[cxs], tc_rcp(sqrt(1.0 + EXP((V - 19.9) * (1.0 / -12.7)))), 0.5 * tc_rcp(a + b), dt, T);
+#endif
     {
       const double ed = EXP((V + 10.0) * (1.0 / -6.24));
       const double td = (V == -10.0) ? 4.579 * tc_rcp(1.0 + ed)
@@ -463,13 +576,14 @@ __device__ __forceinline__ double crn_advance(double V, double* u, double dt, co
     {
       const double ef = EXP(-(V + 28.0) * (1.0 / 6.9));
       const double v10 = V + 10.0;
-      u[cf] = rl_tau(u[cf], ef * tc_rcp(1.0 + ef),
-                     9.0 * tc_rcp(0.0197 * EXP(-0.0337 * 0.0337 * v10 * v10) + 0.02), dt, T);
+      // tau = 9/X
+      u[cf] = CRN_RL_RATE(u[cf], ef * tc_rcp(1.0 + ef),
+                          (0.0197 * EXP(-0.0337 * 0.0337 * v10 * v10) + 0.02) * (1.0 / 9.0));
     }
-    u[cfCa] = rl_tau(u[cfCa], tc_rcp(1.0 + cai * (1.0 / 0.00035)), 2.0, dt, T);
+    u[cfCa] = CRN_RL_RATE(u[cfCa], tc_rcp(1.0 + cai * (1.0 / 0.00035)), 0.5);   // tau = 2 ms
     const double fn = 1000.0 * (1e-15 * P.Vrel * irel - D.fn_c * (0.5 * c.ical - 0.2 * c.inaca));
     const double su = crn_sig(-(fn - 3.4175e-13) * (1.0 / 13.67e-16), T);
-    u[cu] = rl_tau(u[cu], su, P.tauu, dt, T);
+    u[cu] = CRN_RL_RATE(u[cu], su, D.inv_tauu);
     u[cv] = rl_tau(u[cv], 1.0 - crn_sig(-(fn - 6.835e-14) * (1.0 / 13.67e-16), T), 1.91 + 2.09 * su, dt, T);
     const double ew = EXP(-(V - 7.9) * (1.0 / 5.0));
     const double tw = (V == 7.9) ? 6.0 * 0.2 / 1.3 : 6.0 * (1.0 - ew) * tc_rcp((1.0 + 0.3 * ew) * (V - 7.9));
