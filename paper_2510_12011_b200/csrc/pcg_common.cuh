@@ -205,11 +205,44 @@ __device__ __forceinline__ void for_slices(SlicePipe& P, const int64_t* sp, cons
   }
 }
 
+// TCB_STAGED_BATCH = 1: the staged row product issues every gather of a row at
+// once (NB slots in flight, as the latency variant 4 does from global memory):
+// with values and indices already in shared memory the row costs one L2 round
+// trip.  0: an unroll-8 slot loop.
+#ifndef TCB_STAGED_BATCH
+#define TCB_STAGED_BATCH 0
+#endif
+template <bool FIRST, int NB>
+__device__ __forceinline__ double row_Ap_staged_batch(int w, int lane, const double* As, const int* Cs,
+                                                      const double* z, const double* pold, double beta) {
+  double sum = 0.0;
+#pragma unroll 1
+  for (int k0 = 0; k0 < w; k0 += NB) {
+    double av[NB], g[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int kk = min(k0 + j, w - 1);
+      const int64_t t = sell_slot(0, w, kk, lane);
+      const int c = Cs[t];
+      av[j] = As[t];
+      g[j] = FIRST ? z[c] : z[c] + beta * pold[c];
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (k0 + j < w) sum += av[j] * g[j];
+  }
+  return sum;
+}
+
 // q_i = sum_k A_ik p_c, p_c = z_c (+ beta pold_c); slots accumulated in
 // ascending order (the CSR order).  Staged: operands from shared memory.
 template <bool FIRST>
 __device__ __forceinline__ double row_Ap_staged(int w, int lane, const double* As, const int* Cs,
                                                 const double* z, const double* pold, double beta) {
+#if TCB_STAGED_BATCH
+  if (w <= 8) return row_Ap_staged_batch<FIRST, 8>(w, lane, As, Cs, z, pold, beta);
+  return row_Ap_staged_batch<FIRST, kWMax>(w, lane, As, Cs, z, pold, beta);
+#endif
   double sum = 0.0;
 #pragma unroll 8
   for (int k = 0; k < w; ++k) {
