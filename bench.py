@@ -297,7 +297,7 @@ def main():
     ap.add_argument("--partitions", type=int, default=1, help="row-block partitions on this GPU")
     ap.add_argument("--pcg-variant", type=int, default=-1,
                     help="-1 automatic (default), 0 direct loads, 1 TMA-staged, 2 direct + 16-bit indices, "
-                         "3 L2-resident matrix, 4 all slots of a row in flight")
+                         "3 L2-resident matrix, 4 all slots of a row in flight, 6 single-reduction (Chronopoulos-Gear) PCG")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--preroll", type=int, default=None)

@@ -113,7 +113,11 @@ typedef struct {
                             values + indices fit in L2), 4 every slot of a row in flight
                             at once (latency-bound mid-size systems), 5 the solve as a CUDA
                             graph with a device-driven WHILE node (init, S, U, final
-                            kernels; tc_step only); -1 (default):
+                            kernels; tc_step only), 6 the single-reduction (Chronopoulos-Gear)
+                            recurrence: Algorithm 1's iterates in exact arithmetic with one
+                            grid reduction per iteration (not the paper's order
+                            of operations, so opt-in; single-part grid path only -- partitioned
+                            paths run Algorithm 1); -1 (default):
                             automatic, 4 when the system has at most 4 slices per
                             resident warp of variant 0, else 0 */
   int32_t partitions;    /* row-block partitions of the RCM order held by this context on

@@ -285,7 +285,7 @@ tc_status tc_create(const tc_config* cfg, int device, void* cuda_stream, tc_ctx*
   *out = nullptr;
   if (!(cfg->dt > 0) || !(cfg->theta >= 0 && cfg->theta <= 1) || !(cfg->chi > 0) || !(cfg->cm > 0) ||
       cfg->max_iters < 0 || !(cfg->abs_tol >= 0) || !(cfg->rel_tol >= 0) || cfg->model < 0 ||
-      cfg->model > 3 || cfg->pcg_variant < -1 || cfg->pcg_variant > 5 || cfg->partitions < 1 ||
+      cfg->model > 3 || cfg->pcg_variant < -1 || cfg->pcg_variant > 6 || cfg->partitions < 1 ||
       cfg->partitions > 4096 || cfg->check_every < 1 || cfg->engine < 0 || cfg->engine > 3)
     return TC_EINVAL;
   int ndev = 0;
@@ -973,7 +973,7 @@ static tc_status assemble_host(tc_ctx* c, const std::vector<int32_t>& ereg, std:
       P.pcg_var = cg_pick_variant(c->cfg.pcg_variant, P.nslices, c->device);
       P.grid = P.pcg_var == 5 ? g_grid_size(c->device) : cg_grid_size(1, P.pcg_var, P.nslices, c->device);
     }
-    CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
+    CUDA_TRY(c, dalloc(c, &P.d_part, kPartSlots * (int64_t)P.grid));
   }
   int32_t herr = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -1089,7 +1089,7 @@ static tc_status assemble_device(tc_ctx* c, const std::vector<int32_t>& ereg) {
   if (herr == 2) return fail(c, TC_EINVAL, "assembly: pattern slot missing (internal)");
   P.pcg_var = cg_pick_variant(c->cfg.pcg_variant, P.nslices, c->device);
   P.grid = P.pcg_var == 5 ? g_grid_size(c->device) : cg_grid_size(1, P.pcg_var, P.nslices, c->device);
-  CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
+  CUDA_TRY(c, dalloc(c, &P.d_part, kPartSlots * (int64_t)P.grid));
   return TC_OK;
 }
 
@@ -1264,7 +1264,7 @@ static tc_status assemble_device_parts(tc_ctx* c, const std::vector<int32_t>& er
       return fail(c, TC_ECUDA, std::string("assembly kernel: ") + cudaGetErrorString(le != cudaSuccess ? le : ss));
     }
     P.grid = split_grid(P.nslices);
-    CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
+    CUDA_TRY(c, dalloc(c, &P.d_part, kPartSlots * (int64_t)P.grid));
   }
   int32_t herr = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -1472,6 +1472,8 @@ static CgArgs cg_args(tc_ctx* c, Part& P, double* x) {
   a.up = P.d_up;
   a.vp = P.d_vp;
   a.b = P.d_b;
+  a.e0 = P.d_up;   // variant 6's sigma buffers: u', v' are read only by the RHS
+  a.e1 = P.d_vp;
   a.part = P.d_part;
   a.eps_a = c->cfg.abs_tol;
   a.eps_r = c->cfg.rel_tol;
@@ -1983,9 +1985,9 @@ static tc_status enqueue_steps(tc_ctx* c, int64_t nsteps, tc_step_stat* dstats, 
         ca.n_rpart = c->co_grid;
         CUDA_TRY(c, launch_pcg(1, c->co_var, ca, c->co_grid, c->stream));
         c->launches += 2;
-      } else if (P.pcg_var == 4 && TCB_FUSE_RHS4) {   // RHS inside the cooperative kernel
+      } else if ((P.pcg_var == 4 || P.pcg_var == 6) && TCB_FUSE_RHS4) {   // RHS inside the cooperative kernel
         ca.fuse_rhs = 1;
-        CUDA_TRY(c, launch_pcg_only(1, 4, ca, P.grid, c->stream));
+        CUDA_TRY(c, launch_pcg_only(1, P.pcg_var, ca, P.grid, c->stream));
         c->launches += 1;
       } else {
         CUDA_TRY(c, launch_pcg(1, P.pcg_var, ca, P.grid, c->stream));
@@ -2404,7 +2406,7 @@ tc_status tc_csr_upload(tc_ctx* c, int32_t n, int64_t nnz, const int32_t* rowptr
   P.pcg_var = cg_pick_variant(c->cfg.pcg_variant, P.nslices, c->device);
   if (P.pcg_var == 5) P.pcg_var = 0;   // the graph engine serves tc_step only
   P.grid = cg_grid_size(0, P.pcg_var, P.nslices, c->device);
-  CUDA_TRY(c, dalloc(c, &P.d_part, 2 * (int64_t)P.grid));
+  CUDA_TRY(c, dalloc(c, &P.d_part, kPartSlots * (int64_t)P.grid));
   TC_TRY(ensure_stats(c, 1));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->csr_mode = true;
@@ -2888,7 +2890,7 @@ tc_status tc_cohort_step(tc_cohort* co, int64_t nsteps, tc_step_stat* stats) {
         c->co_var = cg_pick_variant_share(c->cfg.pcg_variant, P.nslices, c->device, share);
         c->co_grid = cg_grid_size_share(c->co_var, P.nslices, c->device, share);
         if (c->co_grid > P.grid && c->co_part_cap < c->co_grid) {   // partials: 2 x grid
-          if (dalloc(c, &c->d_co_part, 2 * (int64_t)c->co_grid) != cudaSuccess) sbig[b] = TC_ENOMEM;
+          if (dalloc(c, &c->d_co_part, kPartSlots * (int64_t)c->co_grid) != cudaSuccess) sbig[b] = TC_ENOMEM;
           else c->co_part_cap = c->co_grid;
         }
       }

@@ -141,7 +141,10 @@ struct CgArgs {
   const double2* rpart;  // PCG kernel: the RHS partials it sums first (default part) ...
   int32_t n_rpart;       // ... and how many (default gridDim.x)
   int32_t fuse_rhs;      // PCG kernel, variant 4: compute the RHS itself first (one launch per solve)
+  double* e0;            // variant 6: the two sigma buffers (u', v' of the RHS: free once r_0 is formed)
+  double* e1;
 };
+constexpr int kPartSlots = 4;  // double2 partial-sum slots per CTA (variant 6: two regions of 2 per CTA)
 
 // ---- split-phase (partitioned) PCG: device scalar state of Algorithm 1 -----
 struct Scalars {

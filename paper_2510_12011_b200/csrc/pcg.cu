@@ -151,6 +151,31 @@ __global__ void __launch_bounds__(kCgThreads, VAR == 1 ? TCB_MINB(1) : VAR == 4 
   if (threadIdx.x == 0) a.part[blockIdx.x] = b;
 }
 
+// Variant 4's RHS as the first phase of the cooperative kernel (fuse_rhs): the
+// batched row product r_0 = A u' - K v', z_0, per-CTA partials, grid barrier.
+__device__ __forceinline__ void rhs_phase_batch(const CgArgs& a, int gw, int nw, int lane, double2* sh,
+                                                cg::grid_group& grid) {
+  const int64_t* __restrict__ sp = a.slice_ptr;
+  double2 acc0 = make_double2(0.0, 0.0);
+  for (int s = a.s0 + gw; s < a.s1; s += nw) {
+    const int64_t base = __ldg(sp + s);
+    const int w = (int)((__ldg(sp + s + 1) - base) >> 5);
+    const int64_t i = (int64_t)s * kSellC + lane;
+    const double sum = (TCB_BATCH_SMALL && w <= 8)
+                           ? row_rhs_batch<8>(base, w, lane, a.col, a.A, a.K, a.up, a.vp)
+                           : row_rhs_batch<(TCB_RHS_BATCH_NB > 0 ? TCB_RHS_BATCH_NB : 1)>(base, w, lane, a.col, a.A,
+                                                                                           a.K, a.up, a.vp);
+    const double zi = __ldg(a.dinv + i) * sum;
+    if (a.store_r) a.r[i] = sum;
+    a.z[i] = zi;
+    acc0.x += sum * zi;
+    acc0.y += zi * zi;
+  }
+  const double2 b0 = block_sum2(acc0, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = b0;
+  grid.sync();
+}
+
 // Algorithm 1's loop from r_0, z_0 and the RHS kernel's partials.
 template <int MODE, int VAR>
 __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a) {
@@ -188,26 +213,7 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
   // product), then a grid barrier -- one launch and one kernel boundary per
   // solve fewer (mid-size systems are launch-latency sensitive) --------------
   if constexpr (BATCH && MODE == 1) {
-    if (a.fuse_rhs) {
-      double2 acc0 = make_double2(0.0, 0.0);
-      for (int s = a.s0 + gw; s < a.s1; s += nw) {
-        const int64_t base = __ldg(sp + s);
-        const int w = (int)((__ldg(sp + s + 1) - base) >> 5);
-        const int64_t i = (int64_t)s * kSellC + lane;
-        const double sum = (TCB_BATCH_SMALL && w <= 8)
-                               ? row_rhs_batch<8>(base, w, lane, col, Av, a.K, a.up, a.vp)
-                               : row_rhs_batch<(TCB_RHS_BATCH_NB > 0 ? TCB_RHS_BATCH_NB : 1)>(base, w, lane, col, Av,
-                                                                                               a.K, a.up, a.vp);
-        const double zi = __ldg(dinv + i) * sum;
-        if (a.store_r) a.r[i] = sum;
-        a.z[i] = zi;
-        acc0.x += sum * zi;
-        acc0.y += zi * zi;
-      }
-      const double2 b0 = block_sum2(acc0, sh);
-      if (threadIdx.x == 0) a.part[blockIdx.x] = b0;
-      grid.sync();
-    }
+    if (a.fuse_rhs) rhs_phase_batch(a, gw, nw, lane, sh, grid);
   }
   // ---- rho_0 = r.z, ||z_0|| from the RHS kernel's per-CTA partials ------------
   double2 tot;
@@ -387,6 +393,192 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
   }
 }
 
+// ------------------------------------------------------------------ variant 6
+// Single-reduction PCG (Chronopoulos & Gear's recurrence; SURVEY 8(e) "optional
+// ... not the paper's algorithm, behind a flag and parity-checked";
+// tc_config.pcg_variant = 6): the iterates of Algorithm 1 in exact arithmetic,
+// with the two inner products of an iteration in one reduction, so ONE grid
+// barrier per iteration instead of two.  Jacobi-preconditioned, z-form:
+//   u = D^-1 r (Alg. 1's z), t = D^-1 A u, sigma = D^-1 A p;
+//   init:  t_0 = D^-1 A u_0,  gamma_0 = r_0.u_0,  delta_0 = (A u_0).u_0,  alpha_0 = gamma_0/delta_0
+//   phase i (one pass over the rows, then the reduction):
+//     sigma_i = t_i + beta_i sigma_{i-1}     p_i = u_i + beta_i p_{i-1}
+//     u_{i+1} = u_i - alpha_i sigma_i        x_{i+1} = x_i + alpha_i p_i
+//     w = A u_{i+1} (the gathered u_{i+1} of a neighbour is formed on the fly from
+//       its u_i, t_i, sigma_{i-1} by the same expression its owner uses: bitwise equal)
+//     t_{i+1} = D^-1 w;  partials gamma_{i+1} = sum u^2/D^-1, delta_{i+1} = w.u, |u_{i+1}|^2
+//   then Alg. 1's stopping test on |u_{i+1}| = |z_{i+1}| (readings C1-C3), and
+//     beta_{i+1} = gamma_{i+1}/gamma_i,  alpha_{i+1} = gamma_{i+1}/(delta_{i+1} - beta_{i+1} gamma_{i+1}/alpha_i).
+// u, t and sigma are gathered while being rewritten, so each has two buffers
+// (u: z / r, t: q / p1, sigma: e0 / e1); p and x are own-row only (in place).
+// Bytes per iteration 12 nnz + 4(n+1) + 88 n (vs 72 n); for latency-bound
+// mid-size systems, where a grid barrier and a phase ramp cost more than that.
+#ifndef TCB_1R_NB
+#define TCB_1R_NB 8   // slots in flight per row (three gathers each)
+#endif
+__device__ __forceinline__ double u_next(double u, double t, double so, double alpha, double beta, bool first,
+                                         double& sig) {
+  sig = first ? t : fma(beta, so, t);
+  return fma(-alpha, sig, u);
+}
+
+template <bool FIRST, int NB>
+__device__ __forceinline__ double row_Au_next(int64_t base, int w, int lane, const int* col, const double* A,
+                                              const double* u, const double* t, const double* so,
+                                              double alpha, double beta) {
+  double sum = 0.0;
+#pragma unroll 1
+  for (int k0 = 0; k0 < w; k0 += NB) {
+    double av[NB], g[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int kk = min(k0 + j, w - 1);
+      const int64_t ts = sell_slot(base, w, kk, lane);
+      const int c = ld_mat(col + ts);
+      av[j] = ld_mat(A + ts);
+      double sig;
+      g[j] = u_next(u[c], t[c], FIRST ? 0.0 : so[c], alpha, beta, FIRST, sig);
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (k0 + j < w) sum += av[j] * g[j];
+  }
+  return sum;
+}
+
+// Deterministic grid sum of three values (two double2 slots per CTA per call;
+// the caller alternates buf between two 2 x gridDim.x regions).
+__device__ __forceinline__ double3 grid_sum3(double3 v, double2* buf, double2* sh, cg::grid_group& grid) {
+  const double2 b01 = block_sum2(make_double2(v.x, v.y), sh);
+  const double2 b2 = block_sum2(make_double2(v.z, 0.0), sh);
+  if (threadIdx.x == 0) {
+    buf[blockIdx.x] = b01;
+    buf[gridDim.x + blockIdx.x] = b2;
+  }
+  grid.sync();
+  double2 acc01 = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) {
+    const double2 p = buf[t], q = buf[gridDim.x + t];
+    acc01.x += p.x;
+    acc01.y += p.y;
+    acc2.x += q.x;
+  }
+  const double2 s01 = block_sum2(acc01, sh);
+  const double2 s2 = block_sum2(acc2, sh);
+  return make_double3(s01.x, s01.y, s2.x);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kCgThreads, 1) pcg1r_kernel(CgArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double2 sh[kCgWarps];
+  if (a.flags[0]) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kCgWarps + warp;
+  const int nw = gridDim.x * kCgWarps;
+  const int32_t ns = a.nslices;
+  const int64_t* __restrict__ sp = a.slice_ptr;
+  const int* __restrict__ col = a.col;
+  const double* __restrict__ Av = a.A;
+  const double* __restrict__ dinv = a.dinv;
+  if constexpr (MODE == 1) {
+    if (a.fuse_rhs) rhs_phase_batch(a, gw, nw, lane, sh, grid);
+  }
+  // u_i in (z, r)[i & 1], t_i in (q, p1)[i & 1], sigma_i in (e0, e1)[i & 1]
+  double* __restrict__ p = a.p0;
+  double2* part = a.part;         // 4 x gridDim.x slots: two regions of 2 x gridDim.x
+
+  // gamma_0 = r_0.z_0, |z_0| from the RHS partials
+  double2 tot;
+  {
+    double2 acc0 = make_double2(0.0, 0.0);
+    for (int t = threadIdx.x; t < a.n_rpart; t += blockDim.x) {
+      const double2 u = a.rpart[t];
+      acc0.x += u.x;
+      acc0.y += u.y;
+    }
+    tot = block_sum2(acc0, sh);
+  }
+  double gamma = tot.x;
+  double zeta = sqrt(tot.y);
+  double zref = zeta;
+  int it = 0, conv = 0, nan = 0;
+  if (isnan(gamma) || isnan(zeta)) nan = 1;
+  if (!nan && zeta < a.eps_a) conv = 1;  // reading C4: return x0
+  if (!nan && !conv) {
+    // init: t_0 = D^-1 A u_0, delta_0 = (A u_0).u_0
+    double2 acc = make_double2(0.0, 0.0);
+    for (int s = gw; s < ns; s += nw) {
+      const int64_t base = __ldg(sp + s);
+      const int w = (int)((__ldg(sp + s + 1) - base) >> 5);
+      const int64_t i = (int64_t)s * kSellC + lane;
+      const double wi = row_Ap_batch_w<true>(base, w, lane, col, Av, a.z, nullptr, 0.0);
+      a.q[i] = __ldg(dinv + i) * wi;
+      acc.x += wi * a.z[i];
+    }
+    // the RHS partials live in part[0, grid): this sum uses the second region
+    tot = grid_sum2(acc, part + 2 * gridDim.x, sh, grid);
+    const double delta0 = tot.x;
+    if (isnan(delta0)) nan = 1;
+    double alpha = gamma / delta0, beta = 0.0;
+    for (it = 0; !nan && it < a.max_iters;) {
+      const int c = it & 1;
+      const double* __restrict__ u = c ? a.r : a.z;
+      const double* __restrict__ t = c ? a.p1 : a.q;
+      const double* __restrict__ so = c ? a.e0 : a.e1;   // sigma_{it-1}
+      double* __restrict__ un = c ? a.z : a.r;
+      double* __restrict__ tn = c ? a.q : a.p1;
+      double* __restrict__ sn = c ? a.e1 : a.e0;         // sigma_it
+      double3 acc3 = make_double3(0.0, 0.0, 0.0);
+      for (int s = gw; s < ns; s += nw) {
+        const int64_t base = __ldg(sp + s);
+        const int w = (int)((__ldg(sp + s + 1) - base) >> 5);
+        const int64_t i = (int64_t)s * kSellC + lane;
+        const double wi = it == 0 ? row_Au_next<true, TCB_1R_NB>(base, w, lane, col, Av, u, t, so, alpha, beta)
+                                  : row_Au_next<false, TCB_1R_NB>(base, w, lane, col, Av, u, t, so, alpha, beta);
+        const double ui = u[i], di = __ldg(dinv + i);
+        double sig;
+        const double un_i = u_next(ui, t[i], it == 0 ? 0.0 : so[i], alpha, beta, it == 0, sig);
+        const double pi = it == 0 ? ui : ui + beta * p[i];
+        p[i] = pi;
+        a.x[i] = a.x[i] + alpha * pi;
+        sn[i] = sig;
+        un[i] = un_i;
+        tn[i] = di * wi;
+        acc3.x += di != 0.0 ? un_i * (un_i / di) : 0.0;   // r.z = sum z^2 / D^-1 (z-form)
+        acc3.y += wi * un_i;
+        acc3.z += un_i * un_i;
+      }
+      const double3 r3 = grid_sum3(acc3, part + (c ? 2 * gridDim.x : 0), sh, grid);
+      ++it;
+      const double zeta_new = sqrt(r3.z);
+      zeta = zeta_new;
+      if (isnan(zeta_new) || isnan(r3.x) || isnan(r3.y)) { nan = 1; break; }
+      if (zeta_new < a.eps_a || zeta_new / zref < a.eps_r) { conv = 1; break; }
+      const double beta_n = r3.x / gamma;                       // gamma_{i+1} / gamma_i
+      const double den = r3.y - beta_n * r3.x / alpha;          // = p_{i+1}.A p_{i+1}
+      alpha = r3.x / den;
+      if (isnan(alpha)) { nan = 1; break; }
+      beta = beta_n;
+      gamma = r3.x;
+      if (a.rel_mode == 0) zref = zeta_new;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.stat->iters = it;
+    a.stat->converged = conv;
+    a.stat->znorm = zeta;
+    int32_t* f = a.flags;
+    if (nan) {
+      f[0] = 1; f[1] = 1; f[4] = a.step_tag;
+    } else {
+      f[2] = conv ? 0 : f[2] + 1;
+      if (f[3] > 0 && f[2] >= f[3]) { f[0] = 1; f[4] = a.step_tag; }
+    }
+  }
+}
+
+
 __global__ void spmv_kernel(const int64_t* __restrict__ sp, const int* __restrict__ col,
                             const double* __restrict__ Av, int32_t ns, const double* __restrict__ x,
                             double* __restrict__ y) {
@@ -419,13 +611,14 @@ static int sm_count(int dev) {
 }
 
 static const void* rhs_fn(int mode, int variant) {
-  if (variant == 4) return mode == 1 ? (const void*)rhs_kernel<1, 4> : (const void*)rhs_kernel<0, 4>;
+  if (variant == 4 || variant == 6) return mode == 1 ? (const void*)rhs_kernel<1, 4> : (const void*)rhs_kernel<0, 4>;
   if (variant == 3) return mode == 1 ? (const void*)rhs_kernel<1, 3> : (const void*)rhs_kernel<0, 3>;
   if (variant == 1) return mode == 1 ? (const void*)rhs_kernel<1, 1> : (const void*)rhs_kernel<0, 1>;
   if (variant == 2) return mode == 1 ? (const void*)rhs_kernel<1, 2> : (const void*)rhs_kernel<0, 2>;
   return mode == 1 ? (const void*)rhs_kernel<1, 0> : (const void*)rhs_kernel<0, 0>;
 }
 static const void* pcg_fn(int mode, int variant) {
+  if (variant == 6) return mode == 1 ? (const void*)pcg1r_kernel<1> : (const void*)pcg1r_kernel<0>;
   if (variant == 4) return mode == 1 ? (const void*)pcg_kernel<1, 4> : (const void*)pcg_kernel<0, 4>;
   if (variant == 3) return mode == 1 ? (const void*)pcg_kernel<1, 3> : (const void*)pcg_kernel<0, 3>;
   if (variant == 1) return mode == 1 ? (const void*)pcg_kernel<1, 1> : (const void*)pcg_kernel<0, 1>;

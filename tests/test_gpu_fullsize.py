@@ -218,7 +218,7 @@ def test_fullsize_whole_oracle_step(T, name):
 @pytest.mark.parametrize("case,variant,parts,peer", [("configs2", -1, 1, 1), ("configs2", 0, 1, 1),
                                                      ("configs2", 1, 1, 1), ("slab1.28M_tt", -1, 1, 1),
                                                      ("slab1.28M_tt", 1, 1, 1), ("biv416k_tt", -1, 1, 1),
-                                                     ("biv416k_tt", 0, 1, 1),
+                                                     ("biv416k_tt", 0, 1, 1), ("configs2", 6, 1, 1),
                                                      ("slab1.28M_tt", -1, 4, 1), ("slab1.28M_tt", -1, 3, 0),
                                                      ("biv416k_tt", -1, 4, 1)])
 def test_multislice_full_oracle_step(T, case, variant, parts, peer):

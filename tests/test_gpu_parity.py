@@ -541,7 +541,7 @@ def test_torch_allocator_hook(T):
         T.tc_destroy(ctx)
 
 
-@pytest.mark.parametrize("case", ["grid_v0", "grid_v1", "grid_v2", "grid_v4", "grid_v5", "parts2_peer",
+@pytest.mark.parametrize("case", ["grid_v0", "grid_v1", "grid_v2", "grid_v4", "grid_v5", "grid_v6", "parts2_peer",
                                   "parts3_split", "parts5_peer_host", "sphere_parts3", "biv_parts4", "mms_parts2",
                                   "cluster"])
 def test_index_audit(T, case):
