@@ -33,10 +33,11 @@ for W in slab10M_tt slab10M_crn; do
   ncu --set full --clock-control none --import-source on -k regex:"pcg_kernel|rhs_kernel|ionic_" -s 1509 -c 3 \
       -o gpurun_out/${R}_full_$W $E > gpurun_out/${R}_ncu_full_$W.log 2>&1
 done
-# configs[2]: rhs + pcg of the first timed step (latency variant 4 under the automatic choice)
+# configs[2]: ionic + pcg of the first timed step (latency variant 4 under the automatic
+# choice, RHS fused into the PCG kernel: two launches per step, 503 steps before)
 E="python bench.py --workload nversion_dx0.1_tt --steps 2 --warmup 3 --windows 1 --no-cpu-baseline --e2e-steps 1"
 $E > gpurun_out/${R}_plain_nversion01.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"pcg_kernel|rhs_kernel|ionic_" -s 1509 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"pcg_kernel|rhs_kernel|ionic_" -s 1006 -c 2 \
     -o gpurun_out/${R}_full_nversion01 $E > gpurun_out/${R}_ncu_full_nversion01.log 2>&1
 # the N>1 leg at world size 1 (torchrun, peer-memory PCG with an NCCL communicator of 1)
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
