@@ -34,6 +34,8 @@ def main():
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     data = json.load(open(p)) if os.path.exists(p) else {}
     data[wl] = {"rhs_bytes": rhs, "pcg_bytes": pcg, "iters": iters, "capture": summ}
+    if rhs == 0.0:   # variant 4 with the RHS fused into the PCG kernel: pcg_bytes holds both
+        data[wl]["rhs_fused"] = True
     json.dump(data, open(p, "w"), indent=1)
     print(wl, data[wl])
 
