@@ -9,7 +9,10 @@
 //   U: alpha = rho / p.q;  z -= alpha q / diag(A) (z-form: r = diag(A) z is
 //      not stored);  partials r.z = sum z^2 diag(A), z.z;
 //      then every CTA evaluates the stopping test of Alg. 1 identically.
-// Two memory pipelines (measured side by side):
+// Memory pipelines (tc_config.pcg_variant, measured side
+// by side): 0 direct, 1 TMA-staged, 2 16-bit offsets, 3 L2-kept matrix, 4 every
+// slot of a row in flight (mid-size), 5 the CUDA-graph engine (pcg_graph.cu), and
+// 6 the opt-in single-reduction recurrence (pcg1r_kernel below).  The first two:
 //  * DIRECT (default, variant 0): 32 registers/thread, 64 warps/SM; every warp
 //    streams its slice's values and column indices with evict-first loads and
 //    gathers the vectors from L1/L2; latency is hidden by occupancy.

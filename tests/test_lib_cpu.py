@@ -79,3 +79,23 @@ def test_product_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "oracle.h" not in src and "liboracle" not in src, f
+
+
+def test_create_validates_config_before_any_device_work(lib):
+    """tc_create rejects an out-of-range configuration with TC_EINVAL before it
+    touches a device (include/tcb200.h "Errors"); a valid one -- every PCG
+    variant -1..6, including the opt-in single-reduction 6 -- gets past the
+    check and, on a box without a GPU, fails with TC_ECUDA (no CPU fallback)."""
+    import torch
+    import paper_2510_12011_b200 as T
+    for bad in (dict(pcg_variant=7), dict(pcg_variant=-2), dict(dt=0.0), dict(theta=1.5), dict(partitions=0),
+                dict(model=9), dict(max_iters=-1)):
+        with pytest.raises(T.TcError) as e:
+            T.tc_create(T.tc_config_default(**bad))
+        assert e.value.status == T.TC_EINVAL, bad
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present: the valid configurations would create contexts")
+    for v in range(-1, 7):
+        with pytest.raises(T.TcError) as e:
+            T.tc_create(T.tc_config_default(pcg_variant=v))
+        assert e.value.status == T.TC_ECUDA, v
