@@ -313,6 +313,12 @@ __device__ __forceinline__ ColIdx col_of(const CgArgs& a, int64_t i, int64_t bas
   return ci;
 }
 
+// TCB_COMP_SHFL = 1 (experiment): variant 2's per-(slice, slot) column bases are
+// loaded once per slice (lane k holds slot k's) and broadcast with a shuffle,
+// instead of one broadcast load per slot.
+#ifndef TCB_COMP_SHFL
+#define TCB_COMP_SHFL 0
+#endif
 #ifndef TCB_ROW_BATCH
 #define TCB_ROW_BATCH 0   // 0: unroll-4 loop; N > 0: slots in batches of N with clamped indices
 #endif
@@ -377,6 +383,19 @@ __device__ __forceinline__ double row_Ap_stream(int64_t base, int w, int lane, c
       const int64_t t = base + (int64_t)kSellC * (w - 1) + lane;
       const int c = ld_mat(ci.c32 + t);
       sum += ld_mat(A + t) * (FIRST ? z[c] : z[c] + beta * pold[c]);
+    }
+    return sum;
+  }
+#endif
+#if TCB_COMP_SHFL
+  if (ci.c16 && w <= kSellC) {  // variant 2: the slice's per-slot bases held one per lane, broadcast by shuffle
+    const int kbl = lane < w ? __ldg(ci.kb + lane) : 0;
+#pragma unroll 4
+    for (int k = 0; k < w; ++k) {
+      const int64_t t = sell_slot(base, w, k, lane);
+      const int c = __shfl_sync(0xffffffffu, kbl, k) + (int)ld_mat(ci.c16 + t);
+      const double g = FIRST ? z[c] : z[c] + beta * pold[c];
+      sum += ld_mat(A + t) * g;
     }
     return sum;
   }
