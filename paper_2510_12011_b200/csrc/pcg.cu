@@ -54,6 +54,13 @@ namespace tcb {
 #if TCB_VEC_U && TCB_ZFORM
 #error "TCB_VEC_U has only the r-form U phase: build it with -DTCB_ZFORM=0"
 #endif
+template <bool ODD>
+struct ParityTag {  // compile-time iteration parity (bool(tag) folds to a constant)
+  __device__ constexpr operator bool() const { return ODD; }
+};
+#ifndef TCB_S_PARITY
+#define TCB_S_PARITY 1   // the S phase compiled once per p-buffer parity (0: one copy, runtime parity)
+#endif
 #ifndef TCB_BATCH_UU
 #define TCB_BATCH_UU 1    // slices per warp pass in variant 4's U phase (measured 1 < 2 < 4)
 #endif
@@ -258,12 +265,15 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
                      acc.x += pi * sum;
                    });
       } else {
+        // S of iteration it >= 1 with p_it -> pn, p_{it-1} -> po_ (TCB_S_PARITY: one
+        // copy per parity, so both are kernel-parameter pointers, not registers)
+        auto s_iter = [&](double* __restrict__ pnew, const double* __restrict__ pold, auto odd) {
         for_slices<TMA>(P, sp, Av, col, ns, gw, nw, lane,
                    [&](int64_t i, int64_t base, int w, bool staged, const double* As, const int* Cs) {
                      const double po = pold[i];
                      const double pi = a.z[i] + beta * po;
 #if TCB_XMERGE
-                     if (!(it & 1)) {   // even it >= 2: p_{it-2} (still in pnew) and p_{it-1}, in order
+                     if (!bool(odd)) {   // even it >= 2: p_{it-2} (still in pnew) and p_{it-1}, in order
                        const double xi = a.x[i], p2 = pnew[i];
                        a.x[i] = (xi + alpha_prev * p2) + alpha * po;
                      }
@@ -278,6 +288,13 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
                      a.q[i] = sum;
                      acc.x += pi * sum;
                    });
+        };
+        if (TCB_S_PARITY) {
+          if (it & 1) s_iter(a.p1, a.p0, ParityTag<true>{});
+          else s_iter(a.p0, a.p1, ParityTag<false>{});
+        } else {
+          s_iter(pnew, pold, (bool)(it & 1));
+        }
       }
       last_valid = true;
       tot = grid_sum2(acc, partB, sh, grid);

@@ -313,6 +313,10 @@ __device__ __forceinline__ ColIdx col_of(const CgArgs& a, int64_t i, int64_t bas
   return ci;
 }
 
+// Unroll of the direct variant's slot loop (experiment; 4 = default).
+#ifndef TCB_S_UNROLL
+#define TCB_S_UNROLL 4
+#endif
 // TCB_COMP_SHFL = 1 (experiment): variant 2's per-(slice, slot) column bases are
 // loaded once per slice (lane k holds slot k's) and broadcast with a shuffle,
 // instead of one broadcast load per slot.
@@ -400,7 +404,15 @@ __device__ __forceinline__ double row_Ap_stream(int64_t base, int w, int lane, c
     return sum;
   }
 #endif
+#if TCB_S_UNROLL == 2
+#pragma unroll 2
+#elif TCB_S_UNROLL == 3
+#pragma unroll 3
+#elif TCB_S_UNROLL == 8
+#pragma unroll 8
+#else
 #pragma unroll 4
+#endif
   for (int k = 0; k < w; ++k) {
     const int64_t t = sell_slot(base, w, k, lane);
     const int c = ci(t, k);
