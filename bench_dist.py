@@ -124,7 +124,7 @@ def main(args, w):
             "cpu_baseline": None,
             "e2e": {"value": n * ke / e2e_s, "unit": "node-steps/s",
                     "h2d_bytes_per_step": int(hin.nbytes), "d2h_bytes_per_step": int(hout.nbytes)},
-            "gpu_launches": prof["launches"],
+            "gpu_launches": int(round(prof["launches"])),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

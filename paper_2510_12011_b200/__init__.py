@@ -322,7 +322,7 @@ def tc_profile_read(ctx, reset: bool = False):
     out = np.zeros(6)
     _check(ctx, _L.tc_profile_read(ctx, _ptr(out), int(reset)))
     return dict(ionic_ms=out[0], pcg_ms=out[1], other_ms=out[2], iters=out[3], steps=out[4],
-                launches=int(out[5]))
+                launches=float(out[5]))   # kernel launches (cohort members' shares of a cluster launch are fractions)
 
 
 def tc_matrix_info(ctx) -> dict:
