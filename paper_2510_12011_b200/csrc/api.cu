@@ -689,7 +689,7 @@ static tc_status setup_peer(tc_ctx* c, const std::vector<PartPlan>& plans) {
   if (c->use_comm && !c->d_sync) CUDA_TRY(c, dalloc(c, &c->d_sync, 1));
   for (Part& P : c->parts) {
     CUDA_TRY(c, dalloc(c, &P.d_inbox, (int64_t)inbox_bytes(world)));
-    CUDA_TRY(c, dalloc(c, &P.d_bar, 2));
+    CUDA_TRY(c, dalloc(c, &P.d_bar, 4));   // {barrier count, generation, halo push count, pad}
     CUDA_TRY(c, dalloc(c, &P.d_epoch, 2));
     CUDA_TRY(c, dalloc(c, &P.d_red0, 1));
     CUDA_TRY(c, dalloc(c, &P.d_ppart, 2 * (int64_t)std::max(std::max(bpg, bpg_rhs), 1)));
@@ -796,6 +796,7 @@ static tc_status setup_peer(tc_ctx* c, const std::vector<PartPlan>& plans) {
     X.myred = inbox_red(P.d_inbox);
     X.bar_count = P.d_bar;
     X.bar_gen = P.d_bar + 1;
+    X.push_count = P.d_bar + 2;
     X.epoch = P.d_epoch;
     X.red0 = P.d_red0;
     X.rank = gid;

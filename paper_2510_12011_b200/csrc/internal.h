@@ -27,7 +27,10 @@ namespace tcb {
 // ---------------------------------------------------------------------------
 constexpr int kSellC = 32;
 constexpr int kAutoBatch = 4;          // PCG variant 4 up to this many slices per resident warp (pcg.cu)
-constexpr int kPeerThreadsHost = 256;  // threads per CTA of the peer-memory PCG kernels (pcg_peer.cu)
+#ifndef TCB_PEER_THREADS
+#define TCB_PEER_THREADS 256
+#endif
+constexpr int kPeerThreadsHost = TCB_PEER_THREADS;  // threads per CTA of the peer-memory PCG kernels (pcg_peer.cu)
 #ifndef TCB_SELL_PAIRS
 #define TCB_SELL_PAIRS 0
 #endif
@@ -215,6 +218,7 @@ struct XPart {
   RedSlot* myred;
   unsigned int* bar_count;
   unsigned int* bar_gen;
+  unsigned int* push_count;       // arrive-only halo pushes of the running launch (pcg_peer.cu)
   unsigned long long* epoch;      // [0] epoch counter, [1] cross-rank reductions done
   double2* red0;                  // rho_0, ||z_0||^2 handed from the RHS kernel to the loop
   int32_t rank, world;

@@ -164,9 +164,23 @@ __device__ __forceinline__ double2 cross_sum2(const XPart& X, double2 v, unsigne
 
 // Remote halo: for send entry j, value(j) lands in neighbour send_nbr[j]'s ghost
 // region of the vector selected by `which` (0 z, 1 u', 2 v'); then the flags.
+// TCB_PEER_PUSH_ARRIVE = 1 (experiment, off): arrive-only -- every CTA fences its stores
+// and increments the group's push counter; the LAST CTA to arrive (it sees the
+// count of this launch's push `npush` complete) fences and stores the flags, and
+// nobody waits (0: a full group barrier, then CTA 0 stores the flags).  Ordering:
+// each CTA's remote stores -> fence.sys -> counter RMW; the last RMW -> fence.sys
+// -> flag stores, so a neighbour that sees the flag sees every CTA's data (and a
+// later push's flag can never land before an earlier one's: the thread that
+// stored the earlier flag fences before its next counter RMW).  The counter is
+// reset by CTA 0 after the launch's final group barrier.  Measured neutral on one
+// GPU (emulated partitions, world 1: profiles/r02ap_exp_peer_sync.txt), so the
+// barrier version -- the one exercised since r01 -- stays the default.
+#ifndef TCB_PEER_PUSH_ARRIVE
+#define TCB_PEER_PUSH_ARRIVE 0
+#endif
 template <class ValF>
 __device__ __forceinline__ void halo_push(const XPart& X, int which, unsigned long long epoch, int lb,
-                                          int nb, ValF val) {
+                                          int nb, unsigned int& npush, ValF val) {
   bool wrote = false;
   for (int64_t j = (int64_t)lb * blockDim.x + threadIdx.x; j < X.n_send; j += (int64_t)nb * blockDim.x) {
     const int q = X.send_nbr[j];
@@ -175,8 +189,24 @@ __device__ __forceinline__ void halo_push(const XPart& X, int which, unsigned lo
     wrote = true;
   }
   if (wrote) __threadfence_system();   // this thread's remote stores before the flag
+#if TCB_PEER_PUSH_ARRIVE
+  if (X.nbr_count > 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const unsigned int old = atomicAdd(X.push_count, 1u);
+      if (old == (npush + 1u) * (unsigned int)nb - 1u) {   // every CTA of the group has pushed
+        __threadfence_system();
+        for (int q = 0; q < X.nbr_count; ++q) vstore(X.rflag[q], epoch);
+      }
+    }
+  }
+  ++npush;
+#else
+  (void)npush;
   group_barrier(X, nb);
   if (lb == 0 && threadIdx.x < X.nbr_count) vstore(X.rflag[threadIdx.x], epoch);
+#endif
 }
 
 // Per-warp halo wait (no CTA barrier): lane 0 polls the flags, then the fence
@@ -202,7 +232,7 @@ __device__ __forceinline__ void halo_wait(const XPart& X, unsigned long long epo
 // r_0 = A u' - K v' (== b - A x_0), z_0, and the cross-rank
 // sums rho_0, ||z_0||^2 -> X.red0.  Own launch (64 registers); cooperative so
 // that every group's CTAs are resident while they wait for their neighbours.
-__global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_constant__ PeerRun R) {
+__global__ void __launch_bounds__(kPeerThreads, 1024 / kPeerThreads) rhs_peer_kernel(const __grid_constant__ PeerRun R) {
   __shared__ double2 sh[kPeerWarps];
   __shared__ double2 sh1;
   const int group = blockIdx.x / R.bpg;
@@ -214,10 +244,11 @@ __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_
   const int gw = lb * kPeerWarps + (threadIdx.x >> 5), nw = nb * kPeerWarps;
   unsigned long long ep = X.epoch[0];
   unsigned long long nrx = X.epoch[1];
+  unsigned int npush = 0;   // halo pushes of this launch (TCB_PEER_PUSH_ARRIVE)
   ++ep;
-  halo_push(X, 1, ep, lb, nb, [&](int32_t i) { return X.up[i]; });
+  halo_push(X, 1, ep, lb, nb, npush, [&](int32_t i) { return X.up[i]; });
   ++ep;
-  halo_push(X, 2, ep, lb, nb, [&](int32_t i) { return X.vp[i]; });
+  halo_push(X, 2, ep, lb, nb, npush, [&](int32_t i) { return X.vp[i]; });
   double2 acc = make_double2(0.0, 0.0);
   auto row = [&](int s) {
     const int64_t base = __ldg(X.slice_ptr + s);
@@ -247,18 +278,24 @@ __global__ void __launch_bounds__(kPeerThreads, 4) rhs_peer_kernel(const __grid_
   tot = cross_sum2(X, tot, ep, nrx++, lb, &sh1);
   group_barrier(X, nb);  // every CTA is done with the counters
   if (lb == 0 && threadIdx.x == 0) {
+    *X.push_count = 0u;
     *X.red0 = tot;
     X.epoch[0] = ep;
     X.epoch[1] = nrx;
   }
 }
 
+// TCB_PEER_XMERGE = 1: x updated every other iteration (two pending terms added in
+// their original order, bitwise the sequential result), as the single-GPU kernel does.
+#ifndef TCB_PEER_XMERGE
+#define TCB_PEER_XMERGE 0
+#endif
 // Algorithm 1's loop on the partitioned system (after rhs_peer_kernel).
 // BATCH: the latency variant's row product (row_Ap_batch, every slot of a row in
 // flight; ~128 registers, 2 CTAs of 8 warps per SM) for partitions with few
 // slices per resident warp (variant 4).
 template <bool BATCH>
-__global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(const __grid_constant__ PeerRun R) {
+__global__ void __launch_bounds__(kPeerThreads, BATCH ? (512 / kPeerThreads > 0 ? 512 / kPeerThreads : 1) : 2048 / kPeerThreads) pcg_peer_kernel(const __grid_constant__ PeerRun R) {
   __shared__ double2 sh[kPeerWarps];
   __shared__ double2 sh1;
   const int group = blockIdx.x / R.bpg;
@@ -275,8 +312,9 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
   unsigned int nred = 0;                // partial-buffer parity
   double2 acc;
   double2 tot = *X.red0;
-  double rho = tot.x, zeta = sqrt(tot.y), zref = zeta, alpha = 0.0, beta = 0.0;
+  double rho = tot.x, zeta = sqrt(tot.y), zref = zeta, alpha = 0.0, beta = 0.0, alpha_prev = 0.0;
   int it = 0, conv = 0, nan = 0, plast = -1;
+  unsigned int npush = 0;   // halo pushes of this launch (TCB_PEER_PUSH_ARRIVE)
   if (isnan(rho) || isnan(zeta)) nan = 1;
   if (!nan && zeta < R.eps_a) conv = 1;
   if (!nan && !conv) {
@@ -286,7 +324,7 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
       const bool first = it == 0;
       // halo of p_it into the neighbours' z ghosts
       ++ep;
-      halo_push(X, 0, ep, lb, nb, [&](int32_t i) { return first ? X.z[i] : X.z[i] + beta * pold[i]; });
+      halo_push(X, 0, ep, lb, nb, npush, [&](int32_t i) { return first ? X.z[i] : X.z[i] + beta * pold[i]; });
       // S (separate first / later loops, as in the single-GPU kernel): the
       // interior slices overlap the halo, the boundary slices wait for it
       acc = make_double2(0.0, 0.0);
@@ -318,9 +356,16 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
           const int w = (int)((__ldg(X.slice_ptr + s + 1) - base) >> 5);
           const int64_t i = (int64_t)s * kSellC + lane;
           const double po = pold[i];
-          const double xi = x[i];
           const double pi = X.z[i] + beta * po;
+#if TCB_PEER_XMERGE
+          if (!(it & 1)) {   // even it >= 2: p_{it-2} (still in pnew) and p_{it-1}, in order (pcg.cu TCB_XMERGE)
+            const double xi = x[i], p2 = pnew[i];
+            x[i] = (xi + alpha_prev * p2) + alpha * po;
+          }
+#else
+          const double xi = x[i];
           x[i] = xi + alpha * po;
+#endif
           const double sum = BATCH ? row_Ap_batch_w<false>(base, w, lane, X.col, X.A, X.z, pold, beta)
                                    : row_Ap_direct<false>(base, w, lane, ci, X.A, X.z, pold, beta);
           pnew[i] = pi;
@@ -342,6 +387,7 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
       tot = cross_sum2(X, tot, ep, nrx++, lb, &sh1);
       const double pq = tot.x;
       if (isnan(pq)) { nan = 1; break; }
+      alpha_prev = alpha;
       alpha = rho / pq;
       // U
       acc = make_double2(0.0, 0.0);
@@ -368,14 +414,19 @@ __global__ void __launch_bounds__(kPeerThreads, BATCH ? 2 : 8) pcg_peer_kernel(c
   }
   if (plast >= 0 && !nan) {
     const double* __restrict__ pl = plast ? X.p1 : X.p0;
+    // TCB_PEER_XMERGE: S(it-1) skipped its x update when it-1 was odd -> p_{it-2} pending too
+    const bool two = TCB_PEER_XMERGE && !(it & 1) && it >= 2;
+    const double* __restrict__ pl2 = plast ? X.p0 : X.p1;   // p_{it-2}
     for (int s = gw; s < ns; s += nw) {
       const int64_t i = (int64_t)s * kSellC + lane;
-      x[i] += alpha * pl[i];
+      const double xi = x[i];
+      x[i] = (two ? xi + alpha_prev * pl2[i] : xi) + alpha * pl[i];
     }
   }
-  // all CTAs of the group are past their last use of the epoch counter
+  // all CTAs of the group are past their last use of the epoch / push counters
   group_barrier(X, nb);
   if (lb == 0 && threadIdx.x == 0) {
+    *X.push_count = 0u;
     X.epoch[0] = ep;
     X.epoch[1] = nrx;
     if (group == 0) {
