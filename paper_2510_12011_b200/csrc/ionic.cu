@@ -117,6 +117,62 @@ __device__ __forceinline__ void ion_prefetch(const IonArgs& a, int64_t j) {
 #endif
 }
 
+// TCB_ION_NPT = k > 1 (experiment): k nodes per thread, processed one after the
+// other (the per-CTA table copy and the per-thread constant set-up amortised
+// over k nodes); TCB_ION_NPT_PF = 1 also prefetches the later nodes' V and states
+// into L2 at the start.
+#ifndef TCB_ION_NPT
+#define TCB_ION_NPT 1
+#endif
+#ifndef TCB_ION_NPT_PF
+#define TCB_ION_NPT_PF 0
+#endif
+#if TCB_ION_NPT > 1
+__global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB)
+    ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D, const Exp2Table* __restrict__ G, int64_t pf_dist) {
+  (void)pf_dist;
+  if (a.flags[0]) return;
+  const int64_t i0 = (int64_t)blockIdx.x * (blockDim.x * TCB_ION_NPT) + threadIdx.x;
+  double V = 0.0, Vp = 0.0;
+  double u[kTTStates];
+  if (i0 < a.n) {
+    V = a.Vk[i0];
+    Vp = a.has_prev ? a.Vkm1[i0] : V;
+#pragma unroll
+    for (int s = 0; s < kTTStates; ++s) u[s] = a.U[s * a.stride + i0];
+  }
+#if TCB_ION_NPT_PF
+  for (int q = 1; q < TCB_ION_NPT; ++q) {
+    const int64_t j = i0 + (int64_t)q * blockDim.x;
+    if (j < a.n && (threadIdx.x & 3) == 0) {
+      pf_l2(a.Vk + j);
+      if (a.has_prev) pf_l2(a.Vkm1 + j);
+#pragma unroll
+      for (int s = 0; s < kTTStates; ++s) pf_l2(a.U + s * a.stride + j);
+    }
+  }
+#endif
+  __shared__ Exp2Table Ts;
+  exp2_table_init(&Ts, G);
+  const Exp2Table* T = &Ts;
+#pragma unroll 1
+  for (int q = 0; q < TCB_ION_NPT; ++q) {
+    const int64_t i = i0 + (int64_t)q * blockDim.x;
+    if (i >= a.n) break;
+    if (q > 0) {
+      V = a.Vk[i];
+      Vp = a.has_prev ? a.Vkm1[i] : V;
+#pragma unroll
+      for (int s = 0; s < kTTStates; ++s) u[s] = a.U[s * a.stride + i];
+    }
+    if (a.do_lat) activation_update(a, i, V, Vp);
+    const double In = tt_advance(V, u, a.dt, P, D, T);
+#pragma unroll
+    for (int s = 0; s < kTTStates; ++s) a.U[s * a.stride + i] = u[s];
+    write_rhs(a, i, V, Vp, In);
+  }
+}
+#else
 __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB)
     ionic_tt_kernel(IonArgs a, TTParams P, TTDerived D, const Exp2Table* __restrict__ G, int64_t pf_dist) {
   if (a.flags[0]) return;
@@ -152,6 +208,7 @@ __global__ void __launch_bounds__(kIonThreads, TCB_ION_MINB)
   for (int s = 0; s < kTTStates; ++s) a.U[s * a.stride + i] = u[s];
   write_rhs(a, i, V, Vp, In);
 }
+#endif
 
 // ---- persistent variant with asynchronous state prefetch (TCB_ION_PERSIST) ----
 // One wave of CTAs walks the node tiles (128 nodes each) in a grid-stride loop;
@@ -377,7 +434,8 @@ cudaError_t launch_ionic_tt(const IonArgs& a, const TTParams& p, cudaStream_t s)
   if (TCB_ION_PERSIST) return launch_persist<TC_ION_TT2006_EPI>(a, p, CRNParams{}, s);
   const Exp2Table* G = device_tables();
   if (!G) return cudaErrorMemoryAllocation;
-  ionic_tt_kernel<<<nblk(a.n, kIonThreads), kIonThreads, 0, s>>>(a, p, tt_derived(p), G, ion_wave(ionic_tt_kernel));
+  ionic_tt_kernel<<<nblk(a.n, kIonThreads * TCB_ION_NPT), kIonThreads, 0, s>>>(a, p, tt_derived(p), G,
+                                                                              ion_wave(ionic_tt_kernel));
   return cudaGetLastError();
 }
 cudaError_t launch_ionic_ms(const IonArgs& a, const MSParams& p, cudaStream_t s) {
