@@ -429,6 +429,22 @@ __device__ __forceinline__ double row_Ap_stream(int64_t base, int w, int lane, c
 // Latency variant (VAR 4): all slots of a row in batches of NB loads in flight
 // (values, indices, then the gathers), slots past the row end reload its last
 // slot; accumulation in slot order.  Needs ~100 registers: one 16-warp CTA per SM.
+// TCB_BATCH_MATLOAD (experiment): the latency variant's matrix loads -- 0
+// evict-first streaming (default), 1 cached (__ldg), 2 L2 evict-last (for
+// mid-size systems whose matrix could stay in the 126 MB L2 across iterations).
+#ifndef TCB_BATCH_MATLOAD
+#define TCB_BATCH_MATLOAD 0
+#endif
+template <class T>
+__device__ __forceinline__ T ld_bmat(const T* p) {
+#if TCB_BATCH_MATLOAD == 1
+  return __ldg(p);
+#elif TCB_BATCH_MATLOAD == 2
+  return ld_keep(p);
+#else
+  return ld_mat(p);
+#endif
+}
 template <bool FIRST, int NB>
 __device__ __forceinline__ double row_Ap_batch(int64_t base, int w, int lane, const int* col,
                                                const double* A, const double* z, const double* pold,
@@ -441,8 +457,8 @@ __device__ __forceinline__ double row_Ap_batch(int64_t base, int w, int lane, co
     for (int j = 0; j < NB; ++j) {
       const int kk = min(k0 + j, w - 1);
       const int64_t t = sell_slot(base, w, kk, lane);
-      const int c = ld_mat(col + t);
-      av[j] = ld_mat(A + t);
+      const int c = ld_bmat(col + t);
+      av[j] = ld_bmat(A + t);
       g[j] = FIRST ? z[c] : z[c] + beta * pold[c];
     }
 #pragma unroll
