@@ -209,7 +209,7 @@ def oracle_sample(w, steps=20, warmup=3, preroll=None):
                        G.uniform_fibres(E) if fibre is None else fibre, {0: SIGMA, 1: SIGMA}, cfg,
                        [O.Stimulus(*s) for s in stims])
     n = xyz.shape[0]
-    allc = O.max_threads()
+    allc = host_threads()
     O.set_threads(allc)
     pre = w["preroll"] if preroll is None else preroll
     sim.run(pre + warmup)
@@ -225,6 +225,15 @@ def oracle_sample(w, steps=20, warmup=3, preroll=None):
                         f"{sample[0]}x{sample[1]}x{sample[2]} grid") +
                        f" ({n} nodes, same dx/dt/model/stimulus style), prerolled by the oracle {pre} + {warmup} "
                        f"steps, {steps} steps timed ({el:.1f} s at {allc} threads), mean PCG iters {iters:.1f}")
+
+
+def host_threads():
+    """Host cores this process may run on (the oracle's "all cores" leg): the CPU
+    affinity set, not OMP_NUM_THREADS, which torchrun sets to 1 per rank."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 def measured_peaks():
@@ -386,7 +395,7 @@ def cpu_baseline_injected(w, V_dims, device, stream, steps=20):
     sim = O.Monodomain(xyz, tets, np.zeros(E, np.int32) if region is None else region,
                        G.uniform_fibres(E) if fibre is None else fibre, {0: SIGMA, 1: SIGMA}, ocfg,
                        [O.Stimulus(*st) for st in stims])
-    allc = O.max_threads()
+    allc = host_threads()
     res = {}
     try:
         for th in (1, allc):
