@@ -135,3 +135,33 @@ def test_pcg1r_mms_dirichlet_matches_oracle(T):
         assert st["converged"].all()
         out = O.run_mms(xyz, tets, B, dt=dt, T=0.5, tol=1e-10)
         assert np.abs(v - out["V"]).max() <= 1e-8, N
+
+
+def test_pcg1r_cohort_large_members(T):
+    """Variant 6 on the shared-GPU cohort path (each large member's RHS + single-
+    reduction kernel shaped for its share of the GPU, on its own stream): every
+    member against its own oracle run (Algorithm 1), 30 steps through the upstroke."""
+    members, refs = [], []
+    try:
+        for dims, seed in (((61, 23, 9), 3), ((57, 25, 10), 5)):
+            xyz, tets, region, fib, cond, stims = _slab_case("tt2006", *dims, 0.5, permute=True, seed=seed)
+            refs.append(O.Monodomain(xyz, tets, region, fib, cond,
+                                     O.Config(dt=0.05, model="tt2006", abs_tol=1e-8, rel_tol=0.0), stims))
+            cfg = T.tc_config_default(dt=0.05, model="tt2006", abs_tol=1e-8, rel_tol=0.0, pcg_variant=6,
+                                      engine="grid")
+            members.append(T.Monodomain(xyz, tets, region, fib, cond, cfg, stims))
+        co = T.Cohort(members)
+        try:
+            for c in range(3):
+                stats = co.step(10)
+                for m, (sim, ref) in enumerate(zip(members, refs)):
+                    reps = [ref.step() for _ in range(10)]
+                    rel = np.linalg.norm(sim.V - ref.Vk) / np.linalg.norm(ref.Vk)
+                    assert rel <= 1e-8, (m, c, rel)
+                    for a, b in zip(stats[m], reps):
+                        assert abs(int(a["iters"]) - b.iters) <= 1
+        finally:
+            co.close()
+    finally:
+        for s in members:
+            s.close()
