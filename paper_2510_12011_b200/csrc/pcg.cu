@@ -61,6 +61,9 @@ struct ParityTag {  // compile-time iteration parity (bool(tag) folds to a const
 #ifndef TCB_S_PARITY
 #define TCB_S_PARITY 1   // the S phase compiled once per p-buffer parity (0: one copy, runtime parity)
 #endif
+#ifndef TCB_DIRECT_UU
+#define TCB_DIRECT_UU 1   // slices per warp pass in the direct variants' U phase and final x update
+#endif
 #ifndef TCB_BATCH_UU
 #define TCB_BATCH_UU 1    // slices per warp pass in variant 4's U phase (measured 1 < 2 < 4)
 #endif
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(kCgThreads, TCB_MINB(VAR)) pcg_kernel(CgArgs a
   if (a.flags[0]) return;  // context aborted earlier: uniform across the grid
 
   constexpr bool BATCH = VAR == 4;
-  constexpr int UU = TMA ? 4 : BATCH ? TCB_BATCH_UU : 1;  // slices per warp pass in the streaming phases
+  constexpr int UU = TMA ? 4 : BATCH ? TCB_BATCH_UU : TCB_DIRECT_UU;  // slices per warp pass in the streaming phases
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * kCgWarps + warp;
   const int nw = gridDim.x * kCgWarps;
